@@ -1,0 +1,197 @@
+/*
+ * dfsim_b200.h -- C-ABI of the B200-native batched strategy simulator.
+ *
+ * The reference (arXiv 2002.06790's `dfsim`, pure Python) has no FFI; its
+ * drop-in surface is the Python API re-exported from pkg/src/dfsim/__init__.py:6-43.
+ * Each entry point below replaces one reference function, batched over many
+ * candidate strategies (see INTEGRATION.md for the ctypes binding a dfsim
+ * maintainer would add):
+ *
+ *   dfsim_expand_dp          strategy.py:170-282  expand_data_parallel (+ graph.py:122-135 CSR)
+ *   dfsim_topo_order         graph.py:424-443     topological_order (any valid order)
+ *   dfsim_estimate_batch     costmodel.py:282-376 estimate_all (predict 158-165, comm 168-223)
+ *   dfsim_simulate_batch     engine.py:96-146     simulate (+ _finalize 69-93)
+ *   dfsim_critical_path_batch graph.py:446-485    critical_path on finish-start (reporting.py:128)
+ *   dfsim_argmin             (no reference function: cmd_simulate's per-config makespans,
+ *                            cli.py:133-148, reduced to the first minimum)
+ *
+ * Conventions
+ *  - Every pointer in a *view* struct or argument is a DEVICE pointer owned by
+ *    the caller, unless the name ends in _host.  The library never frees caller
+ *    memory.  Node index == rank of the node-id string in code-point order;
+ *    device index == rank of the device-id string.
+ *  - Calls are asynchronous on the context's stream unless documented otherwise.
+ *    Per-simulation outcomes (cycle, unknown op) are written to caller arrays;
+ *    the return value reports argument/launch problems.
+ *  - Status codes map 1:1 onto the reference exceptions (errors.py:6-92):
+ */
+#ifndef DFSIM_B200_H
+#define DFSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFSIM_OK 0
+#define DFSIM_CYCLE 1            /* CycleError: some node never placed */
+#define DFSIM_MISSING_DURATION 2 /* MissingDurationError */
+#define DFSIM_UNKNOWN_OP 3       /* UnknownOpError: estimation chain exhausted */
+#define DFSIM_CONFIG 4           /* ConfigError */
+#define DFSIM_CUDA 5             /* device / launch failure */
+#define DFSIM_BAD_ARGUMENT 6     /* ValueError-class argument problems */
+#define DFSIM_NEGATIVE_DURATION 7 /* DurationEntry(<0 or NaN) -> ValueError */
+
+/* per-(sim,node) duration source tags written by dfsim_estimate_batch */
+#define DFSIM_SRC_OVERRIDE 0
+#define DFSIM_SRC_EXACT 1
+#define DFSIM_SRC_FITTED 2
+#define DFSIM_SRC_COMM 3
+#define DFSIM_SRC_BAD_BYTES 253  /* Transfer with bytes <= 0: transfer_time raises ValueError */
+#define DFSIM_SRC_NEGATIVE 254   /* value not >= 0 */
+#define DFSIM_SRC_UNKNOWN 255
+
+typedef struct dfsim_ctx dfsim_ctx;
+
+/* One execution context per (device, stream).  stream may be NULL (legacy default). */
+int dfsim_ctx_create(int32_t device, void *stream, dfsim_ctx **out);
+int dfsim_ctx_destroy(dfsim_ctx *ctx);
+int dfsim_ctx_set_stream(dfsim_ctx *ctx, void *stream);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t dfsim_ctx_launch_count(const dfsim_ctx *ctx);
+/* Human-readable text of the last failure on this context (host memory, owned by ctx). */
+const char *dfsim_ctx_last_error(const dfsim_ctx *ctx);
+int32_t dfsim_abi_version(void);
+
+/* ---------------------------------------------------------------- graph (one topology class) */
+typedef struct {
+    int32_t n_nodes;          /* N */
+    int32_t n_devices;        /* D, devices that nodes are placed on (<= 32 for the warp engine) */
+    int64_t n_edges;          /* E, non-dangling successor references */
+    const int32_t *succ_off;  /* [N+1] */
+    const int32_t *succ_idx;  /* [E] consumer ranks, ascending per producer, multiplicity kept */
+    const int32_t *indeg;     /* [N] input references incl. dangling ones (graph.py:133-135) */
+    const int32_t *device;    /* [N] device rank */
+    const int32_t *sources;   /* [n_sources] ranks with indeg == 0, ascending */
+    int32_t n_sources;
+    const int32_t *queue_off; /* [D+1] prefix of per-device node counts (FIFO capacity) */
+    const int32_t *topo;      /* [N] a topological order, or NULL when only simulating */
+    int32_t max_indeg;        /* max over indeg[] (selects 8/16/32-bit packed counters) */
+} dfsim_graph;
+
+/* Kahn order of g into topo[N] (device); *n_ordered_host receives how many were ordered
+ * (< N means a cycle).  Synchronous. */
+int dfsim_topo_order(dfsim_ctx *ctx, const dfsim_graph *g, int32_t *topo, int32_t *n_ordered_host);
+
+/* ---------------------------------------------------------------- expansion (K1) */
+typedef struct {
+    int32_t n_base;            /* N0 nodes in base insertion order */
+    const int32_t *in_off;     /* [N0+1] input refs per base node */
+    const int32_t *in_src;     /* [refs] producer base index, -1 if dangling */
+    const int32_t *base_dev;   /* [N0] expanded-device rank for non-remapped clones */
+    const uint8_t *remap;      /* [N0] 1 if the clone moves to device_map[k] (Compute + device_map) */
+    const int32_t *marked;     /* [N0] collective index g (0..G-1) if the node is a marked gradient, else -1 */
+} dfsim_base_graph;
+
+typedef struct {
+    int32_t replicas;          /* R */
+    int32_t n_collectives;     /* G (0 when R == 1) */
+    const int32_t *clone_rank; /* [R*N0] rank of "<id>@r<k>" at index k*N0+v */
+    const int32_t *coll_rank;  /* [G] rank of "allreduce_<gid>" */
+    const int32_t *map_dev;    /* [R] device rank of device_map[k] (ignored where remap==0) */
+    int32_t fabric_dev;        /* device rank of the collective fabric */
+} dfsim_expand_plan;
+
+/* Emits the expanded graph's CSR (succ_off/succ_idx), indeg, device, sources, queue_off
+ * and topo into the caller-allocated arrays of *out (sizes: N=R*N0+G, E given by
+ * *n_edges_host after the call).  Synchronous (it returns E and the source count). */
+int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, const dfsim_expand_plan *plan,
+                    int32_t *succ_off, int32_t *succ_idx, int64_t succ_capacity, int32_t *indeg,
+                    int32_t *device, int32_t *sources, int32_t *queue_off, int32_t *topo,
+                    int32_t n_devices, int64_t *n_edges_host, int32_t *n_sources_host,
+                    int32_t *n_ordered_host);
+
+/* ---------------------------------------------------------------- profile tables (K2) */
+typedef struct {
+    /* per node */
+    const int32_t *op;          /* [N] op-type id */
+    const uint8_t *kind;        /* [N] 0 Compute, 1 Transfer, 2 Collective */
+    const int32_t *sig;         /* [N] feature-vector id */
+    const int64_t *comm_bytes;  /* [N] attrs["bytes"] when it is a Python int, else ignored */
+    const uint8_t *comm_ok;     /* [N] Transfer: Link device and int bytes; Collective: list group and int bytes */
+    const int32_t *group_size;  /* [N] len(attrs["group"]) for collectives */
+    const double *link_thr;     /* [N] Transfer: link throughput MB/s */
+    const double *link_lat;     /* [N] Transfer: link latency us */
+    /* feature vectors, names sorted by string rank */
+    int32_t n_sigs;
+    const int32_t *sig_off;     /* [n_sigs+1] */
+    const int32_t *sig_name;    /* feature-name ids */
+    const double *sig_val;
+    /* exact records: keys sorted ascending, key = hw<<42 | op<<21 | sig */
+    int32_t n_exact;
+    const uint64_t *exact_key;
+    const double *exact_mean;
+    /* fitted models: keys sorted ascending, key = hw<<21 | op; model m uses
+     * names/coefs[model_off[m] .. model_off[m+1]) and intercept[m] */
+    int32_t n_models;
+    const uint64_t *model_key;
+    const int32_t *model_off;
+    const int32_t *model_name;
+    const double *model_coef;
+    const double *model_icpt;
+    /* links: nccl-allreduce records keyed path<<32 | participants (sorted) and
+     * gpu-gpu-uni/path/2 per path id (uni_ok==0 when absent) */
+    int32_t n_nccl;
+    const uint64_t *nccl_key;
+    const double *nccl_thr;
+    int32_t n_paths;
+    const uint8_t *uni_ok;
+    const double *uni_thr;
+    const double *uni_lat;
+    /* overrides: per override set, sorted node ranks and values */
+    int32_t n_override_sets;
+    const int32_t *ov_off;
+    const int32_t *ov_node;
+    const double *ov_val;
+} dfsim_profile_tables;
+
+typedef struct {
+    int64_t n_sims;
+    const int32_t *hw;         /* [S] hardware-tag id */
+    const double *op_gap;      /* [S] op_gap_us */
+    const uint8_t *algo;       /* [S] 0 MeasuredThroughput, 1 RingAnalytic */
+    const int32_t *path;       /* [S] collective path id */
+    const int32_t *override_set; /* [S] -1 for none */
+} dfsim_strategies;
+
+/* dur[s*N+v], src[s*N+v]; bad[s] = number of nodes whose source is >= 253 */
+int dfsim_estimate_batch(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t,
+                         const dfsim_strategies *st, double *dur, uint8_t *src, int32_t *bad);
+
+/* ---------------------------------------------------------------- simulation (K3) */
+/* dur is [n_sims][dur_stride] (dur_stride >= N, or 0 to broadcast one row).
+ * start/finish are [n_sims][N] (both NULL: makespan-only mode).  busy is
+ * [n_sims][n_devices] or NULL.  n_placed[s] < N marks a CycleError for sim s. */
+int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                         int64_t dur_stride, double *start, double *finish, double *makespan,
+                         double *busy, int32_t *n_placed);
+
+/* ---------------------------------------------------------------- critical path (K4) */
+/* Over d = finish - start (reporting.py:128), or over d = finish when start is NULL
+ * (the plain critical_path(g, durations) call).  cp_len[s]; cp_path [n_sims][N] and
+ * cp_path_len[s] are optional (NULL skips the path walk).  Needs g->topo. */
+int dfsim_critical_path_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *start,
+                              const double *finish, double *cp_len, int32_t *cp_path, int32_t *cp_path_len);
+
+/* ---------------------------------------------------------------- best strategy (K5) */
+/* First minimum of (value, index) over n values; index = index_base + i.
+ * Writes one 16-byte record {double value; int64_t index} to out_record (device). */
+int dfsim_argmin(dfsim_ctx *ctx, int64_t n, const double *values, int64_t index_base, void *out_record);
+/* Lexicographic min over n gathered records (e.g. after an NCCL all-gather). */
+int dfsim_argmin_records(dfsim_ctx *ctx, int64_t n, const void *records, void *out_record);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFSIM_B200_H */

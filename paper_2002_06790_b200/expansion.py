@@ -1,0 +1,218 @@
+"""Drop-in ``expand_data_parallel`` (strategy.py:170-282) with the CSR built on the GPU.
+
+Host side (strings, once per topology class): marker matching (strategy.py:188-200),
+clone / collective ids (162-167) and their code-point ranks, device strings, the
+validation findings that the reference's ``validate(expanded)`` would raise
+(graph.py:331-385) for properties inherited from the base graph.  Device side
+(K1, csrc/expand.cu): per-edge rewiring, rank-sorted successor CSR with
+multiplicity, in-degree, devices, sources, FIFO capacities, topological order.
+The returned ExpandedGraph carries the device CSR, so simulating it needs no
+second lowering.
+"""
+
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+
+from . import native
+from .errors import ConfigError, DfsimError, PatternWarning
+from .lowering import LoweredGraph, _dev_tensor, match_pattern
+from .model import (
+    COLLECTIVE,
+    COMPUTE,
+    DEVICE_COLLECTIVE,
+    DEVICE_COMPUTE,
+    TRANSFER,
+    DataflowGraph,
+    DeviceSpec,
+    ExpandedGraph,
+    OpNode,
+    check_pattern,
+)
+
+
+def _positive_number(v) -> bool:
+    return isinstance(v, (int, float)) and not isinstance(v, bool) and v > 0
+
+
+def marked_gradients(g, cfg) -> list[str]:
+    """strategy.py:188-200."""
+    marked: list[str] = []
+    for pattern in cfg.gradient_markers:
+        check_pattern(pattern)
+        hit = sorted(nid for nid in g.nodes if match_pattern(pattern, nid))
+        if not hit:
+            warnings.warn(f"gradient marker {pattern!r} matched no node", PatternWarning, stacklevel=3)
+        marked.extend(nid for nid in hit if nid not in marked)
+    marked.sort()
+    for nid in marked:
+        node = g.nodes[nid]
+        if node.kind != COMPUTE:
+            raise ConfigError(f"gradient marker matched {node.kind} node {nid!r}; only Compute nodes are supported")
+        if not node.output_shapes or node.output_shapes[0].byte_size() <= 0:
+            raise ConfigError(f"gradient node {nid!r} has no positive-size output tensor to reduce")
+    return marked
+
+
+class ExpansionPlan:
+    """Strings and ranks of one topology class (host), plus its device CSR (K1)."""
+
+    def __init__(self, g, cfg, device: int | None = None, build_objects: bool = True):
+        R = cfg.replicas
+        if cfg.device_map and len(cfg.device_map) != R:
+            raise ConfigError(f"device_map has {len(cfg.device_map)} entries for {R} replicas")
+        if R > 1 and not cfg.device_map:
+            raise ConfigError("device_map is required when replicas > 1")
+        self.marked = marked = marked_gradients(g, cfg)
+        base_ids = list(g.nodes)
+        N0 = len(base_ids)
+        base_index = {nid: i for i, nid in enumerate(base_ids)}
+        dmap = tuple(cfg.device_map)
+        clone_dev = [[(dmap[k] if (dmap and g.nodes[nid].kind == COMPUTE) else g.nodes[nid].device)
+                      for nid in base_ids] for k in range(R)]
+        group = list(dmap) if dmap else sorted({d for row in clone_dev for d in row})
+        path = cfg.collective.path
+        self.fabric = fabric = f"collective:{path}:" + "+".join(group)
+        coll_ids = [f"allreduce_{gid}" for gid in marked] if R > 1 else []
+        clone_ids = [f"{nid}@r{k}" for k in range(R) for nid in base_ids]
+        all_ids = clone_ids + coll_ids
+        if len(set(all_ids)) != len(all_ids):
+            seen = set(clone_ids)
+            dup = next(c for c in coll_ids if c in seen)
+            raise DfsimError(f"collective id {dup!r} collides with an existing node")
+        self._validate_inherited(g, base_index, R, marked, group)
+        order = sorted(range(len(all_ids)), key=all_ids.__getitem__)
+        self.ids = [all_ids[i] for i in order]
+        rank = np.empty(len(all_ids), dtype=np.int32)
+        rank[np.asarray(order, dtype=np.int64)] = np.arange(len(all_ids), dtype=np.int32)
+        devset = {d for row in clone_dev for d in row}
+        if coll_ids:
+            devset.add(fabric)
+        self.devices = sorted(devset)
+        drank = {d: i for i, d in enumerate(self.devices)}
+        self.R, self.N0, self.G = R, N0, len(coll_ids)
+        self.cfg, self.base_ids, self.clone_dev, self.coll_ids, self.group = cfg, base_ids, clone_dev, coll_ids, group
+        # base arrays
+        in_off = np.zeros(N0 + 1, dtype=np.int32)
+        in_src, remap, marked_idx, base_dev = [], np.zeros(N0, np.uint8), np.full(N0, -1, np.int32), []
+        gidx = {gid: i for i, gid in enumerate(marked)} if R > 1 else {}
+        max_in = 0
+        for v, nid in enumerate(base_ids):
+            node = g.nodes[nid]
+            for pid, _ in node.inputs:
+                in_src.append(base_index.get(pid, -1))
+            in_off[v + 1] = len(in_src)
+            max_in = max(max_in, len(node.inputs))
+            remap[v] = 1 if (dmap and node.kind == COMPUTE) else 0
+            base_dev.append(drank.get(node.device, -1))
+            if nid in gidx:
+                marked_idx[v] = gidx[nid]
+        self.max_indeg = max(max_in, R if coll_ids else 0)
+        ctx = native.Context.get(device)
+        self.ctx = ctx
+        d = ctx.device
+        T = lambda a, dt: _dev_tensor(np.asarray(a, dt) if len(a) else np.zeros(1, dt), d, dt)  # noqa: E731
+        self._keep = [T(in_off, np.int32), T(in_src, np.int32), T(base_dev, np.int32), T(remap, np.uint8),
+                      T(marked_idx, np.int32), T(rank[: R * N0], np.int32), T(rank[R * N0:], np.int32),
+                      T([drank[x] for x in dmap] if dmap else [0], np.int32)]
+        k = self._keep
+        base = native.BaseGraph(N0, native.ptr(k[0]), native.ptr(k[1]), native.ptr(k[2]), native.ptr(k[3]),
+                                native.ptr(k[4]))
+        plan = native.ExpandPlan(R, self.G, native.ptr(k[5]), native.ptr(k[6]), native.ptr(k[7]),
+                                 drank.get(fabric, 0))
+        self.lowered = self._run_k1(ctx, base, plan, len(in_src))
+        if self.lowered.n_ordered != self.lowered.n:
+            raise DfsimError("internal: expansion produced an invalid graph: graph contains a cycle")
+        self.graph = self._objects(g, cfg) if build_objects else None
+
+    def _validate_inherited(self, g, base_index, R, marked, group):
+        """Findings of validate(expanded) that come from the base graph (graph.py:331-381)."""
+        findings = []
+        for k in range(R):
+            for nid, node in g.nodes.items():
+                cid = f"{nid}@r{k}"
+                for pid, slot in node.inputs:
+                    if pid not in g.nodes:
+                        findings.append(f"node {cid!r} references missing producer {pid + '@r' + str(k)!r}")
+                    elif not 0 <= slot < max(1, len(g.nodes[pid].output_shapes)):
+                        prod = f"allreduce_{pid}" if (R > 1 and pid in marked) else f"{pid}@r{k}"
+                        findings.append(f"node {cid!r} references invalid slot {slot} of {prod!r}")
+                if node.kind == COLLECTIVE:
+                    grp = node.attrs.get("group")
+                    if not isinstance(grp, (list, tuple)) or len(grp) < 2:
+                        findings.append(f"collective {cid!r} needs attr 'group' with >= 2 devices")
+                    if not _positive_number(node.attrs.get("bytes")):
+                        findings.append(f"collective {cid!r} needs attr 'bytes' > 0")
+                if node.kind == TRANSFER:
+                    src, dst = node.attrs.get("src_device"), node.attrs.get("dst_device")
+                    if src is None or dst is None or src == dst:
+                        findings.append(f"transfer {cid!r} needs distinct 'src_device' and 'dst_device'")
+                    if not _positive_number(node.attrs.get("bytes")):
+                        findings.append(f"transfer {cid!r} needs attr 'bytes' > 0")
+                if len(findings) >= 5:
+                    break
+        if findings:
+            raise DfsimError("internal: expansion produced an invalid graph: " + "; ".join(findings[:5]))
+
+    def _run_k1(self, ctx, base, plan, n_refs) -> LoweredGraph:
+        import torch
+
+        N = len(self.ids)
+        D = len(self.devices)
+        dev = f"cuda:{ctx.device}"
+        cap = self.R * n_refs + self.G * self.R
+        z = lambda n: torch.empty(max(n, 1), dtype=torch.int32, device=dev)  # noqa: E731
+        succ_off, succ_idx, indeg, device = z(N + 1), z(cap), z(N), z(N)
+        sources, queue_off, topo = z(N), z(D + 1), z(N)
+        n_edges, n_src, n_ord = native.I64(0), native.I32(0), native.I32(0)
+        by = native.ctypes.byref
+        ctx.call("dfsim_expand_dp", by(base), by(plan), native.ptr(succ_off), native.ptr(succ_idx), cap,
+                 native.ptr(indeg), native.ptr(device), native.ptr(sources), native.ptr(queue_off), native.ptr(topo),
+                 D, by(n_edges), by(n_src), by(n_ord))
+        return LoweredGraph.from_arrays(self.ids, self.devices, succ_off, succ_idx, indeg, device, sources, queue_off,
+                                        topo, int(n_edges.value), int(n_src.value), self.max_indeg, ctx,
+                                        int(n_ord.value))
+
+    def _objects(self, g, cfg) -> DataflowGraph:
+        """Host node/device objects in the reference's insertion order (strategy.py:202-276)."""
+        R, marked = self.R, set(self.marked) if self.R > 1 else set()
+        nodes = {}
+        for k in range(R):
+            for v, nid in enumerate(self.base_ids):
+                n = g.nodes[nid]
+                ins = tuple(((f"allreduce_{p}" if p in marked else f"{p}@r{k}"), s) for p, s in n.inputs)
+                cid = f"{nid}@r{k}"
+                nodes[cid] = OpNode(cid, n.op_type, self.clone_dev[k][v], n.kind, n.attrs, ins, n.output_shapes)
+        for gid, cid in zip(self.marked, self.coll_ids):
+            grad = g.nodes[gid]
+            nodes[cid] = OpNode(cid, "AllReduce", self.fabric, COLLECTIVE,
+                                {"group": list(self.group), "bytes": grad.output_shapes[0].byte_size(),
+                                 "path": cfg.collective.path},
+                                tuple((f"{gid}@r{k}", 0) for k in range(R)), grad.output_shapes)
+        devices = {}
+        coll = set(self.coll_ids)
+        for n in nodes.values():
+            if n.id in coll or n.device in devices:
+                continue
+            devices[n.device] = g.devices[n.device] if n.device in g.devices else \
+                DeviceSpec(n.device, DEVICE_COMPUTE, cfg.hardware)
+        if self.coll_ids:
+            devices[self.fabric] = DeviceSpec(self.fabric, DEVICE_COLLECTIVE, cfg.hardware, 1.0, 0.0)
+        meta = dict(g.metadata)
+        meta["replicas"] = R
+        gx = DataflowGraph(nodes=nodes, devices=devices, metadata=meta)
+        object.__setattr__(gx, "_dfsim_b200_lowered", ((len(nodes), len(devices), self.ctx.device), self.lowered))
+        return gx
+
+
+def expand_data_parallel(g, cfg, device: int | None = None) -> ExpandedGraph:
+    """strategy.py:170-282; the expanded graph's CSR is built by K1 on the GPU."""
+    plan = ExpansionPlan(g, cfg, device)
+    replica_of = {f"{nid}@r{k}": (nid, k) for k in range(plan.R) for nid in plan.base_ids}
+    return ExpandedGraph(graph=plan.graph, replica_of=replica_of, collective_nodes=list(plan.coll_ids))
+
+
+def expand_class(g, cfg, device: int | None = None) -> ExpansionPlan:
+    return ExpansionPlan(g, cfg, device)

@@ -1,0 +1,517 @@
+"""Host lowering: reference objects -> flat device arrays.
+
+Runs once per graph / topology class; everything per-strategy runs on the GPU.
+
+* :class:`LoweredGraph` -- node index = rank of the id string in code-point
+  order (the reference's every tie-break: engine.py:112,136; graph.py:430,474,483),
+  device index = rank of the device string (engine.py:88 entry order), CSR of
+  ``DataflowGraph.successors()`` with multiplicity (graph.py:122-131),
+  ``in_degree()`` counting dangling refs (graph.py:133-135), sources, per-device
+  FIFO capacities, and a device-computed topological order.
+* :class:`LoweredProfiles` -- the estimate tables of costmodel.py:282-376:
+  per-node op / kind / feature-vector ids (node_features, costmodel.py:226-246),
+  exact records keyed (hw, op, features) (profiledb.py:107-112), host-fitted
+  linear models (fit_for_grid, costmodel.py:253-279, the same numpy lstsq call),
+  link records (profiledb.py:122-125) and resolved override sets
+  (strategy.py:75-87).
+"""
+
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+
+from . import native
+from .errors import CycleError, FitError, FitQualityWarning, PatternWarning
+from .model import (
+    ALGO_MEASURED,
+    ALGO_RING,
+    COLLECTIVE,
+    COMPUTE,
+    DEVICE_LINK,
+    SCENARIO_GPU_GPU_UNI,
+    SCENARIO_NCCL_ALLREDUCE,
+    TRANSFER,
+    FitStats,
+    LinearCostModel,
+)
+
+R_SQUARED_WARN = 0.95
+
+
+def _dev_tensor(a, device, dtype=None):
+    import torch
+
+    arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    if arr.dtype == np.uint64:  # same bits; torch's uint64 support is partial
+        arr = arr.view(np.int64)
+    t = torch.from_numpy(arr)
+    return t.to(device=f"cuda:{device}", non_blocking=False)
+
+
+# ----------------------------------------------------------------------------- graph
+
+
+def host_csr(g, ids=None) -> dict:
+    """Rank-ordered CSR arrays of ``g`` (host numpy; graph.py:122-135 semantics)."""
+    ids = list(ids) if ids is not None else sorted(g.nodes)
+    rank = {nid: i for i, nid in enumerate(ids)}
+    nodes = g.nodes
+    devices = sorted({nodes[nid].device for nid in ids})
+    drank = {d: i for i, d in enumerate(devices)}
+    N, D = len(ids), len(devices)
+    indeg = np.empty(N, dtype=np.int32)
+    dev = np.empty(N, dtype=np.int32)
+    prods, cons = [], []
+    for c, nid in enumerate(ids):
+        node = nodes[nid]
+        indeg[c] = len(node.inputs)
+        dev[c] = drank[node.device]
+        for pid, _slot in node.inputs:
+            r = rank.get(pid)
+            if r is not None:
+                prods.append(r)
+                cons.append(c)
+    prods = np.asarray(prods, dtype=np.int64)
+    cons = np.asarray(cons, dtype=np.int32)
+    succ_idx = cons[np.argsort(prods, kind="stable")]  # consumers already ascending per producer
+    succ_off = np.zeros(N + 1, dtype=np.int32)
+    if len(prods):
+        np.cumsum(np.bincount(prods, minlength=N), out=succ_off[1:])
+    queue_off = np.zeros(D + 1, dtype=np.int32)
+    if N:
+        np.cumsum(np.bincount(dev, minlength=D), out=queue_off[1:])
+    return dict(ids=ids, rank=rank, devices=devices, indeg=indeg, device=dev, succ_off=succ_off,
+                succ_idx=succ_idx, sources=np.nonzero(indeg == 0)[0].astype(np.int32), queue_off=queue_off,
+                max_indeg=int(indeg.max()) if N else 0)
+
+
+
+class LoweredGraph:
+    """Rank-ordered CSR of one graph, resident on one CUDA device."""
+
+    def __init__(self, g, device: int | None = None, ids=None, topo: bool = True):
+        self.ctx = native.Context.get(device)
+        h = host_csr(g, ids)
+        self.ids, self.rank, self.devices = h["ids"], h["rank"], h["devices"]
+        self.n, self.n_devices = len(self.ids), len(self.devices)
+        self.host_dev, self.host_indeg = h["device"], h["indeg"]
+        self.host_succ_off, self.host_succ_idx = h["succ_off"], h["succ_idx"]
+        self._set_device_arrays(h["succ_off"], h["succ_idx"], h["indeg"], h["device"], h["sources"],
+                                h["queue_off"], h["max_indeg"], topo)
+
+    def _set_device_arrays(self, succ_off, succ_idx, indeg, dev, sources, queue_off, max_indeg, topo):
+        import torch
+
+        d = self.ctx.device
+        self.t_succ_off = _dev_tensor(succ_off, d, np.int32)
+        self.t_succ_idx = _dev_tensor(succ_idx if len(succ_idx) else np.zeros(1, np.int32), d, np.int32)
+        self.t_indeg = _dev_tensor(indeg if len(indeg) else np.zeros(1, np.int32), d, np.int32)
+        self.t_dev = _dev_tensor(dev if len(dev) else np.zeros(1, np.int32), d, np.int32)
+        self.t_sources = _dev_tensor(sources if len(sources) else np.zeros(1, np.int32), d, np.int32)
+        self.t_queue_off = _dev_tensor(queue_off, d, np.int32)
+        self.n_sources = int(len(sources))
+        self.n_edges = int(len(succ_idx))
+        self.max_indeg = max_indeg
+        self.t_topo = torch.empty(max(self.n, 1), dtype=torch.int32, device=f"cuda:{d}")
+        self.struct = native.Graph(self.n, self.n_devices, self.n_edges, native.ptr(self.t_succ_off),
+                                   native.ptr(self.t_succ_idx), native.ptr(self.t_indeg), native.ptr(self.t_dev),
+                                   native.ptr(self.t_sources), self.n_sources, native.ptr(self.t_queue_off),
+                                   native.P(0), self.max_indeg)
+        self.n_ordered = None
+        if topo:
+            self.compute_topo()
+
+    def compute_topo(self) -> bool:
+        """Device Kahn order; returns False when the graph has a cycle."""
+        got = native.I32(0)
+        self.ctx.call("dfsim_topo_order", native.ctypes.byref(self.struct), native.ptr(self.t_topo),
+                      native.ctypes.byref(got))
+        self.n_ordered = int(got.value)
+        if self.n_ordered == self.n:
+            self.struct.topo = native.ptr(self.t_topo)
+        return self.n_ordered == self.n
+
+    @property
+    def acyclic(self) -> bool:
+        return self.n_ordered == self.n
+
+    @classmethod
+    def from_arrays(cls, ids, devices, succ_off_t, succ_idx_t, indeg_t, dev_t, sources_t, queue_off_t, topo_t,
+                    n_edges, n_sources, max_indeg, ctx, n_ordered):
+        """Wrap arrays already resident on the device (the expansion kernel's output)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.ids = ids
+        self.rank = None
+        self.devices = devices
+        self.n, self.n_devices = len(ids), len(devices)
+        self.t_succ_off, self.t_succ_idx, self.t_indeg, self.t_dev = succ_off_t, succ_idx_t, indeg_t, dev_t
+        self.t_sources, self.t_queue_off, self.t_topo = sources_t, queue_off_t, topo_t
+        self.n_edges, self.n_sources, self.max_indeg, self.n_ordered = n_edges, n_sources, max_indeg, n_ordered
+        self.host_dev = None
+        self.struct = native.Graph(self.n, self.n_devices, n_edges, native.ptr(succ_off_t), native.ptr(succ_idx_t),
+                                   native.ptr(indeg_t), native.ptr(dev_t), native.ptr(sources_t), n_sources,
+                                   native.ptr(queue_off_t), native.ptr(topo_t) if n_ordered == self.n else native.P(0),
+                                   max_indeg)
+        return self
+
+    def rank_of(self):
+        if self.rank is None:
+            self.rank = {nid: i for i, nid in enumerate(self.ids)}
+        return self.rank
+
+    def device_of_rank(self):
+        if self.host_dev is None:
+            self.host_dev = self.t_dev[: self.n].cpu().numpy()
+        return self.host_dev
+
+
+def lowered(g, device: int | None = None) -> LoweredGraph:
+    """Per-graph cache (graphs are immutable by contract, graph.py:110-116)."""
+    key = (len(g.nodes), len(g.devices), device)
+    cached = getattr(g, "_dfsim_b200_lowered", None)
+    if cached is not None and cached[0] == key:
+        return cached[1]
+    lg = LoweredGraph(g, device)
+    try:
+        object.__setattr__(g, "_dfsim_b200_lowered", (key, lg))
+    except (AttributeError, TypeError):
+        pass
+    return lg
+
+
+def find_cycle(g) -> list[str] | None:
+    """One cycle's ids, DFS from sorted ids (graph.py:392-418); error path only."""
+    succ = {nid: [] for nid in g.nodes}
+    for n in g.nodes.values():
+        for pid, _ in n.inputs:
+            if pid in succ:
+                succ[pid].append(n.id)
+    for v in succ.values():
+        v.sort()
+    color = dict.fromkeys(g.nodes, 0)
+    for root in sorted(g.nodes):
+        if color[root]:
+            continue
+        stack, path = [[root, 0]], [root]
+        color[root] = 1
+        while stack:
+            top = stack[-1]
+            nid, i = top
+            if i < len(succ[nid]):
+                top[1] += 1
+                nxt = succ[nid][i]
+                if color[nxt] == 1:
+                    return path[path.index(nxt):]
+                if color[nxt] == 0:
+                    color[nxt] = 1
+                    stack.append([nxt, 0])
+                    path.append(nxt)
+            else:
+                color[nid] = 2
+                stack.pop()
+                path.pop()
+    return None
+
+
+def raise_topo_cycle(g, lg: LoweredGraph):
+    """topological_order's error (graph.py:440-442)."""
+    cyc = find_cycle(g)
+    if cyc:
+        raise CycleError(cyc)
+    left = {nid: len(n.inputs) for nid, n in g.nodes.items()}
+    raise CycleError([nid for nid, d in left.items() if d > 0])
+
+
+# ----------------------------------------------------------------------------- profiles
+
+
+def node_features(g, node) -> tuple:
+    """costmodel.py:226-246: numeric non-bool attrs + producer dims, sorted by name."""
+    feats = {}
+    for name, value in node.attrs.items():
+        if isinstance(value, bool) or not isinstance(value, (int, float)):
+            continue
+        feats[name] = float(value)
+    for i, (pid, slot) in enumerate(node.inputs):
+        producer = g.nodes.get(pid)
+        if producer is None or slot >= len(producer.output_shapes):
+            continue
+        for j, dim in enumerate(producer.output_shapes[slot].dims):
+            key = f"in{i}_dim{j}"
+            if key in feats:
+                raise ValueError(f"node {node.id!r}: attr name collides with {key!r}")
+            feats[key] = float(dim)
+    out = tuple(sorted(feats.items()))
+    for _, v in out:  # OpSignature's finiteness check (profiledb.py:45-47)
+        if v != v or v in (float("inf"), float("-inf")):
+            raise ValueError(f"non-finite feature value in {out}")
+    return out
+
+
+def fit_linear(records) -> LinearCostModel:
+    """OLS of mean duration on the features (costmodel.py:93-141), same numpy calls."""
+    if not records:
+        raise FitError("no records to fit")
+    op_type, hardware = records[0].signature.op_type, records[0].signature.hardware
+    names = tuple(n for n, _ in records[0].signature.arg_features)
+    for rec in records:
+        if rec.signature.op_type != op_type or rec.signature.hardware != hardware:
+            raise FitError("records mix op types or hardware tags")
+        if tuple(n for n, _ in rec.signature.arg_features) != names:
+            raise FitError("records mix feature names")
+    n, k = len(records), len(names)
+    if n < k + 1:
+        raise FitError(f"underdetermined: {n} records for {k} features (+ intercept)")
+    x = np.array([[v for _, v in rec.signature.arg_features] for rec in records], dtype=float)
+    y = np.array([rec.mean_duration_us for rec in records], dtype=float)
+    design = np.hstack([x, np.ones((n, 1))])
+    if np.linalg.matrix_rank(design) < k + 1:
+        bad = _collinear(x, names)
+        raise FitError("degenerate design matrix; collinear features: " + ", ".join(bad), collinear_features=bad)
+    coef, *_ = np.linalg.lstsq(design, y, rcond=None)
+    pred = design @ coef
+    ss_res = float(np.sum((y - pred) ** 2))
+    ss_tot = float(np.sum((y - np.mean(y)) ** 2))
+    if ss_tot == 0.0:
+        r2 = 1.0 if ss_res < 1e-18 else 0.0
+    else:
+        r2 = min(1.0, max(0.0, 1.0 - ss_res / ss_tot))
+    max_rel = float(np.max(np.abs(pred - y) / np.abs(y)))
+    return LinearCostModel(op_type, hardware, names, tuple(float(c) for c in coef[:k]), float(coef[k]),
+                           FitStats(r2, max_rel, n))
+
+
+def _collinear(x, names):
+    kept = np.ones((x.shape[0], 1))
+    bad = []
+    for j, name in enumerate(names):
+        cand = np.hstack([kept, x[:, j:j + 1]])
+        if np.linalg.matrix_rank(cand) == np.linalg.matrix_rank(kept):
+            bad.append(name)
+        else:
+            kept = cand
+    return bad
+
+
+def fit_for_grid(db, op_type: str, hardware: str):
+    """costmodel.py:253-279: largest same-name group (ties: smallest name tuple)."""
+    grid_map = db.op_records.get((op_type, hardware), {})
+    grid = [grid_map[k] for k in sorted(grid_map)]
+    if not grid:
+        return None
+    groups = {}
+    for rec in grid:
+        groups.setdefault(tuple(n for n, _ in rec.signature.arg_features), []).append(rec)
+    best = max(len(r) for r in groups.values())
+    chosen = min(k for k in groups if len(groups[k]) == best)
+    try:
+        model = fit_linear(groups[chosen])
+    except FitError:
+        return None
+    if model.fit_stats.r_squared < R_SQUARED_WARN:
+        warnings.warn(f"linear model for {op_type}/{hardware} has r_squared={model.fit_stats.r_squared:.4f}; "
+                      "estimates may be unreliable", FitQualityWarning, stacklevel=3)
+    return model
+
+
+def match_pattern(pattern: str, nid: str) -> bool:
+    return nid.startswith(pattern[:-1]) if pattern.endswith("*") else nid == pattern
+
+
+def resolve_overrides(overrides: dict, ids: list) -> dict:
+    """strategy.py:75-87 -- later-listed patterns win; unmatched patterns warn."""
+    out = {}
+    for pattern, value in overrides.items():
+        hit = [nid for nid in ids if match_pattern(pattern, nid)]
+        if not hit:
+            warnings.warn(f"override pattern {pattern!r} matched no node", PatternWarning, stacklevel=3)
+        for nid in hit:
+            out[nid] = float(value)
+    return out
+
+
+class LoweredProfiles:
+    """Device tables for dfsim_estimate_batch over one graph and a list of configs."""
+
+    def __init__(self, g, ids, db, configs, device: int):
+        self.device = device
+        N = len(ids)
+        nodes = g.nodes
+        rank = {nid: i for i, nid in enumerate(ids)}
+        # hardware tags, paths, override sets of the strategies
+        self.hw_ids, self.path_ids = {}, {}
+        ov_sets, ov_key_to_id = [], {}
+        self.strat_hw, self.strat_gap, self.strat_algo, self.strat_path, self.strat_ov = [], [], [], [], []
+        for cfg in configs:
+            self.strat_hw.append(self.hw_ids.setdefault(cfg.hardware, len(self.hw_ids)))
+            self.strat_gap.append(float(cfg.op_gap_us))
+            if cfg.collective.algo not in (ALGO_MEASURED, ALGO_RING):
+                raise ValueError(f"unknown collective algorithm {cfg.collective.algo!r}")
+            self.strat_algo.append(0 if cfg.collective.algo == ALGO_MEASURED else 1)
+            self.strat_path.append(self.path_ids.setdefault(cfg.collective.path, len(self.path_ids)))
+            ov_key = tuple(cfg.overrides.items())
+            if not ov_key:
+                self.strat_ov.append(-1)
+                continue
+            if ov_key not in ov_key_to_id:
+                ov_key_to_id[ov_key] = len(ov_sets)
+                ov_sets.append(resolve_overrides(cfg.overrides, ids))
+            self.strat_ov.append(ov_key_to_id[ov_key])
+        # per node: op, kind, features, comm attributes
+        op_ids, sig_ids = {}, {}
+        op = np.empty(N, np.int32)
+        kind = np.empty(N, np.uint8)
+        sig = np.empty(N, np.int32)
+        cbytes = np.zeros(N, np.int64)
+        cok = np.zeros(N, np.uint8)
+        gsize = np.zeros(N, np.int32)
+        lthr = np.ones(N, np.float64)
+        llat = np.zeros(N, np.float64)
+        self.op_nodes = {}
+        for i, nid in enumerate(ids):
+            n = nodes[nid]
+            op[i] = op_ids.setdefault(n.op_type, len(op_ids))
+            self.op_nodes.setdefault(n.op_type, []).append(i)
+            kind[i] = 0 if n.kind == COMPUTE else (1 if n.kind == TRANSFER else 2)
+            feats = node_features(g, n)
+            sig[i] = sig_ids.setdefault(feats, len(sig_ids))
+            b = n.attrs.get("bytes")
+            if n.kind == TRANSFER:
+                dev = g.devices.get(n.device)
+                if dev is not None and dev.kind == DEVICE_LINK and isinstance(b, int):
+                    cok[i], cbytes[i] = 1, _i64(b)
+                    lthr[i], llat[i] = dev.throughput_mbps, dev.latency_us
+            elif n.kind == COLLECTIVE:
+                grp = n.attrs.get("group")
+                if isinstance(grp, (list, tuple)) and isinstance(b, int):
+                    cok[i], cbytes[i], gsize[i] = 1, _i64(b), len(grp)
+        self.op_ids, self.sig_ids = op_ids, sig_ids
+        # exact records for (hw, op, sig) triples present in the graph
+        ekeys, emeans = [], []
+        for hw, h in self.hw_ids.items():
+            for opname, o in op_ids.items():
+                grid = db.op_records.get((opname, hw))
+                if not grid:
+                    continue
+                for feats, rec in grid.items():
+                    s = sig_ids.get(feats)
+                    if s is not None:
+                        ekeys.append((h << 42) | (o << 21) | s)
+                        emeans.append(rec.mean_duration_us)
+        # fitted models where some node could need one (the reference fits lazily, costmodel.py:313-316)
+        mkeys, moff, mnames, mcoef, micpt = [], [0], [], [], []
+        exact_set = set(ekeys)
+        self.models = {}
+        name_pool = {nm for feats in sig_ids for nm, _ in feats}
+        fitted = []
+        for hw, h in self.hw_ids.items():
+            for opname, o in op_ids.items():
+                if not db.op_records.get((opname, hw)):
+                    continue
+                if not self._needs_model(h, o, opname, sig, ekeys and exact_set, ids, ov_sets, hw):
+                    continue
+                m = fit_for_grid(db, opname, hw)
+                self.models[(opname, hw)] = m
+                if m is None:
+                    continue
+                name_pool.update(m.feature_names)
+                fitted.append(((h << 21) | o, m))
+        names_sorted = sorted(name_pool)
+        name_id = {nm: i for i, nm in enumerate(names_sorted)}
+        fitted.sort(key=lambda kv: kv[0])
+        for key, m in fitted:
+            mkeys.append(key)
+            mnames.extend(name_id[nm] for nm in m.feature_names)
+            mcoef.extend(m.coefficients)
+            moff.append(len(mnames))
+            micpt.append(m.intercept)
+        # feature vectors
+        soff, sname, sval = [0], [], []
+        for feats in sig_ids:  # insertion order == id order
+            for nm, v in feats:
+                sname.append(name_id[nm])
+                sval.append(v)
+            soff.append(len(sname))
+        # links
+        n_paths = len(self.path_ids)
+        uni_ok = np.zeros(max(n_paths, 1), np.uint8)
+        uni_thr = np.ones(max(n_paths, 1), np.float64)
+        uni_lat = np.zeros(max(n_paths, 1), np.float64)
+        nkeys, nthr = [], []
+        for path, p in self.path_ids.items():
+            rec = db.link_records.get((SCENARIO_GPU_GPU_UNI, path, 2))
+            if rec is not None:
+                uni_ok[p], uni_thr[p], uni_lat[p] = 1, rec.throughput_mbps, rec.latency_us
+        for (scen, path, parts), rec in db.link_records.items():
+            if scen == SCENARIO_NCCL_ALLREDUCE and path in self.path_ids:
+                nkeys.append((self.path_ids[path] << 32) | int(parts))
+                nthr.append(rec.throughput_mbps)
+        # overrides
+        ooff, onode, oval = [0], [], []
+        for res in ov_sets:
+            pairs = sorted((rank[nid], val) for nid, val in res.items())
+            onode.extend(p for p, _ in pairs)
+            oval.extend(v for _, v in pairs)
+            ooff.append(len(onode))
+
+        def srt(keys, *vals):
+            if not keys:
+                return (np.zeros(1, np.uint64),) + tuple(np.zeros(1, np.asarray(v).dtype if len(v) else np.float64)
+                                                          for v in vals)
+            o = np.argsort(np.asarray(keys, np.uint64), kind="stable")
+            return (np.asarray(keys, np.uint64)[o],) + tuple(np.asarray(v)[o] for v in vals)
+
+        ek, em = srt(ekeys, np.asarray(emeans, np.float64))
+        nk, nt = srt(nkeys, np.asarray(nthr, np.float64))
+        d = device
+        T = lambda a, dt: _dev_tensor(np.asarray(a, dt) if len(a) else np.zeros(1, dt), d, dt)  # noqa: E731
+        self.tensors = dict(
+            op=T(op, np.int32), kind=T(kind, np.uint8), sig=T(sig, np.int32), cbytes=T(cbytes, np.int64),
+            cok=T(cok, np.uint8), gsize=T(gsize, np.int32), lthr=T(lthr, np.float64), llat=T(llat, np.float64),
+            soff=T(soff, np.int32), sname=T(sname, np.int32), sval=T(sval, np.float64),
+            ek=T(ek, np.uint64), em=T(em, np.float64),
+            mk=T(np.asarray(mkeys, np.uint64), np.uint64), moff=T(moff, np.int32), mname=T(mnames, np.int32),
+            mcoef=T(mcoef, np.float64), micpt=T(micpt, np.float64),
+            nk=T(nk, np.uint64), nt=T(nt, np.float64),
+            uok=T(uni_ok, np.uint8), uthr=T(uni_thr, np.float64), ulat=T(uni_lat, np.float64),
+            ooff=T(ooff, np.int32), onode=T(onode, np.int32), oval=T(oval, np.float64),
+        )
+        t = self.tensors
+        pp = native.ptr
+        self.struct = native.ProfileTables(
+            pp(t["op"]), pp(t["kind"]), pp(t["sig"]), pp(t["cbytes"]), pp(t["cok"]), pp(t["gsize"]),
+            pp(t["lthr"]), pp(t["llat"]),
+            len(sig_ids), pp(t["soff"]), pp(t["sname"]), pp(t["sval"]),
+            len(ekeys), pp(t["ek"]), pp(t["em"]),
+            len(mkeys), pp(t["mk"]), pp(t["moff"]), pp(t["mname"]), pp(t["mcoef"]), pp(t["micpt"]),
+            len(nkeys), pp(t["nk"]), pp(t["nt"]),
+            n_paths, pp(t["uok"]), pp(t["uthr"]), pp(t["ulat"]),
+            len(ov_sets), pp(t["ooff"]), pp(t["onode"]), pp(t["oval"]))
+        self.n_sims = len(configs)
+        self.t_strat = dict(hw=T(self.strat_hw, np.int32), gap=T(self.strat_gap, np.float64),
+                            algo=T(self.strat_algo, np.uint8), path=T(self.strat_path, np.int32),
+                            ov=T(self.strat_ov, np.int32))
+        s = self.t_strat
+        self.strategies = native.Strategies(self.n_sims, pp(s["hw"]), pp(s["gap"]), pp(s["algo"]), pp(s["path"]),
+                                            pp(s["ov"]))
+
+    def _needs_model(self, h, o, opname, sig, exact_set, ids, ov_sets, hw) -> bool:
+        """True if some node of this op, not overridden in every strategy, has no exact record."""
+        for i in self.op_nodes.get(opname, ()):
+            key = (h << 42) | (o << 21) | int(sig[i])
+            if exact_set and key in exact_set:
+                continue
+            if self.strat_ov and all(k >= 0 and ids[i] in ov_sets[k] for k, hh in zip(self.strat_ov, self.strat_hw)
+                                     if hh == h):
+                continue
+            return True
+        return False
+
+
+def _i64(b: int) -> int:
+    if not -(2 ** 63) <= b < 2 ** 63:
+        raise ValueError(f"bytes {b} outside the int64 range of the device tables")
+    return int(b)

@@ -1,0 +1,158 @@
+"""ctypes binding of libdfsim_b200.so (include/dfsim_b200.h).
+
+There is no fallback: if the library is missing, cannot be loaded, or no CUDA
+device is present, every entry point raises :class:`NativeError`.  ctypes drops
+the GIL for the duration of each foreign call, so independent Python threads can
+drive independent contexts concurrently (the reference's ``--jobs`` threads,
+cli.py:133-137).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .errors import (
+    STATUS_BAD_ARGUMENT,
+    STATUS_CUDA,
+    STATUS_OK,
+    NativeError,
+)
+
+LIB_PATH = Path(__file__).resolve().parent / "libdfsim_b200.so"
+
+P = ctypes.c_void_p
+I32, I64, U8 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint8
+
+
+class Graph(ctypes.Structure):
+    _fields_ = [("n_nodes", I32), ("n_devices", I32), ("n_edges", I64), ("succ_off", P), ("succ_idx", P),
+                ("indeg", P), ("device", P), ("sources", P), ("n_sources", I32), ("queue_off", P), ("topo", P),
+                ("max_indeg", I32)]
+
+
+class BaseGraph(ctypes.Structure):
+    _fields_ = [("n_base", I32), ("in_off", P), ("in_src", P), ("base_dev", P), ("remap", P), ("marked", P)]
+
+
+class ExpandPlan(ctypes.Structure):
+    _fields_ = [("replicas", I32), ("n_collectives", I32), ("clone_rank", P), ("coll_rank", P), ("map_dev", P),
+                ("fabric_dev", I32)]
+
+
+class ProfileTables(ctypes.Structure):
+    _fields_ = [("op", P), ("kind", P), ("sig", P), ("comm_bytes", P), ("comm_ok", P), ("group_size", P),
+                ("link_thr", P), ("link_lat", P),
+                ("n_sigs", I32), ("sig_off", P), ("sig_name", P), ("sig_val", P),
+                ("n_exact", I32), ("exact_key", P), ("exact_mean", P),
+                ("n_models", I32), ("model_key", P), ("model_off", P), ("model_name", P), ("model_coef", P),
+                ("model_icpt", P),
+                ("n_nccl", I32), ("nccl_key", P), ("nccl_thr", P),
+                ("n_paths", I32), ("uni_ok", P), ("uni_thr", P), ("uni_lat", P),
+                ("n_override_sets", I32), ("ov_off", P), ("ov_node", P), ("ov_val", P)]
+
+
+class Strategies(ctypes.Structure):
+    _fields_ = [("n_sims", I64), ("hw", P), ("op_gap", P), ("algo", P), ("path", P), ("override_set", P)]
+
+
+_SIGNATURES = {
+    "dfsim_abi_version": (I32, []),
+    "dfsim_ctx_create": (ctypes.c_int, [I32, P, ctypes.POINTER(P)]),
+    "dfsim_ctx_destroy": (ctypes.c_int, [P]),
+    "dfsim_ctx_set_stream": (ctypes.c_int, [P, P]),
+    "dfsim_ctx_launch_count": (I64, [P]),
+    "dfsim_ctx_last_error": (ctypes.c_char_p, [P]),
+    "dfsim_topo_order": (ctypes.c_int, [P, ctypes.POINTER(Graph), P, ctypes.POINTER(I32)]),
+    "dfsim_expand_dp": (ctypes.c_int, [P, ctypes.POINTER(BaseGraph), ctypes.POINTER(ExpandPlan), P, P, I64, P, P, P,
+                                       P, P, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+    "dfsim_estimate_batch": (ctypes.c_int, [P, I32, ctypes.POINTER(ProfileTables), ctypes.POINTER(Strategies), P, P,
+                                            P]),
+    "dfsim_simulate_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P]),
+    "dfsim_critical_path_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, P, P, P, P]),
+    "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),
+    "dfsim_argmin_records": (ctypes.c_int, [P, I64, P, P]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: Path | None = None):
+    """Load (once) and type the shared library; raises NativeError if unavailable."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise NativeError(f"{p} is missing: build it with `python -m paper_2002_06790_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = res, args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+class Context:
+    """One dfsim_ctx per CUDA device; calls run on the caller's current torch stream."""
+
+    _by_device: dict[int, "Context"] = {}
+
+    def __init__(self, device: int):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise NativeError("no CUDA device: the B200 path has no CPU fallback")
+        self.lib = load_library()
+        self.device = device
+        handle = P()
+        with torch.cuda.device(device):
+            torch.cuda.init()
+            self._check(self.lib.dfsim_ctx_create(device, None, ctypes.byref(handle)), "ctx_create", ctx=False)
+        self.handle = handle
+
+    @classmethod
+    def get(cls, device: int | None = None) -> "Context":
+        import torch
+
+        if device is None:
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        ctx = cls._by_device.get(device)
+        if ctx is None:
+            ctx = cls._by_device[device] = Context(device)
+        return ctx
+
+    def bind_stream(self):
+        import torch
+
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.lib.dfsim_ctx_set_stream(self.handle, P(stream))
+
+    def launches(self) -> int:
+        return int(self.lib.dfsim_ctx_launch_count(self.handle))
+
+    def _check(self, rc: int, what: str, ctx: bool = True):
+        if rc == STATUS_OK:
+            return
+        msg = self.lib.dfsim_ctx_last_error(self.handle).decode() if ctx else ""
+        if rc == STATUS_BAD_ARGUMENT:
+            raise ValueError(f"{what}: {msg}")
+        if rc == STATUS_CUDA:
+            raise NativeError(f"{what}: CUDA failure: {msg}")
+        raise NativeError(f"{what}: status {rc}: {msg}")
+
+    def call(self, name: str, *args):
+        self.bind_stream()
+        self._check(getattr(self.lib, name)(self.handle, *args), name)
+
+
+def ptr(t) -> P:
+    """Device (or host) address of a torch tensor / None."""
+    return P(0) if t is None else P(t.data_ptr())

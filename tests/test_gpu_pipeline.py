@@ -1,0 +1,92 @@
+"""GPU parity of the whole per-candidate path (cli.py:83-87) against the reference:
+K1 expand_data_parallel -> K2 estimate_all -> K3 simulate -> K4 critical_path,
+checked on every golden pipeline case (tests/golden/pipeline_cases.json.gz)."""
+
+from __future__ import annotations
+
+import json
+import warnings
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(case):
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200.model import load_profiles, parse_config, parse_graph
+
+    g, db, cfg = parse_graph(case["graph"]), load_profiles(case["profiles"]), parse_config(case["config"])
+    exp = case["expect"]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        if cfg.replicas > 1 or cfg.device_map:
+            ex = fw.expand_data_parallel(g, cfg)
+            ref = parse_graph(exp["expanded"])
+            assert list(ex.graph.nodes) == list(ref.nodes), case["name"]
+            for nid, n in ref.nodes.items():
+                m = ex.graph.nodes[nid]
+                assert (m.op_type, m.device, m.kind, m.inputs, dict(m.attrs), m.output_shapes) == \
+                       (n.op_type, n.device, n.kind, n.inputs, dict(n.attrs), n.output_shapes), (case["name"], nid)
+            assert list(ex.graph.devices) == list(ref.devices)
+            assert ex.graph.devices == ref.devices
+            assert ex.collective_nodes == exp["collective_nodes"]
+            assert {k: list(v) for k, v in ex.replica_of.items()} == exp["replica_of"]
+            g = ex.graph
+        if exp.get("error") == "UnknownOpError":
+            with pytest.raises(fw.UnknownOpError) as err:
+                fw.estimate_all(g, db, cfg)
+            assert err.value.nodes == exp["nodes"], case["name"]
+            return
+        table = fw.estimate_all(g, db, cfg)
+    assert {k: [e.duration_us, e.source] for k, e in table.entries.items()} == exp["durations"], case["name"]
+    assert list(table.entries) == list(exp["durations"])
+    s = fw.simulate(g, table)
+    assert s.to_json() == json.dumps(exp["schedule"]), case["name"]
+    cp = fw.critical_path(g, {e.node_id: e.finish_us - e.start_us for e in s.entries})
+    assert [cp[0], cp[1]] == exp["cp"], case["name"]
+
+
+def test_pipeline_golden_cases(pipeline_cases):
+    for case in pipeline_cases:
+        _run(case)
+
+
+def test_sweep_matches_reference_pipeline(pipeline_cases):
+    """The batched sweep over many configs reproduces each single-candidate result."""
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200.model import load_profiles, parse_config, parse_graph
+
+    by_graph = {}
+    for case in pipeline_cases:
+        if case["expect"].get("error"):
+            continue
+        by_graph.setdefault((case["graph"], case["profiles"]), []).append(case)
+    for (gtxt, dbtxt), cases in by_graph.items():
+        g, db = parse_graph(gtxt), load_profiles(dbtxt)
+        cfgs = [parse_config(c["config"]) for c in cases]
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            res = fw.sweep(g, db, cfgs, keep_schedules=True)
+        for i, c in enumerate(cases):
+            e = c["expect"]
+            assert res.makespan[i] == e["schedule"]["makespan_us"], c["name"]
+            assert res.cp_len[i] == e["cp"][0], c["name"]
+            assert res.schedule(i).to_json() == json.dumps(e["schedule"]), c["name"]
+            assert res.critical_path(i) == (e["cp"][0], e["cp"][1]), c["name"]
+        ms = [c["expect"]["schedule"]["makespan_us"] for c in cases]
+        assert res.best_index == min(range(len(ms)), key=ms.__getitem__)
+
+
+def test_estimate_errors():
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200.model import DeviceSpec, OpNode, ProfileDB, StrategyConfig, make_graph
+
+    link = DeviceSpec("l0", "Link", "", 100.0, 0.0)
+    g = make_graph([OpNode("t", "Send", "l0", "Transfer", {"src_device": "a", "dst_device": "b", "bytes": 0}),
+                    OpNode("u", "Mystery", "gpu0")], [link, DeviceSpec("gpu0", "Compute")])
+    with pytest.raises(ValueError, match="bytes must be > 0"):
+        fw.estimate_all(g, ProfileDB(), StrategyConfig())
+    g2 = make_graph([OpNode("u", "Mystery", "gpu0")], [DeviceSpec("gpu0", "Compute")])
+    with pytest.raises(ValueError, match="nonnegative"):
+        fw.estimate_all(g2, ProfileDB(), StrategyConfig(overrides={"u": -1.0}))
