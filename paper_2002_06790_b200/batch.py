@@ -41,27 +41,58 @@ class TopologyClass:
         ctx = native.Context.get(device)
         self.ctx = ctx
         cfg0 = configs[0]
+        self.plan = None
         if class_key(cfg0) == ("plain",):
             self.graph = g
             self.lg: LoweredGraph = lowered(g, ctx.device)
         else:
-            plan = ExpansionPlan(g, cfg0, ctx.device)
-            self.graph, self.lg = plan.graph, plan.lowered
+            self.plan = ExpansionPlan(g, cfg0, ctx.device)
+            self.graph, self.lg = self.plan.graph, self.plan.lowered
         self.ids = self.lg.ids
         self.configs = list(configs)
         self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device)
 
-    def run(self, *, schedules: bool = True, paths: bool = False, out: dict | None = None) -> dict:
-        """K2 -> K3 -> K4 for every candidate; asynchronous on the current stream."""
+    def expand(self):
+        """Re-run K1 from the resident base arrays (the per-class device step)."""
+        if self.plan is not None:
+            self.plan.reexpand()
+
+    def run(self, *, schedules: bool = True, paths: bool = False, out: dict | None = None,
+            events: dict | None = None) -> dict:
+        """K2 -> K3 -> K4 for every candidate; asynchronous on the current stream.
+
+        ``events`` (optional): dict of stage name -> (start, end) torch.cuda.Event
+        pairs recorded around "estimate", "simulate" and "critical_path".
+        """
         o = out if out is not None else {}
+        ev = events or {}
+
+        def rec(name, i):
+            if name in ev:
+                ev[name][i].record()
+
+        rec("estimate", 0)
         estimate_batch(self.lp, self.lg.n, out=o)
+        rec("estimate", 1)
+        rec("simulate", 0)
         simulate_arrays(self.lg, o["dur"], schedule=True, busy=True, out=o)
+        rec("simulate", 1)
+        rec("critical_path", 0)
         if self.lg.acyclic and self.lg.n:
             critical_path_arrays(self.lg, o["start"], o["finish"], paths=paths, out=o)
+        rec("critical_path", 1)
         if not schedules:
             for k in ("start", "finish", "dur"):
                 o.pop(k, None)
         return o
+
+    def best(self, o: dict, index_base: int = 0, record=None):
+        """K5 on this device: first minimum (makespan, index_base + row) -> 16-byte record."""
+        import torch
+
+        rec = record if record is not None else torch.empty(2, dtype=torch.float64, device=o["makespan"].device)
+        self.ctx.call("dfsim_argmin", self.lp.n_sims, native.ptr(o["makespan"]), index_base, native.ptr(rec))
+        return rec
 
 
 @dataclass

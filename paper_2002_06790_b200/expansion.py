@@ -122,6 +122,7 @@ class ExpansionPlan:
                                 native.ptr(k[4]))
         plan = native.ExpandPlan(R, self.G, native.ptr(k[5]), native.ptr(k[6]), native.ptr(k[7]),
                                  drank.get(fabric, 0))
+        self._structs = (base, plan, len(in_src))
         self.lowered = self._run_k1(ctx, base, plan, len(in_src))
         if self.lowered.n_ordered != self.lowered.n:
             raise DfsimError("internal: expansion produced an invalid graph: graph contains a cycle")
@@ -155,6 +156,20 @@ class ExpansionPlan:
                     break
         if findings:
             raise DfsimError("internal: expansion produced an invalid graph: " + "; ".join(findings[:5]))
+
+    def reexpand(self) -> None:
+        """Run K1 again into the same device arrays (timed per-class device work)."""
+        base, plan, n_refs = self._structs
+        lg = self.lowered
+        N, D = len(self.ids), len(self.devices)
+        cap = self.R * n_refs + self.G * self.R
+        n_edges, n_src, n_ord = native.I64(0), native.I32(0), native.I32(0)
+        by = native.ctypes.byref
+        self.ctx.call("dfsim_expand_dp", by(base), by(plan), native.ptr(lg.t_succ_off), native.ptr(lg.t_succ_idx),
+                      cap, native.ptr(lg.t_indeg), native.ptr(lg.t_dev), native.ptr(lg.t_sources),
+                      native.ptr(lg.t_queue_off), native.ptr(lg.t_topo), D, by(n_edges), by(n_src), by(n_ord))
+        if (int(n_edges.value), int(n_src.value), int(n_ord.value)) != (lg.n_edges, lg.n_sources, lg.n_ordered):
+            raise DfsimError("internal: re-expansion disagrees with the first expansion")
 
     def _run_k1(self, ctx, base, plan, n_refs) -> LoweredGraph:
         import torch
