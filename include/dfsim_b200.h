@@ -177,6 +177,82 @@ int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, c
                          int64_t dur_stride, double *start, double *finish, double *makespan,
                          double *busy, int32_t *n_placed);
 
+/* Exact engine with remapped outputs (the fused engine's overflow fallback):
+ * row s of dur is simulated and written to output row out_rows[s] (or s when
+ * NULL), node v at column pos[v] (or v when NULL). */
+int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                            int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
+                            int32_t *n_placed, const int32_t *pos, const int64_t *out_rows);
+
+/* ---------------------------------------------------------------- fused hot path (K2a + K3 v2 + K4 v2) */
+/* Class tables built once per topology class (paper_2002_06790_b200/prepare.py). */
+typedef struct {
+    int32_t n_nodes;           /* N <= 65535 */
+    int32_t n_devices;         /* D <= 32 */
+    int64_t n_edges;
+    const uint32_t *meta;      /* [N] successor begin (24 bits) | out-degree (8 bits, 255: use succ_off) */
+    const int32_t *succ_off;   /* [N+1] */
+    const uint32_t *succ;      /* [E] consumer rank | device << 16 | single-input << 21 */
+    const uint16_t *cidx;      /* [N] counter slot of nodes with >= 2 input references */
+    const uint32_t *cnt_init;  /* [n_counter_words] packed initial counters */
+    int32_t n_counter_words;
+    int32_t counter_bits;      /* 8 or 16 */
+    const uint16_t *pos;       /* [N] output column (level-order position) of each rank */
+    const int32_t *sources;    /* ascending ranks with in-degree 0 */
+    int32_t n_sources;
+    int32_t qcap;              /* per-device FIFO ring capacity (power of two) */
+    const int32_t *device;     /* [N] device rank */
+} dfsim_sim_tables;
+
+typedef struct {
+    int64_t n_sims;
+    int32_t n_variants;
+    const double *base;        /* [V][N] from dfsim_resolve_variants */
+    int32_t n_chunks;          /* work items of <= 32 candidates sharing one variant */
+    const int64_t *order;      /* [S] candidate indices grouped by variant */
+    const int32_t *chunk_first;
+    const int32_t *chunk_count;
+    const int32_t *chunk_variant;
+    const double *op_gap;      /* [S] */
+    const int32_t *override_set; /* [S] or NULL */
+    const int32_t *ov_off;
+    const int32_t *ov_node;
+    const double *ov_val;
+} dfsim_fused_strategies;
+
+/* K2a: base[var*N+v] = estimate of node v under variant var = (hw, algo, path) with
+ * op_gap 0; sign bit set when the candidate's op_gap must be added.  status is the
+ * DFSIM_SRC_* tag per (var, v). */
+int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t, int32_t n_variants,
+                           const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path, double *base,
+                           uint8_t *status);
+
+/* K3 v2: outputs start/finish [S][N] by level position; flags[s] = 1 when the
+ * FIFO ring overflowed (re-run s with dfsim_simulate_batch_ex); n_placed[s] = -1 then. */
+int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,
+                         double *start, double *finish, double *makespan, double *busy, int32_t *n_placed,
+                         int32_t *flags);
+
+typedef struct {
+    int32_t n_nodes;
+    int32_t n_slots;           /* suffix slots per candidate (interval colouring) */
+    const int32_t *rank_of_pos;
+    const uint16_t *cp_slot;   /* [N] by position */
+    const int32_t *cp_off;     /* [N+1] by position */
+    const uint16_t *cp_succ_slot; /* [E] */
+    const uint8_t *src_flag;   /* [N] by position: in-degree 0 */
+    int32_t n_groups;
+    const int32_t *group_off;  /* <= 32 positions of one level each */
+    int32_t n_chunks;
+    const int32_t *chunk_off;  /* groups per prefetch chunk */
+    int32_t chunk_positions;   /* max positions per chunk */
+} dfsim_cp_tables;
+
+/* K4 v2: critical-path length and its start node per candidate over start/finish
+ * stored by level position. */
+int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *start,
+                               const double *finish, double *cp_len, int32_t *cp_src);
+
 /* ---------------------------------------------------------------- critical path (K4) */
 /* Over d = finish - start (reporting.py:128), or over d = finish when start is NULL
  * (the plain critical_path(g, durations) call).  cp_len[s]; cp_path [n_sims][N] and

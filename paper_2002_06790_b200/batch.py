@@ -24,6 +24,9 @@ from .estimate import estimate_batch, raise_for_row
 from .expansion import ExpansionPlan
 from .lowering import LoweredGraph, LoweredProfiles, lowered
 from .model import SOURCE_TAGS, DurationEntry
+from .prepare import ClassTables
+from .lowering import resolve_overrides
+import warnings
 from .simulator import build_schedule, critical_path_arrays, simulate_arrays
 
 
@@ -35,9 +38,16 @@ def class_key(cfg) -> tuple:
 
 
 class TopologyClass:
-    """One expanded graph resident on a device + profile tables for a candidate list."""
+    """One expanded graph resident on a device + profile tables for a candidate list.
 
-    def __init__(self, g, db, configs, device: int | None = None):
+    ``fused=True`` (default) runs the fused hot path -- K2a variant resolve,
+    K3 v2 engine with on-the-fly durations, K4 v2 level-order critical path --
+    whenever the class fits it (prepare.ClassTables.fused_ok) and every variant
+    resolves without errors; otherwise the unfused K2 -> K3 -> K4 path runs,
+    which also produces the reference's exact error for failing candidates.
+    """
+
+    def __init__(self, g, db, configs, device: int | None = None, fused: bool = True):
         ctx = native.Context.get(device)
         self.ctx = ctx
         cfg0 = configs[0]
@@ -51,6 +61,117 @@ class TopologyClass:
         self.ids = self.lg.ids
         self.configs = list(configs)
         self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device)
+        self.tables = None
+        self.fused = False
+        if fused and self.lg.acyclic and self.lg.n:
+            self.tables = ClassTables(self.lg)
+            if self.tables.fused_ok:
+                self._prepare_variants()
+
+    # ------------------------------------------------------------------ fused path
+    def _prepare_variants(self):
+        import torch
+
+        lp, N = self.lp, self.lg.n
+        keys = list(zip(lp.strat_hw, lp.strat_algo, lp.strat_path))
+        var_ids: dict = {}
+        var_of = np.asarray([var_ids.setdefault(k, len(var_ids)) for k in keys], np.int64)
+        V = len(var_ids)
+        dev = f"cuda:{self.ctx.device}"
+        vk = list(var_ids)
+        self.v_hw = torch.tensor([k[0] for k in vk], dtype=torch.int32, device=dev)
+        self.v_algo = torch.tensor([k[1] for k in vk], dtype=torch.uint8, device=dev)
+        self.v_path = torch.tensor([k[2] for k in vk], dtype=torch.int32, device=dev)
+        self.n_variants = V
+        self.var_of = var_of
+        self.base = torch.empty((V, N), dtype=torch.float64, device=dev)
+        self.status = torch.empty((V, N), dtype=torch.uint8, device=dev)
+        self.resolve()
+        st = self.status.cpu().numpy()
+        if (st >= 253).any():
+            return  # some candidate fails estimation: keep the unfused path (exact error semantics)
+        order = np.argsort(var_of, kind="stable")
+        firsts, counts, variants = [], [], []
+        sorted_var = var_of[order]
+        bounds = np.flatnonzero(np.diff(sorted_var)) + 1
+        for a, b in zip(np.r_[0, bounds], np.r_[bounds, len(order)]):
+            for c in range(a, b, 32):
+                firsts.append(c)
+                counts.append(min(32, b - c))
+                variants.append(int(sorted_var[a]))
+        T = lambda x, dt: torch.as_tensor(np.asarray(x), dtype=dt, device=dev)  # noqa: E731
+        self.f_order = T(order, torch.int64)
+        self.f_first, self.f_count, self.f_var = T(firsts, torch.int32), T(counts, torch.int32), T(variants, torch.int32)
+        t, s = lp.tensors, lp.t_strat
+        self.fused_strat = native.FusedStrategies(
+            lp.n_sims, V, native.ptr(self.base), len(firsts), native.ptr(self.f_order), native.ptr(self.f_first),
+            native.ptr(self.f_count), native.ptr(self.f_var), native.ptr(s["gap"]),
+            native.ptr(s["ov"]) if any(x >= 0 for x in lp.strat_ov) else native.P(0),
+            native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]))
+        self.fused = True
+
+    def resolve(self):
+        """K2a: estimate every node once per (hardware, algorithm, path) variant."""
+        self.ctx.call("dfsim_resolve_variants", self.lg.n, native.ctypes.byref(self.lp.struct), self.n_variants,
+                      native.ptr(self.v_hw), native.ptr(self.v_algo), native.ptr(self.v_path),
+                      native.ptr(self.base), native.ptr(self.status))
+
+    def _fallback(self, o, rows):
+        """Exact engine for candidates whose FIFO ring overflowed (never changes results)."""
+        import torch
+
+        dev = o["makespan"].device
+        idx = torch.as_tensor(rows, dtype=torch.int64, device=dev)
+        s = self.lp.t_strat
+        sub = {k: v.index_select(0, idx).contiguous() for k, v in s.items()}
+        strat = native.Strategies(len(rows), native.ptr(sub["hw"]), native.ptr(sub["gap"]), native.ptr(sub["algo"]),
+                                  native.ptr(sub["path"]), native.ptr(sub["ov"]))
+        N = self.lg.n
+        dur = torch.empty((len(rows), N), dtype=torch.float64, device=dev)
+        src = torch.empty((len(rows), N), dtype=torch.uint8, device=dev)
+        bad = torch.empty(len(rows), dtype=torch.int32, device=dev)
+        self.ctx.call("dfsim_estimate_batch", N, native.ctypes.byref(self.lp.struct), native.ctypes.byref(strat),
+                      native.ptr(dur), native.ptr(src), native.ptr(bad))
+        self.ctx.call("dfsim_simulate_batch_ex", native.ctypes.byref(self.lg.struct), len(rows), native.ptr(dur), N,
+                      native.ptr(o["start"]), native.ptr(o["finish"]), native.ptr(o["makespan"]),
+                      native.ptr(o["busy"]), native.ptr(o["n_placed"]), native.ptr(self.tables.t["pos32"]),
+                      native.ptr(idx))
+        o.setdefault("fallback_rows", []).extend(int(r) for r in rows)
+
+    def run_fused(self, o: dict, ev: dict, paths: bool = False):
+        import torch
+
+        lg, S, N, D = self.lg, self.lp.n_sims, self.lg.n, self.lg.n_devices
+        dev = f"cuda:{self.ctx.device}"
+        if "start" not in o:
+            o["start"] = torch.empty((S, N), dtype=torch.float64, device=dev)
+            o["finish"] = torch.empty((S, N), dtype=torch.float64, device=dev)
+            o["makespan"] = torch.empty(S, dtype=torch.float64, device=dev)
+            o["busy"] = torch.empty((S, max(D, 1)), dtype=torch.float64, device=dev)
+            o["n_placed"] = torch.empty(S, dtype=torch.int32, device=dev)
+            o["flags"] = torch.empty(S, dtype=torch.int32, device=dev)
+            o["cp_len"] = torch.empty(S, dtype=torch.float64, device=dev)
+            o["cp_src"] = torch.empty(S, dtype=torch.int32, device=dev)
+            o["bad"] = torch.zeros(S, dtype=torch.int32, device=dev)
+        o["layout"] = "position"
+        rec = lambda name, i: ev[name][i].record() if name in ev else None  # noqa: E731
+        rec("estimate", 0)
+        self.resolve()
+        rec("estimate", 1)
+        rec("simulate", 0)
+        self.ctx.call("dfsim_simulate_fused", native.ctypes.byref(self.tables.sim_struct),
+                      native.ctypes.byref(self.fused_strat), native.ptr(o["start"]), native.ptr(o["finish"]),
+                      native.ptr(o["makespan"]), native.ptr(o["busy"]), native.ptr(o["n_placed"]),
+                      native.ptr(o["flags"]))
+        rec("simulate", 1)
+        flagged = torch.nonzero(o["flags"]).flatten()
+        if flagged.numel():
+            self._fallback(o, flagged.cpu().tolist())
+        rec("critical_path", 0)
+        self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.tables.cp_struct), S,
+                      native.ptr(o["start"]), native.ptr(o["finish"]), native.ptr(o["cp_len"]), native.ptr(o["cp_src"]))
+        rec("critical_path", 1)
+        return o
 
     def expand(self):
         """Re-run K1 from the resident base arrays (the per-class device step)."""
@@ -66,25 +187,39 @@ class TopologyClass:
         """
         o = out if out is not None else {}
         ev = events or {}
+        if self.fused:
+            self.run_fused(o, ev)
+        else:
+            def rec(name, i):
+                if name in ev:
+                    ev[name][i].record()
 
-        def rec(name, i):
-            if name in ev:
-                ev[name][i].record()
-
-        rec("estimate", 0)
-        estimate_batch(self.lp, self.lg.n, out=o)
-        rec("estimate", 1)
-        rec("simulate", 0)
-        simulate_arrays(self.lg, o["dur"], schedule=True, busy=True, out=o)
-        rec("simulate", 1)
-        rec("critical_path", 0)
-        if self.lg.acyclic and self.lg.n:
-            critical_path_arrays(self.lg, o["start"], o["finish"], paths=paths, out=o)
-        rec("critical_path", 1)
+            rec("estimate", 0)
+            estimate_batch(self.lp, self.lg.n, out=o)
+            rec("estimate", 1)
+            rec("simulate", 0)
+            simulate_arrays(self.lg, o["dur"], schedule=True, busy=True, out=o)
+            rec("simulate", 1)
+            rec("critical_path", 0)
+            if self.lg.acyclic and self.lg.n:
+                critical_path_arrays(self.lg, o["start"], o["finish"], paths=paths, out=o)
+            rec("critical_path", 1)
+            o["layout"] = "rank"
         if not schedules:
             for k in ("start", "finish", "dur"):
                 o.pop(k, None)
         return o
+
+    def rows_by_rank(self, o: dict, row: int):
+        """(start, finish) of one candidate as device tensors in node-rank order."""
+        n = self.lg.n
+        st, fi = o["start"][row, :n], o["finish"][row, :n]
+        if o.get("layout") == "position":
+            import torch
+
+            pos = torch.as_tensor(self.tables.pos, device=st.device)
+            st, fi = st.index_select(0, pos), fi.index_select(0, pos)
+        return st, fi
 
     def best(self, o: dict, index_base: int = 0, record=None):
         """K5 on this device: first minimum (makespan, index_base + row) -> 16-byte record."""
@@ -114,22 +249,38 @@ class SweepResult:
     def schedule(self, i: int):
         """The reference Schedule object of candidate i."""
         tc, o, row = self._row(i)
-        n = tc.lg.n
-        src = o["src"][row, :n].cpu().numpy()
-        dur = o["dur"][row, :n].cpu().numpy()
-        entries = {nid: DurationEntry(float(dur[k]), SOURCE_TAGS[src[k]]) for k, nid in enumerate(tc.ids)}
-        return build_schedule(tc.graph, tc.lg, o["start"][row, :n].cpu().numpy(), o["finish"][row, :n].cpu().numpy(),
+        st, fi = tc.rows_by_rank(o, row)
+        entries = self._entries(tc, o, row)
+        return build_schedule(tc.graph, tc.lg, st.cpu().numpy(), fi.cpu().numpy(),
                               float(o["makespan"][row].item()), o["busy"][row, : tc.lg.n_devices].cpu().numpy(),
                               entries)
 
+    def _entries(self, tc, o, row):
+        """Duration source tags of one candidate (the fused path keeps per-variant tags)."""
+        n = tc.lg.n
+        if "src" in o:
+            src = o["src"][row, :n].cpu().numpy()
+        else:
+            src = tc.status[int(tc.var_of[row])].cpu().numpy().copy()
+            cfg = tc.configs[row]
+            if cfg.overrides:
+                rank = tc.lg.rank_of()
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore")
+                    for nid in resolve_overrides(cfg.overrides, tc.ids):
+                        src[rank[nid]] = 0
+        return {nid: DurationEntry(0.0, SOURCE_TAGS[src[k]]) for k, nid in enumerate(tc.ids)}
+
     def critical_path(self, i: int):
         tc, o, row = self._row(i)
-        p = critical_path_arrays(tc.lg, o["start"][row:row + 1], o["finish"][row:row + 1], paths=True)
+        st, fi = tc.rows_by_rank(o, row)
+        p = critical_path_arrays(tc.lg, st.reshape(1, -1).contiguous(), fi.reshape(1, -1).contiguous(), paths=True)
         k = int(p["cp_path_len"][0].item())
         return float(p["cp_len"][0].item()), [tc.ids[j] for j in p["cp_path"][0, :k].cpu().tolist()]
 
 
-def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = False) -> SweepResult:
+def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = False,
+          fused: bool = True) -> SweepResult:
     """Evaluate every config like ``_run_one_simulation`` and pick the best.
 
     Errors follow the reference sweep: the first failing config (in list order)
@@ -148,7 +299,7 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
     result = SweepResult(np.zeros(0), np.zeros(0), -1, float("nan"))
     failures = []
     for pos, (key, idx) in enumerate(groups.items()):
-        tc = TopologyClass(g, db, [configs[i] for i in idx], ctx.device)
+        tc = TopologyClass(g, db, [configs[i] for i in idx], ctx.device, fused=fused)
         o = tc.run(schedules=True)
         t_idx = torch.as_tensor(idx, dtype=torch.int64, device=dev)
         makespan.index_copy_(0, t_idx, o["makespan"])

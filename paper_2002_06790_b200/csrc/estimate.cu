@@ -124,7 +124,40 @@ __global__ void __launch_bounds__(256) k_estimate(int32_t N, dfsim_profile_table
     }
 }
 
+__global__ void __launch_bounds__(256) k_resolve_variants(int32_t N, dfsim_profile_tables t, int32_t V,
+                                                          const int32_t *var_hw, const uint8_t *var_algo,
+                                                          const int32_t *var_path, double *base, uint8_t *status) {
+    const int64_t total = static_cast<int64_t>(V) * N;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int var = static_cast<int>(i / N);
+        const int v = static_cast<int>(i - static_cast<int64_t>(var) * N);
+        uint8_t src;
+        double val = estimate_one(t, v, __ldg(var_hw + var), 0.0, __ldg(var_algo + var), __ldg(var_path + var), -1, &src);
+        if (src < DFSIM_SRC_BAD_BYTES && !(val >= 0.0)) src = DFSIM_SRC_NEGATIVE;
+        if (src >= DFSIM_SRC_BAD_BYTES) val = __longlong_as_double(0x7ff8000000000000LL);
+        // record/model values get the candidate's op_gap on Compute nodes (costmodel.py:305)
+        const bool add_gap = (src == DFSIM_SRC_EXACT || src == DFSIM_SRC_FITTED) && __ldg(t.kind + v) == 0;
+        base[i] = add_gap ? -val : val;
+        status[i] = src;
+    }
+}
+
 }  // namespace
+
+extern "C" int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t, int32_t n_variants,
+                                      const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path,
+                                      double *base, uint8_t *status) {
+    if (!ctx || !t || !base || !status) return DFSIM_BAD_ARGUMENT;
+    if (n_nodes <= 0 || n_variants <= 0) return DFSIM_OK;
+    DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const int64_t total = (int64_t)n_variants * n_nodes;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)ctx->num_sms * 16) blocks = (int64_t)ctx->num_sms * 16;
+    k_resolve_variants<<<(unsigned)blocks, 256, 0, ctx->stream>>>(n_nodes, *t, n_variants, var_hw, var_algo, var_path,
+                                                                 base, status);
+    return dfsim_after_launch(ctx, "k_resolve_variants");
+}
 
 extern "C" int dfsim_estimate_batch(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t,
                                     const dfsim_strategies *st, double *dur, uint8_t *src, int32_t *bad) {

@@ -1,0 +1,380 @@
+// K2a + K3 v2 + K4 v2: the fused per-candidate hot path.
+//
+// K2a dfsim_resolve_variants: estimate_all's fallback chain (costmodel.py:282-331)
+//     evaluated once per (variant = hardware tag x collective algorithm, node) with
+//     op_gap 0; the sign bit of the stored value marks "add op_gap" (Compute nodes
+//     resolved from an exact record or a fitted model, costmodel.py:305-320).
+// K3 v2 dfsim_simulate_fused: engine.py:96-146 per candidate with durations
+//     formed on the fly: dur = override (302-304) | base + op_gap | base.
+//     One CTA per SM holds the class graph and the staged duration row of the
+//     variant it is working on in shared memory; each warp simulates one candidate
+//     (lane d = device rank d) from ~3 KB of shared state: compact 8/16-bit
+//     dependency counters for multi-input nodes and one 32-entry FIFO ring per
+//     device.  A ring overflow aborts the candidate and flags it for the exact
+//     engine (dfsim_simulate_batch_ex), so results never depend on the ring size.
+// K4 v2 dfsim_critical_path_levels: graph.py:446-474 on finish-start, warp per
+//     candidate, reverse level order; suffix values live in statically allocated
+//     shared-memory slots, schedule rows (stored by level position) are prefetched
+//     with cp.async one chunk ahead.
+#include <cuda_runtime.h>
+
+#include "internal.cuh"
+
+namespace {
+
+// ------------------------------------------------------------------ K3 v2
+
+struct FusedArgs {
+    dfsim_sim_tables g;
+    dfsim_fused_strategies st;
+    double *start, *finish, *makespan, *busy;
+    int32_t *n_placed, *flags;
+    int32_t *chunk_counter;
+    int32_t wpb;
+    int32_t smem_graph;  // bytes of the CTA-shared part
+    int32_t smem_warp;   // bytes per warp
+};
+
+__device__ __forceinline__ double warp_min_nonneg(double x) {
+    // finishes are >= +0.0, so their IEEE bits order like unsigned integers
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned hi = __reduce_min_sync(DFSIM_FULL_MASK, static_cast<unsigned>(b >> 32));
+    const unsigned lo = __reduce_min_sync(DFSIM_FULL_MASK,
+                                          static_cast<unsigned>(b >> 32) == hi ? static_cast<unsigned>(b) : 0xffffffffu);
+    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
+}
+
+template <int kBits>
+__device__ __forceinline__ bool counter_dec(unsigned *words, int c) {
+    constexpr int kPer = 32 / kBits;
+    constexpr unsigned kMask = (1u << kBits) - 1u;
+    const int shift = (c % kPer) * kBits;
+    const unsigned old = atomicSub(words + c / kPer, 1u << shift);
+    return ((old >> shift) & kMask) == 1u;
+}
+
+template <int kBits>
+__global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int N = a.g.n_nodes, D = a.g.n_devices;
+    const int E = static_cast<int>(a.g.n_edges);
+    const int QCAP = a.g.qcap;
+    const unsigned QMASK = static_cast<unsigned>(QCAP - 1);
+
+    // CTA-shared tables
+    uint32_t *s_meta = reinterpret_cast<uint32_t *>(smem);
+    uint32_t *s_succ = s_meta + N;
+    uint16_t *s_cidx = reinterpret_cast<uint16_t *>(s_succ + E);
+    uint16_t *s_pos = s_cidx + N;
+    double *s_base = reinterpret_cast<double *>(smem + ((static_cast<size_t>(N) * 8 + static_cast<size_t>(E) * 4 + 15) / 16) * 16);
+    unsigned char *wbase = smem + a.smem_graph + static_cast<size_t>(warp) * a.smem_warp;
+    int32_t *tails = reinterpret_cast<int32_t *>(wbase);
+    unsigned *cnt = reinterpret_cast<unsigned *>(wbase + 128);
+    uint16_t *q = reinterpret_cast<uint16_t *>(wbase + 128 + a.g.n_counter_words * 4);
+    __shared__ int s_chunk;
+
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        s_meta[i] = __ldg(a.g.meta + i);
+        s_cidx[i] = __ldg(a.g.cidx + i);
+        s_pos[i] = __ldg(reinterpret_cast<const uint16_t *>(a.g.pos) + i);
+    }
+    for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.g.succ + i);
+    int staged = -1;
+
+    for (;;) {
+        if (threadIdx.x == 0) s_chunk = atomicAdd(a.chunk_counter, 1);
+        __syncthreads();
+        const int c = s_chunk;
+        if (c >= a.st.n_chunks) break;
+        const int var = __ldg(a.st.chunk_variant + c);
+        if (var != staged) {
+            const double *row = a.st.base + static_cast<int64_t>(var) * N;
+            for (int i = threadIdx.x; i < N; i += blockDim.x) s_base[i] = __ldg(row + i);
+            staged = var;
+            __syncthreads();
+        }
+        if (warp < __ldg(a.st.chunk_count + c)) {
+            const int64_t s = __ldg(a.st.order + __ldg(a.st.chunk_first + c) + warp);
+            const double gap = __ldg(a.st.op_gap + s);
+            const int ovs = a.st.override_set ? __ldg(a.st.override_set + s) : -1;
+            double *out_s = a.start + s * N;
+            double *out_f = a.finish + s * N;
+            for (int w = lane; w < a.g.n_counter_words; w += 32) cnt[w] = __ldg(a.g.cnt_init + w);
+            if (lane < D) tails[lane] = 0;
+            unsigned head = 0;
+            int flag = 0;
+            __syncwarp();
+            for (int b = 0; b < a.g.n_sources; b += 32) {  // sources in rank order (engine.py:111-114)
+                const int i = b + lane;
+                const bool has = i < a.g.n_sources;
+                const int v = has ? __ldg(a.g.sources + i) : 0;
+                const int dv = has ? __ldg(a.g.device + v) : 32 + lane;
+                const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, dv);
+                const int base = has ? tails[dv] : 0;
+                __syncwarp();
+                if (has) {
+                    const int p = base + __popc(peers & lanemask_lt());
+                    q[dv * QCAP + (p & QMASK)] = static_cast<uint16_t>(v);
+                    if ((peers & lanemask_lt()) == 0) tails[dv] = base + __popc(peers);
+                }
+                __syncwarp();
+            }
+            if (__any_sync(DFSIM_FULL_MASK, lane < D && static_cast<unsigned>(tails[lane]) - head > static_cast<unsigned>(QCAP)))
+                flag = 1;
+
+            bool running = false;
+            int run_v = 0;
+            double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
+            int placed = 0;
+            auto start_idle = [&]() {
+                if (lane < D && !running && static_cast<int>(head) < tails[lane]) {
+                    const int v = q[lane * QCAP + (head & QMASK)];
+                    head++;
+                    const double b = s_base[v];
+                    double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
+                    if (ovs >= 0) {
+                        int lo = __ldg(a.st.ov_off + ovs), hi = __ldg(a.st.ov_off + ovs + 1);
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (__ldg(a.st.ov_node + mid) < v) lo = mid + 1; else hi = mid;
+                        }
+                        if (lo < __ldg(a.st.ov_off + ovs + 1) && __ldg(a.st.ov_node + lo) == v) dur = __ldg(a.st.ov_val + lo);
+                    }
+                    const double f = __dadd_rn(now, dur);
+                    const int p = s_pos[v];
+                    out_s[p] = now;
+                    out_f[p] = f;
+                    running = true;
+                    run_v = v;
+                    run_f = f;
+                    busy_sum = __dadd_rn(busy_sum, __dsub_rn(f, now));
+                    if (f > span) span = f;
+                    placed++;
+                }
+            };
+            if (!flag) start_idle();
+            while (!flag && __any_sync(DFSIM_FULL_MASK, running)) {
+                now = warp_min_nonneg(running ? run_f : __longlong_as_double(0x7ff0000000000000LL));
+                const bool done = running && run_f == now;
+                const int seg_lo = lane < D ? tails[lane] : 0;
+                __syncwarp();
+                if (done) {
+                    running = false;
+                    const uint32_t meta = s_meta[run_v];
+                    const int j0 = static_cast<int>(meta & 0xffffffu);
+                    int deg = static_cast<int>(meta >> 24);
+                    if (deg == 255) deg = __ldg(a.g.succ_off + run_v + 1) - j0;
+                    for (int j = j0; j < j0 + deg; j++) {
+                        const uint32_t e = s_succ[j];
+                        const int m = static_cast<int>(e & 0xffffu);
+                        if ((e >> 21) & 1u || counter_dec<kBits>(cnt, s_cidx[m])) {
+                            const int dv = static_cast<int>((e >> 16) & 31u);
+                            const int p = atomicAdd(tails + dv, 1);
+                            q[dv * QCAP + (p & QMASK)] = static_cast<uint16_t>(m);
+                        }
+                    }
+                }
+                __syncwarp();
+                const int seg_hi = lane < D ? tails[lane] : 0;
+                if (__any_sync(DFSIM_FULL_MASK, lane < D && static_cast<unsigned>(seg_hi) - head > static_cast<unsigned>(QCAP))) {
+                    flag = 1;  // ring overflow: hand this candidate to the exact engine
+                    break;
+                }
+                // enqueue(sorted(newly_ready)): sort each device's new ring segment by rank
+                if (seg_hi - seg_lo > 1) {
+                    uint16_t *qd = q + lane * QCAP;
+                    for (int i = seg_lo + 1; i < seg_hi; i++) {
+                        const uint16_t x = qd[i & QMASK];
+                        int j = i - 1;
+                        while (j >= seg_lo && qd[j & QMASK] > x) {
+                            qd[(j + 1) & QMASK] = qd[j & QMASK];
+                            j--;
+                        }
+                        qd[(j + 1) & QMASK] = x;
+                    }
+                }
+                __syncwarp();
+                start_idle();
+            }
+            const double ms = warp_max_f64(span);
+            const int total = __reduce_add_sync(DFSIM_FULL_MASK, placed);
+            if (lane == 0) {
+                a.makespan[s] = ms;
+                a.n_placed[s] = flag ? -1 : total;
+                a.flags[s] = flag;
+            }
+            if (a.busy && lane < D) a.busy[s * D + lane] = busy_sum;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ K4 v2
+
+struct CpLevelArgs {
+    dfsim_cp_tables t;
+    int64_t S;
+    const double *start, *finish;
+    double *cp_len;
+    int32_t *cp_src;
+    int32_t wpb;
+    int32_t slot_bytes;  // per warp
+};
+
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+
+__global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int N = a.t.n_nodes, K = a.t.chunk_positions;
+    unsigned char *wb = smem + static_cast<size_t>(warp) * (a.slot_bytes + 4 * K * 8);
+    double *slots = reinterpret_cast<double *>(wb);
+    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2][2][K]: (stage, start|finish, pos)
+
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * a.wpb + warp; s < a.S; s += static_cast<int64_t>(gridDim.x) * a.wpb) {
+        const double *st = a.start + s * N;
+        const double *fi = a.finish + s * N;
+        auto prefetch = [&](int c, int stage) {
+            const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
+            const int p0 = __ldg(a.t.group_off + g0), p1 = __ldg(a.t.group_off + g1);
+            double *bs = buf + stage * 2 * K;
+            for (int p = p0 + lane; p < p1; p += 32) {
+                cp_async8(bs + (p - p0), st + p);
+                cp_async8(bs + K + (p - p0), fi + p);
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        double len = 0.0;
+        int src = 0x7fffffff;
+        const int nc = a.t.n_chunks;
+        if (nc > 0) prefetch(nc - 1, (nc - 1) & 1);
+        for (int c = nc - 1; c >= 0; c--) {
+            if (c > 0) {
+                prefetch(c - 1, (c - 1) & 1);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
+            }
+            __syncwarp();
+            const double *bs = buf + (c & 1) * 2 * K;
+            const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
+            const int p0 = __ldg(a.t.group_off + g0);
+            for (int gi = g1 - 1; gi >= g0; gi--) {
+                const int q0 = __ldg(a.t.group_off + gi), q1 = __ldg(a.t.group_off + gi + 1);
+                const int p = q0 + lane;
+                if (p < q1) {
+                    const double d = __dsub_rn(bs[K + (p - p0)], bs[p - p0]);  // finish - start (reporting.py:128)
+                    double best = 0.0;
+                    const int j1 = __ldg(a.t.cp_off + p + 1);
+                    for (int j = __ldg(a.t.cp_off + p); j < j1; j++) {
+                        const double x = slots[__ldg(a.t.cp_succ_slot + j)];
+                        if (x > best) best = x;
+                    }
+                    const double sv = __dadd_rn(d, best);
+                    slots[__ldg(a.t.cp_slot + p)] = sv;
+                    if (__ldg(a.t.src_flag + p)) {
+                        const int r = __ldg(a.t.rank_of_pos + p);
+                        if (sv > len || (sv == len && r < src) || src == 0x7fffffff) {
+                            len = sv;
+                            src = r;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            __syncwarp();
+        }
+        // max over sources, then min id achieving it (graph.py:471-474)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ol = __shfl_xor_sync(DFSIM_FULL_MASK, len, o);
+            const int os = __shfl_xor_sync(DFSIM_FULL_MASK, src, o);
+            if (os != 0x7fffffff && (src == 0x7fffffff || ol > len || (ol == len && os < src))) {
+                len = ol;
+                src = os;
+            }
+        }
+        if (lane == 0) {
+            a.cp_len[s] = src == 0x7fffffff ? 0.0 : len;
+            if (a.cp_src) a.cp_src[s] = src == 0x7fffffff ? -1 : src;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,
+                                    double *start, double *finish, double *makespan, double *busy, int32_t *n_placed,
+                                    int32_t *flags) {
+    if (!ctx || !g || !st) return DFSIM_BAD_ARGUMENT;
+    DFSIM_ARG_CHECK(ctx, start && finish && makespan && n_placed && flags, "outputs are required");
+    DFSIM_ARG_CHECK(ctx, g->n_nodes > 0 && g->n_nodes <= 65535 && g->n_devices <= 32, "fused engine limits");
+    DFSIM_ARG_CHECK(ctx, g->qcap >= 2 && (g->qcap & (g->qcap - 1)) == 0, "qcap must be a power of two");
+    DFSIM_ARG_CHECK(ctx, g->counter_bits == 8 || g->counter_bits == 16, "counter_bits 8 or 16");
+    if (st->n_sims <= 0 || st->n_chunks <= 0) return DFSIM_OK;
+    DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const int N = g->n_nodes;
+    const size_t graph_bytes = ((size_t)N * 8 + (size_t)g->n_edges * 4 + 15) / 16 * 16 + (size_t)N * 8;
+    const size_t warp_bytes = (128 + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * g->qcap * 2 + 15) / 16 * 16;
+    const size_t budget = 227 * 1024 - 64;
+    int wpb = 32;
+    while (wpb > 1 && graph_bytes + wpb * warp_bytes > budget) wpb--;
+    DFSIM_ARG_CHECK(ctx, graph_bytes + wpb * warp_bytes <= budget, "class tables do not fit in shared memory");
+    FusedArgs a;
+    a.g = *g;
+    a.st = *st;
+    a.start = start; a.finish = finish; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed; a.flags = flags;
+    a.wpb = wpb;
+    a.smem_graph = (int)graph_bytes;
+    a.smem_warp = (int)warp_bytes;
+    void *p = nullptr;
+    int rc = dfsim_scratch(ctx, 256, &p);
+    if (rc) return rc;
+    a.chunk_counter = static_cast<int32_t *>(p);
+    DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(a.chunk_counter, 0, sizeof(int32_t), ctx->stream));
+    const size_t smem = graph_bytes + wpb * warp_bytes;
+    const int grid = ctx->num_sms < st->n_chunks ? ctx->num_sms : (int)st->n_chunks;
+    if (g->counter_bits == 8) {
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_simulate_fused<8><<<grid, wpb * 32, smem, ctx->stream>>>(a);
+    } else {
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_simulate_fused<16><<<grid, wpb * 32, smem, ctx->stream>>>(a);
+    }
+    return dfsim_after_launch(ctx, "k_simulate_fused");
+}
+
+extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *start,
+                                          const double *finish, double *cp_len, int32_t *cp_src) {
+    if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
+    DFSIM_ARG_CHECK(ctx, start && finish && cp_len, "start, finish and cp_len are required");
+    DFSIM_ARG_CHECK(ctx, t->chunk_positions >= 32, "chunk_positions >= 32");
+    if (n_sims <= 0) return DFSIM_OK;
+    DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const int slot_bytes = ((t->n_slots > 0 ? t->n_slots : 1) * 8 + 15) / 16 * 16;
+    const size_t per_warp = (size_t)slot_bytes + 4 * (size_t)t->chunk_positions * 8;
+    const size_t budget = 227 * 1024;
+    int wpb = 16;
+    while (wpb > 1 && wpb * per_warp > budget) wpb--;
+    DFSIM_ARG_CHECK(ctx, wpb * per_warp <= budget, "critical-path slots do not fit in shared memory");
+    CpLevelArgs a;
+    a.t = *t;
+    a.S = n_sims;
+    a.start = start; a.finish = finish; a.cp_len = cp_len; a.cp_src = cp_src;
+    a.wpb = wpb;
+    a.slot_bytes = slot_bytes;
+    const size_t smem = wpb * per_warp;
+    DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_critical_path_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int64_t want = (n_sims + wpb - 1) / wpb;
+    int blocks_per_sm = (int)(budget / (smem + 1024));
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    const int64_t cap = (int64_t)ctx->num_sms * blocks_per_sm;
+    const int grid = (int)(want < cap ? want : cap);
+    k_critical_path_levels<<<grid, wpb * 32, smem, ctx->stream>>>(a);
+    return dfsim_after_launch(ctx, "k_critical_path_levels");
+}

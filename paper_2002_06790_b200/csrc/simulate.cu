@@ -36,6 +36,8 @@ struct SimArgs {
     unsigned char *gscratch;  // global-mode state, per_warp bytes per resident warp
     int64_t per_warp;         // bytes of counters+queue per warp (global or shared)
     int32_t cnt_words;        // u32 words of packed counters
+    const int32_t *pos;       // optional output column per node
+    const int64_t *out_rows;  // optional output row per simulated row
 };
 
 template <int kBits>
@@ -104,8 +106,9 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
 
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * wpb + wib; s < a.S; s += static_cast<int64_t>(gridDim.x) * wpb) {
         const double *dur = a.dur + s * a.dur_stride;
-        double *out_start = a.start ? a.start + s * N : nullptr;
-        double *out_finish = a.finish ? a.finish + s * N : nullptr;
+        const int64_t row = a.out_rows ? a.out_rows[s] : s;
+        double *out_start = a.start ? a.start + row * N : nullptr;
+        double *out_finish = a.finish ? a.finish + row * N : nullptr;
 
         Counter<kBits>::init(cnt, a.cnt_words, a.indeg, N, lane);
         if (lane < D) tails[lane] = my_qoff;
@@ -139,8 +142,9 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
                 const int v = q[head++];
                 const double f = __dadd_rn(now, __ldg(dur + v));
                 if (out_start) {
-                    out_start[v] = now;
-                    out_finish[v] = f;
+                    const int col = a.pos ? __ldg(a.pos + v) : v;
+                    out_start[col] = now;
+                    out_finish[col] = f;
                 }
                 running = true;
                 run_v = v;
@@ -186,10 +190,10 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
         const double ms = warp_max_f64(span);
         const int total = warp_sum_i32(placed);
         if (lane == 0) {
-            a.makespan[s] = ms;
-            if (a.n_placed) a.n_placed[s] = total;
+            a.makespan[row] = ms;
+            if (a.n_placed) a.n_placed[row] = total;
         }
-        if (a.busy && lane < D) a.busy[s * D + lane] = busy_sum;
+        if (a.busy && lane < D) a.busy[row * D + lane] = busy_sum;
         __syncwarp();
     }
 }
@@ -213,6 +217,13 @@ int launch_bits(dfsim_ctx *ctx, SimArgs &a, bool shared_mode, int wpb, int grid,
 extern "C" int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
                                     int64_t dur_stride, double *start, double *finish, double *makespan,
                                     double *busy, int32_t *n_placed) {
+    return dfsim_simulate_batch_ex(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed, nullptr,
+                                   nullptr);
+}
+
+extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                                       int64_t dur_stride, double *start, double *finish, double *makespan,
+                                       double *busy, int32_t *n_placed, const int32_t *pos, const int64_t *out_rows) {
     if (!ctx || !g) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, g->n_nodes >= 0 && n_sims >= 0, "negative sizes");
     DFSIM_ARG_CHECK(ctx, g->n_devices >= 0 && g->n_devices <= 32, "the warp engine supports at most 32 devices");
@@ -232,6 +243,7 @@ extern "C" int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_
     a.sources = g->sources; a.queue_off = g->queue_off; a.n_sources = g->n_sources;
     a.S = n_sims; a.dur = dur; a.dur_stride = dur_stride;
     a.start = start; a.finish = finish; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed;
+    a.pos = pos; a.out_rows = out_rows;
     const int per = 32 / bits;
     a.cnt_words = (N + per - 1) / per;
     const bool q16 = N <= 65536;

@@ -57,6 +57,24 @@ class Strategies(ctypes.Structure):
     _fields_ = [("n_sims", I64), ("hw", P), ("op_gap", P), ("algo", P), ("path", P), ("override_set", P)]
 
 
+class SimTables(ctypes.Structure):
+    _fields_ = [("n_nodes", I32), ("n_devices", I32), ("n_edges", I64), ("meta", P), ("succ_off", P), ("succ", P),
+                ("cidx", P), ("cnt_init", P), ("n_counter_words", I32), ("counter_bits", I32), ("pos", P),
+                ("sources", P), ("n_sources", I32), ("qcap", I32), ("device", P)]
+
+
+class FusedStrategies(ctypes.Structure):
+    _fields_ = [("n_sims", I64), ("n_variants", I32), ("base", P), ("n_chunks", I32), ("order", P),
+                ("chunk_first", P), ("chunk_count", P), ("chunk_variant", P), ("op_gap", P), ("override_set", P),
+                ("ov_off", P), ("ov_node", P), ("ov_val", P)]
+
+
+class CpTables(ctypes.Structure):
+    _fields_ = [("n_nodes", I32), ("n_slots", I32), ("rank_of_pos", P), ("cp_slot", P), ("cp_off", P),
+                ("cp_succ_slot", P), ("src_flag", P), ("n_groups", I32), ("group_off", P), ("n_chunks", I32),
+                ("chunk_off", P), ("chunk_positions", I32)]
+
+
 _SIGNATURES = {
     "dfsim_abi_version": (I32, []),
     "dfsim_ctx_create": (ctypes.c_int, [I32, P, ctypes.POINTER(P)]),
@@ -71,6 +89,11 @@ _SIGNATURES = {
                                             P]),
     "dfsim_simulate_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P]),
     "dfsim_critical_path_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, P, P, P, P]),
+    "dfsim_simulate_batch_ex": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P, P, P]),
+    "dfsim_resolve_variants": (ctypes.c_int, [P, I32, ctypes.POINTER(ProfileTables), I32, P, P, P, P, P]),
+    "dfsim_simulate_fused": (ctypes.c_int, [P, ctypes.POINTER(SimTables), ctypes.POINTER(FusedStrategies), P, P, P,
+                                            P, P, P]),
+    "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P, P]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),
     "dfsim_argmin_records": (ctypes.c_int, [P, I64, P, P]),
 }

@@ -1,0 +1,119 @@
+"""GPU: the fused hot path (K2a + K3 v2 + K4 v2) equals the unfused kernels and the oracle.
+
+The unfused path is itself pinned to the reference's golden outputs
+(test_gpu_engine.py, test_gpu_pipeline.py); here the fused engine must reproduce
+it bit-for-bit on the headline ResNet-50 DP8 class, including candidates with
+overrides, and including the exact-engine fallback after a FIFO ring overflow.
+"""
+
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _configs(n, overrides_every=5):
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+
+    dmap = tuple(f"gpu{i}" for i in range(8))
+    out = []
+    for i in range(n):
+        ov = {"wgrad_l1_*": 3.25, "l2_b0_conv1@r3": 0.0} if i % overrides_every == 3 else {}
+        algo = "RingAnalytic" if i % 3 else "MeasuredThroughput"
+        out.append(StrategyConfig(replicas=8, device_map=dmap, collective=CollectiveConfig(algo, "NVLink"),
+                                  gradient_markers=("wgrad_*",), hardware=f"hw{i % 4}", op_gap_us=1e-3 * (i // 4),
+                                  overrides=ov))
+    return out
+
+
+@pytest.fixture(scope="module")
+def resnet():
+    from paper_2002_06790_b200 import workloads as W
+
+    g = W.resnet50_training(batch=32)
+    return g, W.model_profiles(g, [f"hw{i}" for i in range(4)])
+
+
+def _rank_rows(tc, o):
+    return [tuple(t.cpu().numpy() for t in tc.rows_by_rank(o, r)) for r in range(tc.lp.n_sims)]
+
+
+def _compare(tc_f, tc_u):
+    of, ou = tc_f.run(), tc_u.run()
+    assert tc_f.fused and not tc_u.fused
+    assert np.array_equal(of["makespan"].cpu().numpy(), ou["makespan"].cpu().numpy())
+    assert np.array_equal(of["busy"].cpu().numpy(), ou["busy"].cpu().numpy())
+    assert np.array_equal(of["cp_len"].cpu().numpy(), ou["cp_len"].cpu().numpy())
+    assert (of["n_placed"].cpu().numpy() == tc_f.lg.n).all()
+    for (sf, ff), (su, fu) in zip(_rank_rows(tc_f, of), _rank_rows(tc_u, ou)):
+        assert np.array_equal(sf, su) and np.array_equal(ff, fu)
+    return of
+
+
+def test_fused_equals_unfused_resnet_dp8(resnet):
+    from paper_2002_06790_b200.batch import TopologyClass
+
+    g, db = resnet
+    cfgs = _configs(96)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        tf = TopologyClass(g, db, cfgs, fused=True)
+        tu = TopologyClass(g, db, cfgs, fused=False)
+    of = _compare(tf, tu)
+    assert not of.get("fallback_rows")
+    src = of["cp_src"].cpu().numpy()
+    assert (src >= 0).all()
+
+
+def test_fused_ring_overflow_falls_back_exactly(resnet, monkeypatch):
+    from paper_2002_06790_b200.batch import TopologyClass
+    from paper_2002_06790_b200.prepare import ClassTables
+
+    g, db = resnet
+    cfgs = _configs(40)
+    monkeypatch.setattr(ClassTables, "QCAP", 2)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        tf = TopologyClass(g, db, cfgs, fused=True)
+        tu = TopologyClass(g, db, cfgs, fused=False)
+    of = _compare(tf, tu)
+    assert of.get("fallback_rows"), "QCAP=2 must overflow on this graph"
+
+
+def test_fused_spot_check_against_oracle(resnet):
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200 import sweep
+
+    g, db = resnet
+    cfgs = _configs(12)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = sweep(g, db, cfgs, keep_schedules=True)
+        for i in (0, 3, 7, 11):
+            ms, cp_len, entries, busy, cp_path = O.run_candidate(g, db, cfgs[i])
+            assert res.makespan[i] == ms and res.cp_len[i] == cp_len
+            s = res.schedule(i)
+            assert [(e.node_id, e.device, e.start_us, e.finish_us) for e in s.entries] == entries
+            assert res.critical_path(i) == (cp_len, cp_path)
+    ms_all = res.makespan
+    assert res.best_index == int(np.argmin(ms_all))
+
+
+def test_sweep_unfused_matches_fused_on_layered(pipeline_cases):
+    import json
+
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200.model import load_profiles, parse_config, parse_graph
+
+    cases = [c for c in pipeline_cases if c["name"].startswith(("layered_ring", "random30", "c7_r"))]
+    for c in cases:
+        g, db, cfg = parse_graph(c["graph"]), load_profiles(c["profiles"]), parse_config(c["config"])
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            r = fw.sweep(g, db, [cfg] * 3, keep_schedules=True)
+        assert r.schedule(2).to_json() == json.dumps(c["expect"]["schedule"]), c["name"]
+        assert r.cp_len[1] == c["expect"]["cp"][0]
