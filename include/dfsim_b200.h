@@ -236,11 +236,11 @@ int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_
 typedef struct {
     int32_t n_nodes;
     int32_t n_slots;           /* suffix slots per candidate (interval colouring) */
+    int32_t n_edges;
     const int32_t *rank_of_pos;
+    const uint32_t *cp_meta;   /* [N] by position: successor-slot begin | count << 16 | source << 24 */
     const uint16_t *cp_slot;   /* [N] by position */
-    const int32_t *cp_off;     /* [N+1] by position */
     const uint16_t *cp_succ_slot; /* [E] */
-    const uint8_t *src_flag;   /* [N] by position: in-degree 0 */
     int32_t n_groups;
     const int32_t *group_off;  /* <= 32 positions of one level each */
     int32_t n_chunks;

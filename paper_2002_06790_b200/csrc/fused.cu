@@ -219,7 +219,8 @@ struct CpLevelArgs {
     double *cp_len;
     int32_t *cp_src;
     int32_t wpb;
-    int32_t slot_bytes;  // per warp
+    int32_t slot_bytes;   // per warp
+    int32_t table_bytes;  // CTA-shared tables
 };
 
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
@@ -227,20 +228,33 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
 
+// Shared tables (all by level position): meta[p] = successor-slot begin (16 bits) |
+// count (8 bits) << 16 | source << 24; slot[p]; succ_slot[E]; group_off[G+1].
 __global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int N = a.t.n_nodes, K = a.t.chunk_positions;
-    unsigned char *wb = smem + static_cast<size_t>(warp) * (a.slot_bytes + 4 * K * 8);
+    const int N = a.t.n_nodes, K = a.t.chunk_positions, G = a.t.n_groups;
+    const int E = a.t.n_edges;
+    uint32_t *s_meta = reinterpret_cast<uint32_t *>(smem);
+    uint16_t *s_slot = reinterpret_cast<uint16_t *>(s_meta + N);
+    uint16_t *s_succ = s_slot + N;
+    uint16_t *s_goff = s_succ + E;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        s_meta[i] = __ldg(a.t.cp_meta + i);
+        s_slot[i] = __ldg(a.t.cp_slot + i);
+    }
+    for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.t.cp_succ_slot + i);
+    for (int i = threadIdx.x; i <= G; i += blockDim.x) s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
+    __syncthreads();
+    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(warp) * (a.slot_bytes + 4 * K * 8);
     double *slots = reinterpret_cast<double *>(wb);
-    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2][2][K]: (stage, start|finish, pos)
+    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2 stages][start|finish][K]
 
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * a.wpb + warp; s < a.S; s += static_cast<int64_t>(gridDim.x) * a.wpb) {
         const double *st = a.start + s * N;
         const double *fi = a.finish + s * N;
         auto prefetch = [&](int c, int stage) {
-            const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
-            const int p0 = __ldg(a.t.group_off + g0), p1 = __ldg(a.t.group_off + g1);
+            const int p0 = s_goff[__ldg(a.t.chunk_off + c)], p1 = s_goff[__ldg(a.t.chunk_off + c + 1)];
             double *bs = buf + stage * 2 * K;
             for (int p = p0 + lane; p < p1; p += 32) {
                 cp_async8(bs + (p - p0), st + p);
@@ -262,23 +276,23 @@ __global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
             __syncwarp();
             const double *bs = buf + (c & 1) * 2 * K;
             const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
-            const int p0 = __ldg(a.t.group_off + g0);
+            const int p0 = s_goff[g0];
             for (int gi = g1 - 1; gi >= g0; gi--) {
-                const int q0 = __ldg(a.t.group_off + gi), q1 = __ldg(a.t.group_off + gi + 1);
-                const int p = q0 + lane;
-                if (p < q1) {
+                const int p = s_goff[gi] + lane;
+                if (p < s_goff[gi + 1]) {
+                    const uint32_t m = s_meta[p];
+                    const int j0 = static_cast<int>(m & 0xffffu), j1 = j0 + static_cast<int>((m >> 16) & 0xffu);
                     const double d = __dsub_rn(bs[K + (p - p0)], bs[p - p0]);  // finish - start (reporting.py:128)
                     double best = 0.0;
-                    const int j1 = __ldg(a.t.cp_off + p + 1);
-                    for (int j = __ldg(a.t.cp_off + p); j < j1; j++) {
-                        const double x = slots[__ldg(a.t.cp_succ_slot + j)];
+                    for (int j = j0; j < j1; j++) {
+                        const double x = slots[s_succ[j]];
                         if (x > best) best = x;
                     }
                     const double sv = __dadd_rn(d, best);
-                    slots[__ldg(a.t.cp_slot + p)] = sv;
-                    if (__ldg(a.t.src_flag + p)) {
+                    slots[s_slot[p]] = sv;
+                    if (m >> 24) {
                         const int r = __ldg(a.t.rank_of_pos + p);
-                        if (sv > len || (sv == len && r < src) || src == 0x7fffffff) {
+                        if (src == 0x7fffffff || sv > len || (sv == len && r < src)) {
                             len = sv;
                             src = r;
                         }
@@ -286,9 +300,8 @@ __global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
                 }
                 __syncwarp();
             }
-            __syncwarp();
         }
-        // max over sources, then min id achieving it (graph.py:471-474)
+        // max over sources, then the min id achieving it (graph.py:471-474)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double ol = __shfl_xor_sync(DFSIM_FULL_MASK, len, o);
@@ -354,27 +367,27 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, start && finish && cp_len, "start, finish and cp_len are required");
     DFSIM_ARG_CHECK(ctx, t->chunk_positions >= 32, "chunk_positions >= 32");
+    DFSIM_ARG_CHECK(ctx, t->n_nodes <= 65535 && t->n_edges <= 65535 && t->n_slots <= 65535, "level tables use 16-bit ids");
     if (n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const int slot_bytes = ((t->n_slots > 0 ? t->n_slots : 1) * 8 + 15) / 16 * 16;
+    const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 + 15) / 16 * 16;
     const size_t per_warp = (size_t)slot_bytes + 4 * (size_t)t->chunk_positions * 8;
-    const size_t budget = 227 * 1024;
+    const size_t budget = 227 * 1024 - 64;
     int wpb = 16;
-    while (wpb > 1 && wpb * per_warp > budget) wpb--;
-    DFSIM_ARG_CHECK(ctx, wpb * per_warp <= budget, "critical-path slots do not fit in shared memory");
+    while (wpb > 1 && table_bytes + wpb * per_warp > budget) wpb--;
+    DFSIM_ARG_CHECK(ctx, table_bytes + wpb * per_warp <= budget, "critical-path tables do not fit in shared memory");
     CpLevelArgs a;
     a.t = *t;
     a.S = n_sims;
     a.start = start; a.finish = finish; a.cp_len = cp_len; a.cp_src = cp_src;
     a.wpb = wpb;
     a.slot_bytes = slot_bytes;
-    const size_t smem = wpb * per_warp;
+    a.table_bytes = (int)table_bytes;
+    const size_t smem = table_bytes + wpb * per_warp;
     DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_critical_path_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int64_t want = (n_sims + wpb - 1) / wpb;
-    int blocks_per_sm = (int)(budget / (smem + 1024));
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-    const int64_t cap = (int64_t)ctx->num_sms * blocks_per_sm;
-    const int grid = (int)(want < cap ? want : cap);
+    const int64_t want = (n_sims + wpb - 1) / wpb;
+    const int grid = (int)(want < ctx->num_sms ? want : ctx->num_sms);
     k_critical_path_levels<<<grid, wpb * 32, smem, ctx->stream>>>(a);
     return dfsim_after_launch(ctx, "k_critical_path_levels");
 }

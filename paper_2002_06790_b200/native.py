@@ -70,8 +70,8 @@ class FusedStrategies(ctypes.Structure):
 
 
 class CpTables(ctypes.Structure):
-    _fields_ = [("n_nodes", I32), ("n_slots", I32), ("rank_of_pos", P), ("cp_slot", P), ("cp_off", P),
-                ("cp_succ_slot", P), ("src_flag", P), ("n_groups", I32), ("group_off", P), ("n_chunks", I32),
+    _fields_ = [("n_nodes", I32), ("n_slots", I32), ("n_edges", I32), ("rank_of_pos", P), ("cp_meta", P),
+                ("cp_slot", P), ("cp_succ_slot", P), ("n_groups", I32), ("group_off", P), ("n_chunks", I32),
                 ("chunk_off", P), ("chunk_positions", I32)]
 
 

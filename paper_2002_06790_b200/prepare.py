@@ -53,7 +53,7 @@ class ClassTables:
     """Device-resident engine + critical-path tables of one topology class."""
 
     GROUP = 32        # positions processed together (one per lane)
-    CHUNK = 128       # positions prefetched per cp.async batch
+    CHUNK = 64        # positions prefetched per cp.async batch
     QCAP = 32         # per-device FIFO ring capacity of the fused engine
 
     def __init__(self, lg, host=None):
@@ -122,7 +122,7 @@ class ClassTables:
                 slot[v] = s
                 by_release.setdefault(int(release[v]), []).append(s)
         self.n_slots = nslots
-        self.fused_ok = self.fused_ok and nslots < 65536
+        self.fused_ok = self.fused_ok and nslots < 65536 and self.n_edges < 65536 and outdeg.max(initial=0) < 256
         cp_off = np.zeros(N + 1, np.int64)
         cp_off[1:] = np.cumsum(outdeg[order])
         cp_succ = slot[idx[np.concatenate([np.arange(off[v], off[v + 1]) for v in order.tolist()])
@@ -144,21 +144,22 @@ class ClassTables:
             coff.append(goff.size - 1)
         coff = np.asarray(coff, np.int64)
         self.n_groups, self.n_chunks = goff.size - 1, coff.size - 1
-        src_flag = (indeg[order] == 0).astype(np.uint8)
+        src_flag = (indeg[order] == 0).astype(np.int64)
+        cp_meta = (cp_off[:-1] & 0xFFFF) | (np.minimum(outdeg[order], 255) << 16) | (src_flag << 24)
         T = lambda a, dt: _t(a, dt, self.ctx.device)  # noqa: E731
         self.t = dict(meta=T(meta, np.uint32), succ_off=lg.t_succ_off, succ=T(succ, np.uint32),
                       cidx=T(cidx, np.uint16), cnt_init=T(packed, np.uint32), pos=T(pos, np.uint16 if N <= 65535 else np.int32),
                       pos32=T(pos, np.int32),
                       sources=lg.t_sources, rank_of_pos=T(order, np.int32), cp_slot=T(slot[order], np.uint16 if nslots < 65536 else np.int32),
-                      cp_off=T(cp_off, np.int32), cp_succ=T(cp_succ, np.uint16 if nslots < 65536 else np.int32),
-                      group_off=T(goff, np.int32), chunk_off=T(coff, np.int32), src_flag=T(src_flag, np.uint8))
+                      cp_meta=T(cp_meta, np.uint32), cp_succ=T(cp_succ, np.uint16 if nslots < 65536 else np.int32),
+                      group_off=T(goff, np.int32), chunk_off=T(coff, np.int32))
         t = self.t
         p = native.ptr
         self.sim_struct = native.SimTables(N, D, self.n_edges, p(t["meta"]), p(t["succ_off"]), p(t["succ"]),
                                            p(t["cidx"]), p(t["cnt_init"]), words, bits, p(t["pos"]), p(t["sources"]),
                                            lg.n_sources, self.QCAP, p(lg.t_dev))
-        self.cp_struct = native.CpTables(N, self.n_slots, p(t["rank_of_pos"]), p(t["cp_slot"]), p(t["cp_off"]),
-                                         p(t["cp_succ"]), p(t["src_flag"]), self.n_groups, p(t["group_off"]),
+        self.cp_struct = native.CpTables(N, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
+                                         p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
                                          self.n_chunks, p(t["chunk_off"]), self.CHUNK)
 
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
