@@ -227,6 +227,10 @@ int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_
                            const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path, double *base,
                            uint8_t *status);
 
+/* Candidates one CTA of the fused engine holds; chunks of dfsim_fused_strategies
+ * must not exceed it (0: the class does not fit the fused engine). */
+int32_t dfsim_fused_capacity(const dfsim_sim_tables *g);
+
 /* K3 v2: outputs start/finish [S][N] by level position; flags[s] = 1 when the
  * FIFO ring overflowed (re-run s with dfsim_simulate_batch_ex); n_placed[s] = -1 then. */
 int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,

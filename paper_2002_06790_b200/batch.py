@@ -90,14 +90,18 @@ class TopologyClass:
         st = self.status.cpu().numpy()
         if (st >= 253).any():
             return  # some candidate fails estimation: keep the unfused path (exact error semantics)
+        cap = int(self.ctx.lib.dfsim_fused_capacity(native.ctypes.byref(self.tables.sim_struct)))
+        if cap <= 0:
+            return
+        self.chunk_capacity = cap
         order = np.argsort(var_of, kind="stable")
         firsts, counts, variants = [], [], []
         sorted_var = var_of[order]
         bounds = np.flatnonzero(np.diff(sorted_var)) + 1
         for a, b in zip(np.r_[0, bounds], np.r_[bounds, len(order)]):
-            for c in range(a, b, 32):
+            for c in range(a, b, cap):
                 firsts.append(c)
-                counts.append(min(32, b - c))
+                counts.append(min(cap, b - c))
                 variants.append(int(sorted_var[a]))
         T = lambda x, dt: torch.as_tensor(np.asarray(x), dtype=dt, device=dev)  # noqa: E731
         self.f_order = T(order, torch.int64)
@@ -176,7 +180,7 @@ class TopologyClass:
     def expand(self):
         """Re-run K1 from the resident base arrays (the per-class device step)."""
         if self.plan is not None:
-            self.plan.reexpand()
+            self.plan.reexpand(topo=not self.fused)
 
     def run(self, *, schedules: bool = True, paths: bool = False, out: dict | None = None,
             events: dict | None = None) -> dict:

@@ -35,13 +35,52 @@ struct FusedArgs {
     int32_t smem_warp;   // bytes per warp
 };
 
-__device__ __forceinline__ double warp_min_nonneg(double x) {
-    // finishes are >= +0.0, so their IEEE bits order like unsigned integers
+// Reductions over one lane group (kGS = 32: the warp; kGS = 16: one half-warp,
+// two candidates per warp).  redux.sync needs the whole warp, so for half-warps
+// each group's reduction runs with the other group's lanes contributing the identity.
+template <int kGS>
+__device__ __forceinline__ unsigned group_min_u32(unsigned x, int grp) {
+    if constexpr (kGS == 32) {
+        return __reduce_min_sync(DFSIM_FULL_MASK, x);
+    } else {
+        const unsigned a = __reduce_min_sync(DFSIM_FULL_MASK, grp == 0 ? x : 0xffffffffu);
+        const unsigned b = __reduce_min_sync(DFSIM_FULL_MASK, grp == 1 ? x : 0xffffffffu);
+        return grp ? b : a;
+    }
+}
+
+template <int kGS>
+__device__ __forceinline__ unsigned group_add_u32(unsigned x, int grp) {
+    if constexpr (kGS == 32) {
+        return __reduce_add_sync(DFSIM_FULL_MASK, x);
+    } else {
+        const unsigned a = __reduce_add_sync(DFSIM_FULL_MASK, grp == 0 ? x : 0u);
+        const unsigned b = __reduce_add_sync(DFSIM_FULL_MASK, grp == 1 ? x : 0u);
+        return grp ? b : a;
+    }
+}
+
+template <int kGS>
+__device__ __forceinline__ bool group_any(bool p, int grp) {
+    const unsigned b = __ballot_sync(DFSIM_FULL_MASK, p);
+    if constexpr (kGS == 32) return b != 0;
+    return ((b >> (grp * 16)) & 0xffffu) != 0;
+}
+
+// finishes are >= +0.0, so their IEEE bits order like unsigned integers
+template <int kGS>
+__device__ __forceinline__ double group_min_nonneg(double x, int grp) {
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
-    const unsigned hi = __reduce_min_sync(DFSIM_FULL_MASK, static_cast<unsigned>(b >> 32));
-    const unsigned lo = __reduce_min_sync(DFSIM_FULL_MASK,
-                                          static_cast<unsigned>(b >> 32) == hi ? static_cast<unsigned>(b) : 0xffffffffu);
+    const unsigned hi = group_min_u32<kGS>(static_cast<unsigned>(b >> 32), grp);
+    const unsigned lo = group_min_u32<kGS>(static_cast<unsigned>(b >> 32) == hi ? static_cast<unsigned>(b) : 0xffffffffu, grp);
     return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
+}
+
+template <int kGS>
+__device__ __forceinline__ double group_max_f64(double x) {
+#pragma unroll
+    for (int o = kGS / 2; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(DFSIM_FULL_MASK, x, o));
+    return x;
 }
 
 template <int kBits>
@@ -53,10 +92,13 @@ __device__ __forceinline__ bool counter_dec(unsigned *words, int c) {
     return ((old >> shift) & kMask) == 1u;
 }
 
-template <int kBits>
+template <int kBits, int kGS>
 __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int kPerWarp = 32 / kGS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ll = lane % kGS, grp = lane / kGS;
+    const int gid = warp * kPerWarp + grp;  // candidate slot of this lane group inside a chunk
     const int N = a.g.n_nodes, D = a.g.n_devices;
     const int E = static_cast<int>(a.g.n_edges);
     const int QCAP = a.g.qcap;
@@ -68,10 +110,10 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     uint16_t *s_cidx = reinterpret_cast<uint16_t *>(s_succ + E);
     uint16_t *s_pos = s_cidx + N;
     double *s_base = reinterpret_cast<double *>(smem + ((static_cast<size_t>(N) * 8 + static_cast<size_t>(E) * 4 + 15) / 16) * 16);
-    unsigned char *wbase = smem + a.smem_graph + static_cast<size_t>(warp) * a.smem_warp;
-    int32_t *tails = reinterpret_cast<int32_t *>(wbase);
-    unsigned *cnt = reinterpret_cast<unsigned *>(wbase + 128);
-    uint16_t *q = reinterpret_cast<uint16_t *>(wbase + 128 + a.g.n_counter_words * 4);
+    unsigned char *gbase = smem + a.smem_graph + static_cast<size_t>(gid) * a.smem_warp;
+    int32_t *tails = reinterpret_cast<int32_t *>(gbase);
+    unsigned *cnt = reinterpret_cast<unsigned *>(gbase + 128);
+    uint16_t *q = reinterpret_cast<uint16_t *>(gbase + 128 + a.g.n_counter_words * 4);
     __shared__ int s_chunk;
 
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -94,23 +136,26 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             staged = var;
             __syncthreads();
         }
-        if (warp < __ldg(a.st.chunk_count + c)) {
-            const int64_t s = __ldg(a.st.order + __ldg(a.st.chunk_first + c) + warp);
-            const double gap = __ldg(a.st.op_gap + s);
-            const int ovs = a.st.override_set ? __ldg(a.st.override_set + s) : -1;
+        const bool active = gid < __ldg(a.st.chunk_count + c);
+        if (__any_sync(DFSIM_FULL_MASK, active)) {
+            const int64_t s = active ? __ldg(a.st.order + __ldg(a.st.chunk_first + c) + gid) : 0;
+            const double gap = active ? __ldg(a.st.op_gap + s) : 0.0;
+            const int ovs = (active && a.st.override_set) ? __ldg(a.st.override_set + s) : -1;
             double *out_s = a.start + s * N;
             double *out_f = a.finish + s * N;
-            for (int w = lane; w < a.g.n_counter_words; w += 32) cnt[w] = __ldg(a.g.cnt_init + w);
-            if (lane < D) tails[lane] = 0;
+            if (active) {
+                for (int w = ll; w < a.g.n_counter_words; w += kGS) cnt[w] = __ldg(a.g.cnt_init + w);
+                if (ll < D) tails[ll] = 0;
+            }
             unsigned head = 0;
-            int flag = 0;
+            bool flag = false;
             __syncwarp();
-            for (int b = 0; b < a.g.n_sources; b += 32) {  // sources in rank order (engine.py:111-114)
-                const int i = b + lane;
-                const bool has = i < a.g.n_sources;
+            for (int b = 0; b < a.g.n_sources; b += kGS) {  // sources in rank order (engine.py:111-114)
+                const int i = b + ll;
+                const bool has = active && i < a.g.n_sources;
                 const int v = has ? __ldg(a.g.sources + i) : 0;
-                const int dv = has ? __ldg(a.g.device + v) : 32 + lane;
-                const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, dv);
+                const int dv = has ? __ldg(a.g.device + v) : 0;
+                const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, has ? dv + 32 * grp : 64 + lane);
                 const int base = has ? tails[dv] : 0;
                 __syncwarp();
                 if (has) {
@@ -120,26 +165,25 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 }
                 __syncwarp();
             }
-            if (__any_sync(DFSIM_FULL_MASK, lane < D && static_cast<unsigned>(tails[lane]) - head > static_cast<unsigned>(QCAP)))
-                flag = 1;
+            flag = group_any<kGS>(active && ll < D && static_cast<unsigned>(tails[ll]) - head > static_cast<unsigned>(QCAP), grp);
 
             bool running = false;
             int run_v = 0;
             double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
-            int placed = 0;
             auto start_idle = [&]() {
-                if (lane < D && !running && static_cast<int>(head) < tails[lane]) {
-                    const int v = q[lane * QCAP + (head & QMASK)];
+                if (active && !flag && ll < D && !running && static_cast<int>(head) < tails[ll]) {
+                    const int v = q[ll * QCAP + (head & QMASK)];
                     head++;
                     const double b = s_base[v];
                     double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
                     if (ovs >= 0) {
                         int lo = __ldg(a.st.ov_off + ovs), hi = __ldg(a.st.ov_off + ovs + 1);
+                        const int end = hi;
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
                             if (__ldg(a.st.ov_node + mid) < v) lo = mid + 1; else hi = mid;
                         }
-                        if (lo < __ldg(a.st.ov_off + ovs + 1) && __ldg(a.st.ov_node + lo) == v) dur = __ldg(a.st.ov_val + lo);
+                        if (lo < end && __ldg(a.st.ov_node + lo) == v) dur = __ldg(a.st.ov_val + lo);
                     }
                     const double f = __dadd_rn(now, dur);
                     const int p = s_pos[v];
@@ -150,14 +194,13 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     run_f = f;
                     busy_sum = __dadd_rn(busy_sum, __dsub_rn(f, now));
                     if (f > span) span = f;
-                    placed++;
                 }
             };
-            if (!flag) start_idle();
-            while (!flag && __any_sync(DFSIM_FULL_MASK, running)) {
-                now = warp_min_nonneg(running ? run_f : __longlong_as_double(0x7ff0000000000000LL));
+            start_idle();
+            while (__any_sync(DFSIM_FULL_MASK, running)) {
+                now = group_min_nonneg<kGS>(running ? run_f : __longlong_as_double(0x7ff0000000000000LL), grp);
                 const bool done = running && run_f == now;
-                const int seg_lo = lane < D ? tails[lane] : 0;
+                const int seg_lo = ll < D ? tails[ll] : 0;
                 __syncwarp();
                 if (done) {
                     running = false;
@@ -176,14 +219,14 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     }
                 }
                 __syncwarp();
-                const int seg_hi = lane < D ? tails[lane] : 0;
-                if (__any_sync(DFSIM_FULL_MASK, lane < D && static_cast<unsigned>(seg_hi) - head > static_cast<unsigned>(QCAP))) {
-                    flag = 1;  // ring overflow: hand this candidate to the exact engine
-                    break;
+                const int seg_hi = ll < D ? tails[ll] : 0;
+                if (group_any<kGS>(ll < D && static_cast<unsigned>(seg_hi) - head > static_cast<unsigned>(QCAP), grp)) {
+                    flag = true;  // ring overflow: this candidate goes to the exact engine
+                    running = false;
                 }
                 // enqueue(sorted(newly_ready)): sort each device's new ring segment by rank
-                if (seg_hi - seg_lo > 1) {
-                    uint16_t *qd = q + lane * QCAP;
+                if (!flag && seg_hi - seg_lo > 1) {
+                    uint16_t *qd = q + ll * QCAP;
                     for (int i = seg_lo + 1; i < seg_hi; i++) {
                         const uint16_t x = qd[i & QMASK];
                         int j = i - 1;
@@ -197,14 +240,14 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 __syncwarp();
                 start_idle();
             }
-            const double ms = warp_max_f64(span);
-            const int total = __reduce_add_sync(DFSIM_FULL_MASK, placed);
-            if (lane == 0) {
+            const double ms = group_max_f64<kGS>(span);
+            const unsigned total = group_add_u32<kGS>(ll < D ? head : 0u, grp);  // every pop starts a node
+            if (active && ll == 0) {
                 a.makespan[s] = ms;
-                a.n_placed[s] = flag ? -1 : total;
-                a.flags[s] = flag;
+                a.n_placed[s] = flag ? -1 : static_cast<int>(total);
+                a.flags[s] = flag ? 1 : 0;
             }
-            if (a.busy && lane < D) a.busy[s * D + lane] = busy_sum;
+            if (active && a.busy && ll < D) a.busy[s * D + ll] = busy_sum;
         }
         __syncthreads();
     }
@@ -321,6 +364,35 @@ __global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
 
 }  // namespace
 
+namespace {
+struct FusedShape {
+    size_t graph_bytes, warp_bytes, smem;
+    int gs, per_warp, wpb;
+    bool fits;
+};
+
+FusedShape fused_shape(const dfsim_sim_tables *g) {
+    FusedShape f;
+    const size_t N = (size_t)g->n_nodes;
+    f.graph_bytes = (N * 8 + (size_t)g->n_edges * 4 + 15) / 16 * 16 + N * 8;
+    f.warp_bytes = (128 + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * g->qcap * 2 + 15) / 16 * 16;
+    const size_t budget = 227 * 1024 - 64;
+    f.gs = g->n_devices <= 16 ? 16 : 32;
+    f.per_warp = 32 / f.gs;
+    f.wpb = 32;
+    while (f.wpb > 1 && f.graph_bytes + (size_t)f.wpb * f.per_warp * f.warp_bytes > budget) f.wpb--;
+    f.smem = f.graph_bytes + (size_t)f.wpb * f.per_warp * f.warp_bytes;
+    f.fits = f.smem <= budget;
+    return f;
+}
+}  // namespace
+
+extern "C" int32_t dfsim_fused_capacity(const dfsim_sim_tables *g) {
+    if (!g || g->n_nodes <= 0) return 0;
+    const FusedShape f = fused_shape(g);
+    return f.fits ? f.wpb * f.per_warp : 0;
+}
+
 extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,
                                     double *start, double *finish, double *makespan, double *busy, int32_t *n_placed,
                                     int32_t *flags) {
@@ -331,13 +403,11 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     DFSIM_ARG_CHECK(ctx, g->counter_bits == 8 || g->counter_bits == 16, "counter_bits 8 or 16");
     if (st->n_sims <= 0 || st->n_chunks <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    const int N = g->n_nodes;
-    const size_t graph_bytes = ((size_t)N * 8 + (size_t)g->n_edges * 4 + 15) / 16 * 16 + (size_t)N * 8;
-    const size_t warp_bytes = (128 + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * g->qcap * 2 + 15) / 16 * 16;
-    const size_t budget = 227 * 1024 - 64;
-    int wpb = 32;
-    while (wpb > 1 && graph_bytes + wpb * warp_bytes > budget) wpb--;
-    DFSIM_ARG_CHECK(ctx, graph_bytes + wpb * warp_bytes <= budget, "class tables do not fit in shared memory");
+    const FusedShape f = fused_shape(g);
+    DFSIM_ARG_CHECK(ctx, f.fits, "class tables do not fit in shared memory");
+    const size_t graph_bytes = f.graph_bytes, warp_bytes = f.warp_bytes;
+    const int gs = f.gs, wpb = f.wpb;
+    (void)warp_bytes;
     FusedArgs a;
     a.g = *g;
     a.st = *st;
@@ -350,15 +420,20 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     if (rc) return rc;
     a.chunk_counter = static_cast<int32_t *>(p);
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(a.chunk_counter, 0, sizeof(int32_t), ctx->stream));
-    const size_t smem = graph_bytes + wpb * warp_bytes;
+    const size_t smem = f.smem;
     const int grid = ctx->num_sms < st->n_chunks ? ctx->num_sms : (int)st->n_chunks;
+#define DFSIM_LAUNCH_FUSED(BITS, GS)                                                                            \
+    do {                                                                                                       \
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<BITS, GS>,                                   \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
+        k_simulate_fused<BITS, GS><<<grid, wpb * 32, smem, ctx->stream>>>(a);                                  \
+    } while (0)
     if (g->counter_bits == 8) {
-        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_simulate_fused<8><<<grid, wpb * 32, smem, ctx->stream>>>(a);
+        if (gs == 16) DFSIM_LAUNCH_FUSED(8, 16); else DFSIM_LAUNCH_FUSED(8, 32);
     } else {
-        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_simulate_fused<16><<<grid, wpb * 32, smem, ctx->stream>>>(a);
+        if (gs == 16) DFSIM_LAUNCH_FUSED(16, 16); else DFSIM_LAUNCH_FUSED(16, 32);
     }
+#undef DFSIM_LAUNCH_FUSED
     return dfsim_after_launch(ctx, "k_simulate_fused");
 }
 

@@ -157,8 +157,10 @@ class ExpansionPlan:
         if findings:
             raise DfsimError("internal: expansion produced an invalid graph: " + "; ".join(findings[:5]))
 
-    def reexpand(self) -> None:
-        """Run K1 again into the same device arrays (timed per-class device work)."""
+    def reexpand(self, topo: bool = True) -> None:
+        """Run K1 again into the same device arrays (timed per-class device work).
+
+        ``topo=False`` skips the Kahn order (the fused path uses the class level order)."""
         base, plan, n_refs = self._structs
         lg = self.lowered
         N, D = len(self.ids), len(self.devices)
@@ -167,7 +169,8 @@ class ExpansionPlan:
         by = native.ctypes.byref
         self.ctx.call("dfsim_expand_dp", by(base), by(plan), native.ptr(lg.t_succ_off), native.ptr(lg.t_succ_idx),
                       cap, native.ptr(lg.t_indeg), native.ptr(lg.t_dev), native.ptr(lg.t_sources),
-                      native.ptr(lg.t_queue_off), native.ptr(lg.t_topo), D, by(n_edges), by(n_src), by(n_ord))
+                      native.ptr(lg.t_queue_off), native.ptr(lg.t_topo) if topo else native.P(0), D, by(n_edges),
+                      by(n_src), by(n_ord))
         if (int(n_edges.value), int(n_src.value), int(n_ord.value)) != (lg.n_edges, lg.n_sources, lg.n_ordered):
             raise DfsimError("internal: re-expansion disagrees with the first expansion")
 

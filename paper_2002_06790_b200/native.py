@@ -94,6 +94,7 @@ _SIGNATURES = {
     "dfsim_simulate_fused": (ctypes.c_int, [P, ctypes.POINTER(SimTables), ctypes.POINTER(FusedStrategies), P, P, P,
                                             P, P, P]),
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P, P]),
+    "dfsim_fused_capacity": (I32, [ctypes.POINTER(SimTables)]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),
     "dfsim_argmin_records": (ctypes.c_int, [P, I64, P, P]),
 }
