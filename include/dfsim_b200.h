@@ -242,14 +242,19 @@ typedef struct {
     int32_t n_slots;           /* suffix slots per candidate (interval colouring) */
     int32_t n_edges;
     const int32_t *rank_of_pos;
-    const uint32_t *cp_meta;   /* [N] by position: successor-slot begin | count << 16 | source << 24 */
+    const uint32_t *cp_meta;   /* [N] by position: successor begin | count << 16 | source << 24 | spill << 25 */
     const uint16_t *cp_slot;   /* [N] by position */
-    const uint16_t *cp_succ_slot; /* [E] */
+    const uint16_t *cp_succ_slot; /* [E] slot id, or 0x8000 | index into the chunk's prefetched spill values */
     int32_t n_groups;
     const int32_t *group_off;  /* <= 32 positions of one level each */
     int32_t n_chunks;
     const int32_t *chunk_off;  /* groups per prefetch chunk */
     int32_t chunk_positions;   /* max positions per chunk */
+    int32_t n_long;            /* spilled suffix values per candidate (read >= 2 chunks later) */
+    const uint16_t *cp_spill;  /* [N] by position: spill index written (0xFFFF none) */
+    const int32_t *spill_off;  /* [n_chunks+1] spill values each chunk reads */
+    const uint16_t *spill_list;/* spill indices, per chunk */
+    int32_t max_spill_reads;   /* max spill values one chunk reads */
 } dfsim_cp_tables;
 
 /* K4 v2: critical-path length and its start node per candidate over start/finish

@@ -261,8 +261,10 @@ struct CpLevelArgs {
     const double *start, *finish;
     double *cp_len;
     int32_t *cp_src;
+    double *spill;        // [grid * wpb][n_long] rows, one per resident warp
     int32_t wpb;
     int32_t slot_bytes;   // per warp
+    int32_t stage_doubles;  // 2*K + max_spill_reads
     int32_t table_bytes;  // CTA-shared tables
 };
 
@@ -271,38 +273,45 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
 
-// Shared tables (all by level position): meta[p] = successor-slot begin (16 bits) |
-// count (8 bits) << 16 | source << 24; slot[p]; succ_slot[E]; group_off[G+1].
-__global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
+// Shared tables (by level position): meta[p] = successor begin (16 bits) | count
+// (8 bits) << 16 | source << 24 | spill << 25; slot[p] (0xFFFF: none); spill index
+// spill_idx[p]; successor entries succ[E] (slot, or 0x8000 | prefetched spill index);
+// group_off[G+1].
+__global__ void __launch_bounds__(1024) k_critical_path_levels(CpLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int N = a.t.n_nodes, K = a.t.chunk_positions, G = a.t.n_groups;
-    const int E = a.t.n_edges;
+    const int N = a.t.n_nodes, K = a.t.chunk_positions, G = a.t.n_groups, E = a.t.n_edges;
+    const int SD = a.stage_doubles;
     uint32_t *s_meta = reinterpret_cast<uint32_t *>(smem);
     uint16_t *s_slot = reinterpret_cast<uint16_t *>(s_meta + N);
-    uint16_t *s_succ = s_slot + N;
+    uint16_t *s_spix = s_slot + N;
+    uint16_t *s_succ = s_spix + N;
     uint16_t *s_goff = s_succ + E;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         s_meta[i] = __ldg(a.t.cp_meta + i);
         s_slot[i] = __ldg(a.t.cp_slot + i);
+        s_spix[i] = __ldg(a.t.cp_spill + i);
     }
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.t.cp_succ_slot + i);
     for (int i = threadIdx.x; i <= G; i += blockDim.x) s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
     __syncthreads();
-    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(warp) * (a.slot_bytes + 4 * K * 8);
+    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(warp) * (a.slot_bytes + 2 * SD * 8);
     double *slots = reinterpret_cast<double *>(wb);
-    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2 stages][start|finish][K]
+    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2 stages][start K | finish K | spill R]
+    double *spill_row = a.spill + (static_cast<int64_t>(blockIdx.x) * a.wpb + warp) * a.t.n_long;
 
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * a.wpb + warp; s < a.S; s += static_cast<int64_t>(gridDim.x) * a.wpb) {
         const double *st = a.start + s * N;
         const double *fi = a.finish + s * N;
         auto prefetch = [&](int c, int stage) {
             const int p0 = s_goff[__ldg(a.t.chunk_off + c)], p1 = s_goff[__ldg(a.t.chunk_off + c + 1)];
-            double *bs = buf + stage * 2 * K;
+            double *bs = buf + stage * SD;
             for (int p = p0 + lane; p < p1; p += 32) {
                 cp_async8(bs + (p - p0), st + p);
                 cp_async8(bs + K + (p - p0), fi + p);
             }
+            const int r0 = __ldg(a.t.spill_off + c), r1 = __ldg(a.t.spill_off + c + 1);
+            for (int r = r0 + lane; r < r1; r += 32) cp_async8(bs + 2 * K + (r - r0), spill_row + __ldg(a.t.spill_list + r));
             asm volatile("cp.async.commit_group;\n" ::);
         };
         double len = 0.0;
@@ -310,6 +319,8 @@ __global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
         const int nc = a.t.n_chunks;
         if (nc > 0) prefetch(nc - 1, (nc - 1) & 1);
         for (int c = nc - 1; c >= 0; c--) {
+            // chunk c-1 may read spill values written up to chunk c+1: all complete (and
+            // ordered by the __syncwarp that ended chunk c+1) before this prefetch is issued
             if (c > 0) {
                 prefetch(c - 1, (c - 1) & 1);
                 asm volatile("cp.async.wait_group 1;\n" ::);
@@ -317,7 +328,7 @@ __global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
                 asm volatile("cp.async.wait_group 0;\n" ::);
             }
             __syncwarp();
-            const double *bs = buf + (c & 1) * 2 * K;
+            const double *bs = buf + (c & 1) * SD;
             const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
             const int p0 = s_goff[g0];
             for (int gi = g1 - 1; gi >= g0; gi--) {
@@ -328,12 +339,15 @@ __global__ void __launch_bounds__(512) k_critical_path_levels(CpLevelArgs a) {
                     const double d = __dsub_rn(bs[K + (p - p0)], bs[p - p0]);  // finish - start (reporting.py:128)
                     double best = 0.0;
                     for (int j = j0; j < j1; j++) {
-                        const double x = slots[s_succ[j]];
+                        const unsigned e = s_succ[j];
+                        const double x = (e & 0x8000u) ? bs[2 * K + (e & 0x7fffu)] : slots[e];
                         if (x > best) best = x;
                     }
                     const double sv = __dadd_rn(d, best);
-                    slots[s_slot[p]] = sv;
-                    if (m >> 24) {
+                    const unsigned sl = s_slot[p];
+                    if (sl != 0xffffu) slots[sl] = sv;
+                    if ((m >> 25) & 1u) spill_row[s_spix[p]] = sv;
+                    if ((m >> 24) & 1u) {
                         const int r = __ldg(a.t.rank_of_pos + p);
                         if (src == 0x7fffffff || sv > len || (sv == len && r < src)) {
                             len = sv;
@@ -442,27 +456,34 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, start && finish && cp_len, "start, finish and cp_len are required");
     DFSIM_ARG_CHECK(ctx, t->chunk_positions >= 32, "chunk_positions >= 32");
-    DFSIM_ARG_CHECK(ctx, t->n_nodes <= 65535 && t->n_edges <= 65535 && t->n_slots <= 65535, "level tables use 16-bit ids");
+    DFSIM_ARG_CHECK(ctx, t->n_nodes <= 65535 && t->n_edges <= 65535 && t->n_slots < 0x7fff &&
+                         t->max_spill_reads < 0x7fff, "level tables use 16-bit ids");
     if (n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const int slot_bytes = ((t->n_slots > 0 ? t->n_slots : 1) * 8 + 15) / 16 * 16;
+    const int stage_doubles = (2 * t->chunk_positions + t->max_spill_reads + 1) / 2 * 2;
     const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 + 15) / 16 * 16;
-    const size_t per_warp = (size_t)slot_bytes + 4 * (size_t)t->chunk_positions * 8;
+    const size_t per_warp = (size_t)slot_bytes + 2 * (size_t)stage_doubles * 8;
     const size_t budget = 227 * 1024 - 64;
-    int wpb = 16;
+    int wpb = 32;
     while (wpb > 1 && table_bytes + wpb * per_warp > budget) wpb--;
     DFSIM_ARG_CHECK(ctx, table_bytes + wpb * per_warp <= budget, "critical-path tables do not fit in shared memory");
+    const int64_t want = (n_sims + wpb - 1) / wpb;
+    const int grid = (int)(want < ctx->num_sms ? want : ctx->num_sms);
+    void *p = nullptr;
+    int rc = dfsim_scratch(ctx, (size_t)grid * wpb * (size_t)(t->n_long > 0 ? t->n_long : 1) * 8, &p);
+    if (rc) return rc;
     CpLevelArgs a;
     a.t = *t;
     a.S = n_sims;
     a.start = start; a.finish = finish; a.cp_len = cp_len; a.cp_src = cp_src;
+    a.spill = static_cast<double *>(p);
     a.wpb = wpb;
     a.slot_bytes = slot_bytes;
+    a.stage_doubles = stage_doubles;
     a.table_bytes = (int)table_bytes;
     const size_t smem = table_bytes + wpb * per_warp;
     DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_critical_path_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t want = (n_sims + wpb - 1) / wpb;
-    const int grid = (int)(want < ctx->num_sms ? want : ctx->num_sms);
     k_critical_path_levels<<<grid, wpb * 32, smem, ctx->stream>>>(a);
     return dfsim_after_launch(ctx, "k_critical_path_levels");
 }

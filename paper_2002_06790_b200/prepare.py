@@ -2,16 +2,18 @@
 critical path (K4 v2).  Host numpy, once per class.
 
 * level order: Kahn waves (level = longest edge count from a source); the
-  output position of a node is its index in this order, so the critical-path
+  output column of a node is its index in this order, so the critical-path
   pass reads each schedule row contiguously, level by level, backwards.
 * engine tables: ``meta[v]`` = successor begin (24 bits) | out-degree (8 bits,
   255 = read succ_off), ``succ[j]`` = consumer rank | device << 16 | single-input
   << 21 (a consumer with exactly one input reference needs no counter),
   ``cidx[v]`` = counter slot of multi-input nodes, packed initial counters.
-* critical-path tables: for each position its suffix slot and its successors'
-  slots.  Slots are allocated by interval colouring over the reverse level
-  order: a node's suffix lives from its own level until its last predecessor's
-  level (graph.py:463-469 reads suffix only through successor lists).
+* critical-path tables: the reverse pass processes groups (<= GROUP positions of
+  one level) inside prefetch chunks (<= CHUNK positions).  A suffix value read
+  in its own chunk or the next one lives in a shared-memory slot (interval
+  colouring over processing steps); one read two or more chunks later is also
+  written to an L2-resident spill row and prefetched with the reader's chunk.
+  ``cp_succ[j]`` names a slot, or (bit 15) an index into the chunk's spill list.
 """
 
 from __future__ import annotations
@@ -19,6 +21,10 @@ from __future__ import annotations
 import numpy as np
 
 from . import native
+
+GROUP = 32        # positions processed together (one per lane)
+CHUNK = 64        # positions prefetched per cp.async batch
+QCAP = 32         # per-device FIFO ring capacity of the fused engine
 
 
 def level_order(n: int, succ_off: np.ndarray, succ_idx: np.ndarray, indeg: np.ndarray):
@@ -37,8 +43,8 @@ def level_order(n: int, succ_off: np.ndarray, succ_idx: np.ndarray, indeg: np.nd
         cnt = ends - starts
         if cnt.sum() == 0:
             break
-        idx = np.repeat(ends - cnt.cumsum(), cnt) + np.arange(cnt.sum())
-        targets = succ_idx[idx]
+        eidx = np.repeat(ends - cnt.cumsum(), cnt) + np.arange(cnt.sum())
+        targets = succ_idx[eidx]
         np.subtract.at(left, targets, 1)
         cand = np.unique(targets)
         frontier = cand[left[cand] == 0]
@@ -49,39 +55,34 @@ def level_order(n: int, succ_off: np.ndarray, succ_idx: np.ndarray, indeg: np.nd
     return order, level, np.asarray(offsets, dtype=np.int64)
 
 
-class ClassTables:
-    """Device-resident engine + critical-path tables of one topology class."""
+class Tables:
+    """Host arrays + statistics of one class (see module docstring)."""
 
-    GROUP = 32        # positions processed together (one per lane)
-    CHUNK = 64        # positions prefetched per cp.async batch
-    QCAP = 32         # per-device FIFO ring capacity of the fused engine
-
-    def __init__(self, lg, host=None):
-        self.ctx = lg.ctx
-        if host is None:
-            host = dict(succ_off=lg.t_succ_off[: lg.n + 1].cpu().numpy(),
-                        succ_idx=lg.t_succ_idx[: lg.n_edges].cpu().numpy(),
-                        indeg=lg.t_indeg[: lg.n].cpu().numpy(), device=lg.t_dev[: lg.n].cpu().numpy(),
-                        sources=lg.t_sources[: lg.n_sources].cpu().numpy())
-        N, D = lg.n, lg.n_devices
-        off = np.asarray(host["succ_off"], np.int64)
-        idx = np.asarray(host["succ_idx"], np.int64)
-        indeg = np.asarray(host["indeg"], np.int64)
-        dev = np.asarray(host["device"], np.int64)
+    def __init__(self, N: int, D: int, succ_off, succ_idx, indeg, device, group: int = GROUP,
+                 chunk: int = CHUNK):
+        off = np.asarray(succ_off, np.int64)
+        idx = np.asarray(succ_idx, np.int64)
+        indeg = np.asarray(indeg, np.int64)
+        dev = np.asarray(device, np.int64)
         self.n, self.n_devices, self.n_edges = N, D, int(off[-1]) if N else 0
+        self.group, self.chunk = group, chunk
+        outdeg = np.diff(off)
         lo = level_order(N, off, idx, indeg)
         self.acyclic = lo is not None
-        outdeg = np.diff(off)
-        self.fused_ok = (self.acyclic and 0 < N <= 65535 and D <= 32 and self.n_edges < (1 << 24)
-                         and indeg.max(initial=0) <= 65534)
-        if not self.acyclic:
-            self.fused_ok = False
+        self.fused_ok = False
+        if not self.acyclic or N == 0:
             return
         order, level, loff = lo
         pos = np.empty(N, np.int64)
         pos[order] = np.arange(N)
         self.pos, self.rank_of_pos, self.level_off = pos, order, loff
-        # ---- engine tables (rank space)
+        self._engine(N, off, idx, indeg, dev, outdeg)
+        self._critical_path(N, idx, indeg, outdeg, order, pos, loff)
+        self.fused_ok = (N <= 65535 and D <= 32 and self.n_edges < 65536 and outdeg.max(initial=0) < 256
+                         and indeg.max(initial=0) <= 65534 and self.n_slots < 0x7FFF
+                         and self.max_spill_reads < 0x7FFF and self.n_long < 0xFFFF)
+
+    def _engine(self, N, off, idx, indeg, dev, outdeg):
         single = indeg == 1
         multi = np.nonzero(indeg >= 2)[0]
         cidx = np.zeros(N, np.int64)
@@ -95,72 +96,112 @@ class ClassTables:
         packed = np.zeros(words, np.uint64)
         for i in range(per):
             packed |= init[:, i] << np.uint64(i * bits)
-        meta = (off[:-1] & 0xFFFFFF) | (np.minimum(outdeg, 255) << 24)
-        succ = idx | (dev[idx] << 16) | (single[idx].astype(np.int64) << 21)
         self.counter_bits, self.counter_words = bits, words
-        # ---- critical-path tables (position space)
-        n_lv = loff.size - 1
-        pred_last = np.full(N, -1, np.int64)   # last reading level in reverse order (by rank)
-        rlevel = (n_lv - 1) - level            # processing index of each node's level
-        src_of_edge = np.repeat(np.arange(N), outdeg)
-        np.maximum.at(pred_last, idx, rlevel[src_of_edge])
-        release = np.where(pred_last >= 0, pred_last, rlevel)  # sources: only read by the final max
-        slot = np.empty(N, np.int64)
-        free, nslots = [], 0
-        # interval colouring: process reverse levels, free slots released before this level
-        by_release = {}
-        for r in range(n_lv):
-            lv = n_lv - 1 - r
-            for s in by_release.pop(r - 1, ()):
-                free.append(s)
-            nodes = order[loff[lv]:loff[lv + 1]]
-            for v in nodes.tolist():
-                if free:
-                    s = free.pop()
-                else:
-                    s, nslots = nslots, nslots + 1
-                slot[v] = s
-                by_release.setdefault(int(release[v]), []).append(s)
-        self.n_slots = nslots
-        self.fused_ok = self.fused_ok and nslots < 65536 and self.n_edges < 65536 and outdeg.max(initial=0) < 256
-        cp_off = np.zeros(N + 1, np.int64)
-        cp_off[1:] = np.cumsum(outdeg[order])
-        cp_succ = slot[idx[np.concatenate([np.arange(off[v], off[v + 1]) for v in order.tolist()])
-                       if self.n_edges else np.zeros(0, np.int64)]]
-        # groups: <= GROUP positions inside one level; chunks: consecutive groups <= CHUNK positions
+        self.meta = (off[:-1] & 0xFFFFFF) | (np.minimum(outdeg, 255) << 24)
+        self.succ = idx | (dev[idx] << 16) | (single[idx].astype(np.int64) << 21)
+        self.cidx, self.cnt_init = cidx, packed
+
+    def _critical_path(self, N, idx, indeg, outdeg, order, pos, loff):
         goff = [0]
-        for lv in range(n_lv):
+        for lv in range(loff.size - 1):
             a, b = int(loff[lv]), int(loff[lv + 1])
-            for p in range(a, b, self.GROUP):
-                goff.append(min(b, p + self.GROUP))
+            for p in range(a, b, self.group):
+                goff.append(min(b, p + self.group))
         goff = np.asarray(goff, np.int64)
-        coff = [0]
-        start = 0
+        coff, start = [0], 0
         for gi in range(1, goff.size):
-            if goff[gi] - goff[start] > self.CHUNK:
+            if goff[gi] - goff[start] > self.chunk:
                 coff.append(gi - 1)
                 start = gi - 1
         if coff[-1] != goff.size - 1:
             coff.append(goff.size - 1)
         coff = np.asarray(coff, np.int64)
-        self.n_groups, self.n_chunks = goff.size - 1, coff.size - 1
+        n_groups, n_chunks = goff.size - 1, coff.size - 1
+        group_of_pos = np.repeat(np.arange(n_groups), np.diff(goff))
+        chunk_of_pos = np.repeat(np.arange(n_chunks), np.diff(coff))[group_of_pos]
+        step_of_pos = (n_groups - 1) - group_of_pos                  # reverse processing order
+        src_of_edge = np.repeat(np.arange(N), outdeg)
+        pu, pv = pos[src_of_edge], pos[idx]                          # reader u, written value v
+        near = chunk_of_pos[pu] >= chunk_of_pos[pv] - 1
+        far = ~near
+        last_near = np.full(N, -1, np.int64)
+        np.maximum.at(last_near, pv[near], step_of_pos[pu[near]])
+        slot_of_pos = np.full(N, 0xFFFF, np.int64)
+        free, nslots, release = [], 0, {}
+        for g in range(n_groups - 1, -1, -1):
+            step = (n_groups - 1) - g
+            free.extend(release.pop(step - 1, ()))
+            for p in range(int(goff[g]), int(goff[g + 1])):
+                if last_near[p] < 0:
+                    continue
+                if free:
+                    sl = free.pop()
+                else:
+                    sl, nslots = nslots, nslots + 1
+                slot_of_pos[p] = sl
+                release.setdefault(int(last_near[p]), []).append(sl)
+        spill_flag = np.zeros(N, bool)
+        spill_flag[pv[far]] = True
+        spill_of_pos = np.full(N, 0xFFFF, np.int64)
+        spill_of_pos[spill_flag] = np.arange(int(spill_flag.sum()))
+        far_chunk, far_k = chunk_of_pos[pu[far]], spill_of_pos[pv[far]]
+        pairs = np.unique(np.stack([far_chunk, far_k], 1), axis=0) if far.any() else np.zeros((0, 2), np.int64)
+        soff = np.zeros(n_chunks + 1, np.int64)
+        if len(pairs):
+            np.add.at(soff, pairs[:, 0] + 1, 1)
+        soff = np.cumsum(soff)
+        bufidx = {(c_, k_): i_ - int(soff[c_]) for i_, (c_, k_) in enumerate(pairs.tolist())}
+        ent = np.where(near, slot_of_pos[pv], 0)
+        if far.any():
+            ent[far] = [0x8000 | bufidx[(c_, k_)] for c_, k_ in zip(far_chunk.tolist(), far_k.tolist())]
+        cp_succ = ent[np.argsort(pu, kind="stable")]               # CSR by reading position
+        cp_off = np.zeros(N + 1, np.int64)
+        cp_off[1:] = np.cumsum(outdeg[order])
         src_flag = (indeg[order] == 0).astype(np.int64)
-        cp_meta = (cp_off[:-1] & 0xFFFF) | (np.minimum(outdeg[order], 255) << 16) | (src_flag << 24)
-        T = lambda a, dt: _t(a, dt, self.ctx.device)  # noqa: E731
-        self.t = dict(meta=T(meta, np.uint32), succ_off=lg.t_succ_off, succ=T(succ, np.uint32),
-                      cidx=T(cidx, np.uint16), cnt_init=T(packed, np.uint32), pos=T(pos, np.uint16 if N <= 65535 else np.int32),
-                      pos32=T(pos, np.int32),
-                      sources=lg.t_sources, rank_of_pos=T(order, np.int32), cp_slot=T(slot[order], np.uint16 if nslots < 65536 else np.int32),
-                      cp_meta=T(cp_meta, np.uint32), cp_succ=T(cp_succ, np.uint16 if nslots < 65536 else np.int32),
-                      group_off=T(goff, np.int32), chunk_off=T(coff, np.int32))
-        t = self.t
+        self.cp_meta = ((cp_off[:-1] & 0xFFFF) | (np.minimum(outdeg[order], 255) << 16) | (src_flag << 24)
+                        | (spill_flag.astype(np.int64) << 25))
+        self.cp_slot, self.cp_spill, self.cp_succ = slot_of_pos, spill_of_pos, cp_succ
+        self.group_off, self.chunk_off, self.spill_off = goff, coff, soff
+        self.spill_list = pairs[:, 1] if len(pairs) else np.zeros(0, np.int64)
+        self.n_groups, self.n_chunks = n_groups, n_chunks
+        self.n_slots, self.n_long = nslots, int(spill_flag.sum())
+        self.max_spill_reads = int(np.diff(soff).max(initial=0))
+
+
+class ClassTables(Tables):
+    """Tables uploaded to the device, with the C-ABI structs of K3 v2 and K4 v2."""
+
+    GROUP, CHUNK, QCAP = GROUP, CHUNK, QCAP
+
+    def __init__(self, lg, host=None):
+        self.ctx = lg.ctx
+        if host is None:
+            host = dict(succ_off=lg.t_succ_off[: lg.n + 1].cpu().numpy(),
+                        succ_idx=lg.t_succ_idx[: lg.n_edges].cpu().numpy(),
+                        indeg=lg.t_indeg[: lg.n].cpu().numpy(), device=lg.t_dev[: lg.n].cpu().numpy())
+        super().__init__(lg.n, lg.n_devices, host["succ_off"], host["succ_idx"], host["indeg"], host["device"],
+                         self.GROUP, self.CHUNK)
+        if not self.fused_ok:
+            return
+        d = self.ctx.device
+        T = lambda a, dt: _t(a, dt, d)  # noqa: E731
+        self.t = t = dict(
+            meta=T(self.meta, np.uint32), succ=T(self.succ, np.uint32), cidx=T(self.cidx, np.uint16),
+            cnt_init=T(self.cnt_init, np.uint32), pos=T(self.pos, np.uint16), pos32=T(self.pos, np.int32),
+            rank_of_pos=T(self.rank_of_pos, np.int32), cp_slot=T(self.cp_slot, np.uint16),
+            cp_spill=T(self.cp_spill, np.uint16), cp_meta=T(self.cp_meta, np.uint32),
+            cp_succ=T(self.cp_succ, np.uint16), group_off=T(self.group_off, np.int32),
+            chunk_off=T(self.chunk_off, np.int32), spill_off=T(self.spill_off, np.int32),
+            spill_list=T(self.spill_list, np.uint16))
         p = native.ptr
-        self.sim_struct = native.SimTables(N, D, self.n_edges, p(t["meta"]), p(t["succ_off"]), p(t["succ"]),
-                                           p(t["cidx"]), p(t["cnt_init"]), words, bits, p(t["pos"]), p(t["sources"]),
-                                           lg.n_sources, self.QCAP, p(lg.t_dev))
-        self.cp_struct = native.CpTables(N, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
+        self.sim_struct = native.SimTables(lg.n, lg.n_devices, self.n_edges, p(t["meta"]), p(lg.t_succ_off),
+                                           p(t["succ"]), p(t["cidx"]), p(t["cnt_init"]), self.counter_words,
+                                           self.counter_bits, p(t["pos"]), p(lg.t_sources), lg.n_sources, self.QCAP,
+                                           p(lg.t_dev))
+        self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
                                          p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
-                                         self.n_chunks, p(t["chunk_off"]), self.CHUNK)
+                                         self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long, p(t["cp_spill"]),
+                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads)
 
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
         """Schedule row(s) stored by position -> node-rank order."""
@@ -173,10 +214,7 @@ def _t(a, dt, device):
     arr = np.ascontiguousarray(np.asarray(a).astype(dt, copy=False))
     if arr.size == 0:
         arr = np.zeros(1, dt)
-    if arr.dtype == np.uint64:
-        arr = arr.view(np.int64)
-    if arr.dtype == np.uint32:
-        arr = arr.view(np.int32)
-    if arr.dtype == np.uint16:
-        arr = arr.view(np.int16)
+    for src, dst in ((np.uint64, np.int64), (np.uint32, np.int32), (np.uint16, np.int16)):
+        if arr.dtype == src:
+            arr = arr.view(dst)
     return torch.from_numpy(arr).to(f"cuda:{device}")
