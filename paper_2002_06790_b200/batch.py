@@ -336,16 +336,30 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
     return result
 
 
-def gather_best(record, group=None):
-    """All-gather each rank's 16-byte (makespan, global index) winner over NCCL and
-    reduce lexicographically on the device (K5's cross-GPU step)."""
+def shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous candidate slice [lo, hi) of one rank (no data-path collective)."""
+    lo = total * rank // world
+    return lo, total * (rank + 1) // world
+
+
+def exchange_winners(record, group=None):
+    """All-gather every rank's 16-byte winner (makespan f64, global index i64 bits) ->
+    [world, 2] f64.  NCCL over NVLink for CUDA tensors, gloo for CPU tensors."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    allrec = torch.empty(world * 2, dtype=torch.float64, device=record.device)
-    dist.all_gather_into_tensor(allrec, record, group=group)
+    out = torch.empty(world * 2, dtype=torch.float64, device=record.device)
+    dist.all_gather_into_tensor(out, record.reshape(2), group=group)
+    return out.reshape(world, 2)
+
+
+def gather_best(record, group=None):
+    """K5 across GPUs: exchange winners over NCCL, reduce (makespan, index) on the device."""
+    import torch
+
+    allrec = exchange_winners(record, group)
     out = torch.empty(2, dtype=torch.float64, device=record.device)
     ctx = native.Context.get(record.device.index)
-    ctx.call("dfsim_argmin_records", world, native.ptr(allrec), native.ptr(out))
+    ctx.call("dfsim_argmin_records", allrec.shape[0], native.ptr(allrec), native.ptr(out))
     return out
