@@ -92,6 +92,8 @@ __device__ __forceinline__ bool counter_dec(unsigned *words, int c) {
     return ((old >> shift) & kMask) == 1u;
 }
 
+constexpr int kWide = 4;  // out-degree above which a finished node's successors are spread over the group
+
 template <int kBits, int kGS>
 __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -102,6 +104,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     const int N = a.g.n_nodes, D = a.g.n_devices;
     const int E = static_cast<int>(a.g.n_edges);
     const int QCAP = a.g.qcap;
+    const int QSTRIDE = QCAP + 2;  // u16 entries: 17-word stride keeps the 16 lanes' rings on distinct banks
     const unsigned QMASK = static_cast<unsigned>(QCAP - 1);
 
     // CTA-shared tables
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 __syncwarp();
                 if (has) {
                     const int p = base + __popc(peers & lanemask_lt());
-                    q[dv * QCAP + (p & QMASK)] = static_cast<uint16_t>(v);
+                    q[dv * QSTRIDE + (p & QMASK)] = static_cast<uint16_t>(v);
                     if ((peers & lanemask_lt()) == 0) tails[dv] = base + __popc(peers);
                 }
                 __syncwarp();
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
             auto start_idle = [&]() {
                 if (active && !flag && ll < D && !running && static_cast<int>(head) < tails[ll]) {
-                    const int v = q[ll * QCAP + (head & QMASK)];
+                    const int v = q[ll * QSTRIDE + (head & QMASK)];
                     head++;
                     const double b = s_base[v];
                     double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
@@ -202,20 +205,39 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 const bool done = running && run_f == now;
                 const int seg_lo = ll < D ? tails[ll] : 0;
                 __syncwarp();
+                // successors of the finished nodes (engine.py:136-142); a node with a wide
+                // fan-out (e.g. an AllReduce feeding every replica) is spread over the group
+                int j0 = 0, deg = 0;
                 if (done) {
                     running = false;
                     const uint32_t meta = s_meta[run_v];
-                    const int j0 = static_cast<int>(meta & 0xffffffu);
-                    int deg = static_cast<int>(meta >> 24);
+                    j0 = static_cast<int>(meta & 0xffffffu);
+                    deg = static_cast<int>(meta >> 24);
                     if (deg == 255) deg = __ldg(a.g.succ_off + run_v + 1) - j0;
-                    for (int j = j0; j < j0 + deg; j++) {
-                        const uint32_t e = s_succ[j];
-                        const int m = static_cast<int>(e & 0xffffu);
-                        if ((e >> 21) & 1u || counter_dec<kBits>(cnt, s_cidx[m])) {
-                            const int dv = static_cast<int>((e >> 16) & 31u);
-                            const int p = atomicAdd(tails + dv, 1);
-                            q[dv * QCAP + (p & QMASK)] = static_cast<uint16_t>(m);
-                        }
+                }
+                auto relax = [&](int j) {
+                    const uint32_t e = s_succ[j];
+                    const int m = static_cast<int>(e & 0xffffu);
+                    if ((e >> 21) & 1u || counter_dec<kBits>(cnt, s_cidx[m])) {
+                        const int dv = static_cast<int>((e >> 16) & 31u);
+                        const int p = atomicAdd(tails + dv, 1);
+                        q[dv * QSTRIDE + (p & QMASK)] = static_cast<uint16_t>(m);
+                    }
+                };
+                const bool wide = deg > kWide;
+                if (!wide)
+                    for (int j = j0; j < j0 + deg; j++) relax(j);
+                const unsigned wm = __ballot_sync(DFSIM_FULL_MASK, wide);
+                if (wm) {
+                    unsigned mine = kGS == 32 ? wm : (wm >> (grp * 16)) & 0xffffu;  // uniform in the group
+                    while (__any_sync(DFSIM_FULL_MASK, mine != 0)) {
+                        const bool have = mine != 0;
+                        const int src = (have ? __ffs(mine) - 1 : 0) + grp * kGS;
+                        if (have) mine &= mine - 1;
+                        const int wj0 = __shfl_sync(DFSIM_FULL_MASK, j0, src);
+                        const int wdeg = __shfl_sync(DFSIM_FULL_MASK, deg, src);
+                        if (have)
+                            for (int j = wj0 + ll; j < wj0 + wdeg; j += kGS) relax(j);
                     }
                 }
                 __syncwarp();
@@ -226,7 +248,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 }
                 // enqueue(sorted(newly_ready)): sort each device's new ring segment by rank
                 if (!flag && seg_hi - seg_lo > 1) {
-                    uint16_t *qd = q + ll * QCAP;
+                    uint16_t *qd = q + ll * QSTRIDE;
                     for (int i = seg_lo + 1; i < seg_hi; i++) {
                         const uint16_t x = qd[i & QMASK];
                         int j = i - 1;
@@ -389,7 +411,9 @@ FusedShape fused_shape(const dfsim_sim_tables *g) {
     FusedShape f;
     const size_t N = (size_t)g->n_nodes;
     f.graph_bytes = (N * 8 + (size_t)g->n_edges * 4 + 15) / 16 * 16 + N * 8;
-    f.warp_bytes = (128 + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * g->qcap * 2 + 15) / 16 * 16;
+    f.warp_bytes = (128 + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * (g->qcap + 2) * 2 + 15) / 16 * 16;
+    // consecutive candidate groups start 16 banks apart (stride == 64 mod 128 bytes)
+    f.warp_bytes = (f.warp_bytes + 127) / 128 * 128 + 64;
     const size_t budget = 227 * 1024 - 64;
     f.gs = g->n_devices <= 16 ? 16 : 32;
     f.per_warp = 32 / f.gs;
