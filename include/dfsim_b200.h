@@ -255,6 +255,9 @@ typedef struct {
     const int32_t *spill_off;  /* [n_chunks+1] spill values each chunk reads */
     const uint16_t *spill_list;/* spill indices, per chunk */
     int32_t max_spill_reads;   /* max spill values one chunk reads */
+    const uint32_t *pinfo;     /* [N] by position: slot | has-slot << 15 | spill index << 16 | spill << 31 */
+    const uint32_t *gedge;     /* [E] per-group edges: owner lane | from-spill << 5 | value index << 16 */
+    const int32_t *gedge_off;  /* [n_groups+1] first edge of each group */
 } dfsim_cp_tables;
 
 /* K4 v2: critical-path length and its start node per candidate over start/finish

@@ -295,31 +295,31 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
 
-// Shared tables (by level position): meta[p] = successor begin (16 bits) | count
-// (8 bits) << 16 | source << 24 | spill << 25; slot[p] (0xFFFF: none); spill index
-// spill_idx[p]; successor entries succ[E] (slot, or 0x8000 | prefetched spill index);
-// group_off[G+1].
-__global__ void __launch_bounds__(1024) k_critical_path_levels(CpLevelArgs a) {
+// Shared tables: pinfo[p] (slot | has-slot << 15 | spill index << 16 | spill << 31,
+// by level position), gedge[E] (per-group edges: owner lane | from-spill << 5 |
+// value index << 16), group_off / gedge_off [G+1].  One group = <= 32 positions of
+// one level; its edges are spread one per lane and folded into the owners' maxima
+// with shared-memory atomicMax on the IEEE bits (all suffix values are >= +0.0).
+__global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int N = a.t.n_nodes, K = a.t.chunk_positions, G = a.t.n_groups, E = a.t.n_edges;
     const int SD = a.stage_doubles;
-    uint32_t *s_meta = reinterpret_cast<uint32_t *>(smem);
-    uint16_t *s_slot = reinterpret_cast<uint16_t *>(s_meta + N);
-    uint16_t *s_spix = s_slot + N;
-    uint16_t *s_succ = s_spix + N;
-    uint16_t *s_goff = s_succ + E;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        s_meta[i] = __ldg(a.t.cp_meta + i);
-        s_slot[i] = __ldg(a.t.cp_slot + i);
-        s_spix[i] = __ldg(a.t.cp_spill + i);
+    uint32_t *s_info = reinterpret_cast<uint32_t *>(smem);
+    uint32_t *s_edge = s_info + N;
+    uint16_t *s_goff = reinterpret_cast<uint16_t *>(s_edge + E);
+    uint16_t *s_eoff = s_goff + (G + 1);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_info[i] = __ldg(a.t.pinfo + i);
+    for (int i = threadIdx.x; i < E; i += blockDim.x) s_edge[i] = __ldg(a.t.gedge + i);
+    for (int i = threadIdx.x; i <= G; i += blockDim.x) {
+        s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
+        s_eoff[i] = static_cast<uint16_t>(__ldg(a.t.gedge_off + i));
     }
-    for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.t.cp_succ_slot + i);
-    for (int i = threadIdx.x; i <= G; i += blockDim.x) s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
     __syncthreads();
-    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(warp) * (a.slot_bytes + 2 * SD * 8);
-    double *slots = reinterpret_cast<double *>(wb);
-    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2 stages][start K | finish K | spill R]
+    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(warp) * (a.slot_bytes + 2 * SD * 8 + 256);
+    unsigned long long *wbest = reinterpret_cast<unsigned long long *>(wb);        // [32] per-owner max bits
+    double *slots = reinterpret_cast<double *>(wb + 256);
+    double *buf = reinterpret_cast<double *>(wb + 256 + a.slot_bytes);  // [2 stages][start K | finish K | spill R]
     double *spill_row = a.spill + (static_cast<int64_t>(blockIdx.x) * a.wpb + warp) * a.t.n_long;
 
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * a.wpb + warp; s < a.S; s += static_cast<int64_t>(gridDim.x) * a.wpb) {
@@ -354,22 +354,25 @@ __global__ void __launch_bounds__(1024) k_critical_path_levels(CpLevelArgs a) {
             const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
             const int p0 = s_goff[g0];
             for (int gi = g1 - 1; gi >= g0; gi--) {
-                const int p = s_goff[gi] + lane;
-                if (p < s_goff[gi + 1]) {
-                    const uint32_t m = s_meta[p];
-                    const int j0 = static_cast<int>(m & 0xffffu), j1 = j0 + static_cast<int>((m >> 16) & 0xffu);
+                const int q0 = s_goff[gi], np = s_goff[gi + 1] - q0;
+                wbest[lane] = 0ull;  // max(0.0, .) starts at +0.0 (graph.py:465)
+                __syncwarp();
+                for (int e = s_eoff[gi] + lane; e < s_eoff[gi + 1]; e += 32) {
+                    const uint32_t ent = s_edge[e];
+                    const unsigned idx = ent >> 16;
+                    const double x = (ent & 32u) ? bs[2 * K + idx] : slots[idx];
+                    atomicMax(wbest + (ent & 31u), static_cast<unsigned long long>(__double_as_longlong(x)));
+                }
+                __syncwarp();
+                if (lane < np) {
+                    const int p = q0 + lane;
+                    const uint32_t info = s_info[p];
+                    const double best = __longlong_as_double(static_cast<long long>(wbest[lane]));
                     const double d = __dsub_rn(bs[K + (p - p0)], bs[p - p0]);  // finish - start (reporting.py:128)
-                    double best = 0.0;
-                    for (int j = j0; j < j1; j++) {
-                        const unsigned e = s_succ[j];
-                        const double x = (e & 0x8000u) ? bs[2 * K + (e & 0x7fffu)] : slots[e];
-                        if (x > best) best = x;
-                    }
                     const double sv = __dadd_rn(d, best);
-                    const unsigned sl = s_slot[p];
-                    if (sl != 0xffffu) slots[sl] = sv;
-                    if ((m >> 25) & 1u) spill_row[s_spix[p]] = sv;
-                    if ((m >> 24) & 1u) {
+                    if (info & 0x8000u) slots[info & 0x7fffu] = sv;
+                    if (info >> 31) spill_row[(info >> 16) & 0x7fffu] = sv;
+                    if (!(info & 0x80008000u)) {  // a source: nobody reads its suffix
                         const int r = __ldg(a.t.rank_of_pos + p);
                         if (src == 0x7fffffff || sv > len || (sv == len && r < src)) {
                             len = sv;
@@ -486,8 +489,8 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const int slot_bytes = ((t->n_slots > 0 ? t->n_slots : 1) * 8 + 15) / 16 * 16;
     const int stage_doubles = (2 * t->chunk_positions + t->max_spill_reads + 1) / 2 * 2;
-    const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 + 15) / 16 * 16;
-    const size_t per_warp = (size_t)slot_bytes + 2 * (size_t)stage_doubles * 8;
+    const size_t table_bytes = ((size_t)t->n_nodes * 4 + (size_t)t->n_edges * 4 + (size_t)(t->n_groups + 1) * 4 + 15) / 16 * 16;
+    const size_t per_warp = (size_t)slot_bytes + 2 * (size_t)stage_doubles * 8 + 256;
     const size_t budget = 227 * 1024 - 64;
     int wpb = 32;
     while (wpb > 1 && table_bytes + wpb * per_warp > budget) wpb--;

@@ -80,7 +80,7 @@ class Tables:
         self._critical_path(N, idx, indeg, outdeg, order, pos, loff)
         self.fused_ok = (N <= 65535 and D <= 32 and self.n_edges < 65536 and outdeg.max(initial=0) < 256
                          and indeg.max(initial=0) <= 65534 and self.n_slots < 0x7FFF
-                         and self.max_spill_reads < 0x7FFF and self.n_long < 0xFFFF)
+                         and self.max_spill_reads < 0x7FFF and self.n_long < 0x7FFF)
 
     def _engine(self, N, off, idx, indeg, dev, outdeg):
         single = indeg == 1
@@ -161,6 +161,14 @@ class Tables:
         self.cp_meta = ((cp_off[:-1] & 0xFFFF) | (np.minimum(outdeg[order], 255) << 16) | (src_flag << 24)
                         | (spill_flag.astype(np.int64) << 25))
         self.cp_slot, self.cp_spill, self.cp_succ = slot_of_pos, spill_of_pos, cp_succ
+        # flattened per-group edge lists: owner lane | from-spill << 5 | value index << 16
+        owner = np.repeat(np.arange(N) - goff[group_of_pos], outdeg[order])     # lane of the reading position
+        self.gedge = (owner | (((cp_succ >> 15) & 1) << 5) | ((cp_succ & 0x7FFF) << 16)).astype(np.int64)
+        pos_edge_off = cp_off
+        self.gedge_off = pos_edge_off[goff]                                       # group -> first edge
+        has_slot = slot_of_pos != 0xFFFF
+        self.pinfo = ((np.where(has_slot, slot_of_pos, 0) & 0x7FFF) | (has_slot.astype(np.int64) << 15)
+                      | ((np.where(spill_flag, spill_of_pos, 0) & 0x7FFF) << 16) | (spill_flag.astype(np.int64) << 31))
         self.group_off, self.chunk_off, self.spill_off = goff, coff, soff
         self.spill_list = pairs[:, 1] if len(pairs) else np.zeros(0, np.int64)
         self.n_groups, self.n_chunks = n_groups, n_chunks
@@ -192,7 +200,8 @@ class ClassTables(Tables):
             cp_spill=T(self.cp_spill, np.uint16), cp_meta=T(self.cp_meta, np.uint32),
             cp_succ=T(self.cp_succ, np.uint16), group_off=T(self.group_off, np.int32),
             chunk_off=T(self.chunk_off, np.int32), spill_off=T(self.spill_off, np.int32),
-            spill_list=T(self.spill_list, np.uint16))
+            spill_list=T(self.spill_list, np.uint16), pinfo=T(self.pinfo, np.uint32), gedge=T(self.gedge, np.uint32),
+            gedge_off=T(self.gedge_off, np.int32))
         p = native.ptr
         self.sim_struct = native.SimTables(lg.n, lg.n_devices, self.n_edges, p(t["meta"]), p(lg.t_succ_off),
                                            p(t["succ"]), p(t["cidx"]), p(t["cnt_init"]), self.counter_words,
@@ -201,7 +210,8 @@ class ClassTables(Tables):
         self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
                                          p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
                                          self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long, p(t["cp_spill"]),
-                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads)
+                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads, p(t["pinfo"]),
+                                         p(t["gedge"]), p(t["gedge_off"]))
 
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
         """Schedule row(s) stored by position -> node-rank order."""
