@@ -242,11 +242,11 @@ typedef struct {
     int32_t n_slots;           /* suffix slots per candidate (interval colouring) */
     int32_t n_edges;
     const int32_t *rank_of_pos;
-    const uint32_t *cp_meta;   /* [N] by position: successor begin | count << 16 | source << 24 | spill << 25 */
-    const uint16_t *cp_slot;   /* [N] by position */
+    const uint32_t *cp_meta;   /* [N] by position: successor begin | count << 16 | source << 24 */
+    const uint16_t *cp_slot;   /* [N] by position (0xFFFF: none) */
     const uint16_t *cp_succ_slot; /* [E] slot id, or 0x8000 | index into the chunk's prefetched spill values */
     int32_t n_groups;
-    const int32_t *group_off;  /* <= 32 positions of one level each */
+    const int32_t *group_off;  /* <= 16 positions of one level each (a half-warp per candidate) */
     int32_t n_chunks;
     const int32_t *chunk_off;  /* groups per prefetch chunk */
     int32_t chunk_positions;   /* max positions per chunk */
@@ -256,8 +256,6 @@ typedef struct {
     const uint16_t *spill_list;/* spill indices, per chunk */
     int32_t max_spill_reads;   /* max spill values one chunk reads */
     const uint32_t *pinfo;     /* [N] by position: slot | has-slot << 15 | spill index << 16 | spill << 31 */
-    const uint32_t *gedge;     /* [E] per-group edges: owner lane | from-spill << 5 | value index << 16 */
-    const int32_t *gedge_off;  /* [n_groups+1] first edge of each group */
 } dfsim_cp_tables;
 
 /* K4 v2: critical-path length and its start node per candidate over start/finish

@@ -295,45 +295,51 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
 
-// Shared tables: pinfo[p] (slot | has-slot << 15 | spill index << 16 | spill << 31,
-// by level position), gedge[E] (per-group edges: owner lane | from-spill << 5 |
-// value index << 16), group_off / gedge_off [G+1].  One group = <= 32 positions of
-// one level; its edges are spread one per lane and folded into the owners' maxima
-// with shared-memory atomicMax on the IEEE bits (all suffix values are >= +0.0).
+// Two candidates per warp: lanes 0-15 and 16-31 each walk the same class-wide
+// reverse level order for their own candidate (identical control flow, different
+// data).  Shared tables (by level position): pinfo[p] = slot | has-slot << 15 |
+// spill index << 16 | spill << 31; pmeta[p] = successor begin | count << 16 |
+// source << 24; succ[E] = slot id, or 0x8000 | index into the chunk's prefetched
+// spill values; group_off[G+1] (groups of <= 16 positions of one level).
 __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ll = lane & 15, half = lane >> 4;
     const int N = a.t.n_nodes, K = a.t.chunk_positions, G = a.t.n_groups, E = a.t.n_edges;
     const int SD = a.stage_doubles;
     uint32_t *s_info = reinterpret_cast<uint32_t *>(smem);
-    uint32_t *s_edge = s_info + N;
-    uint16_t *s_goff = reinterpret_cast<uint16_t *>(s_edge + E);
-    uint16_t *s_eoff = s_goff + (G + 1);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) s_info[i] = __ldg(a.t.pinfo + i);
-    for (int i = threadIdx.x; i < E; i += blockDim.x) s_edge[i] = __ldg(a.t.gedge + i);
-    for (int i = threadIdx.x; i <= G; i += blockDim.x) {
-        s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
-        s_eoff[i] = static_cast<uint16_t>(__ldg(a.t.gedge_off + i));
+    uint32_t *s_meta = s_info + N;
+    uint16_t *s_succ = reinterpret_cast<uint16_t *>(s_meta + N);
+    uint16_t *s_goff = s_succ + E;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        s_info[i] = __ldg(a.t.pinfo + i);
+        s_meta[i] = __ldg(a.t.cp_meta + i);
     }
+    for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.t.cp_succ_slot + i);
+    for (int i = threadIdx.x; i <= G; i += blockDim.x) s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
     __syncthreads();
-    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(warp) * (a.slot_bytes + 2 * SD * 8 + 256);
-    unsigned long long *wbest = reinterpret_cast<unsigned long long *>(wb);        // [32] per-owner max bits
-    double *slots = reinterpret_cast<double *>(wb + 256);
-    double *buf = reinterpret_cast<double *>(wb + 256 + a.slot_bytes);  // [2 stages][start K | finish K | spill R]
-    double *spill_row = a.spill + (static_cast<int64_t>(blockIdx.x) * a.wpb + warp) * a.t.n_long;
+    const int gid = warp * 2 + half;  // candidate slot of this half-warp in the CTA
+    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(gid) * (a.slot_bytes + 2 * SD * 8);
+    double *slots = reinterpret_cast<double *>(wb);
+    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2 stages][start K | finish K | spill R]
+    double *spill_row = a.spill + (static_cast<int64_t>(blockIdx.x) * a.wpb * 2 + gid) * a.t.n_long;
+    const int64_t per_iter = static_cast<int64_t>(gridDim.x) * a.wpb * 2;
 
-    for (int64_t s = static_cast<int64_t>(blockIdx.x) * a.wpb + warp; s < a.S; s += static_cast<int64_t>(gridDim.x) * a.wpb) {
-        const double *st = a.start + s * N;
-        const double *fi = a.finish + s * N;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * a.wpb * 2 + warp * 2; base < a.S; base += per_iter) {
+        const int64_t s = base + half;
+        const bool live = s < a.S;
+        const int64_t sr = live ? s : base;  // the idle half shadows its partner's reads
+        const double *st = a.start + sr * N;
+        const double *fi = a.finish + sr * N;
         auto prefetch = [&](int c, int stage) {
             const int p0 = s_goff[__ldg(a.t.chunk_off + c)], p1 = s_goff[__ldg(a.t.chunk_off + c + 1)];
             double *bs = buf + stage * SD;
-            for (int p = p0 + lane; p < p1; p += 32) {
+            for (int p = p0 + ll; p < p1; p += 16) {
                 cp_async8(bs + (p - p0), st + p);
                 cp_async8(bs + K + (p - p0), fi + p);
             }
             const int r0 = __ldg(a.t.spill_off + c), r1 = __ldg(a.t.spill_off + c + 1);
-            for (int r = r0 + lane; r < r1; r += 32) cp_async8(bs + 2 * K + (r - r0), spill_row + __ldg(a.t.spill_list + r));
+            for (int r = r0 + ll; r < r1; r += 16) cp_async8(bs + 2 * K + (r - r0), spill_row + __ldg(a.t.spill_list + r));
             asm volatile("cp.async.commit_group;\n" ::);
         };
         double len = 0.0;
@@ -354,25 +360,22 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
             const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
             const int p0 = s_goff[g0];
             for (int gi = g1 - 1; gi >= g0; gi--) {
-                const int q0 = s_goff[gi], np = s_goff[gi + 1] - q0;
-                wbest[lane] = 0ull;  // max(0.0, .) starts at +0.0 (graph.py:465)
-                __syncwarp();
-                for (int e = s_eoff[gi] + lane; e < s_eoff[gi + 1]; e += 32) {
-                    const uint32_t ent = s_edge[e];
-                    const unsigned idx = ent >> 16;
-                    const double x = (ent & 32u) ? bs[2 * K + idx] : slots[idx];
-                    atomicMax(wbest + (ent & 31u), static_cast<unsigned long long>(__double_as_longlong(x)));
-                }
-                __syncwarp();
-                if (lane < np) {
-                    const int p = q0 + lane;
-                    const uint32_t info = s_info[p];
-                    const double best = __longlong_as_double(static_cast<long long>(wbest[lane]));
+                const int p = s_goff[gi] + ll;
+                if (p < s_goff[gi + 1]) {
+                    const uint32_t m = s_meta[p];
+                    const int j0 = static_cast<int>(m & 0xffffu), j1 = j0 + static_cast<int>((m >> 16) & 0xffu);
+                    double best = 0.0;  // max(0.0, .) (graph.py:465-468)
+                    for (int j = j0; j < j1; j++) {
+                        const unsigned e = s_succ[j];
+                        const double x = (e & 0x8000u) ? bs[2 * K + (e & 0x7fffu)] : slots[e];
+                        best = x > best ? x : best;
+                    }
                     const double d = __dsub_rn(bs[K + (p - p0)], bs[p - p0]);  // finish - start (reporting.py:128)
                     const double sv = __dadd_rn(d, best);
+                    const uint32_t info = s_info[p];
                     if (info & 0x8000u) slots[info & 0x7fffu] = sv;
-                    if (info >> 31) spill_row[(info >> 16) & 0x7fffu] = sv;
-                    if (!(info & 0x80008000u)) {  // a source: nobody reads its suffix
+                    if (live && (info >> 31)) spill_row[(info >> 16) & 0x7fffu] = sv;
+                    if ((m >> 24) & 1u) {
                         const int r = __ldg(a.t.rank_of_pos + p);
                         if (src == 0x7fffffff || sv > len || (sv == len && r < src)) {
                             len = sv;
@@ -383,9 +386,9 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                 __syncwarp();
             }
         }
-        // max over sources, then the min id achieving it (graph.py:471-474)
+        // max over sources, then the min id achieving it (graph.py:471-474), per half-warp
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = 8; o > 0; o >>= 1) {
             const double ol = __shfl_xor_sync(DFSIM_FULL_MASK, len, o);
             const int os = __shfl_xor_sync(DFSIM_FULL_MASK, src, o);
             if (os != 0x7fffffff && (src == 0x7fffffff || ol > len || (ol == len && os < src))) {
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                 src = os;
             }
         }
-        if (lane == 0) {
+        if (live && ll == 0) {
             a.cp_len[s] = src == 0x7fffffff ? 0.0 : len;
             if (a.cp_src) a.cp_src[s] = src == 0x7fffffff ? -1 : src;
         }
@@ -482,23 +485,23 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
                                           const double *finish, double *cp_len, int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, start && finish && cp_len, "start, finish and cp_len are required");
-    DFSIM_ARG_CHECK(ctx, t->chunk_positions >= 32, "chunk_positions >= 32");
+    DFSIM_ARG_CHECK(ctx, t->chunk_positions >= 16, "chunk_positions >= 16");
     DFSIM_ARG_CHECK(ctx, t->n_nodes <= 65535 && t->n_edges <= 65535 && t->n_slots < 0x7fff &&
                          t->max_spill_reads < 0x7fff, "level tables use 16-bit ids");
     if (n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const int slot_bytes = ((t->n_slots > 0 ? t->n_slots : 1) * 8 + 15) / 16 * 16;
     const int stage_doubles = (2 * t->chunk_positions + t->max_spill_reads + 1) / 2 * 2;
-    const size_t table_bytes = ((size_t)t->n_nodes * 4 + (size_t)t->n_edges * 4 + (size_t)(t->n_groups + 1) * 4 + 15) / 16 * 16;
-    const size_t per_warp = (size_t)slot_bytes + 2 * (size_t)stage_doubles * 8 + 256;
+    const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 + 15) / 16 * 16;
+    const size_t per_warp = 2 * ((size_t)slot_bytes + 2 * (size_t)stage_doubles * 8);  // two candidates per warp
     const size_t budget = 227 * 1024 - 64;
     int wpb = 32;
     while (wpb > 1 && table_bytes + wpb * per_warp > budget) wpb--;
     DFSIM_ARG_CHECK(ctx, table_bytes + wpb * per_warp <= budget, "critical-path tables do not fit in shared memory");
-    const int64_t want = (n_sims + wpb - 1) / wpb;
+    const int64_t want = (n_sims + 2 * wpb - 1) / (2 * wpb);
     const int grid = (int)(want < ctx->num_sms ? want : ctx->num_sms);
     void *p = nullptr;
-    int rc = dfsim_scratch(ctx, (size_t)grid * wpb * (size_t)(t->n_long > 0 ? t->n_long : 1) * 8, &p);
+    int rc = dfsim_scratch(ctx, (size_t)grid * wpb * 2 * (size_t)(t->n_long > 0 ? t->n_long : 1) * 8, &p);
     if (rc) return rc;
     CpLevelArgs a;
     a.t = *t;

@@ -13,7 +13,8 @@ critical path (K4 v2).  Host numpy, once per class.
   in its own chunk or the next one lives in a shared-memory slot (interval
   colouring over processing steps); one read two or more chunks later is also
   written to an L2-resident spill row and prefetched with the reader's chunk.
-  ``cp_succ[j]`` names a slot, or (bit 15) an index into the chunk's spill list.
+  ``cp_succ[j]`` names a slot, or (bit 15) an index into the chunk's spill list;
+  ``pinfo[p]`` says where position p's own value goes (slot and/or spill row).
 """
 
 from __future__ import annotations
@@ -22,7 +23,7 @@ import numpy as np
 
 from . import native
 
-GROUP = 32        # positions processed together (one per lane)
+GROUP = 16        # positions processed together (one per lane of a half-warp)
 CHUNK = 64        # positions prefetched per cp.async batch
 QCAP = 32         # per-device FIFO ring capacity of the fused engine
 
@@ -158,14 +159,8 @@ class Tables:
         cp_off = np.zeros(N + 1, np.int64)
         cp_off[1:] = np.cumsum(outdeg[order])
         src_flag = (indeg[order] == 0).astype(np.int64)
-        self.cp_meta = ((cp_off[:-1] & 0xFFFF) | (np.minimum(outdeg[order], 255) << 16) | (src_flag << 24)
-                        | (spill_flag.astype(np.int64) << 25))
+        self.cp_meta = (cp_off[:-1] & 0xFFFF) | (np.minimum(outdeg[order], 255) << 16) | (src_flag << 24)
         self.cp_slot, self.cp_spill, self.cp_succ = slot_of_pos, spill_of_pos, cp_succ
-        # flattened per-group edge lists: owner lane | from-spill << 5 | value index << 16
-        owner = np.repeat(np.arange(N) - goff[group_of_pos], outdeg[order])     # lane of the reading position
-        self.gedge = (owner | (((cp_succ >> 15) & 1) << 5) | ((cp_succ & 0x7FFF) << 16)).astype(np.int64)
-        pos_edge_off = cp_off
-        self.gedge_off = pos_edge_off[goff]                                       # group -> first edge
         has_slot = slot_of_pos != 0xFFFF
         self.pinfo = ((np.where(has_slot, slot_of_pos, 0) & 0x7FFF) | (has_slot.astype(np.int64) << 15)
                       | ((np.where(spill_flag, spill_of_pos, 0) & 0x7FFF) << 16) | (spill_flag.astype(np.int64) << 31))
@@ -200,8 +195,7 @@ class ClassTables(Tables):
             cp_spill=T(self.cp_spill, np.uint16), cp_meta=T(self.cp_meta, np.uint32),
             cp_succ=T(self.cp_succ, np.uint16), group_off=T(self.group_off, np.int32),
             chunk_off=T(self.chunk_off, np.int32), spill_off=T(self.spill_off, np.int32),
-            spill_list=T(self.spill_list, np.uint16), pinfo=T(self.pinfo, np.uint32), gedge=T(self.gedge, np.uint32),
-            gedge_off=T(self.gedge_off, np.int32))
+            spill_list=T(self.spill_list, np.uint16), pinfo=T(self.pinfo, np.uint32))
         p = native.ptr
         self.sim_struct = native.SimTables(lg.n, lg.n_devices, self.n_edges, p(t["meta"]), p(lg.t_succ_off),
                                            p(t["succ"]), p(t["cidx"]), p(t["cnt_init"]), self.counter_words,
@@ -210,8 +204,7 @@ class ClassTables(Tables):
         self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
                                          p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
                                          self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long, p(t["cp_spill"]),
-                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads, p(t["pinfo"]),
-                                         p(t["gedge"]), p(t["gedge_off"]))
+                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads, p(t["pinfo"]))
 
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
         """Schedule row(s) stored by position -> node-rank order."""
