@@ -29,24 +29,40 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "strategy simulations/sec (graph-nodes/s) at 1/2/4/8 B200 vs CPU ref; % HBM"
-WORKLOAD = "resnet50-train-dp8-ring-nvlink"
+WORKLOADS = {  # name -> (BASELINE.json config, default candidates per GPU)
+    "resnet50-dp8": ("ResNet-50 training graph, data-parallel 8 workers, ring allreduce over NVLink link model", 65536),
+    "bert-large-dp8": ("BERT-large graph, allreduce per layer gradient, 8 workers over NVLink", 16384),
+    "dag1m": ("synthetic 1M-node DAG x 4096 candidate strategies sharded across 8 GPUs with NCCL argmin", 512),
+}
+WORKLOAD = "resnet50-dp8"
 N_HW = 8
 HW_TAGS = tuple(f"B200-profile-{i}" for i in range(N_HW))
+_GRAPHS = {}
 
 
-def build_workload(rank: int, sims: int):
+def build_workload(rank: int, sims: int, workload: str = WORKLOAD):
     from paper_2002_06790_b200 import workloads as W
     from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
 
-    g = W.resnet50_training(batch=32)
-    db = W.model_profiles(g, HW_TAGS)
+    if workload not in _GRAPHS:
+        if workload == "dag1m":
+            g = W.layered_dag(1_000_000, 1000, devices=8)
+            _GRAPHS[workload] = (g, W.dag_profiles(HW_TAGS))
+        else:
+            g = W.resnet50_training(batch=32) if workload == "resnet50-dp8" else W.bert_large_training()
+            _GRAPHS[workload] = (g, W.model_profiles(g, HW_TAGS))
+    g, db = _GRAPHS[workload]
     dmap = tuple(f"gpu{i}" for i in range(8))
     coll = CollectiveConfig("RingAnalytic", "NVLink")
     configs = []
     for i in range(sims):
         gi = rank * sims + i  # global candidate index
-        configs.append(StrategyConfig(replicas=8, device_map=dmap, collective=coll, gradient_markers=("wgrad_*",),
-                                      hardware=HW_TAGS[gi % N_HW], op_gap_us=1e-3 * (gi // N_HW)))
+        hw, gap = HW_TAGS[gi % N_HW], 1e-3 * (gi // N_HW)
+        if workload == "dag1m":
+            configs.append(StrategyConfig(hardware=hw, op_gap_us=gap))
+        else:
+            configs.append(StrategyConfig(replicas=8, device_map=dmap, collective=coll, gradient_markers=("wgrad_*",),
+                                          hardware=hw, op_gap_us=gap))
     return g, db, configs
 
 
@@ -105,26 +121,60 @@ def _cpu_worker(i):
     return ms
 
 
-def cpu_baseline(sample: int | None = None, workers: int | None = None):
+def cpu_baseline_dag(workers: int, target_s: float):
+    """C5 CPU baseline: the oracle's estimate (Python, once per hardware tag) feeding the
+    C restatement of simulate + critical path (oracle/engine_oracle.c) on all cores."""
+    import numpy as np
+
+    from oracle import dfsim_oracle as O
+    from oracle import native_oracle as NO
+
+    g, db, cfgs = build_workload(0, 2 * N_HW, "dag1m")
+    csr = NO.Csr(g)
+    t0 = time.perf_counter()
+    base = {}
+    rows = []
+    for cfg in cfgs[: N_HW]:
+        tab = O.estimate(g, db, cfg)
+        base[cfg.hardware] = np.array([tab[nid][0] for nid in csr.ids])
+    est_s = (time.perf_counter() - t0) / N_HW
+    for i in range(workers):
+        cfg = cfgs[i % len(cfgs)]
+        rows.append(base[cfg.hardware])  # op_gap of the first 8 candidates is 0
+    dur = np.stack(rows)
+    t0 = time.perf_counter()
+    rc, ms, cp = NO.simulate_batch(csr, dur, threads=workers)
+    sim_s = time.perf_counter() - t0
+    per_cand = est_s + sim_s * workers / len(rows)  # core-seconds per candidate
+    return {"value": workers / per_cand, "unit": "sims/s", "cores": workers, "kind": "port",
+            "sample": f"{len(rows)} candidates of dag1m: oracle Python estimate ({est_s:.1f} s/candidate, "
+                      f"once per hardware tag) + C engine oracle simulate+critical path ({sim_s:.1f} s wall "
+                      f"for {len(rows)} on {workers} threads); value = cores / core-seconds per candidate"}
+
+
+def cpu_baseline(sample: int | None = None, workers: int | None = None, target_s: float = 15.0,
+                 workload: str = WORKLOAD):
     """The oracle's restatement of the reference per-candidate path
     (expand -> estimate -> simulate -> critical path, cli.py:83-87), in Python like
     the reference, over a process pool of all host cores."""
     import multiprocessing as mp
 
     workers = workers or len(os.sched_getaffinity(0))
-    g, db, cfgs = build_workload(0, 64)
+    if workload == "dag1m":
+        return cpu_baseline_dag(workers, target_s)
+    g, db, cfgs = build_workload(0, 64, workload)
     _CPU_STATE["w"] = (g, db, cfgs)
     t0 = time.perf_counter()
     _cpu_worker(0)
     one = time.perf_counter() - t0
-    n = sample or max(workers, min(4 * workers, int(20.0 * workers / max(one, 1e-3))))
+    n = sample or max(workers, int(target_s * workers / max(one, 1e-3)))
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(workers) as pool:
         list(pool.imap_unordered(_cpu_worker, range(n), chunksize=1))
     wall = time.perf_counter() - t0
     return {"value": n / wall, "unit": "sims/s", "cores": workers, "kind": "port",
-            "sample": f"{n} candidates of {WORKLOAD} through oracle/dfsim_oracle.run_candidate "
+            "sample": f"{n} candidates of {workload} through oracle/dfsim_oracle.run_candidate "
                       f"(Python restatement of the reference path) on {workers} processes; "
                       f"single-candidate latency {one:.3f} s"}
 
@@ -151,8 +201,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    S = args.sims
-    g, db, configs = build_workload(rank, S)
+    S = args.sims or WORKLOADS[args.workload][1]
+    g, db, configs = build_workload(rank, S, args.workload)
     t_setup = time.perf_counter()
     tc = TopologyClass(g, db, configs, local)
     setup_s = time.perf_counter() - t_setup
@@ -253,7 +303,7 @@ def run_ours(args):
             "metric": METRIC, "value": sims_per_s, "unit": "sims/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "nodes_per_sim": N, "edges_per_sim": E, "devices_per_sim": D,
+            "config": {"workload": args.workload, "baseline_config": WORKLOADS[args.workload][0], "nodes_per_sim": N, "edges_per_sim": E, "devices_per_sim": D,
                        "sims_per_gpu": S, "hardware_tags": N_HW, "collective": "RingAnalytic/NVLink (synthetic row)",
                        "outputs": "full schedules (start+finish per node), makespan, busy, CP length, argmin",
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
@@ -262,7 +312,7 @@ def run_ours(args):
             "best": {"makespan_us": best_v, "index": best_i},
             "stage_ms": {k: statistics.mean(s[k] for s in ev_steps) for k in stages},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "k_simulate",
+                         "traffic": None, "kernel": "k_simulate_fused" if tc.fused else "k_simulate",
                          "b_sim_bytes": b_sim, "b_table_bytes": b_table,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
             "e2e": {"value": e2e_value, "unit": "sims/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -270,7 +320,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
         }
         if not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
+            line["cpu_baseline"] = cpu_baseline(args.cpu_sample, workload=args.workload)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -281,16 +331,22 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    base = cpu_baseline(args.cpu_sample)
-    vals = [base["value"]]
-    for _ in range(max(0, args.steps - 1)):
-        vals.append(cpu_baseline(args.cpu_sample)["value"])
+    per_step = max(2.0, min(10.0, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline(args.cpu_sample, target_s=per_step, workload=args.workload)
+    vals, base, walls = [], None, []
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        base = cpu_baseline(args.cpu_sample, target_s=per_step, workload=args.workload)
+        walls.append(time.perf_counter() - t0)
+        vals.append(base["value"])
     v = statistics.mean(vals)
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": "sims/s", "n_gpus": int(os.environ.get("WORLD_SIZE", 1)),
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD},
+        "config": {"workload": args.workload, "baseline_config": WORKLOADS[args.workload][0]},
         "cpu_baseline": {**base, "value": v},
         "e2e": {"value": v, "unit": "sims/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -301,7 +357,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--sims", type=int, default=65536, help="candidates per GPU")
+    ap.add_argument("--sims", type=int, default=None, help="candidates per GPU (default per workload)")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default=WORKLOAD)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")

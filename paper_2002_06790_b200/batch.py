@@ -63,7 +63,7 @@ class TopologyClass:
         self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device)
         self.tables = None
         self.fused = False
-        if fused and self.lg.acyclic and self.lg.n:
+        if fused and self.lg.acyclic and 0 < self.lg.n <= 65535:
             self.tables = ClassTables(self.lg)
             if self.tables.fused_ok:
                 self._prepare_variants()

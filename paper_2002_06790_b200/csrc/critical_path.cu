@@ -144,9 +144,9 @@ extern "C" int dfsim_critical_path_batch(dfsim_ctx *ctx, const dfsim_graph *g, i
     DFSIM_ARG_CHECK(ctx, (cp_path == nullptr) == (cp_path_len == nullptr), "cp_path and cp_path_len go together");
     if (n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    // chunk the batch so the [N][chunk] suffix scratch stays bounded (<= 1 GiB)
+    // chunk the batch so the [N][chunk] suffix scratch stays bounded (<= 8 GiB of HBM)
     const int64_t N = g->n_nodes > 0 ? g->n_nodes : 1;
-    int64_t chunk = (int64_t)(1ll << 30) / (8 * N);
+    int64_t chunk = (int64_t)(8ll << 30) / (8 * N);
     chunk = chunk < 128 ? 128 : chunk / 128 * 128;
     if (chunk > n_sims) chunk = n_sims;
     void *p = nullptr;

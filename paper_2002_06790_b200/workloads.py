@@ -498,3 +498,37 @@ def model_profiles(graph, hardware_tags, seed: int = 1, grid_points: int = 16, l
                     db_insert(db, ProfileRecord(OpSignature(op, hw, (("k", k), ("m", m))), mean))
         db_insert(db, ProfileRecord(OpSignature("Input", hw, (("mflops", 0.0),)), 4.0 + h))
     return db
+
+
+def layered_dag(nodes: int = 1_000_000, width: int = 1000, devices: int = 8, seed: int = 5, max_fanin: int = 3):
+    """O(E) layered DAG for config C5: ``nodes / width`` layers; each node of layer l > 0 reads
+    1..max_fanin distinct producers of layer l-1 (SplitMix64-seeded); node j of a layer runs on
+    gpu (j % devices).  Ids are zero-padded so rank order == creation order."""
+    rng = SplitMix64(seed)
+    shape = TensorShape((16, 16), 4)
+    digits = len(str(nodes - 1))
+    ids = [f"n{i:0{digits}d}" for i in range(nodes)]
+    out = []
+    for i in range(nodes):
+        layer, j = divmod(i, width)
+        ins = ()
+        if layer:
+            base = (layer - 1) * width
+            k = 1 + rng.next_u64() % max_fanin
+            picks = sorted({base + (rng.next_u64() % width) for _ in range(k)})
+            ins = tuple((ids[p], 0) for p in picks)
+        out.append(OpNode(ids[i], RANDOM_OPS[i % 4], f"gpu{j % devices}",
+                          attrs={"cost_hint": 1 + rng.next_u64() % 16}, inputs=ins, output_shapes=(shape,)))
+    return make_graph(out, _gpus(devices), {"model": f"layered-dag-{nodes}", "seed": seed})
+
+
+def dag_profiles(hardware_tags, seed: int = 3):
+    """Planted cost_hint laws per (op, hardware tag): each tag its own slope/intercept set."""
+    rng = SplitMix64(seed)
+    db = ProfileDB(hardware_tags=list(hardware_tags), provenance="synthetic planted laws (not measurements)")
+    for hw in hardware_tags:
+        for op in RANDOM_OPS:
+            slope, icpt = 2.0 + 10.0 * rng.uniform(), 1.0 + 5.0 * rng.uniform()
+            for x in DEFAULT_GRID:
+                db_insert(db, ProfileRecord(OpSignature(op, hw, (("cost_hint", x),)), slope * x + icpt))
+    return db
