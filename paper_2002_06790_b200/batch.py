@@ -32,6 +32,9 @@ from .simulator import build_schedule, critical_path_arrays, simulate_arrays
 
 def class_key(cfg) -> tuple:
     """Candidates with equal keys share one expanded graph (cli.py:83 decides expansion)."""
+    if getattr(cfg, "sync", "allreduce") == "parameter_server":
+        return ("ps", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers), cfg.collective.path,
+                cfg.ps_device)
     if not (cfg.replicas > 1 or cfg.device_map):
         return ("plain",)
     return ("dp", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers), cfg.collective.path)
@@ -55,6 +58,11 @@ class TopologyClass:
         if class_key(cfg0) == ("plain",):
             self.graph = g
             self.lg: LoweredGraph = lowered(g, ctx.device)
+        elif class_key(cfg0)[0] == "ps":
+            from .ps import expand_parameter_server
+
+            self.graph = expand_parameter_server(g, cfg0, db, cfg0.ps_device).graph
+            self.lg = lowered(self.graph, ctx.device)
         else:
             self.plan = ExpansionPlan(g, cfg0, ctx.device)
             self.graph, self.lg = self.plan.graph, self.plan.lowered

@@ -383,6 +383,13 @@ class StrategyConfig:
     overrides: dict = field(default_factory=dict)
     hardware: str = ""
     op_gap_us: float = 0.0
+    # extension (not in the reference; its parse_config ignores unknown keys, strategy.py:93-142):
+    # "allreduce" (strategy.py:170-282) or "parameter_server" (ps.py)
+    sync: str = "allreduce"
+    ps_device: str = "ps0"
+
+
+SYNC_ALLREDUCE, SYNC_PS = "allreduce", "parameter_server"
 
 
 @dataclass
@@ -431,9 +438,12 @@ def parse_config(text: str) -> StrategyConfig:
     gap = doc.get("op_gap_us", 0.0)
     if not isinstance(gap, (int, float)) or gap < 0:
         raise ConfigError(f"op_gap_us must be >= 0, got {gap!r}")
+    sync = doc.get("sync", SYNC_ALLREDUCE)
+    if sync not in (SYNC_ALLREDUCE, SYNC_PS):
+        raise ConfigError(f"unknown sync {sync!r}; expected {SYNC_ALLREDUCE!r} or {SYNC_PS!r}")
     return StrategyConfig(replicas, dmap, CollectiveConfig(algo, coll.get("path", "PCIeSwitch")),
                           markers, {k: float(v) for k, v in overrides.items()},
-                          doc.get("hardware", ""), float(gap))
+                          doc.get("hardware", ""), float(gap), sync, doc.get("ps_device", "ps0"))
 
 
 # ----------------------------------------------------------------------------- schedule

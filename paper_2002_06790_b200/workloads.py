@@ -479,7 +479,7 @@ def model_profiles(graph, hardware_tags, seed: int = 1, grid_points: int = 16, l
     db = ProfileDB(hardware_tags=list(hardware_tags), provenance="synthetic planted laws (not measurements)")
     for link in links:
         db_insert(db, link)
-    ops = sorted({n.op_type for n in graph.nodes.values()})
+    ops = sorted({n.op_type for n in graph.nodes.values()} | {"PSAggregate"})  # PS aggregation (ps.py)
     for h, hw in enumerate(hardware_tags):
         speed = 1.0 + 0.37 * h            # tflops-ish scale per hardware generation
         for op in ops:
