@@ -263,6 +263,13 @@ def run_ours(args):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = S * b_sim / (sim_ms / 1e3) / 1e9
+    kernel_name = "k_simulate_fused" if tc.fused else "k_simulate"
+    traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    prof = ROOT / "profiles" / "r1_ncu_full.json"
+    if prof.exists() and args.workload == "resnet50-dp8" and S == 65536:
+        for k in json.loads(prof.read_text()):
+            if kernel_name in k.get("Kernel Name", ""):
+                traffic = k["dram_bytes_per_launch"]
 
     # ---- e2e through the public C-ABI path with host buffers: H2D candidate arrays, D2H results
     strat = lp.t_strat
@@ -312,7 +319,8 @@ def run_ours(args):
             "best": {"makespan_us": best_v, "index": best_i},
             "stage_ms": {k: statistics.mean(s[k] for s in ev_steps) for k in stages},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "k_simulate_fused" if tc.fused else "k_simulate",
+                         "traffic": traffic, "kernel": kernel_name,
+                         "traffic_source": "profiles/r1_ncu_full.json (ncu --set full, same config)" if traffic else None,
                          "b_sim_bytes": b_sim, "b_table_bytes": b_table,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
             "e2e": {"value": e2e_value, "unit": "sims/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
