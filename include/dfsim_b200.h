@@ -190,17 +190,17 @@ typedef struct {
     int32_t n_nodes;           /* N <= 65535 */
     int32_t n_devices;         /* D <= 32 */
     int64_t n_edges;
-    const uint32_t *meta;      /* [N] successor begin (24 bits) | out-degree (8 bits, 255: use succ_off) */
+    const uint32_t *meta;      /* [N] successor begin (24 bits) | out-degree (8 bits, < 255) */
     const int32_t *succ_off;   /* [N+1] */
     const uint32_t *succ;      /* [E] consumer rank | device << 16 | single-input << 21 */
     const uint16_t *cidx;      /* [N] counter slot of nodes with >= 2 input references */
     const uint32_t *cnt_init;  /* [n_counter_words] packed initial counters */
     int32_t n_counter_words;
-    int32_t counter_bits;      /* 8 or 16 */
+    int32_t counter_bits;      /* 4, 8 or 16 */
     const uint16_t *pos;       /* [N] output column (level-order position) of each rank */
     const int32_t *sources;    /* ascending ranks with in-degree 0 */
     int32_t n_sources;
-    int32_t qcap;              /* per-device FIFO ring capacity (power of two) */
+    int32_t qcap;              /* per-device FIFO ring capacity (power of two); overflow flags the candidate */
     const int32_t *device;     /* [N] device rank */
 } dfsim_sim_tables;
 

@@ -32,7 +32,8 @@ struct FusedArgs {
     int32_t *chunk_counter;
     int32_t wpb;
     int32_t smem_graph;  // bytes of the CTA-shared part
-    int32_t smem_warp;   // bytes per warp
+    int32_t smem_warp;   // bytes per candidate group
+    int32_t tail_bytes;  // FIFO tails at the start of each group's state
 };
 
 // Reductions over one lane group (kGS = 32: the warp; kGS = 16: one half-warp,
@@ -115,8 +116,8 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     double *s_base = reinterpret_cast<double *>(smem + ((static_cast<size_t>(N) * 8 + static_cast<size_t>(E) * 4 + 15) / 16) * 16);
     unsigned char *gbase = smem + a.smem_graph + static_cast<size_t>(gid) * a.smem_warp;
     int32_t *tails = reinterpret_cast<int32_t *>(gbase);
-    unsigned *cnt = reinterpret_cast<unsigned *>(gbase + 128);
-    uint16_t *q = reinterpret_cast<uint16_t *>(gbase + 128 + a.g.n_counter_words * 4);
+    unsigned *cnt = reinterpret_cast<unsigned *>(gbase + a.tail_bytes);
+    uint16_t *q = reinterpret_cast<uint16_t *>(gbase + a.tail_bytes + a.g.n_counter_words * 4);
     __shared__ int s_chunk;
 
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -170,11 +171,12 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             }
             flag = group_any<kGS>(active && ll < D && static_cast<unsigned>(tails[ll]) - head > static_cast<unsigned>(QCAP), grp);
 
-            bool running = false;
+            bool running = false, ovf = false;
+            const bool owner = active && !flag && ll < D;  // this lane drives device ll of a live candidate
             int run_v = 0;
             double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
             auto start_idle = [&]() {
-                if (active && !flag && ll < D && !running && static_cast<int>(head) < tails[ll]) {
+                if (owner && !running && static_cast<int>(head) < tails[ll]) {
                     const int v = q[ll * QSTRIDE + (head & QMASK)];
                     head++;
                     const double b = s_base[v];
@@ -212,8 +214,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     running = false;
                     const uint32_t meta = s_meta[run_v];
                     j0 = static_cast<int>(meta & 0xffffffu);
-                    deg = static_cast<int>(meta >> 24);
-                    if (deg == 255) deg = __ldg(a.g.succ_off + run_v + 1) - j0;
+                    deg = static_cast<int>(meta >> 24);  // < 255 in the fused engine (prepare.Tables)
                 }
                 auto relax = [&](int j) {
                     const uint32_t e = s_succ[j];
@@ -242,12 +243,11 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 }
                 __syncwarp();
                 const int seg_hi = ll < D ? tails[ll] : 0;
-                if (group_any<kGS>(ll < D && static_cast<unsigned>(seg_hi) - head > static_cast<unsigned>(QCAP), grp)) {
-                    flag = true;  // ring overflow: this candidate goes to the exact engine
-                    running = false;
-                }
+                // a ring overflow corrupts only this candidate; it keeps running (every
+                // iteration consumes a finish event, so it terminates) and is re-run exactly
+                ovf |= ll < D && static_cast<unsigned>(seg_hi) - head > static_cast<unsigned>(QCAP);
                 // enqueue(sorted(newly_ready)): sort each device's new ring segment by rank
-                if (!flag && seg_hi - seg_lo > 1) {
+                if (seg_hi - seg_lo > 1) {
                     uint16_t *qd = q + ll * QSTRIDE;
                     for (int i = seg_lo + 1; i < seg_hi; i++) {
                         const uint16_t x = qd[i & QMASK];
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 __syncwarp();
                 start_idle();
             }
+            flag = flag || group_any<kGS>(ovf, grp);
             const double ms = group_max_f64<kGS>(span);
             const unsigned total = group_add_u32<kGS>(ll < D ? head : 0u, grp);  // every pop starts a node
             if (active && ll == 0) {
@@ -417,7 +418,8 @@ FusedShape fused_shape(const dfsim_sim_tables *g) {
     FusedShape f;
     const size_t N = (size_t)g->n_nodes;
     f.graph_bytes = (N * 8 + (size_t)g->n_edges * 4 + 15) / 16 * 16 + N * 8;
-    f.warp_bytes = (128 + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * (g->qcap + 2) * 2 + 15) / 16 * 16;
+    const size_t tail_bytes = g->n_devices <= 16 ? 64 : 128;
+    f.warp_bytes = (tail_bytes + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * (g->qcap + 2) * 2 + 15) / 16 * 16;
     // consecutive candidate groups start 16 banks apart (stride == 64 mod 128 bytes)
     f.warp_bytes = (f.warp_bytes + 127) / 128 * 128 + 64;
     const size_t budget = 227 * 1024 - 64;
@@ -444,7 +446,7 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     DFSIM_ARG_CHECK(ctx, start && finish && makespan && n_placed && flags, "outputs are required");
     DFSIM_ARG_CHECK(ctx, g->n_nodes > 0 && g->n_nodes <= 65535 && g->n_devices <= 32, "fused engine limits");
     DFSIM_ARG_CHECK(ctx, g->qcap >= 2 && (g->qcap & (g->qcap - 1)) == 0, "qcap must be a power of two");
-    DFSIM_ARG_CHECK(ctx, g->counter_bits == 8 || g->counter_bits == 16, "counter_bits 8 or 16");
+    DFSIM_ARG_CHECK(ctx, g->counter_bits == 4 || g->counter_bits == 8 || g->counter_bits == 16, "counter_bits 4, 8 or 16");
     if (st->n_sims <= 0 || st->n_chunks <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const FusedShape f = fused_shape(g);
@@ -459,6 +461,7 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     a.wpb = wpb;
     a.smem_graph = (int)graph_bytes;
     a.smem_warp = (int)warp_bytes;
+    a.tail_bytes = g->n_devices <= 16 ? 64 : 128;
     void *p = nullptr;
     int rc = dfsim_scratch(ctx, 256, &p);
     if (rc) return rc;
@@ -472,7 +475,9 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
         k_simulate_fused<BITS, GS><<<grid, wpb * 32, smem, ctx->stream>>>(a);                                  \
     } while (0)
-    if (g->counter_bits == 8) {
+    if (g->counter_bits == 4) {
+        if (gs == 16) DFSIM_LAUNCH_FUSED(4, 16); else DFSIM_LAUNCH_FUSED(4, 32);
+    } else if (g->counter_bits == 8) {
         if (gs == 16) DFSIM_LAUNCH_FUSED(8, 16); else DFSIM_LAUNCH_FUSED(8, 32);
     } else {
         if (gs == 16) DFSIM_LAUNCH_FUSED(16, 16); else DFSIM_LAUNCH_FUSED(16, 32);

@@ -4,10 +4,9 @@ critical path (K4 v2).  Host numpy, once per class.
 * level order: Kahn waves (level = longest edge count from a source); the
   output column of a node is its index in this order, so the critical-path
   pass reads each schedule row contiguously, level by level, backwards.
-* engine tables: ``meta[v]`` = successor begin (24 bits) | out-degree (8 bits,
-  255 = read succ_off), ``succ[j]`` = consumer rank | device << 16 | single-input
+* engine tables: ``meta[v]`` = successor begin (24 bits) | out-degree (8 bits, < 255), ``succ[j]`` = consumer rank | device << 16 | single-input
   << 21 (a consumer with exactly one input reference needs no counter),
-  ``cidx[v]`` = counter slot of multi-input nodes, packed initial counters.
+  ``cidx[v]`` = counter slot of multi-input nodes, packed 4/8/16-bit initial counters.
 * critical-path tables: the reverse pass processes groups (<= GROUP positions of
   one level) inside prefetch chunks (<= CHUNK positions).  A suffix value read
   in its own chunk or the next one lives in a shared-memory slot (interval
@@ -25,7 +24,7 @@ from . import native
 
 GROUP = 16        # positions processed together (one per lane of a half-warp)
 CHUNK = 64        # positions prefetched per cp.async batch
-QCAP = 32         # per-device FIFO ring capacity of the fused engine
+QCAP = 16         # per-device FIFO ring capacity of the fused engine (overflow -> exact engine)
 
 
 def level_order(n: int, succ_off: np.ndarray, succ_idx: np.ndarray, indeg: np.ndarray):
@@ -79,7 +78,7 @@ class Tables:
         self.pos, self.rank_of_pos, self.level_off = pos, order, loff
         self._engine(N, off, idx, indeg, dev, outdeg)
         self._critical_path(N, idx, indeg, outdeg, order, pos, loff)
-        self.fused_ok = (N <= 65535 and D <= 32 and self.n_edges < 65536 and outdeg.max(initial=0) < 256
+        self.fused_ok = (N <= 65535 and D <= 32 and self.n_edges < 65536 and outdeg.max(initial=0) < 255
                          and indeg.max(initial=0) <= 65534 and self.n_slots < 0x7FFF
                          and self.max_spill_reads < 0x7FFF and self.n_long < 0x7FFF)
 
@@ -88,7 +87,8 @@ class Tables:
         multi = np.nonzero(indeg >= 2)[0]
         cidx = np.zeros(N, np.int64)
         cidx[multi] = np.arange(multi.size)
-        bits = 8 if indeg.max(initial=0) < 255 else 16
+        mx = indeg.max(initial=0)
+        bits = 4 if mx < 15 else (8 if mx < 255 else 16)
         per = 32 // bits
         words = max(1, -(-multi.size // per))
         init = np.zeros(words * per, np.uint64)
