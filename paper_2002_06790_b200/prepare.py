@@ -23,7 +23,7 @@ import numpy as np
 from . import native
 
 GROUP = 16        # positions processed together (one per lane of a half-warp)
-CHUNK = 64        # positions prefetched per cp.async batch
+CHUNK = 32        # positions prefetched per cp.async batch
 QCAP = 16         # per-device FIFO ring capacity of the fused engine (overflow -> exact engine)
 
 
