@@ -244,7 +244,8 @@ typedef struct {
     const int32_t *rank_of_pos;
     const uint32_t *cp_meta;   /* [N] by position: successor begin | count << 16 | source << 24 */
     const uint16_t *cp_slot;   /* [N] by position (0xFFFF: none) */
-    const uint16_t *cp_succ_slot; /* [E] slot id, or 0x8000 | index into the chunk's prefetched spill values */
+    const uint16_t *cp_succ_slot; /* [E] index (doubles) of the successor's value in the candidate's shared
+                                     region: a slot, or a prefetched spill value of the reader's chunk stage */
     int32_t n_groups;
     const int32_t *group_off;  /* <= 16 positions of one level each (a half-warp per candidate) */
     int32_t n_chunks;
@@ -256,6 +257,8 @@ typedef struct {
     const uint16_t *spill_list;/* spill indices, per chunk */
     int32_t max_spill_reads;   /* max spill values one chunk reads */
     const uint32_t *pinfo;     /* [N] by position: slot | has-slot << 15 | spill index << 16 | spill << 31 */
+    int32_t slot_region;       /* doubles of suffix slots at the start of a candidate's shared region */
+    int32_t stage_doubles;     /* doubles per prefetch stage: start K | finish K | spill values R */
 } dfsim_cp_tables;
 
 /* K4 v2: critical-path length and its start node per candidate over start/finish

@@ -284,10 +284,8 @@ struct CpLevelArgs {
     const double *start, *finish;
     double *cp_len;
     int32_t *cp_src;
-    double *spill;        // [grid * wpb][n_long] rows, one per resident warp
+    double *spill;        // [grid * wpb * 2][n_long] rows, one per resident candidate slot
     int32_t wpb;
-    int32_t slot_bytes;   // per warp
-    int32_t stage_doubles;  // 2*K + max_spill_reads
     int32_t table_bytes;  // CTA-shared tables
 };
 
@@ -300,29 +298,38 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
 // reverse level order for their own candidate (identical control flow, different
 // data).  Shared tables (by level position): pinfo[p] = slot | has-slot << 15 |
 // spill index << 16 | spill << 31; pmeta[p] = successor begin | count << 16 |
-// source << 24; succ[E] = slot id, or 0x8000 | index into the chunk's prefetched
-// spill values; group_off[G+1] (groups of <= 16 positions of one level).
+// source << 24; succ[E] = index of the successor's value in the candidate's shared
+// region [slots | stage 0 | stage 1] (a slot, or a value prefetched with the
+// reader's chunk); group_off[G+1] (<= 16 positions of one level each), chunk
+// offsets and the per-chunk spill lists.
 __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ll = lane & 15, half = lane >> 4;
     const int N = a.t.n_nodes, K = a.t.chunk_positions, G = a.t.n_groups, E = a.t.n_edges;
-    const int SD = a.stage_doubles;
+    const int NC = a.t.n_chunks, SD = a.t.stage_doubles, SR = a.t.slot_region;
+    const int NS = __ldg(a.t.spill_off + NC);
     uint32_t *s_info = reinterpret_cast<uint32_t *>(smem);
     uint32_t *s_meta = s_info + N;
     uint16_t *s_succ = reinterpret_cast<uint16_t *>(s_meta + N);
     uint16_t *s_goff = s_succ + E;
+    uint16_t *s_coff = s_goff + (G + 1);
+    uint16_t *s_soff = s_coff + (NC + 1);
+    uint16_t *s_slist = s_soff + (NC + 1);
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         s_info[i] = __ldg(a.t.pinfo + i);
         s_meta[i] = __ldg(a.t.cp_meta + i);
     }
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.t.cp_succ_slot + i);
     for (int i = threadIdx.x; i <= G; i += blockDim.x) s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
+    for (int i = threadIdx.x; i <= NC; i += blockDim.x) {
+        s_coff[i] = static_cast<uint16_t>(__ldg(a.t.chunk_off + i));
+        s_soff[i] = static_cast<uint16_t>(__ldg(a.t.spill_off + i));
+    }
+    for (int i = threadIdx.x; i < NS; i += blockDim.x) s_slist[i] = __ldg(a.t.spill_list + i);
     __syncthreads();
     const int gid = warp * 2 + half;  // candidate slot of this half-warp in the CTA
-    unsigned char *wb = smem + a.table_bytes + static_cast<size_t>(gid) * (a.slot_bytes + 2 * SD * 8);
-    double *slots = reinterpret_cast<double *>(wb);
-    double *buf = reinterpret_cast<double *>(wb + a.slot_bytes);  // [2 stages][start K | finish K | spill R]
+    double *region = reinterpret_cast<double *>(smem + a.table_bytes) + static_cast<size_t>(gid) * (SR + 2 * SD);
     double *spill_row = a.spill + (static_cast<int64_t>(blockIdx.x) * a.wpb * 2 + gid) * a.t.n_long;
     const int64_t per_iter = static_cast<int64_t>(gridDim.x) * a.wpb * 2;
 
@@ -332,33 +339,32 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
         const int64_t sr = live ? s : base;  // the idle half shadows its partner's reads
         const double *st = a.start + sr * N;
         const double *fi = a.finish + sr * N;
-        auto prefetch = [&](int c, int stage) {
-            const int p0 = s_goff[__ldg(a.t.chunk_off + c)], p1 = s_goff[__ldg(a.t.chunk_off + c + 1)];
-            double *bs = buf + stage * SD;
+        auto prefetch = [&](int c) {
+            const int p0 = s_goff[s_coff[c]], p1 = s_goff[s_coff[c + 1]];
+            double *bs = region + SR + (c & 1) * SD;
             for (int p = p0 + ll; p < p1; p += 16) {
                 cp_async8(bs + (p - p0), st + p);
                 cp_async8(bs + K + (p - p0), fi + p);
             }
-            const int r0 = __ldg(a.t.spill_off + c), r1 = __ldg(a.t.spill_off + c + 1);
-            for (int r = r0 + ll; r < r1; r += 16) cp_async8(bs + 2 * K + (r - r0), spill_row + __ldg(a.t.spill_list + r));
+            const int r0 = s_soff[c], r1 = s_soff[c + 1];
+            for (int r = r0 + ll; r < r1; r += 16) cp_async8(bs + 2 * K + (r - r0), spill_row + s_slist[r]);
             asm volatile("cp.async.commit_group;\n" ::);
         };
         double len = 0.0;
         int src = 0x7fffffff;
-        const int nc = a.t.n_chunks;
-        if (nc > 0) prefetch(nc - 1, (nc - 1) & 1);
-        for (int c = nc - 1; c >= 0; c--) {
+        if (NC > 0) prefetch(NC - 1);
+        for (int c = NC - 1; c >= 0; c--) {
             // chunk c-1 may read spill values written up to chunk c+1: all complete (and
             // ordered by the __syncwarp that ended chunk c+1) before this prefetch is issued
             if (c > 0) {
-                prefetch(c - 1, (c - 1) & 1);
+                prefetch(c - 1);
                 asm volatile("cp.async.wait_group 1;\n" ::);
             } else {
                 asm volatile("cp.async.wait_group 0;\n" ::);
             }
             __syncwarp();
-            const double *bs = buf + (c & 1) * SD;
-            const int g0 = __ldg(a.t.chunk_off + c), g1 = __ldg(a.t.chunk_off + c + 1);
+            const double *bs = region + SR + (c & 1) * SD;
+            const int g0 = s_coff[c], g1 = s_coff[c + 1];
             const int p0 = s_goff[g0];
             for (int gi = g1 - 1; gi >= g0; gi--) {
                 const int p = s_goff[gi] + ll;
@@ -367,14 +373,13 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                     const int j0 = static_cast<int>(m & 0xffffu), j1 = j0 + static_cast<int>((m >> 16) & 0xffu);
                     double best = 0.0;  // max(0.0, .) (graph.py:465-468)
                     for (int j = j0; j < j1; j++) {
-                        const unsigned e = s_succ[j];
-                        const double x = (e & 0x8000u) ? bs[2 * K + (e & 0x7fffu)] : slots[e];
+                        const double x = region[s_succ[j]];
                         best = x > best ? x : best;
                     }
                     const double d = __dsub_rn(bs[K + (p - p0)], bs[p - p0]);  // finish - start (reporting.py:128)
                     const double sv = __dadd_rn(d, best);
                     const uint32_t info = s_info[p];
-                    if (info & 0x8000u) slots[info & 0x7fffu] = sv;
+                    if (info & 0x8000u) region[info & 0x7fffu] = sv;
                     if (live && (info >> 31)) spill_row[(info >> 16) & 0x7fffu] = sv;
                     if ((m >> 24) & 1u) {
                         const int r = __ldg(a.t.rank_of_pos + p);
@@ -492,13 +497,16 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     DFSIM_ARG_CHECK(ctx, start && finish && cp_len, "start, finish and cp_len are required");
     DFSIM_ARG_CHECK(ctx, t->chunk_positions >= 16, "chunk_positions >= 16");
     DFSIM_ARG_CHECK(ctx, t->n_nodes <= 65535 && t->n_edges <= 65535 && t->n_slots < 0x7fff &&
-                         t->max_spill_reads < 0x7fff, "level tables use 16-bit ids");
+                         t->max_spill_reads < 0x7fff && t->slot_region + 2 * t->stage_doubles < 65536,
+                    "level tables use 16-bit ids");
+    DFSIM_ARG_CHECK(ctx, t->stage_doubles >= 2 * t->chunk_positions + t->max_spill_reads && t->slot_region >= t->n_slots,
+                    "inconsistent critical-path region layout");
     if (n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    const int slot_bytes = ((t->n_slots > 0 ? t->n_slots : 1) * 8 + 15) / 16 * 16;
-    const int stage_doubles = (2 * t->chunk_positions + t->max_spill_reads + 1) / 2 * 2;
-    const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 + 15) / 16 * 16;
-    const size_t per_warp = 2 * ((size_t)slot_bytes + 2 * (size_t)stage_doubles * 8);  // two candidates per warp
+    const size_t n_spill_reads = 0;  // staged list length is read on the device; bound it by E
+    const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 +
+                                (size_t)(t->n_chunks + 1) * 4 + (size_t)t->n_edges * 2 + n_spill_reads + 15) / 16 * 16;
+    const size_t per_warp = 2 * ((size_t)t->slot_region + 2 * (size_t)t->stage_doubles) * 8;  // two candidates
     const size_t budget = 227 * 1024 - 64;
     int wpb = 32;
     while (wpb > 1 && table_bytes + wpb * per_warp > budget) wpb--;
@@ -514,8 +522,6 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     a.start = start; a.finish = finish; a.cp_len = cp_len; a.cp_src = cp_src;
     a.spill = static_cast<double *>(p);
     a.wpb = wpb;
-    a.slot_bytes = slot_bytes;
-    a.stage_doubles = stage_doubles;
     a.table_bytes = (int)table_bytes;
     const size_t smem = table_bytes + wpb * per_warp;
     DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_critical_path_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -73,7 +73,7 @@ class CpTables(ctypes.Structure):
     _fields_ = [("n_nodes", I32), ("n_slots", I32), ("n_edges", I32), ("rank_of_pos", P), ("cp_meta", P),
                 ("cp_slot", P), ("cp_succ_slot", P), ("n_groups", I32), ("group_off", P), ("n_chunks", I32),
                 ("chunk_off", P), ("chunk_positions", I32), ("n_long", I32), ("cp_spill", P), ("spill_off", P),
-                ("spill_list", P), ("max_spill_reads", I32), ("pinfo", P)]
+                ("spill_list", P), ("max_spill_reads", I32), ("pinfo", P), ("slot_region", I32), ("stage_doubles", I32)]
 
 
 _SIGNATURES = {

@@ -80,7 +80,8 @@ class Tables:
         self._critical_path(N, idx, indeg, outdeg, order, pos, loff)
         self.fused_ok = (N <= 65535 and D <= 32 and self.n_edges < 65536 and outdeg.max(initial=0) < 255
                          and indeg.max(initial=0) <= 65534 and self.n_slots < 0x7FFF
-                         and self.max_spill_reads < 0x7FFF and self.n_long < 0x7FFF)
+                         and self.max_spill_reads < 0x7FFF and self.n_long < 0x7FFF
+                         and self.slot_region + 2 * self.stage_doubles < 65536 and len(self.spill_list) < 65536)
 
     def _engine(self, N, off, idx, indeg, dev, outdeg):
         single = indeg == 1
@@ -169,6 +170,17 @@ class Tables:
         self.n_groups, self.n_chunks = n_groups, n_chunks
         self.n_slots, self.n_long = nslots, int(spill_flag.sum())
         self.max_spill_reads = int(np.diff(soff).max(initial=0))
+        # per-candidate shared region (doubles): [slots | stage 0 | stage 1], stage = start K | finish K | spill R;
+        # successor entries become absolute indices into it (the reader's chunk parity picks the stage)
+        self.slot_region = (max(nslots, 1) + 1) // 2 * 2
+        self.stage_doubles = (2 * self.chunk + self.max_spill_reads + 1) // 2 * 2
+        reader_chunk = chunk_of_pos[pu]
+        absent = np.where(near, slot_of_pos[pv], 0)
+        if far.any():
+            absent[far] = [self.slot_region + (c_ & 1) * self.stage_doubles + 2 * self.chunk + bufidx[(c_, k_)]
+                           for c_, k_ in zip(far_chunk.tolist(), far_k.tolist())]
+        del reader_chunk
+        self.cp_succ_abs = absent[np.argsort(pu, kind="stable")]
 
 
 class ClassTables(Tables):
@@ -193,7 +205,7 @@ class ClassTables(Tables):
             cnt_init=T(self.cnt_init, np.uint32), pos=T(self.pos, np.uint16), pos32=T(self.pos, np.int32),
             rank_of_pos=T(self.rank_of_pos, np.int32), cp_slot=T(self.cp_slot, np.uint16),
             cp_spill=T(self.cp_spill, np.uint16), cp_meta=T(self.cp_meta, np.uint32),
-            cp_succ=T(self.cp_succ, np.uint16), group_off=T(self.group_off, np.int32),
+            cp_succ=T(self.cp_succ_abs, np.uint16), group_off=T(self.group_off, np.int32),
             chunk_off=T(self.chunk_off, np.int32), spill_off=T(self.spill_off, np.int32),
             spill_list=T(self.spill_list, np.uint16), pinfo=T(self.pinfo, np.uint32))
         p = native.ptr
@@ -204,7 +216,8 @@ class ClassTables(Tables):
         self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
                                          p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
                                          self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long, p(t["cp_spill"]),
-                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads, p(t["pinfo"]))
+                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads, p(t["pinfo"]),
+                                         self.slot_region, self.stage_doubles)
 
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
         """Schedule row(s) stored by position -> node-rank order."""
