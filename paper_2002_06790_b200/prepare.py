@@ -18,12 +18,14 @@ critical path (K4 v2).  Host numpy, once per class.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import native
 
 GROUP = 16        # positions processed together (one per lane of a half-warp)
-CHUNK = 32        # positions prefetched per cp.async batch
+CHUNK = int(os.environ.get("DFSIM_CP_CHUNK", 32))  # positions prefetched per cp.async batch
 QCAP = 16         # per-device FIFO ring capacity of the fused engine (overflow -> exact engine)
 
 
