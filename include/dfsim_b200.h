@@ -114,15 +114,16 @@ int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, const dfsim_ex
 
 /* ---------------------------------------------------------------- profile tables (K2) */
 typedef struct {
-    /* per node */
+    /* per node; the rows marked [GV][N] hold one row per graph variant (graphs of identical
+     * structure whose attributes / shapes differ, e.g. one per batch size) */
     const int32_t *op;          /* [N] op-type id */
     const uint8_t *kind;        /* [N] 0 Compute, 1 Transfer, 2 Collective */
-    const int32_t *sig;         /* [N] feature-vector id */
-    const int64_t *comm_bytes;  /* [N] attrs["bytes"] when it is a Python int, else ignored */
-    const uint8_t *comm_ok;     /* [N] Transfer: Link device and int bytes; Collective: list group and int bytes */
-    const int32_t *group_size;  /* [N] len(attrs["group"]) for collectives */
-    const double *link_thr;     /* [N] Transfer: link throughput MB/s */
-    const double *link_lat;     /* [N] Transfer: link latency us */
+    const int32_t *sig;         /* [GV][N] feature-vector id */
+    const int64_t *comm_bytes;  /* [GV][N] attrs["bytes"] when it is a Python int, else ignored */
+    const uint8_t *comm_ok;     /* [GV][N] Transfer: Link device and int bytes; Collective: list group and int bytes */
+    const int32_t *group_size;  /* [GV][N] len(attrs["group"]) for collectives */
+    const double *link_thr;     /* [GV][N] Transfer: link throughput MB/s */
+    const double *link_lat;     /* [GV][N] Transfer: link latency us */
     /* feature vectors, names sorted by string rank */
     int32_t n_sigs;
     const int32_t *sig_off;     /* [n_sigs+1] */
@@ -163,6 +164,7 @@ typedef struct {
     const uint8_t *algo;       /* [S] 0 MeasuredThroughput, 1 RingAnalytic */
     const int32_t *path;       /* [S] collective path id */
     const int32_t *override_set; /* [S] -1 for none */
+    const int32_t *gvariant;   /* [S] graph variant, or NULL for variant 0 */
 } dfsim_strategies;
 
 /* dur[s*N+v], src[s*N+v]; bad[s] = number of nodes whose source is >= 253 */
@@ -220,12 +222,12 @@ typedef struct {
     const double *ov_val;
 } dfsim_fused_strategies;
 
-/* K2a: base[var*N+v] = estimate of node v under variant var = (hw, algo, path) with
+/* K2a: base[var*N+v] = estimate of node v under variant var = (graph variant, hw, algo, path) with
  * op_gap 0; sign bit set when the candidate's op_gap must be added.  status is the
  * DFSIM_SRC_* tag per (var, v). */
 int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t, int32_t n_variants,
-                           const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path, double *base,
-                           uint8_t *status);
+                           const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path,
+                           const int32_t *var_gv, double *base, uint8_t *status);
 
 /* Candidates one CTA of the fused engine holds; chunks of dfsim_fused_strategies
  * must not exceed it (0: the class does not fit the fused engine). */

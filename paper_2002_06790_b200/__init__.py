@@ -43,7 +43,7 @@ from .model import (  # noqa: F401
     serialize_graph,
     utilization,
 )
-from .batch import SweepResult, TopologyClass, gather_best, sweep  # noqa: F401
+from .batch import SweepResult, TopologyClass, gather_best, sweep, sweep_variants  # noqa: F401
 from .estimate import estimate_all, estimate_batch  # noqa: F401
 from .expansion import expand_class, expand_data_parallel  # noqa: F401
 from .lowering import fit_for_grid, fit_linear, node_features  # noqa: F401

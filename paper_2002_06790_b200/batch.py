@@ -50,25 +50,44 @@ class TopologyClass:
     which also produces the reference's exact error for failing candidates.
     """
 
-    def __init__(self, g, db, configs, device: int | None = None, fused: bool = True):
+    def __init__(self, g, db, configs, device: int | None = None, fused: bool = True, graphs=None,
+                 graph_of=None):
         ctx = native.Context.get(device)
         self.ctx = ctx
         cfg0 = configs[0]
         self.plan = None
-        if class_key(cfg0) == ("plain",):
-            self.graph = g
+        key = class_key(cfg0)
+        if graphs is not None:
+            g = graphs[graph_of[0]]
+        if key == ("plain",):
+            kind, self.graph = "plain", g
             self.lg: LoweredGraph = lowered(g, ctx.device)
-        elif class_key(cfg0)[0] == "ps":
+            structure = None
+        elif key[0] == "ps":
             from .ps import expand_parameter_server
 
-            self.graph = expand_parameter_server(g, cfg0, db, cfg0.ps_device).graph
+            kind = "ps"
+            structure = expand_parameter_server(g, cfg0, db, cfg0.ps_device)
+            self.graph = structure.graph
             self.lg = lowered(self.graph, ctx.device)
         else:
-            self.plan = ExpansionPlan(g, cfg0, ctx.device)
+            kind = "dp"
+            self.plan = structure = ExpansionPlan(g, cfg0, ctx.device)
             self.graph, self.lg = self.plan.graph, self.plan.lowered
         self.ids = self.lg.ids
         self.configs = list(configs)
-        self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device)
+        variant_rows, strat_gv = None, None
+        if graphs is not None and len(set(graph_of)) > 1:
+            from .variants import rows_for
+
+            gv_of: dict = {}
+            variant_rows = []
+            for gi in graph_of:
+                if gi not in gv_of:
+                    gv_of[gi] = len(variant_rows)
+                    variant_rows.append(rows_for(kind, self.ids, graphs[gi], structure, cfg0, db))
+            strat_gv = [gv_of[gi] for gi in graph_of]
+        self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device, variant_rows, strat_gv)
         self.tables = None
         self.fused = False
         if fused and self.lg.acyclic and 0 < self.lg.n <= 65535:
@@ -81,15 +100,16 @@ class TopologyClass:
         import torch
 
         lp, N = self.lp, self.lg.n
-        keys = list(zip(lp.strat_hw, lp.strat_algo, lp.strat_path))
+        keys = list(zip(lp.strat_gv, lp.strat_hw, lp.strat_algo, lp.strat_path))
         var_ids: dict = {}
         var_of = np.asarray([var_ids.setdefault(k, len(var_ids)) for k in keys], np.int64)
         V = len(var_ids)
         dev = f"cuda:{self.ctx.device}"
         vk = list(var_ids)
-        self.v_hw = torch.tensor([k[0] for k in vk], dtype=torch.int32, device=dev)
-        self.v_algo = torch.tensor([k[1] for k in vk], dtype=torch.uint8, device=dev)
-        self.v_path = torch.tensor([k[2] for k in vk], dtype=torch.int32, device=dev)
+        self.v_gv = torch.tensor([k[0] for k in vk], dtype=torch.int32, device=dev)
+        self.v_hw = torch.tensor([k[1] for k in vk], dtype=torch.int32, device=dev)
+        self.v_algo = torch.tensor([k[2] for k in vk], dtype=torch.uint8, device=dev)
+        self.v_path = torch.tensor([k[3] for k in vk], dtype=torch.int32, device=dev)
         self.n_variants = V
         self.var_of = var_of
         self.base = torch.empty((V, N), dtype=torch.float64, device=dev)
@@ -126,7 +146,20 @@ class TopologyClass:
         """K2a: estimate every node once per (hardware, algorithm, path) variant."""
         self.ctx.call("dfsim_resolve_variants", self.lg.n, native.ctypes.byref(self.lp.struct), self.n_variants,
                       native.ptr(self.v_hw), native.ptr(self.v_algo), native.ptr(self.v_path),
-                      native.ptr(self.base), native.ptr(self.status))
+                      native.ptr(self.v_gv), native.ptr(self.base), native.ptr(self.status))
+
+    def fallback_if_needed(self, o) -> bool:
+        """Re-run ring-overflow candidates on the exact engine (host sync on the flags).
+        Returns True when some candidate was re-run (its critical path must then be redone)."""
+        import torch
+
+        if not self.fused:
+            return False
+        flagged = torch.nonzero(o["flags"]).flatten()
+        if flagged.numel():
+            self._fallback(o, flagged.cpu().tolist())
+            return True
+        return False
 
     def _fallback(self, o, rows):
         """Exact engine for candidates whose FIFO ring overflowed (never changes results)."""
@@ -137,7 +170,7 @@ class TopologyClass:
         s = self.lp.t_strat
         sub = {k: v.index_select(0, idx).contiguous() for k, v in s.items()}
         strat = native.Strategies(len(rows), native.ptr(sub["hw"]), native.ptr(sub["gap"]), native.ptr(sub["algo"]),
-                                  native.ptr(sub["path"]), native.ptr(sub["ov"]))
+                                  native.ptr(sub["path"]), native.ptr(sub["ov"]), native.ptr(sub["gv"]))
         N = self.lg.n
         dur = torch.empty((len(rows), N), dtype=torch.float64, device=dev)
         src = torch.empty((len(rows), N), dtype=torch.uint8, device=dev)
@@ -150,7 +183,7 @@ class TopologyClass:
                       native.ptr(idx))
         o.setdefault("fallback_rows", []).extend(int(r) for r in rows)
 
-    def run_fused(self, o: dict, ev: dict, paths: bool = False):
+    def run_fused(self, o: dict, ev: dict, paths: bool = False, defer_fallback: bool = False):
         import torch
 
         lg, S, N, D = self.lg, self.lp.n_sims, self.lg.n, self.lg.n_devices
@@ -176,9 +209,8 @@ class TopologyClass:
                       native.ptr(o["makespan"]), native.ptr(o["busy"]), native.ptr(o["n_placed"]),
                       native.ptr(o["flags"]))
         rec("simulate", 1)
-        flagged = torch.nonzero(o["flags"]).flatten()
-        if flagged.numel():
-            self._fallback(o, flagged.cpu().tolist())
+        if not defer_fallback:
+            self.fallback_if_needed(o)
         rec("critical_path", 0)
         self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.tables.cp_struct), S,
                       native.ptr(o["start"]), native.ptr(o["finish"]), native.ptr(o["cp_len"]), native.ptr(o["cp_src"]))
@@ -191,7 +223,7 @@ class TopologyClass:
             self.plan.reexpand(topo=not self.fused)
 
     def run(self, *, schedules: bool = True, paths: bool = False, out: dict | None = None,
-            events: dict | None = None) -> dict:
+            events: dict | None = None, defer_fallback: bool = False) -> dict:
         """K2 -> K3 -> K4 for every candidate; asynchronous on the current stream.
 
         ``events`` (optional): dict of stage name -> (start, end) torch.cuda.Event
@@ -200,7 +232,7 @@ class TopologyClass:
         o = out if out is not None else {}
         ev = events or {}
         if self.fused:
-            self.run_fused(o, ev)
+            self.run_fused(o, ev, defer_fallback=defer_fallback)
         else:
             def rec(name, i):
                 if name in ev:
@@ -232,6 +264,15 @@ class TopologyClass:
             pos = torch.as_tensor(self.tables.pos, device=st.device)
             st, fi = st.index_select(0, pos), fi.index_select(0, pos)
         return st, fi
+
+    def critical_path_only(self, o: dict):
+        """Re-run K4 on the current schedules (after a deferred fallback)."""
+        if self.fused:
+            self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.tables.cp_struct), self.lp.n_sims,
+                          native.ptr(o["start"]), native.ptr(o["finish"]), native.ptr(o["cp_len"]),
+                          native.ptr(o["cp_src"]))
+        elif self.lg.acyclic and self.lg.n:
+            critical_path_arrays(self.lg, o["start"], o["finish"], out=o)
 
     def best(self, o: dict, index_base: int = 0, record=None):
         """K5 on this device: first minimum (makespan, index_base + row) -> 16-byte record."""
@@ -298,11 +339,24 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
     Errors follow the reference sweep: the first failing config (in list order)
     raises its UnknownOpError / ValueError / CycleError (cli.py:132-145).
     """
+    return sweep_variants([g], db, configs, [0] * len(configs), device, keep_schedules, fused)
+
+
+def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,
+                   fused: bool = True) -> SweepResult:
+    """``sweep`` where candidate i runs ``configs[i]`` on ``graphs[graph_of[i]]`` (e.g. one graph per
+    batch size).  Graphs of identical structure share a topology class (variants.py)."""
     import torch
 
+    from .variants import structure_key
+
+    skeys = {}
     groups: dict = {}
     for i, cfg in enumerate(configs):
-        groups.setdefault(class_key(cfg), []).append(i)
+        gi = graph_of[i]
+        if gi not in skeys:
+            skeys[gi] = structure_key(graphs[gi])
+        groups.setdefault((class_key(cfg), skeys[gi]), []).append(i)
     S = len(configs)
     ctx = native.Context.get(device)
     dev = f"cuda:{ctx.device}"
@@ -311,7 +365,8 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
     result = SweepResult(np.zeros(0), np.zeros(0), -1, float("nan"))
     failures = []
     for pos, (key, idx) in enumerate(groups.items()):
-        tc = TopologyClass(g, db, [configs[i] for i in idx], ctx.device, fused=fused)
+        tc = TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device, fused=fused,
+                           graphs=graphs, graph_of=[graph_of[i] for i in idx])
         o = tc.run(schedules=True)
         t_idx = torch.as_tensor(idx, dtype=torch.int64, device=dev)
         makespan.index_copy_(0, t_idx, o["makespan"])

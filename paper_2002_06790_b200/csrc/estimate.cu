@@ -64,8 +64,10 @@ __device__ bool predict(const dfsim_profile_tables &t, int m, int sg, double *ou
     return true;
 }
 
-__device__ __forceinline__ double estimate_one(const dfsim_profile_tables &t, int v, int hw, double gap_s,
-                                               int algo, int path, int ovs, uint8_t *src) {
+// v: node rank; gv: graph variant (per-node feature / comm rows are [n_graph_variants][N])
+__device__ __forceinline__ double estimate_one(const dfsim_profile_tables &t, int N, int v, int gv, int hw,
+                                               double gap_s, int algo, int path, int ovs, uint8_t *src) {
+    const int64_t vv = static_cast<int64_t>(gv) * N + v;
     if (ovs >= 0) {
         const int o0 = __ldg(t.ov_off + ovs), o1 = __ldg(t.ov_off + ovs + 1);
         const int p = find_i32(t.ov_node, o0, o1, v);
@@ -73,22 +75,22 @@ __device__ __forceinline__ double estimate_one(const dfsim_profile_tables &t, in
     }
     const int kind = __ldg(t.kind + v);
     const double gap = kind == 0 ? gap_s : 0.0;
-    const int op = __ldg(t.op + v), sg = __ldg(t.sig + v);
+    const int op = __ldg(t.op + v), sg = __ldg(t.sig + vv);
     const uint64_t ekey = (static_cast<uint64_t>(hw) << 42) | (static_cast<uint64_t>(op) << 21) | static_cast<uint64_t>(sg);
     const int e = find_u64(t.exact_key, t.n_exact, ekey);
     if (e >= 0) { *src = DFSIM_SRC_EXACT; return __dadd_rn(__ldg(t.exact_mean + e), gap); }
     const int m = find_u64(t.model_key, t.n_models, (static_cast<uint64_t>(hw) << 21) | static_cast<uint64_t>(op));
     double pv;
     if (m >= 0 && predict(t, m, sg, &pv)) { *src = DFSIM_SRC_FITTED; return __dadd_rn(pv, gap); }
-    if (kind != 0 && __ldg(t.comm_ok + v)) {
-        const long long b = __ldg(reinterpret_cast<const long long *>(t.comm_bytes) + v);
+    if (kind != 0 && __ldg(t.comm_ok + vv)) {
+        const long long b = __ldg(reinterpret_cast<const long long *>(t.comm_bytes) + vv);
         const double bd = __ll2double_rn(b);
         if (kind == 1) {  // Transfer over its Link device (transfer_time)
             if (b <= 0) { *src = DFSIM_SRC_BAD_BYTES; return 0.0; }
             *src = DFSIM_SRC_COMM;
-            return comm_time(bd, __ldg(t.link_thr + v), __ldg(t.link_lat + v));
+            return comm_time(bd, __ldg(t.link_thr + vv), __ldg(t.link_lat + vv));
         }
-        const int n = __ldg(t.group_size + v);  // Collective (allreduce_time)
+        const int n = __ldg(t.group_size + vv);  // Collective (allreduce_time)
         if (b > 0 && n >= 2 && path >= 0 && path < t.n_paths) {
             if (algo == 0) {
                 const int r = find_u64(t.nccl_key, t.n_nccl, (static_cast<uint64_t>(path) << 32) | static_cast<uint32_t>(n));
@@ -115,8 +117,9 @@ __global__ void __launch_bounds__(256) k_estimate(int32_t N, dfsim_profile_table
         const int64_t s = i / N;
         const int v = static_cast<int>(i - s * N);
         uint8_t src;
-        double val = estimate_one(t, v, __ldg(st.hw + s), __ldg(st.op_gap + s), __ldg(st.algo + s),
-                                  __ldg(st.path + s), st.override_set ? __ldg(st.override_set + s) : -1, &src);
+        double val = estimate_one(t, N, v, st.gvariant ? __ldg(st.gvariant + s) : 0, __ldg(st.hw + s),
+                                  __ldg(st.op_gap + s), __ldg(st.algo + s), __ldg(st.path + s),
+                                  st.override_set ? __ldg(st.override_set + s) : -1, &src);
         if (src < DFSIM_SRC_BAD_BYTES && !(val >= 0.0)) src = DFSIM_SRC_NEGATIVE;  // DurationEntry check
         dur[i] = val;
         if (src_out) src_out[i] = src;
@@ -126,14 +129,16 @@ __global__ void __launch_bounds__(256) k_estimate(int32_t N, dfsim_profile_table
 
 __global__ void __launch_bounds__(256) k_resolve_variants(int32_t N, dfsim_profile_tables t, int32_t V,
                                                           const int32_t *var_hw, const uint8_t *var_algo,
-                                                          const int32_t *var_path, double *base, uint8_t *status) {
+                                                          const int32_t *var_path, const int32_t *var_gv,
+                                                          double *base, uint8_t *status) {
     const int64_t total = static_cast<int64_t>(V) * N;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int var = static_cast<int>(i / N);
         const int v = static_cast<int>(i - static_cast<int64_t>(var) * N);
         uint8_t src;
-        double val = estimate_one(t, v, __ldg(var_hw + var), 0.0, __ldg(var_algo + var), __ldg(var_path + var), -1, &src);
+        double val = estimate_one(t, N, v, var_gv ? __ldg(var_gv + var) : 0, __ldg(var_hw + var), 0.0,
+                                  __ldg(var_algo + var), __ldg(var_path + var), -1, &src);
         if (src < DFSIM_SRC_BAD_BYTES && !(val >= 0.0)) src = DFSIM_SRC_NEGATIVE;
         if (src >= DFSIM_SRC_BAD_BYTES) val = __longlong_as_double(0x7ff8000000000000LL);
         // record/model values get the candidate's op_gap on Compute nodes (costmodel.py:305)
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(256) k_resolve_variants(int32_t N, dfsim_profi
 
 extern "C" int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t, int32_t n_variants,
                                       const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path,
-                                      double *base, uint8_t *status) {
+                                      const int32_t *var_gv, double *base, uint8_t *status) {
     if (!ctx || !t || !base || !status) return DFSIM_BAD_ARGUMENT;
     if (n_nodes <= 0 || n_variants <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
@@ -155,7 +160,7 @@ extern "C" int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfs
     int64_t blocks = (total + 255) / 256;
     if (blocks > (int64_t)ctx->num_sms * 16) blocks = (int64_t)ctx->num_sms * 16;
     k_resolve_variants<<<(unsigned)blocks, 256, 0, ctx->stream>>>(n_nodes, *t, n_variants, var_hw, var_algo, var_path,
-                                                                 base, status);
+                                                                 var_gv, base, status);
     return dfsim_after_launch(ctx, "k_resolve_variants");
 }
 

@@ -59,7 +59,7 @@ def marked_gradients(g, cfg) -> list[str]:
 class ExpansionPlan:
     """Strings and ranks of one topology class (host), plus its device CSR (K1)."""
 
-    def __init__(self, g, cfg, device: int | None = None, build_objects: bool = True):
+    def __init__(self, g, cfg, device: int | None = None, build_objects: bool = True, run_k1: bool = True):
         R = cfg.replicas
         if cfg.device_map and len(cfg.device_map) != R:
             raise ConfigError(f"device_map has {len(cfg.device_map)} entries for {R} replicas")
@@ -83,6 +83,8 @@ class ExpansionPlan:
             dup = next(c for c in coll_ids if c in seen)
             raise DfsimError(f"collective id {dup!r} collides with an existing node")
         self._validate_inherited(g, base_index, R, marked, group)
+        self.origin = {f"{nid}@r{k}": ("clone", nid) for k in range(R) for nid in base_ids}
+        self.origin.update({cid: ("coll", gid) for gid, cid in zip(marked, coll_ids)})
         order = sorted(range(len(all_ids)), key=all_ids.__getitem__)
         self.ids = [all_ids[i] for i in order]
         rank = np.empty(len(all_ids), dtype=np.int32)
@@ -110,6 +112,9 @@ class ExpansionPlan:
             if nid in gidx:
                 marked_idx[v] = gidx[nid]
         self.max_indeg = max(max_in, R if coll_ids else 0)
+        if not run_k1:  # host strings only (ids, origins, collective nodes); no device arrays
+            self.ctx, self.lowered, self.graph = None, None, None
+            return
         ctx = native.Context.get(device)
         self.ctx = ctx
         d = ctx.device
@@ -193,6 +198,13 @@ class ExpansionPlan:
                                         topo, int(n_edges.value), int(n_src.value), self.max_indeg, ctx,
                                         int(n_ord.value))
 
+    def collective_node(self, gid, grad) -> OpNode:
+        """AllReduce node of gradient ``gid`` (strategy.py:239-251)."""
+        return OpNode(f"allreduce_{gid}", "AllReduce", self.fabric, COLLECTIVE,
+                      {"group": list(self.group), "bytes": grad.output_shapes[0].byte_size(),
+                       "path": self.cfg.collective.path},
+                      tuple((f"{gid}@r{k}", 0) for k in range(self.R)), grad.output_shapes)
+
     def _objects(self, g, cfg) -> DataflowGraph:
         """Host node/device objects in the reference's insertion order (strategy.py:202-276)."""
         R, marked = self.R, set(self.marked) if self.R > 1 else set()
@@ -204,11 +216,7 @@ class ExpansionPlan:
                 cid = f"{nid}@r{k}"
                 nodes[cid] = OpNode(cid, n.op_type, self.clone_dev[k][v], n.kind, n.attrs, ins, n.output_shapes)
         for gid, cid in zip(self.marked, self.coll_ids):
-            grad = g.nodes[gid]
-            nodes[cid] = OpNode(cid, "AllReduce", self.fabric, COLLECTIVE,
-                                {"group": list(self.group), "bytes": grad.output_shapes[0].byte_size(),
-                                 "path": cfg.collective.path},
-                                tuple((f"{gid}@r{k}", 0) for k in range(R)), grad.output_shapes)
+            nodes[cid] = self.collective_node(gid, g.nodes[gid])
         devices = {}
         coll = set(self.coll_ids)
         for n in nodes.values():

@@ -333,10 +333,37 @@ def resolve_overrides(overrides: dict, ids: list) -> dict:
     return out
 
 
-class LoweredProfiles:
-    """Device tables for dfsim_estimate_batch over one graph and a list of configs."""
+def node_rows(g, ids) -> list:
+    """Per node (rank order): (features, comm_ok, bytes, group size, link thr, link lat) -- the
+    graph-dependent inputs of estimate_all (costmodel.py:226-246, 347-376)."""
+    rows = []
+    nodes = g.nodes
+    for nid in ids:
+        n = nodes[nid]
+        feats = node_features(g, n)
+        b = n.attrs.get("bytes")
+        row = (feats, 0, 0, 0, 1.0, 0.0)
+        if n.kind == TRANSFER:
+            dev = g.devices.get(n.device)
+            if dev is not None and dev.kind == DEVICE_LINK and isinstance(b, int):
+                row = (feats, 1, _i64(b), 0, dev.throughput_mbps, dev.latency_us)
+        elif n.kind == COLLECTIVE:
+            grp = n.attrs.get("group")
+            if isinstance(grp, (list, tuple)) and isinstance(b, int):
+                row = (feats, 1, _i64(b), len(grp), 1.0, 0.0)
+        rows.append(row)
+    return rows
 
-    def __init__(self, g, ids, db, configs, device: int):
+
+class LoweredProfiles:
+    """Device tables for dfsim_estimate_batch over one graph and a list of configs.
+
+    ``variant_rows`` (optional): one ``node_rows`` list per graph variant -- graphs with
+    g's structure whose attributes / shapes differ (e.g. one per batch size); candidate i
+    then reads variant ``strat_gv[i]``.  Without it there is one variant, g itself.
+    """
+
+    def __init__(self, g, ids, db, configs, device: int, variant_rows=None, strat_gv=None):
         self.device = device
         N = len(ids)
         nodes = g.nodes
@@ -360,34 +387,33 @@ class LoweredProfiles:
                 ov_key_to_id[ov_key] = len(ov_sets)
                 ov_sets.append(resolve_overrides(cfg.overrides, ids))
             self.strat_ov.append(ov_key_to_id[ov_key])
-        # per node: op, kind, features, comm attributes
+        if variant_rows is None:
+            variant_rows = [node_rows(g, ids)]
+        GV = len(variant_rows)
+        self.n_gvariants = GV
+        self.strat_gv = list(strat_gv) if strat_gv is not None else [0] * len(configs)
+        # per node: op, kind (structural); per (variant, node): features and comm attributes
         op_ids, sig_ids = {}, {}
         op = np.empty(N, np.int32)
         kind = np.empty(N, np.uint8)
-        sig = np.empty(N, np.int32)
-        cbytes = np.zeros(N, np.int64)
-        cok = np.zeros(N, np.uint8)
-        gsize = np.zeros(N, np.int32)
-        lthr = np.ones(N, np.float64)
-        llat = np.zeros(N, np.float64)
         self.op_nodes = {}
         for i, nid in enumerate(ids):
             n = nodes[nid]
             op[i] = op_ids.setdefault(n.op_type, len(op_ids))
             self.op_nodes.setdefault(n.op_type, []).append(i)
             kind[i] = 0 if n.kind == COMPUTE else (1 if n.kind == TRANSFER else 2)
-            feats = node_features(g, n)
-            sig[i] = sig_ids.setdefault(feats, len(sig_ids))
-            b = n.attrs.get("bytes")
-            if n.kind == TRANSFER:
-                dev = g.devices.get(n.device)
-                if dev is not None and dev.kind == DEVICE_LINK and isinstance(b, int):
-                    cok[i], cbytes[i] = 1, _i64(b)
-                    lthr[i], llat[i] = dev.throughput_mbps, dev.latency_us
-            elif n.kind == COLLECTIVE:
-                grp = n.attrs.get("group")
-                if isinstance(grp, (list, tuple)) and isinstance(b, int):
-                    cok[i], cbytes[i], gsize[i] = 1, _i64(b), len(grp)
+        sig = np.empty((GV, N), np.int32)
+        cbytes = np.zeros((GV, N), np.int64)
+        cok = np.zeros((GV, N), np.uint8)
+        gsize = np.zeros((GV, N), np.int32)
+        lthr = np.ones((GV, N), np.float64)
+        llat = np.zeros((GV, N), np.float64)
+        for gv, rows in enumerate(variant_rows):
+            if len(rows) != N:
+                raise ValueError("graph variants must share the class structure")
+            for i, (feats, ok, b, gs, thr, lat) in enumerate(rows):
+                sig[gv, i] = sig_ids.setdefault(feats, len(sig_ids))
+                cok[gv, i], cbytes[gv, i], gsize[gv, i], lthr[gv, i], llat[gv, i] = ok, b, gs, thr, lat
         self.op_ids, self.sig_ids = op_ids, sig_ids
         # exact records for (hw, op, sig) triples present in the graph
         ekeys, emeans = [], []
@@ -411,7 +437,7 @@ class LoweredProfiles:
             for opname, o in op_ids.items():
                 if not db.op_records.get((opname, hw)):
                     continue
-                if not self._needs_model(h, o, opname, sig, ekeys and exact_set, ids, ov_sets, hw):
+                if not self._needs_model(h, o, opname, sig, exact_set, ids, ov_sets):
                     continue
                 m = fit_for_grid(db, opname, hw)
                 self.models[(opname, hw)] = m
@@ -467,7 +493,7 @@ class LoweredProfiles:
         ek, em = srt(ekeys, np.asarray(emeans, np.float64))
         nk, nt = srt(nkeys, np.asarray(nthr, np.float64))
         d = device
-        T = lambda a, dt: _dev_tensor(np.asarray(a, dt) if len(a) else np.zeros(1, dt), d, dt)  # noqa: E731
+        T = lambda a, dt: _dev_tensor(np.asarray(a, dt).ravel() if np.size(a) else np.zeros(1, dt), d, dt)  # noqa: E731
         self.tensors = dict(
             op=T(op, np.int32), kind=T(kind, np.uint8), sig=T(sig, np.int32), cbytes=T(cbytes, np.int64),
             cok=T(cok, np.uint8), gsize=T(gsize, np.int32), lthr=T(lthr, np.float64), llat=T(llat, np.float64),
@@ -493,21 +519,22 @@ class LoweredProfiles:
         self.n_sims = len(configs)
         self.t_strat = dict(hw=T(self.strat_hw, np.int32), gap=T(self.strat_gap, np.float64),
                             algo=T(self.strat_algo, np.uint8), path=T(self.strat_path, np.int32),
-                            ov=T(self.strat_ov, np.int32))
+                            ov=T(self.strat_ov, np.int32), gv=T(self.strat_gv, np.int32))
         s = self.t_strat
         self.strategies = native.Strategies(self.n_sims, pp(s["hw"]), pp(s["gap"]), pp(s["algo"]), pp(s["path"]),
-                                            pp(s["ov"]))
+                                            pp(s["ov"]), pp(s["gv"]))
 
-    def _needs_model(self, h, o, opname, sig, exact_set, ids, ov_sets, hw) -> bool:
+    def _needs_model(self, h, o, opname, sig, exact_set, ids, ov_sets) -> bool:
         """True if some node of this op, not overridden in every strategy, has no exact record."""
         for i in self.op_nodes.get(opname, ()):
-            key = (h << 42) | (o << 21) | int(sig[i])
-            if exact_set and key in exact_set:
-                continue
-            if self.strat_ov and all(k >= 0 and ids[i] in ov_sets[k] for k, hh in zip(self.strat_ov, self.strat_hw)
-                                     if hh == h):
-                continue
-            return True
+            for gv in range(sig.shape[0]):
+                key = (h << 42) | (o << 21) | int(sig[gv, i])
+                if key in exact_set:
+                    continue
+                if self.strat_ov and all(k >= 0 and ids[i] in ov_sets[k]
+                                         for k, hh in zip(self.strat_ov, self.strat_hw) if hh == h):
+                    continue
+                return True
         return False
 
 

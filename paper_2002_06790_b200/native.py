@@ -54,7 +54,8 @@ class ProfileTables(ctypes.Structure):
 
 
 class Strategies(ctypes.Structure):
-    _fields_ = [("n_sims", I64), ("hw", P), ("op_gap", P), ("algo", P), ("path", P), ("override_set", P)]
+    _fields_ = [("n_sims", I64), ("hw", P), ("op_gap", P), ("algo", P), ("path", P), ("override_set", P),
+                ("gvariant", P)]
 
 
 class SimTables(ctypes.Structure):
@@ -91,7 +92,7 @@ _SIGNATURES = {
     "dfsim_simulate_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P]),
     "dfsim_critical_path_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, P, P, P, P]),
     "dfsim_simulate_batch_ex": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P, P, P]),
-    "dfsim_resolve_variants": (ctypes.c_int, [P, I32, ctypes.POINTER(ProfileTables), I32, P, P, P, P, P]),
+    "dfsim_resolve_variants": (ctypes.c_int, [P, I32, ctypes.POINTER(ProfileTables), I32, P, P, P, P, P, P]),
     "dfsim_simulate_fused": (ctypes.c_int, [P, ctypes.POINTER(SimTables), ctypes.POINTER(FusedStrategies), P, P, P,
                                             P, P, P]),
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P, P]),

@@ -72,26 +72,36 @@ def expand_parameter_server(g, cfg, db, ps_device: str = "ps0") -> ExpandedGraph
         for lid in (f"link:{path}:{w}->{ps_device}", f"link:{path}:{ps_device}->{w}"):
             devices[lid] = DeviceSpec(lid, DEVICE_LINK, cfg.hardware, link.throughput_mbps, link.latency_us)
     comm_nodes = []
+    origin = {cid: ("clone", nid) for cid, (nid, _k) in replica_of.items()}
     for gid in sorted(marked):
-        grad = g.nodes[gid]
-        nbytes = grad.output_shapes[0].byte_size()
-        for k, w in enumerate(cfg.device_map):
-            pid = f"push_{gid}@r{k}"
-            nodes[pid] = OpNode(pid, PUSH_OP, f"link:{path}:{w}->{ps_device}", TRANSFER,
-                                {"src_device": w, "dst_device": ps_device, "bytes": nbytes},
-                                ((f"{gid}@r{k}", 0),), grad.output_shapes)
-            comm_nodes.append(pid)
-        aid = f"aggregate_{gid}"
-        nodes[aid] = OpNode(aid, AGGREGATE_OP, ps_device, COMPUTE,
-                            {"replicas": R, "bytes": nbytes, "mflops": round(R * nbytes / 4 / 1e6, 6)},
-                            tuple((f"push_{gid}@r{k}", 0) for k in range(R)), grad.output_shapes)
-        for k, w in enumerate(cfg.device_map):
-            qid = f"pull_{gid}@r{k}"
-            nodes[qid] = OpNode(qid, PULL_OP, f"link:{path}:{ps_device}->{w}", TRANSFER,
-                                {"src_device": ps_device, "dst_device": w, "bytes": nbytes},
-                                ((aid, 0),), grad.output_shapes)
-            comm_nodes.append(qid)
+        for node in ps_nodes(gid, g.nodes[gid], cfg, ps_device):
+            nodes[node.id] = node
+            origin[node.id] = ("ps", gid)
+            if node.kind == TRANSFER:
+                comm_nodes.append(node.id)
     meta = dict(g.metadata)
     meta.update(replicas=R, sync="parameter_server")
-    return ExpandedGraph(graph=DataflowGraph(nodes=nodes, devices=devices, metadata=meta),
-                         replica_of=replica_of, collective_nodes=comm_nodes)
+    ex = ExpandedGraph(graph=DataflowGraph(nodes=nodes, devices=devices, metadata=meta),
+                       replica_of=replica_of, collective_nodes=comm_nodes)
+    ex.origin = origin
+    return ex
+
+
+def ps_nodes(gid, grad, cfg, ps_device: str) -> list:
+    """push_<g>@r<k>, aggregate_<g>, pull_<g>@r<k> for one marked gradient (module docstring)."""
+    R, path = cfg.replicas, cfg.collective.path
+    nbytes = grad.output_shapes[0].byte_size()
+    out = []
+    for k, w in enumerate(cfg.device_map):
+        out.append(OpNode(f"push_{gid}@r{k}", PUSH_OP, f"link:{path}:{w}->{ps_device}", TRANSFER,
+                          {"src_device": w, "dst_device": ps_device, "bytes": nbytes},
+                          ((f"{gid}@r{k}", 0),), grad.output_shapes))
+    aid = f"aggregate_{gid}"
+    out.append(OpNode(aid, AGGREGATE_OP, ps_device, COMPUTE,
+                      {"replicas": R, "bytes": nbytes, "mflops": round(R * nbytes / 4 / 1e6, 6)},
+                      tuple((f"push_{gid}@r{k}", 0) for k in range(R)), grad.output_shapes))
+    for k, w in enumerate(cfg.device_map):
+        out.append(OpNode(f"pull_{gid}@r{k}", PULL_OP, f"link:{path}:{ps_device}->{w}", TRANSFER,
+                          {"src_device": ps_device, "dst_device": w, "bytes": nbytes},
+                          ((aid, 0),), grad.output_shapes))
+    return out

@@ -1,0 +1,53 @@
+"""CPU: estimate-input rows of graph variants derived by origin (variants.py) equal the rows of
+the fully materialised expanded graphs (lowering.node_rows on the oracle's expansion)."""
+
+from __future__ import annotations
+
+import warnings
+
+import pytest
+
+from oracle import dfsim_oracle as O
+from paper_2002_06790_b200 import workloads as W
+from paper_2002_06790_b200.expansion import ExpansionPlan
+from paper_2002_06790_b200.lowering import node_rows
+from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+from paper_2002_06790_b200.ps import expand_parameter_server
+from paper_2002_06790_b200.variants import rows_for, structure_key
+
+
+def _cfg(R, sync="allreduce", path="NVLink"):
+    return StrategyConfig(replicas=R, device_map=tuple(f"gpu{i}" for i in range(R)),
+                          collective=CollectiveConfig("RingAnalytic", path), gradient_markers=("wgrad_*",),
+                          hardware="hw0", sync=sync)
+
+
+@pytest.mark.parametrize("R", [2, 5])
+def test_dp_rows_match_materialised(R):
+    g0, g1 = W.vgg16_training(batch=8), W.vgg16_training(batch=48)
+    assert structure_key(g0) == structure_key(g1)
+    cfg = _cfg(R)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        plan = ExpansionPlan(g0, cfg, run_k1=False)
+    for gb in (g0, g1):
+        gx = O.expand(gb, cfg)[0]
+        assert rows_for("dp", plan.ids, gb, plan, cfg) == node_rows(gx, plan.ids)
+
+
+def test_ps_rows_match_materialised():
+    g0, g1 = W.vgg16_training(batch=8), W.vgg16_training(batch=40)
+    db = W.model_profiles(g0, ["hw0"])
+    cfg = _cfg(4, "parameter_server", "RDMA")
+    ex0 = expand_parameter_server(g0, cfg, db)
+    ids = sorted(ex0.graph.nodes)
+    for gb in (g0, g1):
+        gx = expand_parameter_server(gb, cfg, db).graph
+        assert rows_for("ps", ids, gb, ex0, cfg, db) == node_rows(gx, ids)
+
+
+def test_plain_rows_and_batch_dependence():
+    g0, g1 = W.vgg16_training(batch=8), W.vgg16_training(batch=16)
+    ids = sorted(g0.nodes)
+    r0, r1 = rows_for("plain", ids, g0, None), rows_for("plain", ids, g1, None)
+    assert r0 != r1 and [x[1:] for x in r0] == [x[1:] for x in r1]  # features differ, comm rows equal
