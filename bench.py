@@ -363,7 +363,7 @@ def run_ours(args):
         for (tc, _, _), o in zip(classes, outs):
             if tc.fused:
                 ctx.call("dfsim_simulate_fused", native.ctypes.byref(tc.tables.sim_struct),
-                         native.ctypes.byref(tc.fused_strat), native.ptr(o["start"]), native.ptr(o["finish"]),
+                         native.ctypes.byref(tc.fused_strat), native.ptr(o["sched"]),
                          native.ptr(o["makespan"]), native.ptr(o["busy"]), native.ptr(o["n_placed"]),
                          native.ptr(o["flags"]))
         b.record()

@@ -181,10 +181,11 @@ int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, c
 
 /* Exact engine with remapped outputs (the fused engine's overflow fallback):
  * row s of dur is simulated and written to output row out_rows[s] (or s when
- * NULL), node v at column pos[v] (or v when NULL). */
+ * NULL), node v at column pos[v] (or v when NULL).  interleaved != 0: start points at
+ * [rows][N] (start, finish) pairs (the fused layout) and finish is ignored. */
 int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
                             int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
-                            int32_t *n_placed, const int32_t *pos, const int64_t *out_rows);
+                            int32_t *n_placed, const int32_t *pos, const int64_t *out_rows, int32_t interleaved);
 
 /* ---------------------------------------------------------------- fused hot path (K2a + K3 v2 + K4 v2) */
 /* Class tables built once per topology class (paper_2002_06790_b200/prepare.py). */
@@ -233,11 +234,11 @@ int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_
  * must not exceed it (0: the class does not fit the fused engine). */
 int32_t dfsim_fused_capacity(const dfsim_sim_tables *g);
 
-/* K3 v2: outputs start/finish [S][N] by level position; flags[s] = 1 when the
- * FIFO ring overflowed (re-run s with dfsim_simulate_batch_ex); n_placed[s] = -1 then. */
+/* K3 v2: outputs sched[S][N][2] = (start, finish) by level position (16-byte aligned);
+ * flags[s] = 1 when the FIFO ring overflowed (re-run s with dfsim_simulate_batch_ex);
+ * n_placed[s] = -1 then. */
 int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,
-                         double *start, double *finish, double *makespan, double *busy, int32_t *n_placed,
-                         int32_t *flags);
+                         double *sched, double *makespan, double *busy, int32_t *n_placed, int32_t *flags);
 
 typedef struct {
     int32_t n_nodes;
@@ -260,13 +261,13 @@ typedef struct {
     int32_t max_spill_reads;   /* max spill values one chunk reads */
     const uint32_t *pinfo;     /* [N] by position: slot | has-slot << 15 | spill index << 16 | spill << 31 */
     int32_t slot_region;       /* doubles of suffix slots at the start of a candidate's shared region */
-    int32_t stage_doubles;     /* doubles per prefetch stage: start K | finish K | spill values R */
+    int32_t stage_doubles;     /* doubles per prefetch stage: (start, finish) x K | spill values R */
 } dfsim_cp_tables;
 
-/* K4 v2: critical-path length and its start node per candidate over start/finish
- * stored by level position. */
-int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *start,
-                               const double *finish, double *cp_len, int32_t *cp_src);
+/* K4 v2: critical-path length and its start node per candidate over the fused
+ * engine's sched[S][N][2] (start, finish) pairs stored by level position. */
+int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *sched,
+                               double *cp_len, int32_t *cp_src);
 
 /* ---------------------------------------------------------------- critical path (K4) */
 /* Over d = finish - start (reporting.py:128), or over d = finish when start is NULL

@@ -178,9 +178,9 @@ class TopologyClass:
         self.ctx.call("dfsim_estimate_batch", N, native.ctypes.byref(self.lp.struct), native.ctypes.byref(strat),
                       native.ptr(dur), native.ptr(src), native.ptr(bad))
         self.ctx.call("dfsim_simulate_batch_ex", native.ctypes.byref(self.lg.struct), len(rows), native.ptr(dur), N,
-                      native.ptr(o["start"]), native.ptr(o["finish"]), native.ptr(o["makespan"]),
+                      native.ptr(o["sched"]), native.P(0), native.ptr(o["makespan"]),
                       native.ptr(o["busy"]), native.ptr(o["n_placed"]), native.ptr(self.tables.t["pos32"]),
-                      native.ptr(idx))
+                      native.ptr(idx), 1)
         o.setdefault("fallback_rows", []).extend(int(r) for r in rows)
 
     def run_fused(self, o: dict, ev: dict, paths: bool = False, defer_fallback: bool = False):
@@ -188,9 +188,9 @@ class TopologyClass:
 
         lg, S, N, D = self.lg, self.lp.n_sims, self.lg.n, self.lg.n_devices
         dev = f"cuda:{self.ctx.device}"
-        if "start" not in o:
-            o["start"] = torch.empty((S, N), dtype=torch.float64, device=dev)
-            o["finish"] = torch.empty((S, N), dtype=torch.float64, device=dev)
+        if "sched" not in o:
+            o["sched"] = torch.empty((S, N, 2), dtype=torch.float64, device=dev)  # (start, finish) pairs
+            o["start"], o["finish"] = o["sched"][..., 0], o["sched"][..., 1]
             o["makespan"] = torch.empty(S, dtype=torch.float64, device=dev)
             o["busy"] = torch.empty((S, max(D, 1)), dtype=torch.float64, device=dev)
             o["n_placed"] = torch.empty(S, dtype=torch.int32, device=dev)
@@ -205,7 +205,7 @@ class TopologyClass:
         rec("estimate", 1)
         rec("simulate", 0)
         self.ctx.call("dfsim_simulate_fused", native.ctypes.byref(self.tables.sim_struct),
-                      native.ctypes.byref(self.fused_strat), native.ptr(o["start"]), native.ptr(o["finish"]),
+                      native.ctypes.byref(self.fused_strat), native.ptr(o["sched"]),
                       native.ptr(o["makespan"]), native.ptr(o["busy"]), native.ptr(o["n_placed"]),
                       native.ptr(o["flags"]))
         rec("simulate", 1)
@@ -213,7 +213,7 @@ class TopologyClass:
             self.fallback_if_needed(o)
         rec("critical_path", 0)
         self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.tables.cp_struct), S,
-                      native.ptr(o["start"]), native.ptr(o["finish"]), native.ptr(o["cp_len"]), native.ptr(o["cp_src"]))
+                      native.ptr(o["sched"]), native.ptr(o["cp_len"]), native.ptr(o["cp_src"]))
         rec("critical_path", 1)
         return o
 
@@ -250,7 +250,7 @@ class TopologyClass:
             rec("critical_path", 1)
             o["layout"] = "rank"
         if not schedules:
-            for k in ("start", "finish", "dur"):
+            for k in ("start", "finish", "sched", "dur"):
                 o.pop(k, None)
         return o
 
@@ -269,8 +269,7 @@ class TopologyClass:
         """Re-run K4 on the current schedules (after a deferred fallback)."""
         if self.fused:
             self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.tables.cp_struct), self.lp.n_sims,
-                          native.ptr(o["start"]), native.ptr(o["finish"]), native.ptr(o["cp_len"]),
-                          native.ptr(o["cp_src"]))
+                          native.ptr(o["sched"]), native.ptr(o["cp_len"]), native.ptr(o["cp_src"]))
         elif self.lg.acyclic and self.lg.n:
             critical_path_arrays(self.lg, o["start"], o["finish"], out=o)
 
@@ -377,7 +376,7 @@ def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, kee
         for row in np.nonzero((bad > 0) | (placed != tc.lg.n))[0].tolist():
             failures.append((idx[row], tc, o, row))
         if not keep_schedules:
-            for k in ("start", "finish"):
+            for k in ("start", "finish", "sched"):
                 o.pop(k, None)
         result.classes.append((tc, idx, o))
         for row, i in enumerate(idx):

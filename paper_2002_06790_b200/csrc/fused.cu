@@ -27,7 +27,7 @@ namespace {
 struct FusedArgs {
     dfsim_sim_tables g;
     dfsim_fused_strategies st;
-    double *start, *finish, *makespan, *busy;
+    double *sched, *makespan, *busy;  // sched[s][pos] = (start, finish) pairs
     int32_t *n_placed, *flags;
     int32_t *chunk_counter;
     int32_t wpb;
@@ -145,8 +145,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             const int64_t s = active ? __ldg(a.st.order + __ldg(a.st.chunk_first + c) + gid) : 0;
             const double gap = active ? __ldg(a.st.op_gap + s) : 0.0;
             const int ovs = (active && a.st.override_set) ? __ldg(a.st.override_set + s) : -1;
-            double *out_s = a.start + s * N;
-            double *out_f = a.finish + s * N;
+            double2 *out = reinterpret_cast<double2 *>(a.sched) + s * N;
             if (active) {
                 for (int w = ll; w < a.g.n_counter_words; w += kGS) cnt[w] = __ldg(a.g.cnt_init + w);
                 if (ll < D) tails[ll] = 0;
@@ -191,9 +190,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                         if (lo < end && __ldg(a.st.ov_node + lo) == v) dur = __ldg(a.st.ov_val + lo);
                     }
                     const double f = __dadd_rn(now, dur);
-                    const int p = s_pos[v];
-                    out_s[p] = now;
-                    out_f[p] = f;
+                    out[s_pos[v]] = make_double2(now, f);
                     running = true;
                     run_v = v;
                     run_f = f;
@@ -278,10 +275,15 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
 
 // ------------------------------------------------------------------ K4 v2
 
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
 struct CpLevelArgs {
     dfsim_cp_tables t;
     int64_t S;
-    const double *start, *finish;
+    const double *sched;  // [S][N] (start, finish) pairs by level position
     double *cp_len;
     int32_t *cp_src;
     double *spill;        // [grid * wpb * 2][n_long] rows, one per resident candidate slot
@@ -337,15 +339,11 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
         const int64_t s = base + half;
         const bool live = s < a.S;
         const int64_t sr = live ? s : base;  // the idle half shadows its partner's reads
-        const double *st = a.start + sr * N;
-        const double *fi = a.finish + sr * N;
+        const double *row = a.sched + 2 * sr * N;
         auto prefetch = [&](int c) {
             const int p0 = s_goff[s_coff[c]], p1 = s_goff[s_coff[c + 1]];
             double *bs = region + SR + (c & 1) * SD;
-            for (int p = p0 + ll; p < p1; p += 16) {
-                cp_async8(bs + (p - p0), st + p);
-                cp_async8(bs + K + (p - p0), fi + p);
-            }
+            for (int p = p0 + ll; p < p1; p += 16) cp_async16(bs + 2 * (p - p0), row + 2 * p);
             const int r0 = s_soff[c], r1 = s_soff[c + 1];
             for (int r = r0 + ll; r < r1; r += 16) cp_async8(bs + 2 * K + (r - r0), spill_row + s_slist[r]);
             asm volatile("cp.async.commit_group;\n" ::);
@@ -376,7 +374,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                         const double x = region[s_succ[j]];
                         best = x > best ? x : best;
                     }
-                    const double d = __dsub_rn(bs[K + (p - p0)], bs[p - p0]);  // finish - start (reporting.py:128)
+                    const double d = __dsub_rn(bs[2 * (p - p0) + 1], bs[2 * (p - p0)]);  // finish - start (reporting.py:128)
                     const double sv = __dadd_rn(d, best);
                     const uint32_t info = s_info[p];
                     if (info & 0x8000u) region[info & 0x7fffu] = sv;
@@ -445,10 +443,11 @@ extern "C" int32_t dfsim_fused_capacity(const dfsim_sim_tables *g) {
 }
 
 extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,
-                                    double *start, double *finish, double *makespan, double *busy, int32_t *n_placed,
+                                    double *sched, double *makespan, double *busy, int32_t *n_placed,
                                     int32_t *flags) {
     if (!ctx || !g || !st) return DFSIM_BAD_ARGUMENT;
-    DFSIM_ARG_CHECK(ctx, start && finish && makespan && n_placed && flags, "outputs are required");
+    DFSIM_ARG_CHECK(ctx, sched && makespan && n_placed && flags, "outputs are required");
+    DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
     DFSIM_ARG_CHECK(ctx, g->n_nodes > 0 && g->n_nodes <= 65535 && g->n_devices <= 32, "fused engine limits");
     DFSIM_ARG_CHECK(ctx, g->qcap >= 2 && (g->qcap & (g->qcap - 1)) == 0, "qcap must be a power of two");
     DFSIM_ARG_CHECK(ctx, g->counter_bits == 4 || g->counter_bits == 8 || g->counter_bits == 16, "counter_bits 4, 8 or 16");
@@ -462,7 +461,7 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     FusedArgs a;
     a.g = *g;
     a.st = *st;
-    a.start = start; a.finish = finish; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed; a.flags = flags;
+    a.sched = sched; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed; a.flags = flags;
     a.wpb = wpb;
     a.smem_graph = (int)graph_bytes;
     a.smem_warp = (int)warp_bytes;
@@ -491,10 +490,11 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     return dfsim_after_launch(ctx, "k_simulate_fused");
 }
 
-extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *start,
-                                          const double *finish, double *cp_len, int32_t *cp_src) {
+extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *sched,
+                                          double *cp_len, int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
-    DFSIM_ARG_CHECK(ctx, start && finish && cp_len, "start, finish and cp_len are required");
+    DFSIM_ARG_CHECK(ctx, sched && cp_len, "sched and cp_len are required");
+    DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
     DFSIM_ARG_CHECK(ctx, t->chunk_positions >= 16, "chunk_positions >= 16");
     DFSIM_ARG_CHECK(ctx, t->n_nodes <= 65535 && t->n_edges <= 65535 && t->n_slots < 0x7fff &&
                          t->max_spill_reads < 0x7fff && t->slot_region + 2 * t->stage_doubles < 65536,
@@ -519,7 +519,7 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     CpLevelArgs a;
     a.t = *t;
     a.S = n_sims;
-    a.start = start; a.finish = finish; a.cp_len = cp_len; a.cp_src = cp_src;
+    a.sched = sched; a.cp_len = cp_len; a.cp_src = cp_src;
     a.spill = static_cast<double *>(p);
     a.wpb = wpb;
     a.table_bytes = (int)table_bytes;

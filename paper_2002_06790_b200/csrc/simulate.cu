@@ -38,6 +38,7 @@ struct SimArgs {
     int32_t cnt_words;        // u32 words of packed counters
     const int32_t *pos;       // optional output column per node
     const int64_t *out_rows;  // optional output row per simulated row
+    int32_t interleaved;      // start points at (start, finish) pairs; finish unused
 };
 
 template <int kBits>
@@ -107,8 +108,9 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * wpb + wib; s < a.S; s += static_cast<int64_t>(gridDim.x) * wpb) {
         const double *dur = a.dur + s * a.dur_stride;
         const int64_t row = a.out_rows ? a.out_rows[s] : s;
-        double *out_start = a.start ? a.start + row * N : nullptr;
-        double *out_finish = a.finish ? a.finish + row * N : nullptr;
+        double *out_start = a.start ? a.start + row * N * (a.interleaved ? 2 : 1) : nullptr;
+        double *out_finish = a.interleaved ? (out_start ? out_start + 1 : nullptr) : (a.finish ? a.finish + row * N : nullptr);
+        const int ostride = a.interleaved ? 2 : 1;
 
         Counter<kBits>::init(cnt, a.cnt_words, a.indeg, N, lane);
         if (lane < D) tails[lane] = my_qoff;
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
                 const int v = q[head++];
                 const double f = __dadd_rn(now, __ldg(dur + v));
                 if (out_start) {
-                    const int col = a.pos ? __ldg(a.pos + v) : v;
+                    const int col = (a.pos ? __ldg(a.pos + v) : v) * ostride;
                     out_start[col] = now;
                     out_finish[col] = f;
                 }
@@ -218,17 +220,18 @@ extern "C" int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_
                                     int64_t dur_stride, double *start, double *finish, double *makespan,
                                     double *busy, int32_t *n_placed) {
     return dfsim_simulate_batch_ex(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed, nullptr,
-                                   nullptr);
+                                   nullptr, 0);
 }
 
 extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
                                        int64_t dur_stride, double *start, double *finish, double *makespan,
-                                       double *busy, int32_t *n_placed, const int32_t *pos, const int64_t *out_rows) {
+                                       double *busy, int32_t *n_placed, const int32_t *pos, const int64_t *out_rows,
+                                       int32_t interleaved) {
     if (!ctx || !g) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, g->n_nodes >= 0 && n_sims >= 0, "negative sizes");
     DFSIM_ARG_CHECK(ctx, g->n_devices >= 0 && g->n_devices <= 32, "the warp engine supports at most 32 devices");
     DFSIM_ARG_CHECK(ctx, makespan != nullptr, "makespan output is required");
-    DFSIM_ARG_CHECK(ctx, (start == nullptr) == (finish == nullptr), "start and finish go together");
+    DFSIM_ARG_CHECK(ctx, interleaved || (start == nullptr) == (finish == nullptr), "start and finish go together");
     DFSIM_ARG_CHECK(ctx, dur_stride == 0 || dur_stride >= g->n_nodes, "dur_stride < n_nodes");
     if (n_sims == 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
@@ -243,7 +246,7 @@ extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int
     a.sources = g->sources; a.queue_off = g->queue_off; a.n_sources = g->n_sources;
     a.S = n_sims; a.dur = dur; a.dur_stride = dur_stride;
     a.start = start; a.finish = finish; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed;
-    a.pos = pos; a.out_rows = out_rows;
+    a.pos = pos; a.out_rows = out_rows; a.interleaved = interleaved;
     const int per = 32 / bits;
     a.cnt_words = (N + per - 1) / per;
     const bool q16 = N <= 65536;
