@@ -205,6 +205,8 @@ typedef struct {
     int32_t n_sources;
     int32_t qcap;              /* per-device FIFO ring capacity (power of two); overflow flags the candidate */
     const int32_t *device;     /* [N] device rank */
+    int32_t succ_packed;       /* 1: succ[j] = consumer (13 bits) | device << 13 | single << 18 | counter
+                                  slot << 19 (N <= 8192, cidx unused); 0: the layout above */
 } dfsim_sim_tables;
 
 typedef struct {

@@ -95,7 +95,9 @@ __device__ __forceinline__ bool counter_dec(unsigned *words, int c) {
 
 constexpr int kWide = 4;  // out-degree above which a finished node's successors are spread over the group
 
-template <int kBits, int kGS>
+// Successor entry formats: kPacked (N <= 8192): consumer (13 bits) | device << 13 | single << 18 |
+// counter slot << 19; otherwise consumer (16) | device << 16 | single << 21 with cidx[] in smem.
+template <int kBits, int kGS, bool kPacked>
 __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kPerWarp = 32 / kGS;
@@ -175,7 +177,11 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             int run_v = 0;
             double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
             auto start_idle = [&]() {
-                if (owner && !running && static_cast<int>(head) < tails[ll]) {
+                const int t = owner ? tails[ll] : 0;
+                if (owner && !running && static_cast<int>(head) < t) {
+                    // a busy device only gains entries until its next pop, so checking the
+                    // occupancy before every pop catches every ring overflow
+                    ovf |= static_cast<unsigned>(t) - head > static_cast<unsigned>(QCAP);
                     const int v = q[ll * QSTRIDE + (head & QMASK)];
                     head++;
                     const double b = s_base[v];
@@ -215,9 +221,10 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 }
                 auto relax = [&](int j) {
                     const uint32_t e = s_succ[j];
-                    const int m = static_cast<int>(e & 0xffffu);
-                    if ((e >> 21) & 1u || counter_dec<kBits>(cnt, s_cidx[m])) {
-                        const int dv = static_cast<int>((e >> 16) & 31u);
+                    const int m = static_cast<int>(kPacked ? e & 0x1fffu : e & 0xffffu);
+                    const bool single = kPacked ? (e >> 18) & 1u : (e >> 21) & 1u;
+                    if (single || counter_dec<kBits>(cnt, kPacked ? static_cast<int>(e >> 19) : s_cidx[m])) {
+                        const int dv = static_cast<int>(kPacked ? (e >> 13) & 31u : (e >> 16) & 31u);
                         const int p = atomicAdd(tails + dv, 1);
                         q[dv * QSTRIDE + (p & QMASK)] = static_cast<uint16_t>(m);
                     }
@@ -242,7 +249,6 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 const int seg_hi = ll < D ? tails[ll] : 0;
                 // a ring overflow corrupts only this candidate; it keeps running (every
                 // iteration consumes a finish event, so it terminates) and is re-run exactly
-                ovf |= ll < D && static_cast<unsigned>(seg_hi) - head > static_cast<unsigned>(QCAP);
                 // enqueue(sorted(newly_ready)): sort each device's new ring segment by rank
                 if (seg_hi - seg_lo > 1) {
                     uint16_t *qd = q + ll * QSTRIDE;
@@ -473,11 +479,15 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(a.chunk_counter, 0, sizeof(int32_t), ctx->stream));
     const size_t smem = f.smem;
     const int grid = ctx->num_sms < st->n_chunks ? ctx->num_sms : (int)st->n_chunks;
-#define DFSIM_LAUNCH_FUSED(BITS, GS)                                                                            \
+#define DFSIM_LAUNCH_FUSED_P(BITS, GS, PK)                                                                      \
     do {                                                                                                       \
-        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<BITS, GS>,                                   \
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<BITS, GS, PK>,                               \
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
-        k_simulate_fused<BITS, GS><<<grid, wpb * 32, smem, ctx->stream>>>(a);                                  \
+        k_simulate_fused<BITS, GS, PK><<<grid, wpb * 32, smem, ctx->stream>>>(a);                              \
+    } while (0)
+#define DFSIM_LAUNCH_FUSED(BITS, GS)                                                                           \
+    do {                                                                                                       \
+        if (g->succ_packed) DFSIM_LAUNCH_FUSED_P(BITS, GS, true); else DFSIM_LAUNCH_FUSED_P(BITS, GS, false);   \
     } while (0)
     if (g->counter_bits == 4) {
         if (gs == 16) DFSIM_LAUNCH_FUSED(4, 16); else DFSIM_LAUNCH_FUSED(4, 32);
@@ -487,6 +497,7 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
         if (gs == 16) DFSIM_LAUNCH_FUSED(16, 16); else DFSIM_LAUNCH_FUSED(16, 32);
     }
 #undef DFSIM_LAUNCH_FUSED
+#undef DFSIM_LAUNCH_FUSED_P
     return dfsim_after_launch(ctx, "k_simulate_fused");
 }
 

@@ -102,7 +102,11 @@ class Tables:
             packed |= init[:, i] << np.uint64(i * bits)
         self.counter_bits, self.counter_words = bits, words
         self.meta = (off[:-1] & 0xFFFFFF) | (np.minimum(outdeg, 255) << 24)
-        self.succ = idx | (dev[idx] << 16) | (single[idx].astype(np.int64) << 21)
+        self.succ_packed = N <= 8192 and multi.size <= 8192
+        if self.succ_packed:  # consumer | device << 13 | single << 18 | counter slot << 19
+            self.succ = idx | (dev[idx] << 13) | (single[idx].astype(np.int64) << 18) | (cidx[idx] << 19)
+        else:
+            self.succ = idx | (dev[idx] << 16) | (single[idx].astype(np.int64) << 21)
         self.cidx, self.cnt_init = cidx, packed
 
     def _critical_path(self, N, idx, indeg, outdeg, order, pos, loff):
@@ -214,7 +218,7 @@ class ClassTables(Tables):
         self.sim_struct = native.SimTables(lg.n, lg.n_devices, self.n_edges, p(t["meta"]), p(lg.t_succ_off),
                                            p(t["succ"]), p(t["cidx"]), p(t["cnt_init"]), self.counter_words,
                                            self.counter_bits, p(t["pos"]), p(lg.t_sources), lg.n_sources, self.QCAP,
-                                           p(lg.t_dev))
+                                           p(lg.t_dev), int(self.succ_packed))
         self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
                                          p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
                                          self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long, p(t["cp_spill"]),
