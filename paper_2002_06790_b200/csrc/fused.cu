@@ -317,17 +317,13 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
     const int N = a.t.n_nodes, K = a.t.chunk_positions, G = a.t.n_groups, E = a.t.n_edges;
     const int NC = a.t.n_chunks, SD = a.t.stage_doubles, SR = a.t.slot_region;
     const int NS = __ldg(a.t.spill_off + NC);
-    uint32_t *s_info = reinterpret_cast<uint32_t *>(smem);
-    uint32_t *s_meta = s_info + N;
-    uint16_t *s_succ = reinterpret_cast<uint16_t *>(s_meta + N);
+    uint2 *s_pm = reinterpret_cast<uint2 *>(smem);  // per position: (cp_meta, pinfo)
+    uint16_t *s_succ = reinterpret_cast<uint16_t *>(s_pm + N);
     uint16_t *s_goff = s_succ + E;
     uint16_t *s_coff = s_goff + (G + 1);
     uint16_t *s_soff = s_coff + (NC + 1);
     uint16_t *s_slist = s_soff + (NC + 1);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        s_info[i] = __ldg(a.t.pinfo + i);
-        s_meta[i] = __ldg(a.t.cp_meta + i);
-    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_pm[i] = make_uint2(__ldg(a.t.cp_meta + i), __ldg(a.t.pinfo + i));
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.t.cp_succ_slot + i);
     for (int i = threadIdx.x; i <= G; i += blockDim.x) s_goff[i] = static_cast<uint16_t>(__ldg(a.t.group_off + i));
     for (int i = threadIdx.x; i <= NC; i += blockDim.x) {
@@ -367,22 +363,24 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                 asm volatile("cp.async.wait_group 0;\n" ::);
             }
             __syncwarp();
-            const double *bs = region + SR + (c & 1) * SD;
+            const double2 *bs = reinterpret_cast<const double2 *>(region + SR + (c & 1) * SD);
             const int g0 = s_coff[c], g1 = s_coff[c + 1];
             const int p0 = s_goff[g0];
+            int q1 = s_goff[g1];  // groups are contiguous: group gi ends where gi+1 began
             for (int gi = g1 - 1; gi >= g0; gi--) {
-                const int p = s_goff[gi] + ll;
-                if (p < s_goff[gi + 1]) {
-                    const uint32_t m = s_meta[p];
+                const int q0 = s_goff[gi];
+                const int p = q0 + ll;
+                if (p < q1) {
+                    const uint2 pm = s_pm[p];
+                    const uint32_t m = pm.x, info = pm.y;
                     const int j0 = static_cast<int>(m & 0xffffu), j1 = j0 + static_cast<int>((m >> 16) & 0xffu);
                     double best = 0.0;  // max(0.0, .) (graph.py:465-468)
                     for (int j = j0; j < j1; j++) {
                         const double x = region[s_succ[j]];
                         best = x > best ? x : best;
                     }
-                    const double d = __dsub_rn(bs[2 * (p - p0) + 1], bs[2 * (p - p0)]);  // finish - start (reporting.py:128)
-                    const double sv = __dadd_rn(d, best);
-                    const uint32_t info = s_info[p];
+                    const double2 sf = bs[p - p0];
+                    const double sv = __dadd_rn(__dsub_rn(sf.y, sf.x), best);  // finish - start (reporting.py:128)
                     if (info & 0x8000u) region[info & 0x7fffu] = sv;
                     if (live && (info >> 31)) spill_row[(info >> 16) & 0x7fffu] = sv;
                     if ((m >> 24) & 1u) {
@@ -393,6 +391,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                         }
                     }
                 }
+                q1 = q0;
                 __syncwarp();
             }
         }
@@ -517,6 +516,7 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     const size_t n_spill_reads = 0;  // staged list length is read on the device; bound it by E
     const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 +
                                 (size_t)(t->n_chunks + 1) * 4 + (size_t)t->n_edges * 2 + n_spill_reads + 15) / 16 * 16;
+    // layout: (cp_meta, pinfo) pairs 8N | succ 2E | group_off 2(G+1) | chunk/spill offsets 4(NC+1) | spill list <= 2E
     const size_t per_warp = 2 * ((size_t)t->slot_region + 2 * (size_t)t->stage_doubles) * 8;  // two candidates
     const size_t budget = 227 * 1024 - 64;
     int wpb = 32;
