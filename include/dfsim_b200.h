@@ -92,6 +92,7 @@ typedef struct {
     const int32_t *base_dev;   /* [N0] expanded-device rank for non-remapped clones */
     const uint8_t *remap;      /* [N0] 1 if the clone moves to device_map[k] (Compute + device_map) */
     const int32_t *marked;     /* [N0] collective index g (0..G-1) if the node is a marked gradient, else -1 */
+    int32_t n_refs;            /* in_off[N0] if known on the host, else -1 (read back, synchronising) */
 } dfsim_base_graph;
 
 typedef struct {
@@ -105,7 +106,8 @@ typedef struct {
 
 /* Emits the expanded graph's CSR (succ_off/succ_idx), indeg, device, sources, queue_off
  * and topo into the caller-allocated arrays of *out (sizes: N=R*N0+G, E given by
- * *n_edges_host after the call).  Synchronous (it returns E and the source count). */
+ * *n_edges_host after the call).  Synchronous when the three *_host count pointers are
+ * given; with all three NULL (and base->n_refs >= 0) it is fully asynchronous. */
 int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, const dfsim_expand_plan *plan,
                     int32_t *succ_off, int32_t *succ_idx, int64_t succ_capacity, int32_t *indeg,
                     int32_t *device, int32_t *sources, int32_t *queue_off, int32_t *topo,

@@ -106,20 +106,23 @@ extern "C" int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, con
                                int32_t *device, int32_t *sources, int32_t *queue_off, int32_t *topo,
                                int32_t n_devices, int64_t *n_edges_host, int32_t *n_sources_host,
                                int32_t *n_ordered_host) {
-    if (!ctx || !base || !plan || !n_edges_host || !n_sources_host || !n_ordered_host) return DFSIM_BAD_ARGUMENT;
+    if (!ctx || !base || !plan) return DFSIM_BAD_ARGUMENT;
+    DFSIM_ARG_CHECK(ctx, (n_edges_host == nullptr) == (n_sources_host == nullptr) &&
+                         (n_edges_host == nullptr) == (n_ordered_host == nullptr), "count outputs go together");
     DFSIM_ARG_CHECK(ctx, plan->replicas >= 1 && base->n_base >= 0, "bad replicas / base size");
     DFSIM_ARG_CHECK(ctx, plan->replicas > 1 || plan->n_collectives == 0, "collectives need replicas > 1");
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const int32_t R = plan->replicas, N0 = base->n_base, G = plan->n_collectives;
     const int64_t N = (int64_t)R * N0 + G;
     DFSIM_ARG_CHECK(ctx, N < (1ll << 31), "expanded graph too large");
-    // number of base refs (host copy of in_off[N0])
-    int32_t n_refs32 = 0;
-    if (N0 > 0) {
+    // number of base refs: given by the caller, or read back from in_off[N0]
+    int32_t n_refs32 = base->n_refs;
+    if (n_refs32 < 0 && N0 > 0) {
         DFSIM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_small, base->in_off + N0, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
         DFSIM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
         n_refs32 = *static_cast<int32_t *>(ctx->host_small);
     }
+    if (n_refs32 < 0) n_refs32 = 0;
     const int64_t n_refs = n_refs32;
     const int64_t n_keys = (int64_t)R * n_refs + (int64_t)G * R;
     DFSIM_ARG_CHECK(ctx, succ_capacity >= n_keys, "succ_capacity below R*refs + G*R");
@@ -186,6 +189,7 @@ extern "C" int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, con
         if ((rc = dfsim_topo_launch(ctx, (int32_t)N, succ_off, succ_idx, indeg, topo,
                                     reinterpret_cast<int32_t *>(small + 2), left))) return rc;
     }
+    if (!n_edges_host) return DFSIM_OK;  // asynchronous re-expansion: counts are not read back
     DFSIM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_small, small, 32, cudaMemcpyDeviceToHost, ctx->stream));
     DFSIM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     const unsigned long long *h = static_cast<const unsigned long long *>(ctx->host_small);

@@ -124,7 +124,7 @@ class ExpansionPlan:
                       T([drank[x] for x in dmap] if dmap else [0], np.int32)]
         k = self._keep
         base = native.BaseGraph(N0, native.ptr(k[0]), native.ptr(k[1]), native.ptr(k[2]), native.ptr(k[3]),
-                                native.ptr(k[4]))
+                                native.ptr(k[4]), len(in_src))
         plan = native.ExpandPlan(R, self.G, native.ptr(k[5]), native.ptr(k[6]), native.ptr(k[7]),
                                  drank.get(fabric, 0))
         self._structs = (base, plan, len(in_src))
@@ -162,21 +162,29 @@ class ExpansionPlan:
         if findings:
             raise DfsimError("internal: expansion produced an invalid graph: " + "; ".join(findings[:5]))
 
-    def reexpand(self, topo: bool = True) -> None:
+    def reexpand(self, topo: bool = True, check: bool = False) -> None:
         """Run K1 again into the same device arrays (timed per-class device work).
 
-        ``topo=False`` skips the Kahn order (the fused path uses the class level order)."""
+        ``topo=False`` skips the Kahn order (the fused path uses the class level order);
+        ``check=True`` reads the counts back (synchronising) and compares them."""
         base, plan, n_refs = self._structs
         lg = self.lowered
         N, D = len(self.ids), len(self.devices)
         cap = self.R * n_refs + self.G * self.R
-        n_edges, n_src, n_ord = native.I64(0), native.I32(0), native.I32(0)
         by = native.ctypes.byref
+        P0 = native.P(0)
+        if not check:
+            self.ctx.call("dfsim_expand_dp", by(base), by(plan), native.ptr(lg.t_succ_off), native.ptr(lg.t_succ_idx),
+                          cap, native.ptr(lg.t_indeg), native.ptr(lg.t_dev), native.ptr(lg.t_sources),
+                          native.ptr(lg.t_queue_off), native.ptr(lg.t_topo) if topo else P0, D, None, None, None)
+            return
+        n_edges, n_src, n_ord = native.I64(0), native.I32(0), native.I32(0)
         self.ctx.call("dfsim_expand_dp", by(base), by(plan), native.ptr(lg.t_succ_off), native.ptr(lg.t_succ_idx),
                       cap, native.ptr(lg.t_indeg), native.ptr(lg.t_dev), native.ptr(lg.t_sources),
-                      native.ptr(lg.t_queue_off), native.ptr(lg.t_topo) if topo else native.P(0), D, by(n_edges),
+                      native.ptr(lg.t_queue_off), native.ptr(lg.t_topo) if topo else P0, D, by(n_edges),
                       by(n_src), by(n_ord))
-        if (int(n_edges.value), int(n_src.value), int(n_ord.value)) != (lg.n_edges, lg.n_sources, lg.n_ordered):
+        if (int(n_edges.value), int(n_src.value), int(n_ord.value)) != (lg.n_edges, lg.n_sources,
+                                                                         lg.n_ordered if topo else lg.n):
             raise DfsimError("internal: re-expansion disagrees with the first expansion")
 
     def _run_k1(self, ctx, base, plan, n_refs) -> LoweredGraph:

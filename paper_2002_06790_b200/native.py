@@ -33,7 +33,8 @@ class Graph(ctypes.Structure):
 
 
 class BaseGraph(ctypes.Structure):
-    _fields_ = [("n_base", I32), ("in_off", P), ("in_src", P), ("base_dev", P), ("remap", P), ("marked", P)]
+    _fields_ = [("n_base", I32), ("in_off", P), ("in_src", P), ("base_dev", P), ("remap", P), ("marked", P),
+                ("n_refs", I32)]
 
 
 class ExpandPlan(ctypes.Structure):

@@ -69,6 +69,51 @@ def test_fused_equals_unfused_resnet_dp8(resnet):
     assert (src >= 0).all()
 
 
+def test_reexpand_async_reproduces_first_expansion(resnet):
+    """K1 re-run without host round-trips (n_refs given, no count read-back) rewrites
+    the same CSR; the synchronising variant (n_refs = -1, counts read back) agrees."""
+    import torch
+
+    from paper_2002_06790_b200.batch import TopologyClass
+
+    g, db = resnet
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        tu = TopologyClass(g, db, _configs(8), fused=False)
+    lg, plan = tu.lg, tu.plan
+    names = ("t_succ_off", "t_succ_idx", "t_indeg", "t_dev", "t_sources", "t_queue_off")
+    used = dict(t_succ_idx=lg.n_edges, t_sources=lg.n_sources)
+
+    def view(k):
+        t = getattr(lg, k)
+        return t[: used[k]] if k in used else t
+
+    before = {k: view(k).clone() for k in names}
+    for k in names:
+        getattr(lg, k).fill_(-7)
+    plan.reexpand(topo=True)
+    torch.cuda.synchronize()
+    for k in names:
+        assert torch.equal(view(k), before[k]), k
+    _assert_topological(lg)
+    plan._structs[0].n_refs = -1
+    plan.reexpand(topo=True, check=True)
+    for k in names:
+        assert torch.equal(view(k), before[k]), k
+    _assert_topological(lg)
+
+
+def _assert_topological(lg):
+    """The Kahn order may differ run to run (frontier order); it must be a topological order."""
+    topo = lg.t_topo[: lg.n].cpu().numpy()
+    off, idx = lg.t_succ_off.cpu().numpy(), lg.t_succ_idx[: lg.n_edges].cpu().numpy()
+    pos = np.full(lg.n, -1)
+    pos[topo] = np.arange(lg.n)
+    assert (pos >= 0).all()
+    src = np.repeat(np.arange(lg.n), np.diff(off[: lg.n + 1]))
+    assert (pos[src] < pos[idx]).all()
+
+
 def test_fused_ring_overflow_falls_back_exactly(resnet, monkeypatch):
     from paper_2002_06790_b200.batch import TopologyClass
     from paper_2002_06790_b200.prepare import ClassTables
