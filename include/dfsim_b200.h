@@ -14,6 +14,8 @@
  *   dfsim_critical_path_batch graph.py:446-485    critical_path on finish-start (reporting.py:128)
  *   dfsim_argmin             (no reference function: cmd_simulate's per-config makespans,
  *                            cli.py:133-148, reduced to the first minimum)
+ *   dfsim_summarize          reporting.py:117-162 summarize (op shares, busy folds, overlap)
+ *   dfsim_trace_write        reporting.py:43-74   to_trace (host-side writer, byte-identical)
  *
  * Conventions
  *  - Every pointer in a *view* struct or argument is a DEVICE pointer owned by
@@ -286,6 +288,48 @@ int dfsim_critical_path_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_si
 int dfsim_argmin(dfsim_ctx *ctx, int64_t n, const double *values, int64_t index_base, void *out_record);
 /* Lexicographic min over n gathered records (e.g. after an NCCL all-gather). */
 int dfsim_argmin_records(dfsim_ctx *ctx, int64_t n, const void *records, void *out_record);
+
+/* ---------------------------------------------------------------- schedule summary (K6) */
+/* reporting.summarize (reporting.py:117-162) for a batch of schedules resident on the
+ * device.  Class-wide tables, indexed by node rank: */
+typedef struct {
+    int32_t n_nodes;
+    int32_t n_keys;              /* distinct op keys (`op_type or node_id`, reporting.py:132) */
+    const int32_t *base_order;   /* [N] node ranks sorted by (device string rank, node rank) */
+    const int32_t *key;          /* [N] op key index of each node (0..n_keys-1) */
+    const uint8_t *comm;         /* [N] 1 when the node's device is not Compute (reporting.py:140) */
+} dfsim_summary_tables;
+
+/* start/finish: [n_rows][ld] by node rank.  entry_order [n_rows][N]: the schedule's entry
+ * order (engine.py:88), written unless order_given (then read, e.g. a drop-in Schedule).
+ * Outputs: key_total/key_first [n_rows][n_keys] (per-key total folded in entry order;
+ * entry index of the key's first appearance or -1), sums [n_rows][3] = compute_us,
+ * comm_us, overlap_us.  Asynchronous on the ctx stream. */
+int dfsim_summarize(dfsim_ctx *ctx, const dfsim_summary_tables *t, int64_t n_rows, const double *start,
+                    const double *finish, int64_t ld, int32_t *entry_order, int32_t order_given,
+                    double *key_total, int32_t *key_first, double *sums);
+
+/* ---------------------------------------------------------------- Chrome trace (host) */
+/* reporting.to_trace (reporting.py:43-74), byte-identical: json.dumps(events, indent=1)
+ * with ensure_ascii escaping and round-half-even integer ts/dur.  Host memory only. */
+typedef struct {
+    int32_t n_nodes;
+    int32_t n_tracks;             /* devices of the schedule's busy dict, sorted (tid order) */
+    const char *id_blob;          /* node ids, UTF-8: node v = id_blob[id_off[v] .. id_off[v+1]) */
+    const int64_t *id_off;        /* [N+1] */
+    const char *name_blob;        /* event names (`op_type or node_id`) */
+    const int64_t *name_off;      /* [N+1] */
+    const uint8_t *tag;           /* [N] duration source tag index */
+    const char *const *tag_name;  /* tag strings (NUL-terminated) */
+    const int32_t *track;         /* [N] tid of the node's device (n_tracks when absent) */
+    const char *const *track_name;/* [n_tracks] NUL-terminated UTF-8 */
+} dfsim_trace_tables;
+
+/* Writes the document for entries entry_node[0..n_entries) (node indices in entry order)
+ * with start/finish indexed by node.  Returns the document length in bytes; the text is
+ * copied to buf only when it fits in cap (call with cap = 0 to size it).  < 0 on bad args. */
+int64_t dfsim_trace_write(const dfsim_trace_tables *t, int64_t n_entries, const int32_t *entry_node,
+                          const double *start, const double *finish, char *buf, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,9 @@ duck-typed containers, the reference algorithms of arXiv 2002.06790's ``dfsim``:
                      comm formulas 168-223, features 226-246
 * ``simulate``    -- engine.py:96-146 and _finalize 69-93
 * ``critical_path`` -- graph.py:424-485 (Kahn + suffix DP + min-id walk)
+* ``summarize``   -- reporting.py:117-162 (op shares, compute/comm busy, interval
+                     overlap 92-114, critical path on finish - start)
+* ``to_trace``    -- reporting.py:43-74 (Chrome trace JSON, indent 1)
 
 Pinning: ``tests/test_oracle.py`` checks every function here against the golden
 fixtures in ``tests/golden/`` that ``tests/golden/make_golden.py`` produced by
@@ -386,3 +389,106 @@ def run_candidate(g, db, cfg):
     entries, makespan, busy = simulate(g, durs)
     cp = critical_path(g, {nid: f - s for nid, _, s, f in entries})
     return makespan, cp[0], entries, busy, cp[1]
+
+
+# ----------------------------------------------------------------------------- reporting
+
+
+def _union(spans):
+    """Union components of closed intervals, in start order (reporting.py:92-99)."""
+    comps = []
+    for lo, hi in sorted(spans):
+        if comps and lo <= comps[-1][1]:
+            if hi > comps[-1][1]:
+                comps[-1][1] = hi
+        else:
+            comps.append([lo, hi])
+    return comps
+
+
+def _overlap(a, b):
+    """Two-pointer intersection length of two component lists (reporting.py:102-114)."""
+    i = j = 0
+    total = 0.0
+    while i < len(a) and j < len(b):
+        lo = a[i][0] if a[i][0] >= b[j][0] else b[j][0]
+        hi = a[i][1] if a[i][1] <= b[j][1] else b[j][1]
+        if hi > lo:
+            total += hi - lo
+        if a[i][1] <= b[j][1]:
+            i += 1
+        else:
+            j += 1
+    return total
+
+
+def summarize(entries, op_type: dict, kinds: dict, busy: dict, makespan: float, cp, top_k: int = 10):
+    """reporting.summarize on oracle entries [(nid, device, start, finish)] in entry order.
+
+    ``op_type[nid]`` is the node's op type, ``kinds[device]`` the device kind of the
+    graph's device table (absent -> Compute), ``cp`` the critical_path result on
+    finish - start.  Returns the SummaryReport fields as a dict."""
+    totals = {}
+    compute = comm = 0.0
+    cspans, mspans = [], []
+    for nid, dev, s, f in entries:
+        key = op_type[nid] or nid
+        totals[key] = totals.get(key, 0.0) + (f - s)
+        if kinds.get(dev, COMPUTE) == COMPUTE:
+            compute += f - s
+            cspans.append((s, f))
+        else:
+            comm += f - s
+            mspans.append((s, f))
+    grand = sum(totals.values())
+    ranked = sorted(totals.items(), key=lambda kv: (-kv[1], kv[0]))[: max(0, top_k)]
+    return {
+        "makespan_us": makespan,
+        "per_device_busy_us": dict(busy),
+        "utilization": {d: (b / makespan if makespan > 0 else 0.0) for d, b in busy.items()},
+        "device_kinds": dict(kinds),
+        "top_k_ops": [[k, t, (t / grand if grand > 0 else 0.0)] for k, t in ranked],
+        "compute_us": compute,
+        "comm_us": comm,
+        "overlap_us": _overlap(_union(cspans), _union(mspans)),
+        "critical_path_nodes": list(cp[1]),
+        "critical_path_us": cp[0],
+    }
+
+
+def _json_str(x: str) -> str:
+    out = ['"']
+    for ch in x:
+        o = ord(ch)
+        if ch == '"':
+            out.append('\\"')
+        elif ch == "\\":
+            out.append("\\\\")
+        elif ch in "\n\r\t\b\f":
+            out.append({"\n": "\\n", "\r": "\\r", "\t": "\\t", "\b": "\\b", "\f": "\\f"}[ch])
+        elif o < 0x20 or o > 0x7E:
+            if o > 0xFFFF:
+                o -= 0x10000
+                out.append("\\u%04x\\u%04x" % (0xD800 | (o >> 10), 0xDC00 | (o & 0x3FF)))
+            else:
+                out.append("\\u%04x" % o)
+        else:
+            out.append(ch)
+    out.append('"')
+    return "".join(out)
+
+
+def to_trace(entries, op_type: dict, source: dict, devices) -> str:
+    """reporting.to_trace: ``devices`` = the schedule's busy-dict keys; entries as in summarize."""
+    devs = sorted(devices)
+    tid = {d: i for i, d in enumerate(devs)}
+    parts = []
+    for d in devs:
+        parts.append(' {\n  "name": "thread_name",\n  "ph": "M",\n  "pid": 0,\n  "tid": %d,\n  "args": {\n'
+                     '   "name": %s\n  }\n }' % (tid[d], _json_str(d)))
+    for nid, dev, s, f in entries:
+        parts.append(' {\n  "name": %s,\n  "ph": "X",\n  "ts": %d,\n  "dur": %d,\n  "pid": 0,\n  "tid": %d,\n'
+                     '  "args": {\n   "node": %s,\n   "source": %s\n  }\n }'
+                     % (_json_str(op_type[nid] or nid), round(s), round(f - s), tid.get(dev, len(devs)),
+                        _json_str(nid), _json_str(source[nid])))
+    return ("[\n" + ",\n".join(parts) + "\n]\n") if parts else "[]\n"

@@ -2,7 +2,9 @@
 
 Drop-in surface (same names and signatures as the reference's pkg/src/dfsim/__init__.py:6-43
 for the hot path): ``simulate``, ``critical_path``, ``estimate_all``,
-``expand_data_parallel``; batched entry point: ``sweep``.  Every compute call runs
+``expand_data_parallel``, and the schedule consumers ``summarize`` / ``to_trace``;
+batched entry point: ``sweep`` (``SweepResult.summaries`` / ``.trace`` report on the
+schedules left in HBM).  Every compute call runs
 hand-written sm_100a kernels from ``libdfsim_b200.so`` through the C-ABI in
 ``include/dfsim_b200.h``; there is no CPU fallback.
 """
@@ -48,6 +50,7 @@ from .estimate import estimate_all, estimate_batch  # noqa: F401
 from .expansion import expand_class, expand_data_parallel  # noqa: F401
 from .lowering import fit_for_grid, fit_linear, node_features  # noqa: F401
 from .ps import expand_parameter_server  # noqa: F401
+from .reporting import SummaryReport, render_summary_text, summarize, to_trace, trace_intervals  # noqa: F401
 from .simulator import critical_path, simulate  # noqa: F401
 
 __version__ = "0.1.0"

@@ -265,6 +265,31 @@ class TopologyClass:
             st, fi = st.index_select(0, pos), fi.index_select(0, pos)
         return st, fi
 
+    def rows_by_rank_batch(self, o: dict, rows):
+        """(start, finish) of several candidates as contiguous [R][N] device tensors by node rank."""
+        import torch
+
+        n = self.lg.n
+        r = torch.as_tensor(list(rows), dtype=torch.int64, device=o["makespan"].device)
+        st, fi = o["start"].index_select(0, r)[:, :n], o["finish"].index_select(0, r)[:, :n]
+        if o.get("layout") == "position":
+            pos = torch.as_tensor(self.tables.pos, device=st.device)
+            st, fi = st.index_select(1, pos), fi.index_select(1, pos)
+        return st.contiguous(), fi.contiguous()
+
+    def summary_tables(self):
+        """K6 tables of this class (cached): op key, comm flag and (device, id) order per node rank."""
+        if getattr(self, "_summary", None) is None:
+            from .model import DEVICE_COMPUTE
+            from .reporting import SummaryTables
+
+            g = self.graph
+            kinds = {d: spec.kind for d, spec in g.devices.items()}
+            keys = [g.nodes[nid].op_type or nid for nid in self.ids]
+            comm = [kinds.get(g.nodes[nid].device, DEVICE_COMPUTE) != DEVICE_COMPUTE for nid in self.ids]
+            self._summary = SummaryTables(keys, comm, self.lg.device_of_rank(), self.ctx.device)
+        return self._summary
+
     def critical_path_only(self, o: dict):
         """Re-run K4 on the current schedules (after a deferred fallback)."""
         if self.fused:
@@ -322,6 +347,82 @@ class SweepResult:
                     for nid in resolve_overrides(cfg.overrides, tc.ids):
                         src[rank[nid]] = 0
         return {nid: DurationEntry(0.0, SOURCE_TAGS[src[k]]) for k, nid in enumerate(tc.ids)}
+
+    def summaries(self, indices, top_k: int = 10) -> list:
+        """reporting.summarize (reporting.py:117-162) of several candidates' schedules, computed
+        from the schedules still in HBM: K6 folds + K4 paths on the device, one launch
+        sequence per topology class.  Returns SummaryReport objects in ``indices`` order."""
+        from .reporting import SummaryReport, rank_ops, run_summary
+
+        indices = list(indices)
+        out = [None] * len(indices)
+        by_class: dict = {}
+        for k, i in enumerate(indices):
+            c, row = self._where[i]
+            by_class.setdefault(c, []).append((k, row))
+        for c, items in by_class.items():
+            tc, _, o = self.classes[c]
+            if "start" not in o:
+                raise ValueError("run sweep(..., keep_schedules=True) to summarise schedules")
+            rows = [row for _, row in items]
+            st, fi = tc.rows_by_rank_batch(o, rows)
+            tables = tc.summary_tables()
+            order, key_total, key_first, sums = run_summary(tc.ctx, tables, st, fi)
+            p = critical_path_arrays(tc.lg, st, fi, paths=True) if tc.lg.n else None
+            g, lg = tc.graph, tc.lg
+            kinds = {d: spec.kind for d, spec in g.devices.items()}
+            extra = [d for d in lg.devices if d not in g.devices]
+            kt, kf, sm = key_total.cpu().numpy(), key_first.cpu().numpy(), sums.cpu().numpy()
+            ms = o["makespan"].cpu().numpy()
+            busy_rows = o["busy"].cpu().numpy()
+            order_h = order.cpu().numpy() if extra else None
+            cp_len = p["cp_len"].cpu().numpy() if p else None
+            cp_path = p["cp_path"].cpu().numpy() if p else None
+            cp_plen = p["cp_path_len"].cpu().numpy() if p else None
+            dev_of = lg.device_of_rank()
+            for j, (k, row) in enumerate(items):
+                busy = {d: 0.0 for d in g.devices}
+                rank_busy = {lg.devices[r]: float(busy_rows[row, r]) for r in range(lg.n_devices)}
+                for d in g.devices:
+                    if d in rank_busy:
+                        busy[d] = rank_busy[d]
+                if extra:  # devices outside g.devices join in entry order (engine.py:90-92)
+                    for v in order_h[j, : lg.n].tolist():
+                        d = lg.devices[dev_of[v]]
+                        if d not in busy:
+                            busy[d] = rank_busy[d]
+                makespan = float(ms[row])
+                util = {d: (b / makespan if makespan > 0 else 0.0) for d, b in busy.items()}
+                path = [tc.ids[v] for v in cp_path[j, : int(cp_plen[j])].tolist()] if p else []
+                out[k] = SummaryReport(
+                    makespan_us=makespan, per_device_busy_us=busy, utilization=util, device_kinds=dict(kinds),
+                    top_k_ops=rank_ops(tables.keys, kt[j], kf[j], top_k) if lg.n else [],
+                    compute_us=float(sm[j, 0]), comm_us=float(sm[j, 1]), overlap_us=float(sm[j, 2]),
+                    critical_path_nodes=path, critical_path_us=float(cp_len[j]) if p else 0.0)
+        return out
+
+    def summary(self, i: int, top_k: int = 10):
+        return self.summaries([i], top_k)[0]
+
+    def trace(self, i: int) -> str:
+        """reporting.to_trace of candidate i's schedule (byte-identical; C++ writer)."""
+        from .reporting import TraceTables, run_summary
+
+        tc, o, row = self._row(i)
+        st, fi = tc.rows_by_rank_batch(o, [row])
+        order, _, _, _ = run_summary(tc.ctx, tc.summary_tables(), st, fi)
+        g, lg = tc.graph, tc.lg
+        busy_keys = set(g.devices) | set(lg.devices)
+        tracks = sorted(busy_keys)
+        tid = {d: k for k, d in enumerate(tracks)}
+        dev_of = lg.device_of_rank()
+        if getattr(tc, "_trace_tables", None) is None:
+            tc._trace_tables = TraceTables(tc.ids, [g.nodes[nid].op_type or nid for nid in tc.ids],
+                                           np.zeros(lg.n, np.uint8), [tid[lg.devices[d]] for d in dev_of], tracks)
+        src = self._entries(tc, o, row)
+        tags = np.fromiter((SOURCE_TAGS.index(src[nid].source) for nid in tc.ids), dtype=np.uint8, count=lg.n)
+        return tc._trace_tables.write(order.cpu().numpy()[0, : lg.n], st.cpu().numpy()[0], fi.cpu().numpy()[0],
+                                      tags=tags)
 
     def critical_path(self, i: int):
         tc, o, row = self._row(i)

@@ -29,7 +29,8 @@ def nvcc() -> str:
 
 
 def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu"))
+    """CUDA translation units plus the host-only C++ ones (trace writer)."""
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def needs_build() -> bool:
@@ -52,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     procs = []
     for src in sources():
-        obj = objdir / (src.stem + ".o")
+        obj = objdir / (src.name + ".o")
         objs.append(obj)
         procs.append((src, subprocess.Popen([nvcc(), *flags, "-c", str(src), "-o", str(obj)],
                                             stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))

@@ -78,6 +78,15 @@ class CpTables(ctypes.Structure):
                 ("spill_list", P), ("max_spill_reads", I32), ("pinfo", P), ("slot_region", I32), ("stage_doubles", I32)]
 
 
+class SummaryTables(ctypes.Structure):
+    _fields_ = [("n_nodes", I32), ("n_keys", I32), ("base_order", P), ("key", P), ("comm", P)]
+
+
+class TraceTables(ctypes.Structure):
+    _fields_ = [("n_nodes", I32), ("n_tracks", I32), ("id_blob", P), ("id_off", P), ("name_blob", P),
+                ("name_off", P), ("tag", P), ("tag_name", P), ("track", P), ("track_name", P)]
+
+
 _SIGNATURES = {
     "dfsim_abi_version": (I32, []),
     "dfsim_ctx_create": (ctypes.c_int, [I32, P, ctypes.POINTER(P)]),
@@ -100,6 +109,8 @@ _SIGNATURES = {
     "dfsim_fused_capacity": (I32, [ctypes.POINTER(SimTables)]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),
     "dfsim_argmin_records": (ctypes.c_int, [P, I64, P, P]),
+    "dfsim_summarize": (ctypes.c_int, [P, ctypes.POINTER(SummaryTables), I64, P, P, I64, P, I32, P, P, P]),
+    "dfsim_trace_write": (I64, [ctypes.POINTER(TraceTables), I64, P, P, P, P, I64]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

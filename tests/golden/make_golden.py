@@ -17,6 +17,7 @@ test_acceptance.py:40-48, test_costmodel.py, test_strategy.py).
 from __future__ import annotations
 
 import gzip
+import hashlib
 import json
 import sys
 import warnings
@@ -41,6 +42,7 @@ from dfsim.errors import CycleError, DfsimError, MissingDurationError, UnknownOp
 from dfsim.graph import (  # noqa: E402
     COLLECTIVE, COMPUTE, TRANSFER, DeviceSpec, OpNode, TensorShape, critical_path, make_graph, serialize_graph,
 )
+from dfsim.reporting import summarize, to_trace  # noqa: E402
 from dfsim.profiledb import LinkRecord, OpSignature, ProfileDB, ProfileRecord, _insert_inplace, load_profiles, save_profiles  # noqa: E402
 from dfsim.strategy import CollectiveConfig, StrategyConfig, expand_data_parallel, parse_config, serialize_config  # noqa: E402
 from dfsim.synth import DurationLaw, SplitMix64, SynthSpec, gen_durations, gen_graph, gen_profiles, parse_synth_spec  # noqa: E402
@@ -80,7 +82,26 @@ def run_engine(g, table):
         return {"error": "MissingDurationError", "ids": exc.node_ids}
     durs = {e.node_id: e.finish_us - e.start_us for e in s.entries}
     cp_len, cp_path = critical_path(g, durs)
-    return {"schedule": json.loads(s.to_json()), "cp": [cp_len, cp_path]}
+    return {"schedule": json.loads(s.to_json()), "cp": [cp_len, cp_path], "summary": summary_doc(s, g),
+            **trace_doc(s)}
+
+
+def summary_doc(s, g, top_k=10):
+    """reporting.summarize (reporting.py:117-162) of the schedule, JSON-ready."""
+    r = summarize(s, g, top_k=top_k)
+    return {"makespan_us": r.makespan_us, "per_device_busy_us": r.per_device_busy_us, "utilization": r.utilization,
+            "device_kinds": r.device_kinds, "top_k_ops": [list(t) for t in r.top_k_ops], "compute_us": r.compute_us,
+            "comm_us": r.comm_us, "overlap_us": r.overlap_us, "critical_path_nodes": r.critical_path_nodes,
+            "critical_path_us": r.critical_path_us}
+
+
+def trace_doc(s):
+    """reporting.to_trace (reporting.py:43-74): sha256 of the document; the text itself for small schedules."""
+    text = to_trace(s)
+    out = {"trace_sha256": hashlib.sha256(text.encode()).hexdigest(), "trace_bytes": len(text.encode())}
+    if len(s.entries) <= 12:
+        out["trace"] = text
+    return out
 
 
 # ----------------------------------------------------------------------------- engine cases
@@ -122,6 +143,39 @@ def engine_cases():
     # rank inversions of expanded ids (F4e): "a0@r0" < "a@r0", "x@r10" < "x@r2"
     inv_nodes = [mk_node(n, device=f"gpu{i % 3}") for i, n in enumerate(["a@r0", "a0@r0", "x@r10", "x@r2", "x@r1"])]
     add("rank_inversions", mk_graph(inv_nodes), mk_table({n.id: 1.0 for n in inv_nodes}))
+
+    # summary / trace coverage: link + collective devices, empty op types (key = node id),
+    # zero durations, start ties across devices, non-ASCII and escaped characters in ids
+    links = [DeviceSpec(id="link:a", kind="Link", hardware="test-hw", throughput_mbps=1000.0, latency_us=1.0),
+             DeviceSpec(id="fabric", kind="CollectiveResource", hardware="test-hw", throughput_mbps=1.0,
+                        latency_us=0.0)]
+    mixed = [mk_node("c0", op="Conv2D"), mk_node("c1", ["c0"], op=""), mk_node("t0", ["c0"], device="link:a",
+             kind=TRANSFER, op="Send"), mk_node("t1", ["t0"], device="link:a", kind=TRANSFER, op="Send"),
+             mk_node("ar", ["c1", "t1"], device="fabric", kind=COLLECTIVE, op="AllReduce"),
+             mk_node("c2", ["c0"], device="gpu1", op="Conv2D"), mk_node("z\u00e9\"q", ["c2"], device="gpu1", op=""),
+             mk_node("c3", ["ar"], op="Conv2D"), mk_node("c4", ["c2"], device="gpu1", op="MatMul")]
+    add("summary_mixed", mk_graph(mixed, extra_devices=links),
+        mk_table({"c0": 2.5, "c1": 0.0, "t0": 3.25, "t1": 1.5, "ar": 4.0, "c2": 1.0, "z\u00e9\"q": 2.0, "c3": 0.5,
+                  "c4": 0.0}))
+    for seed in range(6):
+        rng = SplitMix64(seed + 77)
+        g0 = gen_graph(SynthSpec(kind="RandomDAG", nodes=50 + 20 * seed, density=0.08, seed=500 + seed, num_devices=4))
+        devs = [DeviceSpec(id=f"link:{k}", kind="Link", hardware="test-hw", throughput_mbps=100.0, latency_us=1.0)
+                for k in range(2)]
+        nodes = []
+        for nid in sorted(g0.nodes):
+            n = g0.nodes[nid]
+            r = rng.randint(0, 9)
+            if r < 3:
+                n = OpNode(n.id, ("Send", "Recv", "")[r], f"link:{r % 2}", TRANSFER, n.attrs, n.inputs, n.output_shapes)
+            elif r == 3:
+                n = OpNode(n.id, "", n.device, n.kind, n.attrs, n.inputs, n.output_shapes)
+            nodes.append(n)
+        durs = {}
+        for nid in sorted(g0.nodes):
+            u = rng.uniform()
+            durs[nid] = 0.0 if u < 0.1 else (float(rng.randint(1, 3)) * 0.1 if u < 0.3 else u * 7.0)
+        add(f"summary_random_{seed}", mk_graph(nodes, extra_devices=devs), mk_table(durs))
 
     # random DAG families of the reference tests
     for seed in range(25):  # test_engine.random_instance

@@ -94,6 +94,47 @@ def test_python_pipeline_matches_golden(pipeline_cases):
         assert [cp[0], cp[1]] == exp["cp"], case["name"]
 
 
+def _summary_and_trace(g, durs, sources):
+    entries, makespan, busy = O.simulate(g, durs)
+    cp = O.critical_path(g, {nid: f - s for nid, _, s, f in entries})
+    op = {nid: n.op_type for nid, n in g.nodes.items()}
+    kinds = {d: spec.kind for d, spec in g.devices.items()}
+    return (O.summarize(entries, op, kinds, busy, makespan, cp), O.to_trace(entries, op, sources, busy))
+
+
+def _check_report(case, g, durs, sources):
+    import hashlib
+    import json
+
+    exp = case["expect"]
+    rep, trace = _summary_and_trace(g, durs, sources)
+    # dict order matters (the reference's report iterates these dicts)
+    assert json.dumps(rep) == json.dumps(exp["summary"]), case["name"]
+    if "trace" in exp:
+        assert trace == exp["trace"], case["name"]
+    assert hashlib.sha256(trace.encode()).hexdigest() == exp["trace_sha256"], case["name"]
+
+
+def test_python_summary_and_trace_match_golden(engine_cases, pipeline_cases):
+    """summarize (reporting.py:117-162) and to_trace (43-74) restated, pinned on every fixture."""
+    n = 0
+    for case in engine_cases:
+        if "summary" not in case["expect"]:
+            continue
+        d = case["durations"]
+        _check_report(case, case_graph(case), {k: v for k, (v, _) in d.items()}, {k: s for k, (_, s) in d.items()})
+        n += 1
+    for case in pipeline_cases:
+        exp = case["expect"]
+        if "summary" not in exp:
+            continue
+        g = parse_graph(exp["expanded"]) if "expanded" in exp else parse_graph(case["graph"])
+        d = exp["durations"]
+        _check_report(case, g, {k: v for k, (v, _) in d.items()}, {k: s for k, (_, s) in d.items()})
+        n += 1
+    assert n > 150
+
+
 def test_python_predict_is_cpython_sum():
     """predict's sum is CPython's float sum (Neumaier since 3.12); pinned here on random data."""
     rng = np.random.default_rng(7)
