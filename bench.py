@@ -459,12 +459,79 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
+        if single and not args.no_reports:
+            line["reports"] = measure_reports(classes[0][0], classes[0][2], args.report_rows)
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample, workload=args.workload)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def measure_reports(tc, o, rows: int, cpu_rows: int = 8):
+    """SURVEY.md §8f consumers of the schedules left in HBM: K6 summaries (+ K4 critical
+    paths) for ``rows`` candidates timed on the device, and the Chrome trace of one
+    schedule through the C++ writer; beside them the oracle's Python summarize/to_trace
+    on the same schedules (1 core) as the CPU reference for these rows."""
+    import numpy as np
+    import torch
+
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200.reporting import TraceTables, run_summary
+    from paper_2002_06790_b200.simulator import critical_path_arrays
+
+    rows = min(rows, tc.lp.n_sims)
+    tables = tc.summary_tables()
+    ctx = tc.ctx
+
+    def device_pass():
+        st, fi = tc.rows_by_rank_batch(o, range(rows))
+        out = run_summary(ctx, tables, st, fi)
+        critical_path_arrays(tc.lg, st, fi, paths=True)
+        return st, fi, out
+
+    device_pass()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    st, fi, (order, _, _, _) = device_pass()
+    b.record()
+    torch.cuda.synchronize()
+    dev_ms = a.elapsed_time(b)
+    # CPU reference on the same schedules (entries rebuilt from the device result)
+    g, lg = tc.graph, tc.lg
+    ids = tc.ids
+    dev_of = lg.device_of_rank()
+    op = {nid: n.op_type for nid, n in g.nodes.items()}
+    kinds = {d: spec.kind for d, spec in g.devices.items()}
+    sh, fh, oh = st[:cpu_rows].cpu().numpy(), fi[:cpu_rows].cpu().numpy(), order[:cpu_rows].cpu().numpy()
+    t0 = time.perf_counter()
+    for j in range(min(cpu_rows, rows)):
+        entries = [(ids[v], lg.devices[dev_of[v]], float(sh[j, v]), float(fh[j, v])) for v in oh[j, : lg.n].tolist()]
+        busy = {}
+        for nid, d, s_, f_ in entries:
+            busy[d] = busy.get(d, 0.0) + (f_ - s_)
+        cp = O.critical_path(g, {nid: f_ - s_ for nid, _, s_, f_ in entries})
+        O.summarize(entries, op, kinds, busy, max(e[3] for e in entries), cp)
+    cpu_s = (time.perf_counter() - t0) / min(cpu_rows, rows)
+    # trace of one schedule: C++ writer vs the oracle's Python writer
+    tracks = sorted(set(g.devices) | set(lg.devices))
+    tid = {d: k for k, d in enumerate(tracks)}
+    tt = TraceTables(ids, [g.nodes[nid].op_type or nid for nid in ids], np.zeros(lg.n, np.uint8),
+                     [tid[lg.devices[d]] for d in dev_of], tracks)
+    tt.write(oh[0, : lg.n], sh[0], fh[0])  # warm: first call sizes the reusable output buffer
+    t0 = time.perf_counter()
+    text = tt.write(oh[0, : lg.n], sh[0], fh[0])
+    cpp_ms = (time.perf_counter() - t0) * 1e3
+    entries = [(ids[v], lg.devices[dev_of[v]], float(sh[0, v]), float(fh[0, v])) for v in oh[0, : lg.n].tolist()]
+    t0 = time.perf_counter()
+    ref_text = O.to_trace(entries, op, {nid: "Override" for nid in ids}, {d: 0.0 for d in tracks})
+    py_ms = (time.perf_counter() - t0) * 1e3
+    return {"summaries": rows, "device_ms": dev_ms, "summaries_per_s": rows / (dev_ms / 1e3),
+            "cpu_summaries_per_s": 1.0 / cpu_s, "cpu_kind": "port (oracle summarize + critical_path, 1 core)",
+            "trace_bytes": len(text), "trace_ms_cpp": cpp_ms, "trace_ms_python_oracle": py_ms,
+            "trace_identical": text == ref_text}
 
 
 def run_reference(args):
@@ -502,6 +569,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-reports", action="store_true", help="skip the summary/trace measurement")
+    ap.add_argument("--report-rows", type=int, default=1024, help="schedules summarised in the reports line")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -9,6 +9,7 @@
 // point outside 0x20..0x7e as \uXXXX (UTF-16 surrogate pairs above 0xFFFF).
 // Host code only: the schedule is already on the host when a trace is wanted.
 #include <cfenv>
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -34,6 +35,13 @@ void put_str(std::string &o, const char *p, size_t n) {
     const auto *s = reinterpret_cast<const unsigned char *>(p);
     size_t i = 0;
     while (i < n) {
+        size_t j = i;  // copy the longest run that needs no escaping in one append
+        while (j < n && s[j] >= 0x20 && s[j] < 0x7f && s[j] != '"' && s[j] != '\\') j++;
+        if (j > i) {
+            o.append(p + i, j - i);
+            i = j;
+            continue;
+        }
         unsigned c = s[i];
         if (c < 0x80) {
             i++;
@@ -74,17 +82,18 @@ void put_round(std::string &o, double x) {
     const double r = std::nearbyint(x) + 0.0;  // FE_TONEAREST: ties to even; + 0.0 drops -0
     char buf[400];
     if (std::fabs(r) < 9.0e15) {
-        std::snprintf(buf, sizeof buf, "%lld", static_cast<long long>(r));
+        const auto res = std::to_chars(buf, buf + sizeof buf, static_cast<long long>(r));
+        o.append(buf, res.ptr);
     } else {
         std::snprintf(buf, sizeof buf, "%.0f", r);  // exact integer value of the double
+        o += buf;
     }
-    o += buf;
 }
 
 void put_int(std::string &o, long long v) {
     char buf[32];
-    std::snprintf(buf, sizeof buf, "%lld", v);
-    o += buf;
+    const auto res = std::to_chars(buf, buf + sizeof buf, v);
+    o.append(buf, res.ptr);
 }
 
 }  // namespace

@@ -180,14 +180,16 @@ class TraceTables:
         fi = np.ascontiguousarray(finish, dtype=np.float64)
         args = (ctypes.byref(self.struct), len(en), en.ctypes.data, st.ctypes.data, fi.ctypes.data)
         cap = 256 + 200 * len(en) + 96 * self.struct.n_tracks + len(self._id_blob) * 6 + len(self._name_blob) * 6
-        buf = ctypes.create_string_buffer(cap)
-        size = lib.dfsim_trace_write(*args, buf, cap)
+        buf = getattr(self, "_buf", None)  # reused between calls (no zero-fill, no fresh pages)
+        if buf is None or len(buf) < cap:
+            buf = self._buf = np.empty(cap, np.uint8)
+        size = lib.dfsim_trace_write(*args, buf.ctypes.data, len(buf))
         if size < 0:
             raise ValueError("dfsim_trace_write: bad arguments")
-        if size > cap:
-            buf = ctypes.create_string_buffer(size)
-            lib.dfsim_trace_write(*args, buf, size)
-        return buf.raw[:size].decode("ascii")
+        if size > len(buf):
+            buf = self._buf = np.empty(size, np.uint8)
+            lib.dfsim_trace_write(*args, buf.ctypes.data, size)
+        return buf[:size].tobytes().decode("ascii")
 
 
 def _blob(strings):
