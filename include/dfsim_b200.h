@@ -192,25 +192,27 @@ int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims
                             int32_t *n_placed, const int32_t *pos, const int64_t *out_rows, int32_t interleaved);
 
 /* ---------------------------------------------------------------- fused hot path (K2a + K3 v2 + K4 v2) */
-/* Class tables built once per topology class (paper_2002_06790_b200/prepare.py). */
+/* Class tables built once per topology class (paper_2002_06790_b200/prepare.py).
+ * Nodes are numbered by level position p (the output column); rank[p] is the node's
+ * rank (id order), used for the FIFO tie-break, overrides and the source order. */
 typedef struct {
     int32_t n_nodes;           /* N <= 65535 */
     int32_t n_devices;         /* D <= 32 */
     int64_t n_edges;
-    const uint32_t *meta;      /* [N] successor begin (24 bits) | out-degree (8 bits, < 255) */
-    const int32_t *succ_off;   /* [N+1] */
-    const uint32_t *succ;      /* [E] consumer rank | device << 16 | single-input << 21 */
-    const uint16_t *cidx;      /* [N] counter slot of nodes with >= 2 input references */
+    const uint32_t *meta;      /* [N] by position: successor begin (24 bits) | out-degree (8 bits, < 255) */
+    const int32_t *succ_off;   /* [N+1] (rank CSR; sizes only) */
+    const uint32_t *succ;      /* [E] by reading position: consumer position | device << 16 | single-input << 21 */
+    const uint16_t *cidx;      /* [N] by position: counter slot of nodes with >= 2 input references */
     const uint32_t *cnt_init;  /* [n_counter_words] packed initial counters */
     int32_t n_counter_words;
     int32_t counter_bits;      /* 4, 8 or 16 */
-    const uint16_t *pos;       /* [N] output column (level-order position) of each rank */
-    const int32_t *sources;    /* ascending ranks with in-degree 0 */
+    const uint16_t *rank;      /* [N] rank of the node at position p */
+    const int32_t *sources;    /* positions of the in-degree-0 nodes, in ascending rank */
     int32_t n_sources;
     int32_t qcap;              /* per-device FIFO ring capacity (power of two); overflow flags the candidate */
-    const int32_t *device;     /* [N] device rank */
-    int32_t succ_packed;       /* 1: succ[j] = consumer (13 bits) | device << 13 | single << 18 | counter
-                                  slot << 19 (N <= 8192, cidx unused); 0: the layout above */
+    const int32_t *device;     /* [N] device index by rank */
+    int32_t succ_packed;       /* 1: succ[j] = consumer position (13 bits) | device << 13 | single << 18 |
+                                  counter slot << 19 (N <= 8192, cidx unused); 0: the layout above */
 } dfsim_sim_tables;
 
 typedef struct {

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     uint32_t *s_meta = reinterpret_cast<uint32_t *>(smem);
     uint32_t *s_succ = s_meta + N;
     uint16_t *s_cidx = reinterpret_cast<uint16_t *>(s_succ + E);
-    uint16_t *s_pos = s_cidx + N;
+    uint16_t *s_rank = s_cidx + N;  // nodes are numbered by position; rank only for tie-breaks
     double *s_base = reinterpret_cast<double *>(smem + ((static_cast<size_t>(N) * 8 + static_cast<size_t>(E) * 4 + 15) / 16) * 16);
     unsigned char *gbase = smem + a.smem_graph + static_cast<size_t>(gid) * a.smem_warp;
     int32_t *tails = reinterpret_cast<int32_t *>(gbase);
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         s_meta[i] = __ldg(a.g.meta + i);
         s_cidx[i] = __ldg(a.g.cidx + i);
-        s_pos[i] = __ldg(reinterpret_cast<const uint16_t *>(a.g.pos) + i);
+        s_rank[i] = __ldg(a.g.rank + i);
     }
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.g.succ + i);
     int staged = -1;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
         const int var = __ldg(a.st.chunk_variant + c);
         if (var != staged) {
             const double *row = a.st.base + static_cast<int64_t>(var) * N;
-            for (int i = threadIdx.x; i < N; i += blockDim.x) s_base[i] = __ldg(row + i);
+            for (int i = threadIdx.x; i < N; i += blockDim.x) s_base[i] = __ldg(row + s_rank[i]);
             staged = var;
             __syncthreads();
         }
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 const int i = b + ll;
                 const bool has = active && i < a.g.n_sources;
                 const int v = has ? __ldg(a.g.sources + i) : 0;
-                const int dv = has ? __ldg(a.g.device + v) : 0;
+                const int dv = has ? __ldg(a.g.device + s_rank[v]) : 0;
                 const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, has ? dv + 32 * grp : 64 + lane);
                 const int base = has ? tails[dv] : 0;
                 __syncwarp();
@@ -186,17 +186,18 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     head++;
                     const double b = s_base[v];
                     double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
-                    if (ovs >= 0) {
+                    if (ovs >= 0) {  // override tables are by rank
+                        const int vr = s_rank[v];
                         int lo = __ldg(a.st.ov_off + ovs), hi = __ldg(a.st.ov_off + ovs + 1);
                         const int end = hi;
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
-                            if (__ldg(a.st.ov_node + mid) < v) lo = mid + 1; else hi = mid;
+                            if (__ldg(a.st.ov_node + mid) < vr) lo = mid + 1; else hi = mid;
                         }
-                        if (lo < end && __ldg(a.st.ov_node + lo) == v) dur = __ldg(a.st.ov_val + lo);
+                        if (lo < end && __ldg(a.st.ov_node + lo) == vr) dur = __ldg(a.st.ov_val + lo);
                     }
                     const double f = __dadd_rn(now, dur);
-                    out[s_pos[v]] = make_double2(now, f);
+                    out[v] = make_double2(now, f);
                     running = true;
                     run_v = v;
                     run_f = f;
@@ -254,8 +255,9 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     uint16_t *qd = q + ll * QSTRIDE;
                     for (int i = seg_lo + 1; i < seg_hi; i++) {
                         const uint16_t x = qd[i & QMASK];
+                        const unsigned xr = s_rank[x];
                         int j = i - 1;
-                        while (j >= seg_lo && qd[j & QMASK] > x) {
+                        while (j >= seg_lo && s_rank[qd[j & QMASK]] > xr) {
                             qd[(j + 1) & QMASK] = qd[j & QMASK];
                             j--;
                         }

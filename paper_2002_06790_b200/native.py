@@ -61,7 +61,7 @@ class Strategies(ctypes.Structure):
 
 class SimTables(ctypes.Structure):
     _fields_ = [("n_nodes", I32), ("n_devices", I32), ("n_edges", I64), ("meta", P), ("succ_off", P), ("succ", P),
-                ("cidx", P), ("cnt_init", P), ("n_counter_words", I32), ("counter_bits", I32), ("pos", P),
+                ("cidx", P), ("cnt_init", P), ("n_counter_words", I32), ("counter_bits", I32), ("rank", P),
                 ("sources", P), ("n_sources", I32), ("qcap", I32), ("device", P), ("succ_packed", I32)]
 
 

@@ -86,28 +86,39 @@ class Tables:
                          and self.slot_region + 2 * self.stage_doubles < 65536 and len(self.spill_list) < 65536)
 
     def _engine(self, N, off, idx, indeg, dev, outdeg):
+        """K3 v2 tables with nodes numbered by level position p (pos[rank]); ranks survive only
+        as ``rank[p]`` for the FIFO tie-break sort, override lookups and the source order."""
+        order, pos = self.rank_of_pos, self.pos
         single = indeg == 1
-        multi = np.nonzero(indeg >= 2)[0]
-        cidx = np.zeros(N, np.int64)
-        cidx[multi] = np.arange(multi.size)
+        multi_p = np.nonzero(indeg[order] >= 2)[0]              # counter slots in position order
+        cslot = np.zeros(N, np.int64)
+        cslot[multi_p] = np.arange(multi_p.size)
         mx = indeg.max(initial=0)
         bits = 4 if mx < 15 else (8 if mx < 255 else 16)
         per = 32 // bits
-        words = max(1, -(-multi.size // per))
+        words = max(1, -(-multi_p.size // per))
         init = np.zeros(words * per, np.uint64)
-        init[: multi.size] = indeg[multi]
+        init[: multi_p.size] = indeg[order[multi_p]]
         init = init.reshape(words, per)
         packed = np.zeros(words, np.uint64)
         for i in range(per):
             packed |= init[:, i] << np.uint64(i * bits)
         self.counter_bits, self.counter_words = bits, words
-        self.meta = (off[:-1] & 0xFFFFFF) | (np.minimum(outdeg, 255) << 24)
-        self.succ_packed = N <= 8192 and multi.size <= 8192
-        if self.succ_packed:  # consumer | device << 13 | single << 18 | counter slot << 19
-            self.succ = idx | (dev[idx] << 13) | (single[idx].astype(np.int64) << 18) | (cidx[idx] << 19)
+        # successor CSR by position: the successors of the node at position p, in its rank-CSR order
+        deg_p = outdeg[order]
+        off_p = np.zeros(N + 1, np.int64)
+        np.cumsum(deg_p, out=off_p[1:])
+        take = np.arange(int(off_p[-1]), dtype=np.int64) + np.repeat(off[order] - off_p[:-1], deg_p)
+        cons = idx[take]                                         # consumer ranks
+        cpos = pos[cons]
+        self.meta = (off_p[:-1] & 0xFFFFFF) | (np.minimum(deg_p, 255) << 24)
+        self.succ_packed = N <= 8192 and multi_p.size <= 8192
+        if self.succ_packed:  # consumer position | device << 13 | single << 18 | counter slot << 19
+            self.succ = cpos | (dev[cons] << 13) | (single[cons].astype(np.int64) << 18) | (cslot[cpos] << 19)
         else:
-            self.succ = idx | (dev[idx] << 16) | (single[idx].astype(np.int64) << 21)
-        self.cidx, self.cnt_init = cidx, packed
+            self.succ = cpos | (dev[cons] << 16) | (single[cons].astype(np.int64) << 21)
+        self.cidx, self.cnt_init = cslot, packed
+        self.eng_sources = pos[np.nonzero(indeg == 0)[0]]        # ascending ranks, as positions
 
     def _critical_path(self, N, idx, indeg, outdeg, order, pos, loff):
         goff = [0]
@@ -208,7 +219,8 @@ class ClassTables(Tables):
         T = lambda a, dt: _t(a, dt, d)  # noqa: E731
         self.t = t = dict(
             meta=T(self.meta, np.uint32), succ=T(self.succ, np.uint32), cidx=T(self.cidx, np.uint16),
-            cnt_init=T(self.cnt_init, np.uint32), pos=T(self.pos, np.uint16), pos32=T(self.pos, np.int32),
+            cnt_init=T(self.cnt_init, np.uint32), rank16=T(self.rank_of_pos, np.uint16),
+            eng_sources=T(self.eng_sources, np.int32), pos32=T(self.pos, np.int32),
             rank_of_pos=T(self.rank_of_pos, np.int32), cp_slot=T(self.cp_slot, np.uint16),
             cp_spill=T(self.cp_spill, np.uint16), cp_meta=T(self.cp_meta, np.uint32),
             cp_succ=T(self.cp_succ_abs, np.uint16), group_off=T(self.group_off, np.int32),
@@ -217,7 +229,8 @@ class ClassTables(Tables):
         p = native.ptr
         self.sim_struct = native.SimTables(lg.n, lg.n_devices, self.n_edges, p(t["meta"]), p(lg.t_succ_off),
                                            p(t["succ"]), p(t["cidx"]), p(t["cnt_init"]), self.counter_words,
-                                           self.counter_bits, p(t["pos"]), p(lg.t_sources), lg.n_sources, self.QCAP,
+                                           self.counter_bits, p(t["rank16"]), p(t["eng_sources"]), lg.n_sources,
+                                           self.QCAP,
                                            p(lg.t_dev), int(self.succ_packed))
         self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
                                          p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),

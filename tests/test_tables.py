@@ -110,19 +110,25 @@ def test_engine_tables_packing(seed):
     t = Tables(len(h["ids"]), len(h["devices"]), h["succ_off"], h["succ_idx"], h["indeg"], h["device"])
     indeg, off, idx, dev = h["indeg"], h["succ_off"], h["succ_idx"], h["device"]
     per, bits = 32 // t.counter_bits, t.counter_bits
-    for v in range(t.n):
-        m = int(t.meta[v])
-        assert m & 0xFFFFFF == off[v] and (m >> 24) == off[v + 1] - off[v]
-        if indeg[v] >= 2:
-            c = int(t.cidx[v])
-            word = int(t.cnt_init[c // per])
-            assert (word >> ((c % per) * bits)) & ((1 << bits) - 1) == indeg[v]
-    for j in range(t.n_edges):
-        e = int(t.succ[j])
-        if t.succ_packed:
-            m, d, single, c = e & 0x1FFF, (e >> 13) & 31, (e >> 18) & 1, e >> 19
-            if indeg[m] >= 2:
-                assert c == t.cidx[m]
-        else:
-            m, d, single = e & 0xFFFF, (e >> 16) & 31, (e >> 21) & 1
-        assert m == idx[j] and d == dev[m] and single == (indeg[m] == 1)
+    pos, rank = t.pos, t.rank_of_pos
+    for p in range(t.n):  # engine tables are numbered by level position
+        v = int(rank[p])
+        m = int(t.meta[p])
+        b, d = m & 0xFFFFFF, m >> 24
+        assert d == off[v + 1] - off[v]
+        got = []
+        for j in range(b, b + d):
+            e = int(t.succ[j])
+            if t.succ_packed:
+                mp, dv, single, c = e & 0x1FFF, (e >> 13) & 31, (e >> 18) & 1, e >> 19
+            else:
+                mp, dv, single, c = e & 0xFFFF, (e >> 16) & 31, (e >> 21) & 1, int(t.cidx[e & 0xFFFF])
+            mr = int(rank[mp])
+            assert dv == dev[mr] and single == (indeg[mr] == 1)
+            if indeg[mr] >= 2:
+                word = int(t.cnt_init[c // per])
+                assert (word >> ((c % per) * bits)) & ((1 << bits) - 1) == indeg[mr]
+            got.append(mr)
+        assert got == list(idx[off[v]:off[v + 1]])
+    assert [int(rank[p]) for p in t.eng_sources] == [v for v in range(t.n) if indeg[v] == 0]
+    assert (pos[rank] == np.arange(t.n)).all()
