@@ -284,6 +284,14 @@ int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t
 int dfsim_critical_path_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *start,
                               const double *finish, double *cp_len, int32_t *cp_path, int32_t *cp_path_len);
 
+/* K4 wide, for graphs beyond dfsim_critical_path_levels (N > 65535): one CTA per candidate
+ * walks the levels in reverse (order[N]: ranks grouped by level, level_off[n_levels+1]; every
+ * edge goes to a higher level), one thread per node of a level.  cp_len[s]; cp_src[s] = rank
+ * of the path's start node (optional).  start NULL: finish holds durations.  [n_sims][N] by rank. */
+int dfsim_critical_path_wide(dfsim_ctx *ctx, const dfsim_graph *g, const int32_t *order, const int32_t *level_off,
+                             int32_t n_levels, int64_t n_sims, const double *start, const double *finish,
+                             double *cp_len, int32_t *cp_src);
+
 /* ---------------------------------------------------------------- best strategy (K5) */
 /* First minimum of (value, index) over n values; index = index_base + i.
  * Writes one 16-byte record {double value; int64_t index} to out_record (device). */

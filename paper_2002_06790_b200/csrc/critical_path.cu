@@ -9,6 +9,8 @@
 // uniform and the per-node suffix values (layout [node][sim]) are coalesced.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace {
@@ -167,4 +169,117 @@ extern "C" int dfsim_critical_path_batch(dfsim_ctx *ctx, const dfsim_graph *g, i
         if (rc) return rc;
     }
     return DFSIM_OK;
+}
+
+// ------------------------------------------------------------------ K4 wide (large graphs)
+//
+// The same suffix DP, parallel inside a candidate: one CTA walks the class's levels
+// in reverse (every edge goes from a lower to a higher level), one thread per node of
+// the level.  Values of one level are final before the barrier that ends it, so each
+// value is still one exact max and one add (order-independent).  Suffix
+// values live in a global row per resident CTA (L2: one level's neighbourhood at a time).
+namespace {
+
+struct CpWideArgs {
+    int32_t N;
+    const int32_t *succ_off, *succ_idx;
+    const int32_t *order, *level_off;  // ranks by level; level_off[n_levels + 1]
+    int32_t n_levels;
+    int64_t S;
+    const double *start, *finish;      // [S][N] by rank; start NULL: finish holds durations
+    double *cp_len;
+    int32_t *cp_src;
+    double *suffix;                    // [gridDim.x][N]
+};
+
+__global__ void __launch_bounds__(1024) k_critical_path_wide(CpWideArgs a) {
+    __shared__ double s_len[32];
+    __shared__ int32_t s_src[32];
+    const int32_t N = a.N;
+    double *suf = a.suffix + static_cast<int64_t>(blockIdx.x) * N;
+    for (int64_t s = blockIdx.x; s < a.S; s += gridDim.x) {
+        const double *st = a.start ? a.start + s * N : nullptr;
+        const double *fi = a.finish + s * N;
+        double len = 0.0;
+        int32_t src = 0x7fffffff;
+        for (int32_t L = a.n_levels - 1; L >= 0; L--) {
+            const int32_t p1 = __ldg(a.level_off + L + 1);
+            for (int32_t p = __ldg(a.level_off + L) + threadIdx.x; p < p1; p += blockDim.x) {
+                const int32_t v = __ldg(a.order + p);
+                const double d = st ? __dsub_rn(fi[v], st[v]) : fi[v];  // finish - start (reporting.py:128)
+                double best = 0.0;  // max(0.0, .) (graph.py:465-468)
+                const int32_t e1 = __ldg(a.succ_off + v + 1);
+                for (int32_t j = __ldg(a.succ_off + v); j < e1; j++) {
+                    const double x = suf[__ldg(a.succ_idx + j)];
+                    if (x > best) best = x;
+                }
+                const double sv = __dadd_rn(d, best);
+                suf[v] = sv;
+                // level 0 == the sources: length = max, start node = the min id reaching it (graph.py:471-474)
+                if (L == 0 && (src == 0x7fffffff || sv > len || (sv == len && v < src))) {
+                    len = sv;
+                    src = v;
+                }
+            }
+            __syncthreads();
+        }
+        // block reduction of (len max, src min among equal)
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ol = __shfl_xor_sync(DFSIM_FULL_MASK, len, o);
+            const int32_t os = __shfl_xor_sync(DFSIM_FULL_MASK, src, o);
+            if (os != 0x7fffffff && (src == 0x7fffffff || ol > len || (ol == len && os < src))) {
+                len = ol;
+                src = os;
+            }
+        }
+        if (lane == 0) {
+            s_len[w] = len;
+            s_src[w] = src;
+        }
+        __syncthreads();
+        if (w == 0) {
+            const int nw = blockDim.x >> 5;
+            len = lane < nw ? s_len[lane] : 0.0;
+            src = lane < nw ? s_src[lane] : 0x7fffffff;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ol = __shfl_xor_sync(DFSIM_FULL_MASK, len, o);
+                const int32_t os = __shfl_xor_sync(DFSIM_FULL_MASK, src, o);
+                if (os != 0x7fffffff && (src == 0x7fffffff || ol > len || (ol == len && os < src))) {
+                    len = ol;
+                    src = os;
+                }
+            }
+            if (lane == 0) {
+                a.cp_len[s] = src == 0x7fffffff ? 0.0 : len;
+                if (a.cp_src) a.cp_src[s] = src == 0x7fffffff ? -1 : src;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+extern "C" int dfsim_critical_path_wide(dfsim_ctx *ctx, const dfsim_graph *g, const int32_t *order,
+                                        const int32_t *level_off, int32_t n_levels, int64_t n_sims,
+                                        const double *start, const double *finish, double *cp_len,
+                                        int32_t *cp_src) {
+    if (!ctx || !g) return DFSIM_BAD_ARGUMENT;
+    DFSIM_ARG_CHECK(ctx, g->n_nodes >= 0 && n_sims >= 0 && n_levels >= 0, "negative sizes");
+    DFSIM_ARG_CHECK(ctx, cp_len && finish && (g->n_nodes == 0 || (order && level_off)), "null argument");
+    if (n_sims == 0) return DFSIM_OK;
+    DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const int32_t N = g->n_nodes;
+    const int threads = 1024;
+    int64_t grid = std::min<int64_t>(n_sims, static_cast<int64_t>(ctx->num_sms) * 2);
+    void *scratch = nullptr;
+    int rc = dfsim_scratch(ctx, static_cast<size_t>(grid) * std::max(N, 1) * sizeof(double), &scratch);
+    if (rc) return rc;
+    CpWideArgs a{N, g->succ_off, g->succ_idx, order, level_off, n_levels, n_sims, start, finish, cp_len, cp_src,
+                 static_cast<double *>(scratch)};
+    k_critical_path_wide<<<static_cast<int>(grid), threads, 0, ctx->stream>>>(a);
+    return dfsim_after_launch(ctx, "k_critical_path_wide");
 }

@@ -157,6 +157,24 @@ class LoweredGraph:
                                    max_indeg)
         return self
 
+    def levels(self):
+        """(order, level_off, n_levels) of the Kahn waves as device int32 tensors (cached);
+        K4 wide walks them in reverse.  None for a cyclic graph."""
+        if getattr(self, "_levels", None) is None:
+            from .prepare import level_order
+
+            off = self.t_succ_off[: self.n + 1].cpu().numpy().astype(np.int64)
+            idx = self.t_succ_idx[: self.n_edges].cpu().numpy().astype(np.int64)
+            indeg = self.t_indeg[: self.n].cpu().numpy().astype(np.int64)
+            lo = level_order(self.n, off, idx, indeg)
+            if lo is None:
+                return None
+            order, _, loff = lo
+            d = self.ctx.device
+            self._levels = (_dev_tensor(order if len(order) else np.zeros(1, np.int32), d, np.int32),
+                            _dev_tensor(loff, d, np.int32), len(loff) - 1)
+        return self._levels
+
     def rank_of(self):
         if self.rank is None:
             self.rank = {nid: i for i, nid in enumerate(self.ids)}

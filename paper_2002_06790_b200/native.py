@@ -101,6 +101,7 @@ _SIGNATURES = {
                                             P]),
     "dfsim_simulate_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P]),
     "dfsim_critical_path_batch": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, P, P, P, P]),
+    "dfsim_critical_path_wide": (ctypes.c_int, [P, ctypes.POINTER(Graph), P, P, I32, I64, P, P, P, P]),
     "dfsim_simulate_batch_ex": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P, P, P, I32]),
     "dfsim_resolve_variants": (ctypes.c_int, [P, I32, ctypes.POINTER(ProfileTables), I32, P, P, P, P, P, P]),
     "dfsim_simulate_fused": (ctypes.c_int, [P, ctypes.POINTER(SimTables), ctypes.POINTER(FusedStrategies), P, P, P,

@@ -53,6 +53,9 @@ def simulate_arrays(lg: LoweredGraph, dur, *, schedule: bool = True, busy: bool 
     return o
 
 
+WIDE_CP_NODES = 65536  # from here on one CTA per candidate beats one thread per candidate
+
+
 def critical_path_arrays(lg: LoweredGraph, start, finish, *, paths: bool = False, out=None) -> dict:
     """K4 over [S, N] schedules (``start`` None: ``finish`` holds plain durations)."""
     torch = _torch()
@@ -62,6 +65,11 @@ def critical_path_arrays(lg: LoweredGraph, start, finish, *, paths: bool = False
     dev = finish.device
     o = out if out is not None else {}
     o.setdefault("cp_len", torch.empty(S, dtype=torch.float64, device=dev))
+    if not paths and lg.n >= WIDE_CP_NODES and lg.levels() is not None:
+        order, loff, n_levels = lg.levels()  # K4 wide: level-parallel inside each candidate
+        lg.ctx.call("dfsim_critical_path_wide", native.ctypes.byref(lg.struct), native.ptr(order), native.ptr(loff),
+                    n_levels, S, native.ptr(start), native.ptr(finish), native.ptr(o["cp_len"]), native.P(0))
+        return o
     if paths:
         o.setdefault("cp_path", torch.empty((S, max(lg.n, 1)), dtype=torch.int32, device=dev))
         o.setdefault("cp_path_len", torch.empty(S, dtype=torch.int32, device=dev))
