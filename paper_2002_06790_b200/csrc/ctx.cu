@@ -30,6 +30,7 @@ extern "C" int dfsim_ctx_destroy(dfsim_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->aux) cudaFree(ctx->aux);
     if (ctx->host_small) cudaFreeHost(ctx->host_small);
     delete ctx;
     return DFSIM_OK;
@@ -57,16 +58,22 @@ int dfsim_after_launch(dfsim_ctx *ctx, const char *what) {
     return DFSIM_OK;
 }
 
-int dfsim_scratch(dfsim_ctx *ctx, size_t bytes, void **out) {
-    if (bytes > ctx->scratch_bytes) {
+static int grow(dfsim_ctx *ctx, void **buf, size_t *have, size_t bytes, void **out) {
+    if (bytes > *have) {
         DFSIM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-        if (ctx->scratch) DFSIM_CUDA_TRY(ctx, cudaFree(ctx->scratch));
-        ctx->scratch = nullptr;
-        ctx->scratch_bytes = 0;
+        if (*buf) DFSIM_CUDA_TRY(ctx, cudaFree(*buf));
+        *buf = nullptr;
+        *have = 0;
         size_t grown = bytes + bytes / 4 + (1 << 20);
-        DFSIM_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, grown));
-        ctx->scratch_bytes = grown;
+        DFSIM_CUDA_TRY(ctx, cudaMalloc(buf, grown));
+        *have = grown;
     }
-    *out = ctx->scratch;
+    *out = *buf;
     return DFSIM_OK;
 }
+
+int dfsim_scratch(dfsim_ctx *ctx, size_t bytes, void **out) {
+    return grow(ctx, &ctx->scratch, &ctx->scratch_bytes, bytes, out);
+}
+
+int dfsim_aux(dfsim_ctx *ctx, size_t bytes, void **out) { return grow(ctx, &ctx->aux, &ctx->aux_bytes, bytes, out); }

@@ -16,6 +16,10 @@ struct dfsim_ctx {
     // growable device scratch (per-warp engine state in global mode, CP suffix values, cub temp)
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
+    // second growable device buffer for small per-call arrays that must survive a
+    // dfsim_scratch reallocation inside the same call (e.g. overflow flags)
+    void *aux = nullptr;
+    size_t aux_bytes = 0;
     // pinned host staging for small synchronous results
     void *host_small = nullptr;
     std::string last_error;
@@ -45,6 +49,8 @@ struct dfsim_ctx {
 int dfsim_after_launch(dfsim_ctx *ctx, const char *what);
 // Grow ctx->scratch to at least `bytes` (stream-ordered: synchronises the stream first).
 int dfsim_scratch(dfsim_ctx *ctx, size_t bytes, void **out);
+// Grow ctx->aux (same rules); independent of ctx->scratch.
+int dfsim_aux(dfsim_ctx *ctx, size_t bytes, void **out);
 
 // ------------------------------------------------------------------ device helpers
 

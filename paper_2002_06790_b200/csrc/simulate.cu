@@ -39,6 +39,7 @@ struct SimArgs {
     const int32_t *pos;       // optional output column per node
     const int64_t *out_rows;  // optional output row per simulated row
     int32_t interleaved;      // start points at (start, finish) pairs; finish unused
+    const int32_t *redo;      // optional: simulate only rows s with redo[s] != 0
 };
 
 template <int kBits>
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
     const int my_qoff = lane < D ? __ldg(a.queue_off + lane) : 0;
 
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * wpb + wib; s < a.S; s += static_cast<int64_t>(gridDim.x) * wpb) {
+        if (a.redo && !a.redo[s]) continue;
         const double *dur = a.dur + s * a.dur_stride;
         const int64_t row = a.out_rows ? a.out_rows[s] : s;
         double *out_start = a.start ? a.start + row * N * (a.interleaved ? 2 : 1) : nullptr;
@@ -216,6 +218,14 @@ int launch_bits(dfsim_ctx *ctx, SimArgs &a, bool shared_mode, int wpb, int grid,
 
 }  // namespace
 
+int dfsim_simulate_large(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                         int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
+                         int32_t *n_placed);
+static int simulate_exact(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                          int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
+                          int32_t *n_placed, const int32_t *pos, const int64_t *out_rows, int32_t interleaved,
+                          const int32_t *redo, bool allow_large);
+
 extern "C" int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
                                     int64_t dur_stride, double *start, double *finish, double *makespan,
                                     double *busy, int32_t *n_placed) {
@@ -223,10 +233,10 @@ extern "C" int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_
                                    nullptr, 0);
 }
 
-extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
-                                       int64_t dur_stride, double *start, double *finish, double *makespan,
-                                       double *busy, int32_t *n_placed, const int32_t *pos, const int64_t *out_rows,
-                                       int32_t interleaved) {
+static int simulate_exact(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                          int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
+                          int32_t *n_placed, const int32_t *pos, const int64_t *out_rows, int32_t interleaved,
+                          const int32_t *redo, bool allow_large) {
     if (!ctx || !g) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, g->n_nodes >= 0 && n_sims >= 0, "negative sizes");
     DFSIM_ARG_CHECK(ctx, g->n_devices >= 0 && g->n_devices <= 32, "the warp engine supports at most 32 devices");
@@ -246,7 +256,7 @@ extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int
     a.sources = g->sources; a.queue_off = g->queue_off; a.n_sources = g->n_sources;
     a.S = n_sims; a.dur = dur; a.dur_stride = dur_stride;
     a.start = start; a.finish = finish; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed;
-    a.pos = pos; a.out_rows = out_rows; a.interleaved = interleaved;
+    a.pos = pos; a.out_rows = out_rows; a.interleaved = interleaved; a.redo = redo;
     const int per = 32 / bits;
     a.cnt_words = (N + per - 1) / per;
     const bool q16 = N <= 65536;
@@ -259,6 +269,8 @@ extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int
     bool shared_mode = true;
     while (wpb > 1 && wpb * (a.per_warp + 128) > kSmemBudget) wpb >>= 1;
     if (wpb * (a.per_warp + 128) > kSmemBudget) { shared_mode = false; wpb = 4; }
+    if (!shared_mode && allow_large && !pos && !out_rows && !interleaved)  // K3 large (simulate_large.cu)
+        return dfsim_simulate_large(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed);
     size_t smem = (size_t)wpb * 128 + (shared_mode ? (size_t)wpb * a.per_warp : 0);
 
     int blocks_per_sm = 1;
@@ -285,4 +297,20 @@ extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int
                                : launch_bits<16, uint32_t>(ctx, a, shared_mode, wpb, grid, smem);
     return q16 ? launch_bits<32, uint16_t>(ctx, a, shared_mode, wpb, grid, smem)
                : launch_bits<32, uint32_t>(ctx, a, shared_mode, wpb, grid, smem);
+}
+
+extern "C" int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                                       int64_t dur_stride, double *start, double *finish, double *makespan,
+                                       double *busy, int32_t *n_placed, const int32_t *pos, const int64_t *out_rows,
+                                       int32_t interleaved) {
+    return simulate_exact(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed, pos, out_rows,
+                          interleaved, nullptr, true);
+}
+
+// The exact-capacity engine over the rows flagged in redo (ring overflows of K3 large).
+int dfsim_simulate_exact_flagged(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                                 int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
+                                 int32_t *n_placed, const int32_t *redo) {
+    return simulate_exact(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed, nullptr, nullptr,
+                          0, redo, false);
 }

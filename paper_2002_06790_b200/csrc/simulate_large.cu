@@ -1,0 +1,278 @@
+// K3 large: the exact event loop (engine.py:96-146) for graphs whose per-candidate
+// state cannot live in shared memory (C5: 1M nodes), one warp per candidate.
+//
+// With a few hundred candidates per GPU each candidate is one long serial chain of
+// event iterations (~N of them), so the design goal is the latency of one iteration,
+// not bandwidth.  Against the exact-capacity engine (simulate.cu, global mode) it
+// removes every dependent global round trip from the iteration:
+//   * FIFO rings in shared memory hold (node, duration) pairs: a pop needs no global
+//     load.  Ring occupancy is checked before every pop (a device only gains entries
+//     until its next pop); an overflowed candidate is re-run by the exact engine.
+//   * While a node runs, its lane prefetches, one stage per iteration, the successor
+//     range, up to kPre successor ids, and their devices and durations; at finish the
+//     relax step reads registers only (longer lists fall back to direct loads).
+//   * Dependency counters are plain byte/short loads and stores in a global row per
+//     warp, L1-resident for the active frontier.  Lanes relaxing the same node in one
+//     iteration are combined with __match_any_sync (the leader subtracts the group
+//     size), so no atomics are needed: one warp owns the row.
+// The iteration itself is the reference's: now = min finish (exact, via redux over the
+// IEEE bits of non-negative doubles), every device finishing at `now` releases its
+// successors, each device's newly ready nodes are appended in rank order, idle devices
+// pop at `now` (start == now).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+
+int dfsim_simulate_exact_flagged(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                                 int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
+                                 int32_t *n_placed, const int32_t *redo);
+
+namespace {
+
+constexpr int kPre = 4;  // successors prefetched per running node
+
+struct LargeArgs {
+    int32_t N, D;
+    const int32_t *succ_off, *succ_idx, *indeg, *device, *sources;
+    int32_t n_sources;
+    int64_t S;
+    const double *dur;
+    int64_t dur_stride;
+    double *start, *finish, *makespan, *busy;
+    int32_t *n_placed;
+    int32_t *redo;             // [S] 1 when the candidate overflowed a ring
+    unsigned char *gcnt;       // counters, cnt_bytes per resident warp
+    int64_t cnt_bytes;
+    int32_t qcap;              // ring entries per device (power of two)
+    int32_t warp_smem;         // bytes of shared state per warp
+};
+
+__device__ __forceinline__ double warp_min_nonneg(double x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned hi = __reduce_min_sync(DFSIM_FULL_MASK, static_cast<unsigned>(b >> 32));
+    const unsigned lo = __reduce_min_sync(DFSIM_FULL_MASK, static_cast<unsigned>(b >> 32) == hi
+                                                               ? static_cast<unsigned>(b) : 0xffffffffu);
+    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
+}
+
+template <typename CT>
+__global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int N = a.N, D = a.D, QC = a.qcap;
+    const unsigned QM = static_cast<unsigned>(QC - 1);
+    unsigned char *ws = smem + static_cast<size_t>(wib) * a.warp_smem;
+    int32_t *tails = reinterpret_cast<int32_t *>(ws);                  // [32]
+    double *rdur = reinterpret_cast<double *>(ws + 128);               // [D][QC]
+    int32_t *rnode = reinterpret_cast<int32_t *>(rdur + static_cast<size_t>(D) * QC);  // [D][QC]
+    CT *cnt = reinterpret_cast<CT *>(a.gcnt + (static_cast<int64_t>(blockIdx.x) * wpb + wib) * a.cnt_bytes);
+
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * wpb + wib; s < a.S; s += static_cast<int64_t>(gridDim.x) * wpb) {
+        const double *dur = a.dur + s * a.dur_stride;
+        double *out_s = a.start ? a.start + s * N : nullptr;
+        double *out_f = a.finish ? a.finish + s * N : nullptr;
+        for (int v = lane; v < N; v += 32) cnt[v] = static_cast<CT>(__ldg(a.indeg + v));
+        if (lane < D) tails[lane] = 0;
+        __syncwarp();
+        // sources in rank order (engine.py:111-114)
+        for (int b = 0; b < a.n_sources; b += 32) {
+            const int i = b + lane;
+            const bool has = i < a.n_sources;
+            const int v = has ? __ldg(a.sources + i) : 0;
+            const int dv = has ? __ldg(a.device + v) : 32 + lane;
+            const double dd = has ? __ldg(dur + v) : 0.0;
+            const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, dv);
+            const int base = has ? tails[dv] : 0;
+            __syncwarp();
+            if (has) {
+                const int p = base + __popc(peers & lanemask_lt());
+                rnode[dv * QC + (p & QM)] = v;
+                rdur[dv * QC + (p & QM)] = dd;
+                if ((peers & lanemask_lt()) == 0) tails[dv] = base + __popc(peers);
+            }
+            __syncwarp();
+        }
+        bool ovf = lane < D && tails[lane] > QC;
+
+        unsigned head = 0;
+        bool running = false;
+        int run_v = 0, stage = 0, j0 = 0, j1 = 0;
+        int pm[kPre];
+        unsigned pdev = 0;  // 5 bits per prefetched successor
+        double pdur[kPre];
+        double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
+        int placed = 0;
+#pragma unroll
+        for (int k = 0; k < kPre; k++) { pm[k] = 0; pdur[k] = 0.0; }
+
+        auto prefetch_step = [&]() {  // one stage per call; loads land while the node runs
+            if (stage == 1) {
+#pragma unroll
+                for (int k = 0; k < kPre; k++) pm[k] = j0 + k < j1 ? __ldg(a.succ_idx + j0 + k) : 0;
+                stage = 2;
+            } else if (stage == 2) {
+                pdev = 0;
+#pragma unroll
+                for (int k = 0; k < kPre; k++) {
+                    if (j0 + k < j1) {
+                        pdev |= static_cast<unsigned>(__ldg(a.device + pm[k])) << (5 * k);
+                        pdur[k] = __ldg(dur + pm[k]);
+                    }
+                }
+                stage = 3;
+            }
+        };
+        auto start_idle = [&]() {
+            const int t = lane < D ? tails[lane] : 0;
+            if (lane < D && !running && static_cast<int>(head) < t) {
+                ovf |= static_cast<unsigned>(t) - head > static_cast<unsigned>(QC);
+                const int slot = lane * QC + static_cast<int>(head & QM);
+                const int v = rnode[slot];
+                const double f = __dadd_rn(now, rdur[slot]);
+                head++;
+                if (out_s) {
+                    out_s[v] = now;
+                    out_f[v] = f;
+                }
+                running = true;
+                run_v = v;
+                run_f = f;
+                busy_sum = __dadd_rn(busy_sum, __dsub_rn(f, now));
+                if (f > span) span = f;
+                placed++;
+                j0 = __ldg(a.succ_off + v);
+                j1 = __ldg(a.succ_off + v + 1);
+                stage = 1;
+            }
+        };
+
+        start_idle();
+        while (__any_sync(DFSIM_FULL_MASK, running)) {
+            now = warp_min_nonneg(running ? run_f : __longlong_as_double(0x7ff0000000000000LL));
+            const bool done = running && run_f == now;
+            const int seg_lo = lane < D ? tails[lane] : 0;
+            if (running && !done) prefetch_step();
+            int deg = 0;
+            if (done) {
+                running = false;
+                while (stage < 3) prefetch_step();
+                deg = j1 - j0;
+            }
+            // relax in rounds: round r handles successor r of every finishing device
+            const int rounds = __reduce_max_sync(DFSIM_FULL_MASK, static_cast<unsigned>(deg));
+            for (int r = 0; r < rounds; r++) {
+                const bool act = r < deg;
+                const unsigned am = __ballot_sync(DFSIM_FULL_MASK, act);
+                if (act) {
+                    int m, dv;
+                    double dd;
+                    if (r < kPre) {
+                        m = pm[0];
+                        dv = static_cast<int>(pdev & 31u);
+                        dd = pdur[0];
+#pragma unroll
+                        for (int k = 1; k < kPre; k++)
+                            if (r == k) { m = pm[k]; dv = static_cast<int>((pdev >> (5 * k)) & 31u); dd = pdur[k]; }
+                    } else {
+                        m = __ldg(a.succ_idx + j0 + r);
+                        dv = __ldg(a.device + m);
+                        dd = __ldg(dur + m);
+                    }
+                    const unsigned grp = __match_any_sync(am, m);
+                    if ((grp & lanemask_lt()) == 0) {  // group leader: one plain read-modify-write
+                        const int k = __popc(grp);
+                        const int c = static_cast<int>(cnt[m]);
+                        cnt[m] = static_cast<CT>(c - k);
+                        if (c == k) {
+                            const int p = atomicAdd(tails + dv, 1);
+                            rnode[dv * QC + (p & QM)] = m;
+                            rdur[dv * QC + (p & QM)] = dd;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            const int seg_hi = lane < D ? tails[lane] : 0;
+            if (seg_hi - seg_lo > 1) {  // enqueue(sorted(newly_ready)) (engine.py:139-142)
+                for (int i = seg_lo + 1; i < seg_hi; i++) {
+                    const int xs = lane * QC + (i & QM);
+                    const int x = rnode[xs];
+                    const double xd = rdur[xs];
+                    int j = i - 1;
+                    while (j >= seg_lo && rnode[lane * QC + (j & QM)] > x) {
+                        rnode[lane * QC + ((j + 1) & QM)] = rnode[lane * QC + (j & QM)];
+                        rdur[lane * QC + ((j + 1) & QM)] = rdur[lane * QC + (j & QM)];
+                        j--;
+                    }
+                    rnode[lane * QC + ((j + 1) & QM)] = x;
+                    rdur[lane * QC + ((j + 1) & QM)] = xd;
+                }
+            }
+            __syncwarp();
+            start_idle();
+        }
+        const bool bad = __any_sync(DFSIM_FULL_MASK, ovf);
+        const double ms = warp_max_f64(span);
+        const int total = warp_sum_i32(placed);
+        if (lane == 0) {
+            a.makespan[s] = ms;
+            if (a.n_placed) a.n_placed[s] = total;
+            a.redo[s] = bad ? 1 : 0;
+        }
+        if (a.busy && lane < D) a.busy[s * D + lane] = busy_sum;
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+// Called by dfsim_simulate_batch_ex for graphs beyond the shared-memory engine with the
+// plain [S][N] layout.  Returns DFSIM_OK after queueing the kernel and the exact re-run
+// of any overflowed candidate (stream-ordered; no host synchronisation).
+int dfsim_simulate_large(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
+                         int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
+                         int32_t *n_placed) {
+    const int32_t N = g->n_nodes, D = g->n_devices;
+    const int cbytes = g->max_indeg < 255 ? 1 : (g->max_indeg < 65535 ? 2 : 4);
+    int wpb = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, (n_sims + ctx->num_sms - 1) / ctx->num_sms)));
+    const int budget = 220 * 1024 / wpb;
+    // small rings: the rest of the SM's 256 KB stays L1 for the counter rows' active frontier
+    int qcap = 512;
+    while (qcap > 16 && 128 + static_cast<int64_t>(std::max(D, 1)) * qcap * 12 > budget) qcap >>= 1;
+    const int warp_smem = (128 + std::max(D, 1) * qcap * 12 + 15) / 16 * 16;
+    const int64_t want = (n_sims + wpb - 1) / wpb;
+    const int grid = static_cast<int>(std::min<int64_t>(want, ctx->num_sms));
+    const int64_t cnt_bytes = (static_cast<int64_t>(N) * cbytes + 127) / 128 * 128;
+    void *p = nullptr, *redo = nullptr;
+    int rc = dfsim_scratch(ctx, static_cast<size_t>(grid) * wpb * cnt_bytes, &p);
+    if (rc) return rc;
+    rc = dfsim_aux(ctx, sizeof(int32_t) * n_sims, &redo);
+    if (rc) return rc;
+    LargeArgs a;
+    a.N = N; a.D = D;
+    a.succ_off = g->succ_off; a.succ_idx = g->succ_idx; a.indeg = g->indeg; a.device = g->device;
+    a.sources = g->sources; a.n_sources = g->n_sources;
+    a.S = n_sims; a.dur = dur; a.dur_stride = dur_stride;
+    a.start = start; a.finish = finish; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed;
+    a.gcnt = static_cast<unsigned char *>(p);
+    a.redo = static_cast<int32_t *>(redo);
+    a.cnt_bytes = cnt_bytes;
+    a.qcap = qcap;
+    a.warp_smem = warp_smem;
+    const size_t smem = static_cast<size_t>(wpb) * warp_smem;
+    auto launch = [&](auto kern) -> int {
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                 static_cast<int>((smem * 100 + 228 * 1024 - 1) / (228 * 1024))));
+        kern<<<grid, wpb * 32, smem, ctx->stream>>>(a);
+        return dfsim_after_launch(ctx, "k_simulate_large");
+    };
+    rc = cbytes == 1 ? launch(k_simulate_large<uint8_t>)
+                     : (cbytes == 2 ? launch(k_simulate_large<uint16_t>) : launch(k_simulate_large<uint32_t>));
+    if (rc) return rc;
+    // exact re-run of ring overflows (flags in ctx->aux survive the exact engine's scratch growth)
+    return dfsim_simulate_exact_flagged(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed,
+                                        a.redo);
+}

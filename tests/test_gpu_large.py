@@ -67,3 +67,51 @@ def test_wide_cp_layered_dag_vs_oracle():
     assert torch.equal(cp, ref["cp_len"]) and torch.equal(src, ref["cp_path"][:, 0])
     want = O.critical_path(g, {nid: d[0, i] for i, nid in enumerate(lg.ids)})
     assert float(cp[0]) == want[0] and lg.ids[int(src[0])] == want[1][0]
+
+
+def _check_engine(g, rows):
+    import torch
+
+    from oracle import native_oracle as NO
+    from paper_2002_06790_b200.lowering import LoweredGraph
+    from paper_2002_06790_b200.simulator import critical_path_arrays, simulate_arrays
+
+    lg = LoweredGraph(g, 0)
+    csr = NO.Csr(g)
+    assert list(csr.ids) == list(lg.ids)
+    o = simulate_arrays(lg, torch.tensor(np.stack(rows), device="cuda:0"))
+    cp = critical_path_arrays(lg, o["start"], o["finish"])["cp_len"].cpu().numpy()
+    st, fi = o["start"].cpu().numpy(), o["finish"].cpu().numpy()
+    for s, row in enumerate(rows):
+        rc, ws, wf, wbusy, wms, _ = NO.simulate(csr, row)
+        assert rc == 0 and int(o["n_placed"][s]) == lg.n
+        assert np.array_equal(st[s, : lg.n], ws) and np.array_equal(fi[s, : lg.n], wf), s
+        assert float(o["makespan"][s]) == wms
+        assert np.array_equal(o["busy"][s, : lg.n_devices].cpu().numpy(), wbusy)
+        assert cp[s] == NO.critical_path(csr, wf - ws)[1]
+
+
+def test_large_engine_matches_c_oracle():
+    """K3 large (smem rings, prefetched successors, plain counters) == the C oracle."""
+    from paper_2002_06790_b200 import workloads as W
+
+    g = W.layered_dag(150_000, 500, devices=8)
+    rng = np.random.default_rng(5)
+    n = len(g.nodes)
+    rows = [rng.uniform(0.5, 30, n), rng.integers(1, 5, n).astype(np.float64),
+            np.where(rng.random(n) < 0.3, 0.0, rng.uniform(0, 3, n)), np.round(rng.uniform(0, 8, n) * 4) / 4]
+    _check_engine(g, rows)
+
+
+def test_large_engine_ring_overflow_falls_back():
+    """A fan-out of 9,000 ready nodes on one device and 100,000 sources on another overflow
+    the shared-memory rings; those candidates are re-run exactly."""
+    from paper_2002_06790_b200.model import DeviceSpec, OpNode, make_graph
+
+    nodes = [OpNode("a", "Op", "gpu0")]
+    nodes += [OpNode(f"b{i:05d}", "Op", "gpu0", inputs=(("a", 0),)) for i in range(9000)]
+    nodes += [OpNode(f"c{i:06d}", "Op", "gpu1") for i in range(100_000)]
+    g = make_graph(nodes, [DeviceSpec("gpu0", "Compute"), DeviceSpec("gpu1", "Compute")])
+    rng = np.random.default_rng(2)
+    n = len(nodes)
+    _check_engine(g, [rng.uniform(0.5, 3, n), np.ones(n)])
