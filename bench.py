@@ -4,8 +4,9 @@ Default workload (BASELINE.json configs[1], `--workload resnet50-dp8`): ResNet-5
 training graph (564 nodes/replica), data-parallel over 8 workers, one ring allreduce
 per parameter gradient over the (synthetic) NVLink link model.  Candidates =
 hardware tag (8 planted profile sets) x op_gap_us grid, one topology class.
-Other workloads: `bert-large-dp8` (configs[3]), `vgg16-sweep` (configs[2]: 209 batch
-sizes x 8 worker counts x PS/allreduce x PCIe/NVLink/RDMA = 10,032 candidates in 48
+Other workloads: `bert-large-ps-ar` (configs[3]: BERT-large, {PS, allreduce} x {2, 4, 8}
+workers x {PCIe, NVLink, RDMA}, 18 topology classes), `vgg16-sweep` (configs[2]: 209 batch
+sizes x 8 worker counts x PS/allreduce x PCIe/NVLink/RDMA = 10,032 candidates in 45
 topology classes), `dag1m` (configs[4]: 1M-node DAG).
 
 One step = the hot path over one batch, per topology class: K1 expand (device) ->
@@ -38,8 +39,8 @@ WORKLOADS = {  # name -> (BASELINE.json config, default candidates per GPU)
     "resnet50-dp8": ("ResNet-50 training graph, data-parallel 8 workers, ring allreduce over NVLink link model", 65536),
     "vgg16-sweep": ("VGG-16 strategy sweep: 10k candidates over batch size x worker count x PS/allreduce x "
                     "PCIe/NVLink/RDMA", 10032),
-    "bert-large-dp8": ("BERT-large graph, parameter-server vs allreduce with per-layer gradient comm overlap "
-                       "(allreduce arm, 8 workers over NVLink)", 16384),
+    "bert-large-ps-ar": ("BERT-large graph, parameter-server vs allreduce with per-layer gradient comm overlap",
+                         16384),
     "dag1m": ("synthetic 1M-node DAG x 4096 candidate strategies sharded across 8 GPUs with NCCL argmin", 512),
 }
 WORKLOAD = "resnet50-dp8"
@@ -74,7 +75,7 @@ def build_workload(rank: int, sims: int, workload: str = WORKLOAD):
             graphs = [W.vgg16_training(batch=b) for b in VGG_BATCHES]
             _CACHE[workload] = (graphs, W.model_profiles(graphs[0], HW_TAGS[:1]))
         else:
-            g = W.resnet50_training(batch=32) if workload == "resnet50-dp8" else W.bert_large_training()
+            g = W.resnet50_training(batch=32) if workload == "resnet50-dp8" else W.bert_large_training()  # C2 / C4
             _CACHE[workload] = ([g], W.model_profiles(g, HW_TAGS))
     graphs, db = _CACHE[workload]
     configs, graph_of = [], []
@@ -89,6 +90,21 @@ def build_workload(rank: int, sims: int, workload: str = WORKLOAD):
                                           collective=CollectiveConfig("MeasuredThroughput", path),
                                           gradient_markers=("wgrad_*",), hardware=HW_TAGS[0], sync=sync))
             graph_of.append(b)
+        return graphs, db, configs, graph_of
+    if workload == "bert-large-ps-ar":
+        # C4: {allreduce, parameter server} x workers {2, 4, 8} x links, one gradient exchange per
+        # layer parameter (the wgrad_* nodes) so communication overlaps the rest of the backward pass
+        grid = [(R, sync, path) for R in (2, 4, 8) for sync in ("allreduce", "parameter_server")
+                for path in VGG_PATHS]
+        for i in range(sims):
+            gi = rank * sims + i
+            R, sync, path = grid[gi % len(grid)]
+            k = gi // len(grid)
+            configs.append(StrategyConfig(replicas=R, device_map=tuple(f"gpu{j}" for j in range(R)),
+                                          collective=CollectiveConfig("RingAnalytic", path),
+                                          gradient_markers=("wgrad_*",), hardware=HW_TAGS[k % N_HW],
+                                          op_gap_us=1e-3 * (k // N_HW), sync=sync))
+            graph_of.append(0)
         return graphs, db, configs, graph_of
     dmap = tuple(f"gpu{i}" for i in range(8))
     coll = CollectiveConfig("RingAnalytic", "NVLink")
@@ -239,7 +255,7 @@ def cpu_baseline(sample: int | None = None, workers: int | None = None, target_s
     if workload == "dag1m":
         return cpu_baseline_dag(workers, target_s)
     _CPU_STATE["w"] = build_workload(0, 64 if workload != "vgg16-sweep" else 10032, workload)
-    worker = _cpu_worker_mixed if workload == "vgg16-sweep" else _cpu_worker
+    worker = _cpu_worker_mixed if workload in ("vgg16-sweep", "bert-large-ps-ar") else _cpu_worker
     t0 = time.perf_counter()
     worker(0)
     one = time.perf_counter() - t0
@@ -305,8 +321,23 @@ def run_ours(args):
     t_idx = [torch.as_tensor(idx, dtype=torch.int64, device=dev) for _, idx, _ in classes]
     single = len(classes) == 1
 
+    # several topology classes: each class's launches go to one of up to 8 streams so that small
+    # classes (a few chunks each) share the GPU instead of running one after another; every
+    # stream has its own device scratch inside the context (csrc/ctx.cu)
+    streams = [torch.cuda.Stream(local) for _ in range(min(len(classes), 8))] if not single else []
+
     def step(events=None):
-        for tc, _, o in classes:
+        if streams:
+            cur = torch.cuda.current_stream(local)
+            for st in streams:
+                st.wait_stream(cur)
+            for k, (tc, _, o) in enumerate(classes):
+                with torch.cuda.stream(streams[k % len(streams)]):
+                    tc.expand()
+                    tc.run(schedules=True, out=o, defer_fallback=True)
+            for st in streams:
+                cur.wait_stream(st)
+        for tc, _, o in (classes if not streams else ()):
             tc.expand()
             tc.run(schedules=True, out=o, events=events if single else None, defer_fallback=True)
         for tc, _, o in classes:  # exact re-run of ring overflows, then their critical paths

@@ -443,9 +443,12 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
 
 
 def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,
-                   fused: bool = True) -> SweepResult:
+                   fused: bool = True, streams: int = 8) -> SweepResult:
     """``sweep`` where candidate i runs ``configs[i]`` on ``graphs[graph_of[i]]`` (e.g. one graph per
-    batch size).  Graphs of identical structure share a topology class (variants.py)."""
+    batch size).  Graphs of identical structure share a topology class (variants.py).
+
+    Classes are launched round-robin on up to ``streams`` CUDA streams (each stream has its
+    own device scratch in the context), so many small classes share the GPU."""
     import torch
 
     from .variants import structure_key
@@ -464,10 +467,25 @@ def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, kee
     cp_len = torch.zeros(max(S, 1), dtype=torch.float64, device=dev)
     result = SweepResult(np.zeros(0), np.zeros(0), -1, float("nan"))
     failures = []
-    for pos, (key, idx) in enumerate(groups.items()):
-        tc = TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device, fused=fused,
-                           graphs=graphs, graph_of=[graph_of[i] for i in idx])
-        o = tc.run(schedules=True)
+    built = [(idx, TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device, fused=fused,
+                                 graphs=graphs, graph_of=[graph_of[i] for i in idx])) for idx in groups.values()]
+    outs = [{} for _ in built]
+    side = [torch.cuda.Stream(ctx.device) for _ in range(min(max(streams, 1), len(built)))] if len(built) > 1 else []
+    cur = torch.cuda.current_stream(ctx.device)
+    for st in side:
+        st.wait_stream(cur)
+    for k, ((idx, tc), o) in enumerate(zip(built, outs)):
+        if side:
+            with torch.cuda.stream(side[k % len(side)]):
+                tc.run(schedules=True, out=o, defer_fallback=True)
+        else:
+            tc.run(schedules=True, out=o, defer_fallback=True)
+    for st in side:
+        cur.wait_stream(st)
+    for (idx, tc), o in zip(built, outs):  # exact re-run of ring overflows, then their critical paths
+        if tc.fallback_if_needed(o):
+            tc.critical_path_only(o)
+    for pos, ((idx, tc), o) in enumerate(zip(built, outs)):
         t_idx = torch.as_tensor(idx, dtype=torch.int64, device=dev)
         makespan.index_copy_(0, t_idx, o["makespan"])
         if "cp_len" in o:

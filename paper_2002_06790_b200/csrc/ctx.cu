@@ -29,8 +29,11 @@ extern "C" int dfsim_ctx_destroy(dfsim_ctx *ctx) {
     if (!ctx) return DFSIM_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    if (ctx->scratch) cudaFree(ctx->scratch);
-    if (ctx->aux) cudaFree(ctx->aux);
+    for (auto &e : ctx->per_stream) {
+        if (e.stream) cudaStreamSynchronize(e.stream);
+        if (e.scratch) cudaFree(e.scratch);
+        if (e.aux) cudaFree(e.aux);
+    }
     if (ctx->host_small) cudaFreeHost(ctx->host_small);
     delete ctx;
     return DFSIM_OK;
@@ -72,8 +75,20 @@ static int grow(dfsim_ctx *ctx, void **buf, size_t *have, size_t bytes, void **o
     return DFSIM_OK;
 }
 
-int dfsim_scratch(dfsim_ctx *ctx, size_t bytes, void **out) {
-    return grow(ctx, &ctx->scratch, &ctx->scratch_bytes, bytes, out);
+static dfsim_stream_scratch &entry(dfsim_ctx *ctx) {
+    for (auto &e : ctx->per_stream)
+        if (e.stream == ctx->stream) return e;
+    ctx->per_stream.emplace_back();
+    ctx->per_stream.back().stream = ctx->stream;
+    return ctx->per_stream.back();
 }
 
-int dfsim_aux(dfsim_ctx *ctx, size_t bytes, void **out) { return grow(ctx, &ctx->aux, &ctx->aux_bytes, bytes, out); }
+int dfsim_scratch(dfsim_ctx *ctx, size_t bytes, void **out) {
+    auto &e = entry(ctx);
+    return grow(ctx, &e.scratch, &e.scratch_bytes, bytes, out);
+}
+
+int dfsim_aux(dfsim_ctx *ctx, size_t bytes, void **out) {
+    auto &e = entry(ctx);
+    return grow(ctx, &e.aux, &e.aux_bytes, bytes, out);
+}

@@ -5,21 +5,26 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "dfsim_b200.h"
+
+// Device scratch belongs to (context, stream): kernels of different topology classes may
+// run concurrently on different streams of one context without sharing scratch.
+struct dfsim_stream_scratch {
+    cudaStream_t stream = nullptr;
+    void *scratch = nullptr;  // per-warp engine state in global mode, CP suffix values, cub temp
+    size_t scratch_bytes = 0;
+    void *aux = nullptr;      // small per-call arrays that must survive a scratch reallocation
+    size_t aux_bytes = 0;
+};
 
 struct dfsim_ctx {
     int32_t device = 0;
     cudaStream_t stream = nullptr;
     int32_t num_sms = 148;
     int64_t launches = 0;
-    // growable device scratch (per-warp engine state in global mode, CP suffix values, cub temp)
-    void *scratch = nullptr;
-    size_t scratch_bytes = 0;
-    // second growable device buffer for small per-call arrays that must survive a
-    // dfsim_scratch reallocation inside the same call (e.g. overflow flags)
-    void *aux = nullptr;
-    size_t aux_bytes = 0;
+    std::vector<dfsim_stream_scratch> per_stream;
     // pinned host staging for small synchronous results
     void *host_small = nullptr;
     std::string last_error;

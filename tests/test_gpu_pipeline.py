@@ -90,3 +90,39 @@ def test_estimate_errors():
     g2 = make_graph([OpNode("u", "Mystery", "gpu0")], [DeviceSpec("gpu0", "Compute")])
     with pytest.raises(ValueError, match="nonnegative"):
         fw.estimate_all(g2, ProfileDB(), StrategyConfig(overrides={"u": -1.0}))
+
+
+def test_sweep_concurrent_streams_match_serial():
+    """Many small topology classes launched on 8 streams == one after another on one stream
+    (per-stream scratch in the context), and AR candidates match the oracle."""
+    import numpy as np
+
+    import paper_2002_06790_b200 as fw
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+
+    graphs = [W.vgg16_training(batch=b) for b in (8, 32)]
+    db = W.model_profiles(graphs[0], ["hw0"])
+    cfgs, gof = [], []
+    for gi in range(2):
+        for R in (1, 2, 4):
+            for sync in ("allreduce", "parameter_server"):
+                for path in ("NVLink", "PCIeSwitch"):
+                    for gap in (0.0, 0.5):
+                        cfgs.append(StrategyConfig(replicas=R, device_map=tuple(f"gpu{k}" for k in range(R)),
+                                                   collective=CollectiveConfig("MeasuredThroughput", path),
+                                                   gradient_markers=("wgrad_*",), hardware="hw0", op_gap_us=gap,
+                                                   sync=sync if R > 1 else "allreduce"))
+                        gof.append(gi)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        a = fw.sweep_variants(graphs, db, cfgs, gof, streams=1)
+        b = fw.sweep_variants(graphs, db, cfgs, gof, streams=8)
+    assert len(b.classes) > 8
+    assert np.array_equal(a.makespan, b.makespan) and np.array_equal(a.cp_len, b.cp_len)
+    assert (a.best_index, a.best_makespan) == (b.best_index, b.best_makespan)
+    for i in (0, 5, 17, 40):
+        if cfgs[i].sync == "allreduce":
+            ms, cp, *_ = O.run_candidate(graphs[gof[i]], db, cfgs[i])
+            assert (b.makespan[i], b.cp_len[i]) == (ms, cp), i
