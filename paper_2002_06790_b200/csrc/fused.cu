@@ -93,6 +93,29 @@ __device__ __forceinline__ bool counter_dec(unsigned *words, int c) {
     return ((old >> shift) & kMask) == 1u;
 }
 
+// Read-only CTA tables through 32-bit shared-window addresses computed once: with generic
+// pointers the compiler re-derives each table's base (S2R SR_CgaCtaId + LEA) inside the loop.
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+    unsigned r;  // opaque to the compiler, so the value stays in a register instead of being re-derived
+    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds_u32(unsigned a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned lds_u16(unsigned a) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
 constexpr int kWide = 4;  // out-degree above which a finished node's successors are spread over the group
 
 // Successor entry formats: kPacked (N <= 8192): consumer (13 bits) | device << 13 | single << 18 |
@@ -121,6 +144,8 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     unsigned *cnt = reinterpret_cast<unsigned *>(gbase + a.tail_bytes);
     uint16_t *q = reinterpret_cast<uint16_t *>(gbase + a.tail_bytes + a.g.n_counter_words * 4);
     __shared__ int s_chunk;
+    const unsigned a_meta = smem_addr(s_meta), a_succ = smem_addr(s_succ), a_cidx = smem_addr(s_cidx);
+    const unsigned a_rank = smem_addr(s_rank), a_base = smem_addr(s_base);
 
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         s_meta[i] = __ldg(a.g.meta + i);
@@ -184,10 +209,10 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     ovf |= static_cast<unsigned>(t) - head > static_cast<unsigned>(QCAP);
                     const int v = q[ll * QSTRIDE + (head & QMASK)];
                     head++;
-                    const double b = s_base[v];
+                    const double b = lds_f64(a_base + 8u * v);
                     double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
                     if (ovs >= 0) {  // override tables are by rank
-                        const int vr = s_rank[v];
+                        const int vr = static_cast<int>(lds_u16(a_rank + 2u * v));
                         int lo = __ldg(a.st.ov_off + ovs), hi = __ldg(a.st.ov_off + ovs + 1);
                         const int end = hi;
                         while (lo < hi) {
@@ -216,15 +241,15 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 int j0 = 0, deg = 0;
                 if (done) {
                     running = false;
-                    const uint32_t meta = s_meta[run_v];
+                    const uint32_t meta = lds_u32(a_meta + 4u * run_v);
                     j0 = static_cast<int>(meta & 0xffffffu);
                     deg = static_cast<int>(meta >> 24);  // < 255 in the fused engine (prepare.Tables)
                 }
                 auto relax = [&](int j) {
-                    const uint32_t e = s_succ[j];
+                    const uint32_t e = lds_u32(a_succ + 4u * j);
                     const int m = static_cast<int>(kPacked ? e & 0x1fffu : e & 0xffffu);
                     const bool single = kPacked ? (e >> 18) & 1u : (e >> 21) & 1u;
-                    if (single || counter_dec<kBits>(cnt, kPacked ? static_cast<int>(e >> 19) : s_cidx[m])) {
+                    if (single || counter_dec<kBits>(cnt, kPacked ? static_cast<int>(e >> 19) : static_cast<int>(lds_u16(a_cidx + 2u * m)))) {
                         const int dv = static_cast<int>(kPacked ? (e >> 13) & 31u : (e >> 16) & 31u);
                         const int p = atomicAdd(tails + dv, 1);
                         q[dv * QSTRIDE + (p & QMASK)] = static_cast<uint16_t>(m);
@@ -255,9 +280,9 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     uint16_t *qd = q + ll * QSTRIDE;
                     for (int i = seg_lo + 1; i < seg_hi; i++) {
                         const uint16_t x = qd[i & QMASK];
-                        const unsigned xr = s_rank[x];
+                        const unsigned xr = lds_u16(a_rank + 2u * x);
                         int j = i - 1;
-                        while (j >= seg_lo && s_rank[qd[j & QMASK]] > xr) {
+                        while (j >= seg_lo && lds_u16(a_rank + 2u * qd[j & QMASK]) > xr) {
                             qd[(j + 1) & QMASK] = qd[j & QMASK];
                             j--;
                         }
