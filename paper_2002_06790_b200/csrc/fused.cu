@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
     const int NC = a.t.n_chunks, SD = a.t.stage_doubles, SR = a.t.slot_region;
     const int NS = __ldg(a.t.spill_off + NC);
     uint2 *s_pm = reinterpret_cast<uint2 *>(smem);  // per position: (cp_meta, pinfo)
+    const unsigned a_pm = smem_addr(s_pm);
     uint16_t *s_succ = reinterpret_cast<uint16_t *>(s_pm + N);
     uint16_t *s_goff = s_succ + E;
     uint16_t *s_coff = s_goff + (G + 1);
@@ -398,7 +399,8 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                 const int q0 = s_goff[gi];
                 const int p = q0 + ll;
                 if (p < q1) {
-                    const uint2 pm = s_pm[p];
+                    uint2 pm;
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(pm.x), "=r"(pm.y) : "r"(a_pm + 8u * p));
                     const uint32_t m = pm.x, info = pm.y;
                     const int j0 = static_cast<int>(m & 0xffffu), j1 = j0 + static_cast<int>((m >> 16) & 0xffu);
                     double best = 0.0;  // max(0.0, .) (graph.py:465-468)

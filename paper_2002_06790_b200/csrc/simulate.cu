@@ -269,7 +269,7 @@ static int simulate_exact(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, 
     bool shared_mode = true;
     while (wpb > 1 && wpb * (a.per_warp + 128) > kSmemBudget) wpb >>= 1;
     if (wpb * (a.per_warp + 128) > kSmemBudget) { shared_mode = false; wpb = 4; }
-    if (!shared_mode && allow_large && !pos && !out_rows && !interleaved)  // K3 large (simulate_large.cu)
+    if (!shared_mode && allow_large && !pos && !out_rows && !interleaved && N < (1 << 27))  // K3 large
         return dfsim_simulate_large(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed);
     size_t smem = (size_t)wpb * 128 + (shared_mode ? (size_t)wpb * a.per_warp : 0);
 

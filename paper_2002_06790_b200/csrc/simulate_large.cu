@@ -8,9 +8,12 @@
 //   * FIFO rings in shared memory hold (node, duration) pairs: a pop needs no global
 //     load.  Ring occupancy is checked before every pop (a device only gains entries
 //     until its next pop); an overflowed candidate is re-run by the exact engine.
-//   * While a node runs, its lane prefetches, one stage per iteration, the successor
-//     range, up to kPre successor ids, and their devices and durations; at finish the
-//     relax step reads registers only (longer lists fall back to direct loads).
+//   * A start loads the node's 32-byte successor record (range + the first kPre
+//     successors with their devices, built once per launch); the next iteration loads
+//     those successors' durations.  At finish the relax step reads registers only
+//     (longer lists fall back to direct loads).
+//   * One finishing device per iteration (the common case) relaxes alone with plain
+//     counter and ring-tail updates; ties between devices take the combining path.
 //   * Dependency counters are plain byte/short loads and stores in a global row per
 //     warp, L1-resident for the active frontier.  Lanes relaxing the same node in one
 //     iteration are combined with __match_any_sync (the leader subtracts the group
@@ -22,6 +25,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -31,7 +36,7 @@ int dfsim_simulate_exact_flagged(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n
 
 namespace {
 
-constexpr int kPre = 4;  // successors prefetched per running node
+constexpr int kPre = 4;  // successors carried in a node's prefetch record
 
 struct LargeArgs {
     int32_t N, D;
@@ -43,11 +48,32 @@ struct LargeArgs {
     double *start, *finish, *makespan, *busy;
     int32_t *n_placed;
     int32_t *redo;             // [S] 1 when the candidate overflowed a ring
+    const uint4 *srec;         // [N][2] successor record: {j0, deg, s0, s1}, {s2, s3, -, -}; s = m | dev << 27
     unsigned char *gcnt;       // counters, cnt_bytes per resident warp
     int64_t cnt_bytes;
     int32_t qcap;              // ring entries per device (power of two)
     int32_t warp_smem;         // bytes of shared state per warp
 };
+
+// One 32-byte record per node: its successor range and the first kPre successors with
+// their devices, so a start issues one load and the finish needs no dependent loads.
+__global__ void k_successor_records(int32_t N, const int32_t *succ_off, const int32_t *succ_idx,
+                                    const int32_t *device, uint4 *srec) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += gridDim.x * blockDim.x) {
+        const int32_t j0 = succ_off[v], deg = succ_off[v + 1] - j0;
+        unsigned pk[kPre];
+#pragma unroll
+        for (int k = 0; k < kPre; k++) {
+            pk[k] = 0;
+            if (k < deg) {
+                const int32_t m = succ_idx[j0 + k];
+                pk[k] = static_cast<unsigned>(m) | (static_cast<unsigned>(device[m]) << 27);
+            }
+        }
+        srec[2 * v] = make_uint4(static_cast<unsigned>(j0), static_cast<unsigned>(deg), pk[0], pk[1]);
+        srec[2 * v + 1] = make_uint4(pk[2], pk[3], 0u, 0u);
+    }
+}
 
 __device__ __forceinline__ double warp_min_nonneg(double x) {
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
@@ -97,32 +123,19 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
         bool ovf = lane < D && tails[lane] > QC;
 
         unsigned head = 0;
-        bool running = false;
-        int run_v = 0, stage = 0, j0 = 0, j1 = 0;
-        int pm[kPre];
-        unsigned pdev = 0;  // 5 bits per prefetched successor
+        bool running = false, have_dur = false;
+        uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);  // successor record of the running node
         double pdur[kPre];
         double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
         int placed = 0;
 #pragma unroll
-        for (int k = 0; k < kPre; k++) { pm[k] = 0; pdur[k] = 0.0; }
-
-        auto prefetch_step = [&]() {  // one stage per call; loads land while the node runs
-            if (stage == 1) {
+        for (int k = 0; k < kPre; k++) pdur[k] = 0.0;
+        auto succ_of = [&](int k) -> unsigned { return k == 0 ? r0.z : (k == 1 ? r0.w : (k == 2 ? r1.x : r1.y)); };
+        auto load_durs = [&]() {  // second stage, one iteration after the start
 #pragma unroll
-                for (int k = 0; k < kPre; k++) pm[k] = j0 + k < j1 ? __ldg(a.succ_idx + j0 + k) : 0;
-                stage = 2;
-            } else if (stage == 2) {
-                pdev = 0;
-#pragma unroll
-                for (int k = 0; k < kPre; k++) {
-                    if (j0 + k < j1) {
-                        pdev |= static_cast<unsigned>(__ldg(a.device + pm[k])) << (5 * k);
-                        pdur[k] = __ldg(dur + pm[k]);
-                    }
-                }
-                stage = 3;
-            }
+            for (int k = 0; k < kPre; k++)
+                if (k < static_cast<int>(r0.y)) pdur[k] = __ldg(dur + (succ_of(k) & 0x7ffffffu));
+            have_dur = true;
         };
         auto start_idle = [&]() {
             const int t = lane < D ? tails[lane] : 0;
@@ -133,18 +146,17 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                 const double f = __dadd_rn(now, rdur[slot]);
                 head++;
                 if (out_s) {
-                    out_s[v] = now;
-                    out_f[v] = f;
+                    __stcs(out_s + v, now);
+                    __stcs(out_f + v, f);
                 }
                 running = true;
-                run_v = v;
                 run_f = f;
                 busy_sum = __dadd_rn(busy_sum, __dsub_rn(f, now));
                 if (f > span) span = f;
                 placed++;
-                j0 = __ldg(a.succ_off + v);
-                j1 = __ldg(a.succ_off + v + 1);
-                stage = 1;
+                r0 = __ldg(a.srec + 2 * static_cast<int64_t>(v));
+                r1 = __ldg(a.srec + 2 * static_cast<int64_t>(v) + 1);
+                have_dur = false;
             }
         };
 
@@ -153,47 +165,71 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
             now = warp_min_nonneg(running ? run_f : __longlong_as_double(0x7ff0000000000000LL));
             const bool done = running && run_f == now;
             const int seg_lo = lane < D ? tails[lane] : 0;
-            if (running && !done) prefetch_step();
-            int deg = 0;
-            if (done) {
-                running = false;
-                while (stage < 3) prefetch_step();
-                deg = j1 - j0;
-            }
-            // relax in rounds: round r handles successor r of every finishing device
-            const int rounds = __reduce_max_sync(DFSIM_FULL_MASK, static_cast<unsigned>(deg));
-            for (int r = 0; r < rounds; r++) {
-                const bool act = r < deg;
-                const unsigned am = __ballot_sync(DFSIM_FULL_MASK, act);
-                if (act) {
-                    int m, dv;
-                    double dd;
-                    if (r < kPre) {
-                        m = pm[0];
-                        dv = static_cast<int>(pdev & 31u);
-                        dd = pdur[0];
-#pragma unroll
-                        for (int k = 1; k < kPre; k++)
-                            if (r == k) { m = pm[k]; dv = static_cast<int>((pdev >> (5 * k)) & 31u); dd = pdur[k]; }
-                    } else {
-                        m = __ldg(a.succ_idx + j0 + r);
-                        dv = __ldg(a.device + m);
-                        dd = __ldg(dur + m);
-                    }
-                    const unsigned grp = __match_any_sync(am, m);
-                    if ((grp & lanemask_lt()) == 0) {  // group leader: one plain read-modify-write
-                        const int k = __popc(grp);
+            if (running && !have_dur) load_durs();
+            const unsigned dm = __ballot_sync(DFSIM_FULL_MASK, done);
+            if (done) running = false;
+            if ((dm & (dm - 1)) == 0) {
+                // one device finished (the common case): it alone updates counters and rings
+                if (done) {
+                    const int deg = static_cast<int>(r0.y);
+                    for (int k = 0; k < deg; k++) {
+                        unsigned e;
+                        double dd;
+                        if (k < kPre) {
+                            e = succ_of(k);
+                            dd = k == 0 ? pdur[0] : (k == 1 ? pdur[1] : (k == 2 ? pdur[2] : pdur[3]));
+                        } else {
+                            const int m = __ldg(a.succ_idx + static_cast<int>(r0.x) + k);
+                            e = static_cast<unsigned>(m) | (static_cast<unsigned>(__ldg(a.device + m)) << 27);
+                            dd = __ldg(dur + m);
+                        }
+                        const int m = static_cast<int>(e & 0x7ffffffu), dv = static_cast<int>(e >> 27);
                         const int c = static_cast<int>(cnt[m]);
-                        cnt[m] = static_cast<CT>(c - k);
-                        if (c == k) {
-                            const int p = atomicAdd(tails + dv, 1);
+                        cnt[m] = static_cast<CT>(c - 1);
+                        if (c == 1) {
+                            const int p = tails[dv];
+                            tails[dv] = p + 1;
                             rnode[dv * QC + (p & QM)] = m;
                             rdur[dv * QC + (p & QM)] = dd;
                         }
                     }
                 }
-                __syncwarp();
+            } else {
+                // several devices finished at `now`: relax in rounds, lanes releasing the same
+                // node combined by __match_any_sync (the leader subtracts the group size)
+                const int deg = done ? static_cast<int>(r0.y) : 0;
+                const int rounds = __reduce_max_sync(DFSIM_FULL_MASK, static_cast<unsigned>(deg));
+                for (int r = 0; r < rounds; r++) {
+                    const bool act = r < deg;
+                    const unsigned am = __ballot_sync(DFSIM_FULL_MASK, act);
+                    if (act) {
+                        unsigned e;
+                        double dd;
+                        if (r < kPre) {
+                            e = succ_of(r);
+                            dd = r == 0 ? pdur[0] : (r == 1 ? pdur[1] : (r == 2 ? pdur[2] : pdur[3]));
+                        } else {
+                            const int m = __ldg(a.succ_idx + static_cast<int>(r0.x) + r);
+                            e = static_cast<unsigned>(m) | (static_cast<unsigned>(__ldg(a.device + m)) << 27);
+                            dd = __ldg(dur + m);
+                        }
+                        const int m = static_cast<int>(e & 0x7ffffffu), dv = static_cast<int>(e >> 27);
+                        const unsigned grp = __match_any_sync(am, m);
+                        if ((grp & lanemask_lt()) == 0) {
+                            const int k = __popc(grp);
+                            const int c = static_cast<int>(cnt[m]);
+                            cnt[m] = static_cast<CT>(c - k);
+                            if (c == k) {
+                                const int p = atomicAdd(tails + dv, 1);
+                                rnode[dv * QC + (p & QM)] = m;
+                                rdur[dv * QC + (p & QM)] = dd;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
             }
+            __syncwarp();
             const int seg_hi = lane < D ? tails[lane] : 0;
             if (seg_hi - seg_lo > 1) {  // enqueue(sorted(newly_ready)) (engine.py:139-142)
                 for (int i = seg_lo + 1; i < seg_hi; i++) {
@@ -239,14 +275,25 @@ int dfsim_simulate_large(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, c
     int wpb = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, (n_sims + ctx->num_sms - 1) / ctx->num_sms)));
     const int budget = 220 * 1024 / wpb;
     // small rings: the rest of the SM's 256 KB stays L1 for the counter rows' active frontier
-    int qcap = 512;
+    static const int kQcapMax = [] {  // ring entries per device; DFSIM_LARGE_QCAP overrides (power of two)
+        const char *e = std::getenv("DFSIM_LARGE_QCAP");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 16 && (v & (v - 1)) == 0 ? v : 512;
+    }();
+    int qcap = kQcapMax;
     while (qcap > 16 && 128 + static_cast<int64_t>(std::max(D, 1)) * qcap * 12 > budget) qcap >>= 1;
     const int warp_smem = (128 + std::max(D, 1) * qcap * 12 + 15) / 16 * 16;
     const int64_t want = (n_sims + wpb - 1) / wpb;
     const int grid = static_cast<int>(std::min<int64_t>(want, ctx->num_sms));
     const int64_t cnt_bytes = (static_cast<int64_t>(N) * cbytes + 127) / 128 * 128;
     void *p = nullptr, *redo = nullptr;
-    int rc = dfsim_scratch(ctx, static_cast<size_t>(grid) * wpb * cnt_bytes, &p);
+    const size_t rec_off = static_cast<size_t>(grid) * wpb * cnt_bytes;
+    int rc = dfsim_scratch(ctx, rec_off + 32 * static_cast<size_t>(std::max(N, 1)) + 256, &p);
+    if (rc) return rc;
+    uint4 *srec = reinterpret_cast<uint4 *>(static_cast<unsigned char *>(p) + (rec_off + 255) / 256 * 256);
+    k_successor_records<<<std::max(1, std::min((N + 255) / 256, ctx->num_sms * 8)), 256, 0, ctx->stream>>>(
+        N, g->succ_off, g->succ_idx, g->device, srec);
+    rc = dfsim_after_launch(ctx, "k_successor_records");
     if (rc) return rc;
     rc = dfsim_aux(ctx, sizeof(int32_t) * n_sims, &redo);
     if (rc) return rc;
@@ -257,6 +304,7 @@ int dfsim_simulate_large(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, c
     a.S = n_sims; a.dur = dur; a.dur_stride = dur_stride;
     a.start = start; a.finish = finish; a.makespan = makespan; a.busy = busy; a.n_placed = n_placed;
     a.gcnt = static_cast<unsigned char *>(p);
+    a.srec = srec;
     a.redo = static_cast<int32_t *>(redo);
     a.cnt_bytes = cnt_bytes;
     a.qcap = qcap;
