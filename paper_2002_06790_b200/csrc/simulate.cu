@@ -1,7 +1,7 @@
 // K3: batched event-driven list scheduling -- the reference's engine.simulate
 // (pkg/src/dfsim/engine.py:96-146) and _finalize (69-93), one warp per strategy.
 //
-// Mapping: lane d owns device rank d (D <= 32): its running node, its finish
+// Mapping: lane d owns device rank d (D <= 32; beyond that lane l owns l, l + 32, ...): its running node, its finish
 // time, its FIFO head and its busy accumulator live in registers.  The per-strategy
 // dependency counters (packed 8/16/32-bit, decremented with 32-bit shared-memory
 // atomics) and the per-device FIFOs (one segment of queue_off[d]..queue_off[d+1]
@@ -91,7 +91,9 @@ __device__ void warp_sort(QT *q, int lo, int hi, int lane) {
 
 constexpr int kShortRun = 24;
 
-template <int kBits, typename QT, bool kShared>
+// kV devices per lane (device d = lane + 32 k): kV = 1 covers D <= 32, larger kV the
+// wide device sets of big parameter-server or data-parallel expansions (D <= 32 kV).
+template <int kBits, typename QT, bool kShared, int kV>
 __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
@@ -99,12 +101,14 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
     const int wpb = blockDim.x >> 5;
     const int N = a.N, D = a.D;
 
-    int32_t *tails = reinterpret_cast<int32_t *>(smem) + wib * 32;  // per-warp FIFO tails
-    unsigned char *state = kShared ? smem + wpb * 32 * sizeof(int32_t) + wib * a.per_warp
+    int32_t *tails = reinterpret_cast<int32_t *>(smem) + wib * 32 * kV;  // per-warp FIFO tails
+    unsigned char *state = kShared ? smem + wpb * 32 * kV * sizeof(int32_t) + wib * a.per_warp
                                    : a.gscratch + (static_cast<int64_t>(blockIdx.x) * wpb + wib) * a.per_warp;
     unsigned *cnt = reinterpret_cast<unsigned *>(state);
     QT *q = reinterpret_cast<QT *>(state + static_cast<int64_t>(a.cnt_words) * 4);
-    const int my_qoff = lane < D ? __ldg(a.queue_off + lane) : 0;
+    int my_qoff[kV];
+#pragma unroll
+    for (int k = 0; k < kV; k++) my_qoff[k] = lane + 32 * k < D ? __ldg(a.queue_off + lane + 32 * k) : 0;
 
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * wpb + wib; s < a.S; s += static_cast<int64_t>(gridDim.x) * wpb) {
         if (a.redo && !a.redo[s]) continue;
@@ -115,8 +119,12 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
         const int ostride = a.interleaved ? 2 : 1;
 
         Counter<kBits>::init(cnt, a.cnt_words, a.indeg, N, lane);
-        if (lane < D) tails[lane] = my_qoff;
-        int head = my_qoff;
+        int head[kV];
+#pragma unroll
+        for (int k = 0; k < kV; k++) {
+            if (lane + 32 * k < D) tails[lane + 32 * k] = my_qoff[k];
+            head[k] = my_qoff[k];
+        }
         __syncwarp();
 
         // sources, already in rank order: append chunk by chunk (engine.py:111-114)
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
             const int i = b + lane;
             const bool has = i < a.n_sources;
             const int v = has ? __ldg(a.sources + i) : 0;
-            const int dv = has ? __ldg(a.device + v) : 32 + lane;
+            const int dv = has ? __ldg(a.device + v) : 32 * kV + lane;
             const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, dv);
             const int base = has ? tails[dv] : 0;
             __syncwarp();
@@ -135,57 +143,86 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
             __syncwarp();
         }
 
-        bool running = false;
-        int run_v = 0;
-        double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
+        bool running[kV];
+        int run_v[kV];
+        double run_f[kV], busy_sum[kV];
+        double span = 0.0, now = 0.0;
         int placed = 0;
+#pragma unroll
+        for (int k = 0; k < kV; k++) {
+            running[k] = false;
+            run_v[k] = 0;
+            run_f[k] = 0.0;
+            busy_sum[k] = 0.0;
+        }
 
         // start_idle_devices (engine.py:116-125) at `now`
         auto start_idle = [&]() {
-            if (lane < D && !running && head < tails[lane]) {
-                const int v = q[head++];
-                const double f = __dadd_rn(now, __ldg(dur + v));
-                if (out_start) {
-                    const int col = (a.pos ? __ldg(a.pos + v) : v) * ostride;
-                    out_start[col] = now;
-                    out_finish[col] = f;
+#pragma unroll
+            for (int k = 0; k < kV; k++) {
+                const int d = lane + 32 * k;
+                if (d < D && !running[k] && head[k] < tails[d]) {
+                    const int v = q[head[k]++];
+                    const double f = __dadd_rn(now, __ldg(dur + v));
+                    if (out_start) {
+                        const int col = (a.pos ? __ldg(a.pos + v) : v) * ostride;
+                        out_start[col] = now;
+                        out_finish[col] = f;
+                    }
+                    running[k] = true;
+                    run_v[k] = v;
+                    run_f[k] = f;
+                    busy_sum[k] = __dadd_rn(busy_sum[k], __dsub_rn(f, now));
+                    if (f > span) span = f;
+                    placed++;
                 }
-                running = true;
-                run_v = v;
-                run_f = f;
-                busy_sum = __dadd_rn(busy_sum, __dsub_rn(f, now));
-                if (f > span) span = f;
-                placed++;
             }
+        };
+        auto any_running = [&]() {
+            bool r = false;
+#pragma unroll
+            for (int k = 0; k < kV; k++) r |= running[k];
+            return r;
         };
 
         start_idle();
-        while (__any_sync(DFSIM_FULL_MASK, running)) {
-            now = warp_min_f64(running ? run_f : __longlong_as_double(0x7ff0000000000000LL));
-            const bool done = running && run_f == now;
-            const int seg_lo = lane < D ? tails[lane] : 0;
+        while (__any_sync(DFSIM_FULL_MASK, any_running())) {
+            double mine = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+            for (int k = 0; k < kV; k++)
+                if (running[k] && run_f[k] < mine) mine = run_f[k];
+            now = warp_min_f64(mine);
+            int seg_lo[kV];
+#pragma unroll
+            for (int k = 0; k < kV; k++) seg_lo[k] = lane + 32 * k < D ? tails[lane + 32 * k] : 0;
             __syncwarp();
-            if (done) {
-                running = false;
-                const int e1 = __ldg(a.succ_off + run_v + 1);
-                for (int j = __ldg(a.succ_off + run_v); j < e1; j++) {
-                    const int m = __ldg(a.succ_idx + j);
-                    if (Counter<kBits>::dec(cnt, m)) {
-                        const int pos = atomicAdd(tails + __ldg(a.device + m), 1);
-                        q[pos] = static_cast<QT>(m);
+#pragma unroll
+            for (int k = 0; k < kV; k++) {
+                if (running[k] && run_f[k] == now) {
+                    running[k] = false;
+                    const int e1 = __ldg(a.succ_off + run_v[k] + 1);
+                    for (int j = __ldg(a.succ_off + run_v[k]); j < e1; j++) {
+                        const int m = __ldg(a.succ_idx + j);
+                        if (Counter<kBits>::dec(cnt, m)) {
+                            const int pos = atomicAdd(tails + __ldg(a.device + m), 1);
+                            q[pos] = static_cast<QT>(m);
+                        }
                     }
                 }
             }
             __syncwarp();
-            const int seg_hi = lane < D ? tails[lane] : 0;
-            if (seg_hi - seg_lo > 1 && seg_hi - seg_lo <= kShortRun) insertion_sort(q, seg_lo, seg_hi);
-            unsigned long_runs = __ballot_sync(DFSIM_FULL_MASK, seg_hi - seg_lo > kShortRun);
-            while (long_runs) {
-                const int d = __ffs(long_runs) - 1;
-                long_runs &= long_runs - 1;
-                const int lo = __shfl_sync(DFSIM_FULL_MASK, seg_lo, d);
-                const int hi = __shfl_sync(DFSIM_FULL_MASK, seg_hi, d);
-                warp_sort(q, lo, hi, lane);
+#pragma unroll
+            for (int k = 0; k < kV; k++) {
+                const int seg_hi = lane + 32 * k < D ? tails[lane + 32 * k] : 0;
+                if (seg_hi - seg_lo[k] > 1 && seg_hi - seg_lo[k] <= kShortRun) insertion_sort(q, seg_lo[k], seg_hi);
+                unsigned long_runs = __ballot_sync(DFSIM_FULL_MASK, seg_hi - seg_lo[k] > kShortRun);
+                while (long_runs) {
+                    const int d = __ffs(long_runs) - 1;
+                    long_runs &= long_runs - 1;
+                    const int lo = __shfl_sync(DFSIM_FULL_MASK, seg_lo[k], d);
+                    const int hi = __shfl_sync(DFSIM_FULL_MASK, seg_hi, d);
+                    warp_sort(q, lo, hi, lane);
+                }
             }
             __syncwarp();
             start_idle();
@@ -197,23 +234,31 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
             a.makespan[row] = ms;
             if (a.n_placed) a.n_placed[row] = total;
         }
-        if (a.busy && lane < D) a.busy[row * D + lane] = busy_sum;
+#pragma unroll
+        for (int k = 0; k < kV; k++)
+            if (a.busy && lane + 32 * k < D) a.busy[row * D + lane + 32 * k] = busy_sum[k];
         __syncwarp();
     }
 }
 
-template <int kBits, typename QT>
-int launch_bits(dfsim_ctx *ctx, SimArgs &a, bool shared_mode, int wpb, int grid, size_t smem) {
+template <int kBits, typename QT, int kV>
+int launch_v(dfsim_ctx *ctx, SimArgs &a, bool shared_mode, int wpb, int grid, size_t smem) {
     if (shared_mode) {
-        auto kern = k_simulate<kBits, QT, true>;
+        auto kern = k_simulate<kBits, QT, true, kV>;
         DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<grid, wpb * 32, smem, ctx->stream>>>(a);
     } else {
-        auto kern = k_simulate<kBits, QT, false>;
-        k_simulate<kBits, QT, false><<<grid, wpb * 32, smem, ctx->stream>>>(a);
-        (void)kern;
+        k_simulate<kBits, QT, false, kV><<<grid, wpb * 32, smem, ctx->stream>>>(a);
     }
     return dfsim_after_launch(ctx, "k_simulate");
+}
+
+constexpr int kWideV = 8;  // devices per lane of the wide-device instantiation (D <= 256)
+
+template <int kBits, typename QT>
+int launch_bits(dfsim_ctx *ctx, SimArgs &a, bool shared_mode, int wpb, int grid, size_t smem) {
+    return a.D <= 32 ? launch_v<kBits, QT, 1>(ctx, a, shared_mode, wpb, grid, smem)
+                     : launch_v<kBits, QT, kWideV>(ctx, a, shared_mode, wpb, grid, smem);
 }
 
 }  // namespace
@@ -239,7 +284,7 @@ static int simulate_exact(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, 
                           const int32_t *redo, bool allow_large) {
     if (!ctx || !g) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, g->n_nodes >= 0 && n_sims >= 0, "negative sizes");
-    DFSIM_ARG_CHECK(ctx, g->n_devices >= 0 && g->n_devices <= 32, "the warp engine supports at most 32 devices");
+    DFSIM_ARG_CHECK(ctx, g->n_devices >= 0 && g->n_devices <= 32 * kWideV, "the warp engine supports at most 256 devices");
     DFSIM_ARG_CHECK(ctx, makespan != nullptr, "makespan output is required");
     DFSIM_ARG_CHECK(ctx, interleaved || (start == nullptr) == (finish == nullptr), "start and finish go together");
     DFSIM_ARG_CHECK(ctx, dur_stride == 0 || dur_stride >= g->n_nodes, "dur_stride < n_nodes");
@@ -267,11 +312,13 @@ static int simulate_exact(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, 
     const int64_t kSmemBudget = 200 * 1024;
     int wpb = 8;
     bool shared_mode = true;
-    while (wpb > 1 && wpb * (a.per_warp + 128) > kSmemBudget) wpb >>= 1;
-    if (wpb * (a.per_warp + 128) > kSmemBudget) { shared_mode = false; wpb = 4; }
-    if (!shared_mode && allow_large && !pos && !out_rows && !interleaved && N < (1 << 27))  // K3 large
+    const int64_t tail_bytes = g->n_devices <= 32 ? 128 : 128 * kWideV;  // per-warp FIFO tails
+    while (wpb > 1 && wpb * (a.per_warp + tail_bytes) > kSmemBudget) wpb >>= 1;
+    if (wpb * (a.per_warp + tail_bytes) > kSmemBudget) { shared_mode = false; wpb = 4; }
+    if (!shared_mode && allow_large && !pos && !out_rows && !interleaved && N < (1 << 27) &&
+        g->n_devices <= 32)  // K3 large
         return dfsim_simulate_large(ctx, g, n_sims, dur, dur_stride, start, finish, makespan, busy, n_placed);
-    size_t smem = (size_t)wpb * 128 + (shared_mode ? (size_t)wpb * a.per_warp : 0);
+    size_t smem = (size_t)wpb * tail_bytes + (shared_mode ? (size_t)wpb * a.per_warp : 0);
 
     int blocks_per_sm = 1;
     if (shared_mode) {

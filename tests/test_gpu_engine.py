@@ -76,3 +76,60 @@ def test_batched_engine_matches_c_oracle():
         assert length == cp["cp_len"][s].item()
         k = cp["cp_path_len"][s].item()
         assert list(path) == cp["cp_path"][s, :k].cpu().tolist()
+
+
+@pytest.mark.parametrize("ndev", [33, 100, 256])
+def test_engine_many_devices_matches_c_oracle(ndev):
+    """More devices than warp lanes (wide PS / DP expansions): lane l owns l, l+32, ..."""
+    import torch
+
+    from oracle import native_oracle as NO
+    from paper_2002_06790_b200.lowering import LoweredGraph
+    from paper_2002_06790_b200.simulator import critical_path_arrays, simulate_arrays
+    from paper_2002_06790_b200.workloads import random_dag
+
+    g = random_dag(700, 0.01, seed=ndev, num_devices=ndev)
+    lg = LoweredGraph(g)
+    csr = NO.Csr(g)
+    assert csr.ids == lg.ids and lg.n_devices > 32
+    rng = np.random.default_rng(ndev)
+    rows = [rng.uniform(0, 9, lg.n), rng.integers(0, 3, lg.n).astype(np.float64)]
+    o = simulate_arrays(lg, torch.tensor(np.stack(rows), device="cuda:0"))
+    cp = critical_path_arrays(lg, o["start"], o["finish"])["cp_len"].cpu().numpy()
+    for s, row in enumerate(rows):
+        rc, ws, wf, wbusy, wms, _ = NO.simulate(csr, row)
+        assert rc == 0 and int(o["n_placed"][s]) == lg.n
+        assert np.array_equal(o["start"][s, : lg.n].cpu().numpy(), ws)
+        assert np.array_equal(o["finish"][s, : lg.n].cpu().numpy(), wf)
+        assert float(o["makespan"][s]) == wms
+        got = dict(zip(lg.devices, o["busy"][s, : lg.n_devices].cpu().numpy().tolist()))
+        want = dict(zip(csr.devices, wbusy.tolist()))
+        assert got == {d: b for d, b in want.items() if d in got} and all(want[d] == 0.0 for d in want if d not in got)
+        assert cp[s] == NO.critical_path(csr, wf - ws)[1]
+
+
+def test_parameter_server_sixteen_workers_vs_oracle():
+    """PS with 16 workers has 49 devices (PS + 16 GPUs + 32 links): the wide-device engine."""
+    import warnings
+
+    import paper_2002_06790_b200 as fw
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+    from paper_2002_06790_b200.ps import expand_parameter_server
+
+    g = W.vgg16_training(batch=16)
+    db = W.model_profiles(g, ["hw0"])
+    cfgs = [StrategyConfig(replicas=16, device_map=tuple(f"gpu{k}" for k in range(16)),
+                           collective=CollectiveConfig("MeasuredThroughput", "NVLink"), gradient_markers=("wgrad_*",),
+                           hardware="hw0", op_gap_us=0.1 * i, sync="parameter_server") for i in range(3)]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = fw.sweep(g, db, cfgs, keep_schedules=True)
+    for i, cfg in enumerate(cfgs):
+        gx = expand_parameter_server(g, cfg, db).graph
+        assert len(gx.devices) > 32
+        table = O.estimate(gx, db, cfg)
+        entries, ms, busy = O.simulate(gx, {k: v for k, (v, _) in table.items()})
+        cp = O.critical_path(gx, {nid: f - s for nid, _, s, f in entries})
+        assert res.makespan[i] == ms and res.cp_len[i] == cp[0], i
