@@ -202,17 +202,19 @@ typedef struct {
     const uint32_t *meta;      /* [N] by position: successor begin (24 bits) | out-degree (8 bits, < 255) */
     const int32_t *succ_off;   /* [N+1] (rank CSR; sizes only) */
     const uint32_t *succ;      /* [E] by reading position: consumer position | device << 16 | single-input << 21 */
-    const uint16_t *cidx;      /* [N] by position: counter slot of nodes with >= 2 input references */
-    const uint32_t *cnt_init;  /* [n_counter_words] packed initial counters */
+    const uint16_t *cidx;      /* [N] by position: counter code of nodes with >= 2 input references:
+                                  word << 7 | bit shift << 2 | log2(width) - 1, width 2/4/8/16 bits */
+    const uint32_t *cnt_init;  /* [n_counter_words] packed initial counters (<= 512 words) */
     int32_t n_counter_words;
-    int32_t counter_bits;      /* 4, 8 or 16 */
+    int32_t counter_bits;      /* widest counter field (2, 4, 8 or 16) */
     const uint16_t *rank;      /* [N] rank of the node at position p */
     const int32_t *sources;    /* positions of the in-degree-0 nodes, in ascending rank */
     int32_t n_sources;
     int32_t qcap;              /* per-device FIFO ring capacity (power of two); overflow flags the candidate */
     const int32_t *device;     /* [N] device index by rank */
-    int32_t succ_packed;       /* 1: succ[j] = consumer position (13 bits) | device << 13 | single << 18 |
-                                  counter slot << 19 (N <= 8192, cidx unused); 0: the layout above */
+    int32_t succ_packed;       /* 1: succ[j] = consumer position (13 bits) | device << 13 (4 bits) | single << 17 |
+                                  wide << 18 | shift << 19 | word << 24 (N <= 8192, D <= 16, counters of
+                                  2/4 bits in <= 256 words; cidx unused); 0: the layout above */
 } dfsim_sim_tables;
 
 typedef struct {

@@ -36,17 +36,40 @@ struct FusedArgs {
     int32_t tail_bytes;  // FIFO tails at the start of each group's state
 };
 
-// Reductions over one lane group (kGS = 32: the warp; kGS = 16: one half-warp,
-// two candidates per warp).  redux.sync needs the whole warp, so for half-warps
-// each group's reduction runs with the other group's lanes contributing the identity.
+// Reductions over one lane group: kGS = 32 is the warp, kGS = 16 a half-warp (two
+// candidates per warp), kGS = 10 a third (three candidates per warp; lanes 30-31 idle).
+// redux.sync reduces over the whole warp, so each group's reduction runs with the other
+// lanes contributing the identity (one REDUX per group).
+template <int kGS>
+constexpr int kGroupsOf = 32 / kGS;
+
 template <int kGS>
 __device__ __forceinline__ unsigned group_min_u32(unsigned x, int grp) {
     if constexpr (kGS == 32) {
         return __reduce_min_sync(DFSIM_FULL_MASK, x);
     } else {
-        const unsigned a = __reduce_min_sync(DFSIM_FULL_MASK, grp == 0 ? x : 0xffffffffu);
-        const unsigned b = __reduce_min_sync(DFSIM_FULL_MASK, grp == 1 ? x : 0xffffffffu);
-        return grp ? b : a;
+        unsigned r = 0xffffffffu;
+#pragma unroll
+        for (int g = 0; g < kGroupsOf<kGS>; g++) {
+            const unsigned t = __reduce_min_sync(DFSIM_FULL_MASK, grp == g ? x : 0xffffffffu);
+            if (grp == g) r = t;
+        }
+        return r;
+    }
+}
+
+template <int kGS>
+__device__ __forceinline__ unsigned group_max_u32(unsigned x, int grp) {
+    if constexpr (kGS == 32) {
+        return __reduce_max_sync(DFSIM_FULL_MASK, x);
+    } else {
+        unsigned r = 0u;
+#pragma unroll
+        for (int g = 0; g < kGroupsOf<kGS>; g++) {
+            const unsigned t = __reduce_max_sync(DFSIM_FULL_MASK, grp == g ? x : 0u);
+            if (grp == g) r = t;
+        }
+        return r;
     }
 }
 
@@ -55,17 +78,25 @@ __device__ __forceinline__ unsigned group_add_u32(unsigned x, int grp) {
     if constexpr (kGS == 32) {
         return __reduce_add_sync(DFSIM_FULL_MASK, x);
     } else {
-        const unsigned a = __reduce_add_sync(DFSIM_FULL_MASK, grp == 0 ? x : 0u);
-        const unsigned b = __reduce_add_sync(DFSIM_FULL_MASK, grp == 1 ? x : 0u);
-        return grp ? b : a;
+        unsigned r = 0u;
+#pragma unroll
+        for (int g = 0; g < kGroupsOf<kGS>; g++) {
+            const unsigned t = __reduce_add_sync(DFSIM_FULL_MASK, grp == g ? x : 0u);
+            if (grp == g) r = t;
+        }
+        return r;
     }
 }
 
 template <int kGS>
+__device__ __forceinline__ unsigned group_bits(unsigned b, int grp) {
+    if constexpr (kGS == 32) return b;
+    return (b >> (grp * kGS)) & ((1u << kGS) - 1u);
+}
+
+template <int kGS>
 __device__ __forceinline__ bool group_any(bool p, int grp) {
-    const unsigned b = __ballot_sync(DFSIM_FULL_MASK, p);
-    if constexpr (kGS == 32) return b != 0;
-    return ((b >> (grp * 16)) & 0xffffu) != 0;
+    return group_bits<kGS>(__ballot_sync(DFSIM_FULL_MASK, p), grp) != 0;
 }
 
 // finishes are >= +0.0, so their IEEE bits order like unsigned integers
@@ -78,19 +109,17 @@ __device__ __forceinline__ double group_min_nonneg(double x, int grp) {
 }
 
 template <int kGS>
-__device__ __forceinline__ double group_max_f64(double x) {
-#pragma unroll
-    for (int o = kGS / 2; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(DFSIM_FULL_MASK, x, o));
-    return x;
+__device__ __forceinline__ double group_max_nonneg(double x, int grp) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned hi = group_max_u32<kGS>(static_cast<unsigned>(b >> 32), grp);
+    const unsigned lo = group_max_u32<kGS>(static_cast<unsigned>(b >> 32) == hi ? static_cast<unsigned>(b) : 0u, grp);
+    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo));
 }
 
-template <int kBits>
-__device__ __forceinline__ bool counter_dec(unsigned *words, int c) {
-    constexpr int kPer = 32 / kBits;
-    constexpr unsigned kMask = (1u << kBits) - 1u;
-    const int shift = (c % kPer) * kBits;
-    const unsigned old = atomicSub(words + c / kPer, 1u << shift);
-    return ((old >> shift) & kMask) == 1u;
+// Decrement the counter field (width mask at bit `shift` of cnt[word]); true when it reaches zero.
+__device__ __forceinline__ bool counter_dec(unsigned *cnt, unsigned word, unsigned shift, unsigned mask) {
+    const unsigned old = atomicSub(cnt + word, 1u << shift);
+    return ((old >> shift) & mask) == 1u;
 }
 
 // Read-only CTA tables through 32-bit shared-window addresses computed once: with generic
@@ -118,15 +147,17 @@ __device__ __forceinline__ double lds_f64(unsigned a) {
 
 constexpr int kWide = 4;  // out-degree above which a finished node's successors are spread over the group
 
-// Successor entry formats: kPacked (N <= 8192): consumer (13 bits) | device << 13 | single << 18 |
-// counter slot << 19; otherwise consumer (16) | device << 16 | single << 21 with cidx[] in smem.
-template <int kBits, int kGS, bool kPacked>
+// Successor entry formats: kPacked: consumer (13 bits) | device << 13 (4) | single << 17 | wide << 18 |
+// shift << 19 | word << 24; otherwise consumer (16) | device << 16 | single << 21 with the counter
+// code (word << 7 | shift << 2 | log2(width) - 1) in cidx[] in smem.
+template <int kGS, bool kPacked>
 __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kPerWarp = 32 / kGS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ll = lane % kGS, grp = lane / kGS;
     const int gid = warp * kPerWarp + grp;  // candidate slot of this lane group inside a chunk
+    const bool in_group = grp < kPerWarp;   // kGS = 10: lanes 30-31 belong to no candidate
     const int N = a.g.n_nodes, D = a.g.n_devices;
     const int E = static_cast<int>(a.g.n_edges);
     const int QCAP = a.g.qcap;
@@ -136,10 +167,12 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     // CTA-shared tables
     uint32_t *s_meta = reinterpret_cast<uint32_t *>(smem);
     uint32_t *s_succ = s_meta + N;
-    uint16_t *s_cidx = reinterpret_cast<uint16_t *>(s_succ + E);
-    uint16_t *s_rank = s_cidx + N;  // nodes are numbered by position; rank only for tie-breaks
-    double *s_base = reinterpret_cast<double *>(smem + ((static_cast<size_t>(N) * 8 + static_cast<size_t>(E) * 4 + 15) / 16) * 16);
-    unsigned char *gbase = smem + a.smem_graph + static_cast<size_t>(gid) * a.smem_warp;
+    uint16_t *s_rank = reinterpret_cast<uint16_t *>(s_succ + E);  // nodes are numbered by position; rank only for tie-breaks
+    uint16_t *s_cidx = s_rank + N;                                // counter codes (unpacked format only)
+    double *s_base = reinterpret_cast<double *>(
+        smem + ((static_cast<size_t>(N) * (kPacked ? 6 : 8) + static_cast<size_t>(E) * 4 + 15) / 16) * 16);
+    // idle lanes (kGS = 10) alias their warp's first group for reads; they never write
+    unsigned char *gbase = smem + a.smem_graph + static_cast<size_t>(in_group ? gid : warp * kPerWarp) * a.smem_warp;
     int32_t *tails = reinterpret_cast<int32_t *>(gbase);
     unsigned *cnt = reinterpret_cast<unsigned *>(gbase + a.tail_bytes);
     uint16_t *q = reinterpret_cast<uint16_t *>(gbase + a.tail_bytes + a.g.n_counter_words * 4);
@@ -149,7 +182,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
 
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         s_meta[i] = __ldg(a.g.meta + i);
-        s_cidx[i] = __ldg(a.g.cidx + i);
+        if (!kPacked) s_cidx[i] = __ldg(a.g.cidx + i);
         s_rank[i] = __ldg(a.g.rank + i);
     }
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.g.succ + i);
@@ -167,7 +200,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             staged = var;
             __syncthreads();
         }
-        const bool active = gid < __ldg(a.st.chunk_count + c);
+        const bool active = in_group && gid < __ldg(a.st.chunk_count + c);
         if (__any_sync(DFSIM_FULL_MASK, active)) {
             const int64_t s = active ? __ldg(a.st.order + __ldg(a.st.chunk_first + c) + gid) : 0;
             const double gap = active ? __ldg(a.st.op_gap + s) : 0.0;
@@ -185,7 +218,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 const bool has = active && i < a.g.n_sources;
                 const int v = has ? __ldg(a.g.sources + i) : 0;
                 const int dv = has ? __ldg(a.g.device + s_rank[v]) : 0;
-                const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, has ? dv + 32 * grp : 64 + lane);
+                const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, has ? dv + 32 * grp : 1024 + lane);
                 const int base = has ? tails[dv] : 0;
                 __syncwarp();
                 if (has) {
@@ -247,10 +280,23 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 }
                 auto relax = [&](int j) {
                     const uint32_t e = lds_u32(a_succ + 4u * j);
-                    const int m = static_cast<int>(kPacked ? e & 0x1fffu : e & 0xffffu);
-                    const bool single = kPacked ? (e >> 18) & 1u : (e >> 21) & 1u;
-                    if (single || counter_dec<kBits>(cnt, kPacked ? static_cast<int>(e >> 19) : static_cast<int>(lds_u16(a_cidx + 2u * m)))) {
-                        const int dv = static_cast<int>(kPacked ? (e >> 13) & 31u : (e >> 16) & 31u);
+                    int m, dv;
+                    bool ready;
+                    if constexpr (kPacked) {
+                        m = static_cast<int>(e & 0x1fffu);
+                        dv = static_cast<int>((e >> 13) & 15u);
+                        ready = ((e >> 17) & 1u) || counter_dec(cnt, e >> 24, (e >> 19) & 31u, (e >> 18) & 1u ? 15u : 3u);
+                    } else {
+                        m = static_cast<int>(e & 0xffffu);
+                        dv = static_cast<int>((e >> 16) & 31u);
+                        if ((e >> 21) & 1u) {
+                            ready = true;
+                        } else {
+                            const unsigned code = lds_u16(a_cidx + 2u * m);
+                            ready = counter_dec(cnt, code >> 7, (code >> 2) & 31u, (1u << (2u << (code & 3u))) - 1u);
+                        }
+                    }
+                    if (ready) {
                         const int p = atomicAdd(tails + dv, 1);
                         q[dv * QSTRIDE + (p & QMASK)] = static_cast<uint16_t>(m);
                     }
@@ -260,7 +306,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     for (int j = j0; j < j0 + deg; j++) relax(j);
                 const unsigned wm = __ballot_sync(DFSIM_FULL_MASK, wide);
                 if (wm) {
-                    unsigned mine = kGS == 32 ? wm : (wm >> (grp * 16)) & 0xffffu;  // uniform in the group
+                    unsigned mine = in_group ? group_bits<kGS>(wm, grp) : 0u;  // uniform in the group
                     while (__any_sync(DFSIM_FULL_MASK, mine != 0)) {
                         const bool have = mine != 0;
                         const int src = (have ? __ffs(mine) - 1 : 0) + grp * kGS;
@@ -293,7 +339,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 start_idle();
             }
             flag = flag || group_any<kGS>(ovf, grp);
-            const double ms = group_max_f64<kGS>(span);
+            const double ms = group_max_nonneg<kGS>(span, grp);
             const unsigned total = group_add_u32<kGS>(ll < D ? head : 0u, grp);  // every pop starts a node
             if (active && ll == 0) {
                 a.makespan[s] = ms;
@@ -454,13 +500,13 @@ struct FusedShape {
 FusedShape fused_shape(const dfsim_sim_tables *g) {
     FusedShape f;
     const size_t N = (size_t)g->n_nodes;
-    f.graph_bytes = (N * 8 + (size_t)g->n_edges * 4 + 15) / 16 * 16 + N * 8;
-    const size_t tail_bytes = g->n_devices <= 16 ? 64 : 128;
+    f.graph_bytes = (N * (g->succ_packed ? 6 : 8) + (size_t)g->n_edges * 4 + 15) / 16 * 16 + N * 8;
+    const size_t tail_bytes = g->n_devices <= 16 ? 64 : 128;  // 4-byte tail per device, padded
     f.warp_bytes = (tail_bytes + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * (g->qcap + 2) * 2 + 15) / 16 * 16;
     // consecutive candidate groups start 16 banks apart (stride == 64 mod 128 bytes)
     f.warp_bytes = (f.warp_bytes + 127) / 128 * 128 + 64;
     const size_t budget = 227 * 1024 - 64;
-    f.gs = g->n_devices <= 16 ? 16 : 32;
+    f.gs = g->n_devices <= 10 ? 10 : (g->n_devices <= 16 ? 16 : 32);
     f.per_warp = 32 / f.gs;
     f.wpb = 32;
     while (f.wpb > 1 && f.graph_bytes + (size_t)f.wpb * f.per_warp * f.warp_bytes > budget) f.wpb--;
@@ -484,7 +530,9 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
     DFSIM_ARG_CHECK(ctx, g->n_nodes > 0 && g->n_nodes <= 65535 && g->n_devices <= 32, "fused engine limits");
     DFSIM_ARG_CHECK(ctx, g->qcap >= 2 && (g->qcap & (g->qcap - 1)) == 0, "qcap must be a power of two");
-    DFSIM_ARG_CHECK(ctx, g->counter_bits == 4 || g->counter_bits == 8 || g->counter_bits == 16, "counter_bits 4, 8 or 16");
+    DFSIM_ARG_CHECK(ctx, g->n_counter_words >= 1 && g->n_counter_words <= 512, "1..512 counter words");
+    DFSIM_ARG_CHECK(ctx, !g->succ_packed || (g->n_nodes <= 8192 && g->n_devices <= 16 && g->counter_bits <= 4 &&
+                                             g->n_counter_words <= 256), "packed successor format limits");
     if (st->n_sims <= 0 || st->n_chunks <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const FusedShape f = fused_shape(g);
@@ -507,23 +555,17 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(a.chunk_counter, 0, sizeof(int32_t), ctx->stream));
     const size_t smem = f.smem;
     const int grid = ctx->num_sms < st->n_chunks ? ctx->num_sms : (int)st->n_chunks;
-#define DFSIM_LAUNCH_FUSED_P(BITS, GS, PK)                                                                      \
+#define DFSIM_LAUNCH_FUSED_P(GS, PK)                                                                           \
     do {                                                                                                       \
-        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<BITS, GS, PK>,                               \
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<GS, PK>,                                     \
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
-        k_simulate_fused<BITS, GS, PK><<<grid, wpb * 32, smem, ctx->stream>>>(a);                              \
+        k_simulate_fused<GS, PK><<<grid, wpb * 32, smem, ctx->stream>>>(a);                                    \
     } while (0)
-#define DFSIM_LAUNCH_FUSED(BITS, GS)                                                                           \
+#define DFSIM_LAUNCH_FUSED(GS)                                                                                 \
     do {                                                                                                       \
-        if (g->succ_packed) DFSIM_LAUNCH_FUSED_P(BITS, GS, true); else DFSIM_LAUNCH_FUSED_P(BITS, GS, false);   \
+        if (g->succ_packed) DFSIM_LAUNCH_FUSED_P(GS, true); else DFSIM_LAUNCH_FUSED_P(GS, false);              \
     } while (0)
-    if (g->counter_bits == 4) {
-        if (gs == 16) DFSIM_LAUNCH_FUSED(4, 16); else DFSIM_LAUNCH_FUSED(4, 32);
-    } else if (g->counter_bits == 8) {
-        if (gs == 16) DFSIM_LAUNCH_FUSED(8, 16); else DFSIM_LAUNCH_FUSED(8, 32);
-    } else {
-        if (gs == 16) DFSIM_LAUNCH_FUSED(16, 16); else DFSIM_LAUNCH_FUSED(16, 32);
-    }
+    if (gs == 10) DFSIM_LAUNCH_FUSED(10); else if (gs == 16) DFSIM_LAUNCH_FUSED(16); else DFSIM_LAUNCH_FUSED(32);
 #undef DFSIM_LAUNCH_FUSED
 #undef DFSIM_LAUNCH_FUSED_P
     return dfsim_after_launch(ctx, "k_simulate_fused");

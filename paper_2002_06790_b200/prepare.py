@@ -81,6 +81,7 @@ class Tables:
         self._engine(N, off, idx, indeg, dev, outdeg)
         self._critical_path(N, idx, indeg, outdeg, order, pos, loff)
         self.fused_ok = (N <= 65535 and D <= 32 and self.n_edges < 65536 and outdeg.max(initial=0) < 255
+                         and self.counter_words <= 512
                          and indeg.max(initial=0) <= 65534 and self.n_slots < 0x7FFF
                          and self.max_spill_reads < 0x7FFF and self.n_long < 0x7FFF
                          and self.slot_region + 2 * self.stage_doubles < 65536 and len(self.spill_list) < 65536)
@@ -90,34 +91,52 @@ class Tables:
         as ``rank[p]`` for the FIFO tie-break sort, override lookups and the source order."""
         order, pos = self.rank_of_pos, self.pos
         single = indeg == 1
-        multi_p = np.nonzero(indeg[order] >= 2)[0]              # counter slots in position order
-        cslot = np.zeros(N, np.int64)
-        cslot[multi_p] = np.arange(multi_p.size)
-        mx = indeg.max(initial=0)
-        bits = 4 if mx < 15 else (8 if mx < 255 else 16)
-        per = 32 // bits
-        words = max(1, -(-multi_p.size // per))
-        init = np.zeros(words * per, np.uint64)
-        init[: multi_p.size] = indeg[order[multi_p]]
-        init = init.reshape(words, per)
-        packed = np.zeros(words, np.uint64)
-        for i in range(per):
-            packed |= init[:, i] << np.uint64(i * bits)
-        self.counter_bits, self.counter_words = bits, words
+        # dependency counters of multi-input nodes, each as narrow as its in-degree allows
+        # (2, 4, 8 or 16 bits); every width class starts on a fresh 32-bit word so no field
+        # straddles a word.  code = word << 7 | shift << 2 | log2(width) - 1
+        deg_p = indeg[order]
+        multi_p = np.nonzero(deg_p >= 2)[0]
+        wcode = np.select([deg_p <= 3, deg_p <= 15, deg_p <= 255], [0, 1, 2], 3)
+        code = np.zeros(N, np.int64)
+        words, init_words = 0, []
+        for wc in range(4):
+            sel = multi_p[wcode[multi_p] == wc]
+            if sel.size == 0:
+                continue
+            width = 2 << wc
+            per = 32 // width
+            k = np.arange(sel.size)
+            word, shift = words + k // per, (k % per) * width
+            code[sel] = (word << 7) | (shift << 2) | wc
+            fill = np.zeros(-(-sel.size // per) * per, np.uint64)
+            fill[: sel.size] = deg_p[sel]
+            fill = fill.reshape(-1, per)
+            packed_w = np.zeros(fill.shape[0], np.uint64)
+            for i in range(per):
+                packed_w |= fill[:, i] << np.uint64(i * width)
+            init_words.append(packed_w)
+            words += fill.shape[0]
+        packed = np.concatenate(init_words) if init_words else np.zeros(1, np.uint64)
+        self.counter_bits = int(2 << int(wcode[multi_p].max())) if multi_p.size else 2
+        self.counter_words = max(1, words)
         # successor CSR by position: the successors of the node at position p, in its rank-CSR order
-        deg_p = outdeg[order]
+        outdeg_p = outdeg[order]
         off_p = np.zeros(N + 1, np.int64)
-        np.cumsum(deg_p, out=off_p[1:])
-        take = np.arange(int(off_p[-1]), dtype=np.int64) + np.repeat(off[order] - off_p[:-1], deg_p)
+        np.cumsum(outdeg_p, out=off_p[1:])
+        take = np.arange(int(off_p[-1]), dtype=np.int64) + np.repeat(off[order] - off_p[:-1], outdeg_p)
         cons = idx[take]                                         # consumer ranks
         cpos = pos[cons]
-        self.meta = (off_p[:-1] & 0xFFFFFF) | (np.minimum(deg_p, 255) << 24)
-        self.succ_packed = N <= 8192 and multi_p.size <= 8192
-        if self.succ_packed:  # consumer position | device << 13 | single << 18 | counter slot << 19
-            self.succ = cpos | (dev[cons] << 13) | (single[cons].astype(np.int64) << 18) | (cslot[cpos] << 19)
-        else:
+        self.meta = (off_p[:-1] & 0xFFFFFF) | (np.minimum(outdeg_p, 255) << 24)
+        # packed entry: consumer position 13 | device 4 | single 1 | wide 1 | shift 5 | word 8
+        self.succ_packed = (N <= 8192 and int(dev.max(initial=0)) < 16 and self.counter_bits <= 4
+                            and self.counter_words <= 256)
+        if self.succ_packed:
+            cc = code[cpos]
+            self.succ = (cpos | (dev[cons] << 13) | (single[cons].astype(np.int64) << 17) | ((cc & 3) << 18)
+                         | (((cc >> 2) & 31) << 19) | ((cc >> 7) << 24))
+        else:  # consumer position 16 | device 5 | single 1; the counter code comes from cidx[]
             self.succ = cpos | (dev[cons] << 16) | (single[cons].astype(np.int64) << 21)
-        self.cidx, self.cnt_init = cslot, packed
+        self.cidx, self.cnt_init = code, packed
         self.eng_sources = pos[np.nonzero(indeg == 0)[0]]        # ascending ranks, as positions
 
     def _critical_path(self, N, idx, indeg, outdeg, order, pos, loff):

@@ -109,8 +109,11 @@ def test_engine_tables_packing(seed):
     h = host_csr(g)
     t = Tables(len(h["ids"]), len(h["devices"]), h["succ_off"], h["succ_idx"], h["indeg"], h["device"])
     indeg, off, idx, dev = h["indeg"], h["succ_off"], h["succ_idx"], h["device"]
-    per, bits = 32 // t.counter_bits, t.counter_bits
     pos, rank = t.pos, t.rank_of_pos
+
+    def field(word, shift, width):
+        return (int(t.cnt_init[word]) >> shift) & ((1 << width) - 1)
+
     for p in range(t.n):  # engine tables are numbered by level position
         v = int(rank[p])
         m = int(t.meta[p])
@@ -120,15 +123,39 @@ def test_engine_tables_packing(seed):
         for j in range(b, b + d):
             e = int(t.succ[j])
             if t.succ_packed:
-                mp, dv, single, c = e & 0x1FFF, (e >> 13) & 31, (e >> 18) & 1, e >> 19
+                mp, dv, single = e & 0x1FFF, (e >> 13) & 15, (e >> 17) & 1
+                width, shift, word = (4 if (e >> 18) & 1 else 2), (e >> 19) & 31, e >> 24
             else:
-                mp, dv, single, c = e & 0xFFFF, (e >> 16) & 31, (e >> 21) & 1, int(t.cidx[e & 0xFFFF])
+                mp, dv, single = e & 0xFFFF, (e >> 16) & 31, (e >> 21) & 1
+                code = int(t.cidx[mp])
+                width, shift, word = 2 << (code & 3), (code >> 2) & 31, code >> 7
             mr = int(rank[mp])
             assert dv == dev[mr] and single == (indeg[mr] == 1)
             if indeg[mr] >= 2:
-                word = int(t.cnt_init[c // per])
-                assert (word >> ((c % per) * bits)) & ((1 << bits) - 1) == indeg[mr]
+                assert field(word, shift, width) == indeg[mr] and indeg[mr] < (1 << width)
             got.append(mr)
         assert got == list(idx[off[v]:off[v + 1]])
+    # every multi-input node owns a distinct field
+    codes = [int(t.cidx[p]) for p in range(t.n) if indeg[int(rank[p])] >= 2]
+    assert len(set(codes)) == len(codes)
     assert [int(rank[p]) for p in t.eng_sources] == [v for v in range(t.n) if indeg[v] == 0]
     assert (pos[rank] == np.arange(t.n)).all()
+
+
+def test_engine_tables_wide_counters_unpacked():
+    """In-degrees beyond 15 need 8-bit counter fields: the unpacked format with cidx codes."""
+    from paper_2002_06790_b200.model import DeviceSpec, OpNode, make_graph
+
+    nodes = [OpNode(f"s{i:02d}", "Op", f"gpu{i % 3}") for i in range(20)]
+    nodes.append(OpNode("sink", "Op", "gpu0", inputs=tuple((f"s{i:02d}", 0) for i in range(20))))
+    nodes += [OpNode(f"t{i}", "Op", "gpu1", inputs=(("sink", 0), ("s00", 0))) for i in range(3)]
+    g = make_graph(nodes, [DeviceSpec(f"gpu{i}", "Compute") for i in range(3)])
+    h = host_csr(g)
+    t = Tables(len(h["ids"]), len(h["devices"]), h["succ_off"], h["succ_idx"], h["indeg"], h["device"])
+    assert t.fused_ok and not t.succ_packed and t.counter_bits == 8
+    for p in range(t.n):
+        v = int(t.rank_of_pos[p])
+        if h["indeg"][v] >= 2:
+            code = int(t.cidx[p])
+            width, shift, word = 2 << (code & 3), (code >> 2) & 31, code >> 7
+            assert (int(t.cnt_init[word]) >> shift) & ((1 << width) - 1) == h["indeg"][v]
