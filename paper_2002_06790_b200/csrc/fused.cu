@@ -503,10 +503,11 @@ FusedShape fused_shape(const dfsim_sim_tables *g) {
     f.graph_bytes = (N * (g->succ_packed ? 6 : 8) + (size_t)g->n_edges * 4 + 15) / 16 * 16 + N * 8;
     const size_t tail_bytes = g->n_devices <= 16 ? 64 : 128;  // 4-byte tail per device, padded
     f.warp_bytes = (tail_bytes + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * (g->qcap + 2) * 2 + 15) / 16 * 16;
-    // consecutive candidate groups start 16 banks apart (stride == 64 mod 128 bytes)
-    f.warp_bytes = (f.warp_bytes + 127) / 128 * 128 + 64;
-    const size_t budget = 227 * 1024 - 64;
     f.gs = g->n_devices <= 10 ? 10 : (g->n_devices <= 16 ? 16 : 32);
+    // the candidate groups of one warp start on spread-out banks: 16 banks apart for two
+    // groups (stride == 64 mod 128 bytes), 11 banks apart for three (== 44 mod 128)
+    f.warp_bytes = (f.warp_bytes + 127) / 128 * 128 + (f.gs == 10 ? 44 : 64);
+    const size_t budget = 227 * 1024 - 64;
     f.per_warp = 32 / f.gs;
     f.wpb = 32;
     while (f.wpb > 1 && f.graph_bytes + (size_t)f.wpb * f.per_warp * f.warp_bytes > budget) f.wpb--;
