@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kPerWarp = 32 / kGS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ll = lane % kGS, grp = lane / kGS;
+    int ll, grp;  // opaque copies: otherwise lane % 10 and lane / 10 are re-derived at every use
+    asm volatile("mov.u32 %0, %1;" : "=r"(ll) : "r"(lane % kGS));
+    asm volatile("mov.u32 %0, %1;" : "=r"(grp) : "r"(lane / kGS));
     const int gid = warp * kPerWarp + grp;  // candidate slot of this lane group inside a chunk
     const bool in_group = grp < kPerWarp;   // kGS = 10: lanes 30-31 belong to no candidate
     const int N = a.g.n_nodes, D = a.g.n_devices;
