@@ -321,12 +321,20 @@ def run_ours(args):
     t_idx = [torch.as_tensor(idx, dtype=torch.int64, device=dev) for _, idx, _ in classes]
     single = len(classes) == 1
 
-    # several topology classes: each class's launches go to one of up to 8 streams so that small
+    # several topology classes: each class's launches go to one of --streams streams so that small
     # classes (a few chunks each) share the GPU instead of running one after another; every
-    # stream has its own device scratch inside the context (csrc/ctx.cu)
-    streams = [torch.cuda.Stream(local) for _ in range(min(len(classes), 8))] if not single else []
+    # stream has its own device scratch inside the context (csrc/ctx.cu).  The whole multi-class
+    # launch sequence is captured once into a CUDA graph and replayed per step (it is launch-
+    # bound otherwise); ring-overflow flags of all classes share one buffer, so a step needs a
+    # single device->host check before the (rare) exact re-runs.
+    streams = [torch.cuda.Stream(local) for _ in range(min(len(classes), args.streams))] if not single else []
+    flags_all = torch.zeros(S, dtype=torch.int32, device=dev)
+    off = 0
+    for tc, idx, o in classes:
+        o["flags"] = flags_all[off:off + len(idx)]
+        off += len(idx)
 
-    def step(events=None):
+    def launch_all(events=None):
         if streams:
             cur = torch.cuda.current_stream(local)
             for st in streams:
@@ -340,9 +348,6 @@ def run_ours(args):
         for tc, _, o in (classes if not streams else ()):
             tc.expand()
             tc.run(schedules=True, out=o, events=events if single else None, defer_fallback=True)
-        for tc, _, o in classes:  # exact re-run of ring overflows, then their critical paths
-            if tc.fallback_if_needed(o):
-                tc.critical_path_only(o)
         if single:
             o = classes[0][2]
             ms_all, cp_all = o["makespan"], o["cp_len"]
@@ -352,17 +357,55 @@ def run_ours(args):
                 cp_len.index_copy_(0, ti, o["cp_len"])
             ms_all, cp_all = makespan, cp_len
         ctx.call("dfsim_argmin", S, native.ptr(ms_all), index_base, native.ptr(rec))
+        return ms_all, cp_all
+
+    graph = None
+    replays = [0, 0]  # [our kernel launches per replay, replays so far]
+
+    def step(events=None):
+        nonlocal graph
+        if graph is not None:
+            graph.replay()
+            replays[1] += 1
+            ms_all, cp_all = (makespan, cp_len)
+        else:
+            ms_all, cp_all = launch_all(events)
+        if bool(flags_all.any()):  # exact re-run of ring overflows, then their critical paths
+            for tc, _, o in classes:
+                if tc.fallback_if_needed(o):
+                    tc.critical_path_only(o)
+            if not single:
+                for (tc, _, o), ti in zip(classes, t_idx):
+                    makespan.index_copy_(0, ti, o["makespan"])
+                    cp_len.index_copy_(0, ti, o["cp_len"])
+            ctx.call("dfsim_argmin", S, native.ptr(ms_all), index_base, native.ptr(rec))
         r = gather_best(rec) if world > 1 else rec
         return r, ms_all, cp_all
+
+    def capture():
+        nonlocal graph
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = ctx.launches()
+        with torch.cuda.graph(g):
+            launch_all()
+        torch.cuda.synchronize()
+        replays[0] = ctx.launches() - n0
+        graph = g
 
     clocks = ClockSampler(local).start()  # sampled through warm-up, timed steps and e2e
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if not single and not args.no_graph:
+        capture()
+        step()  # one replay before timing
+        torch.cuda.synchronize()
 
     stages = ("estimate", "simulate", "critical_path")
     ev_steps, step_ms = [], []
     launches0 = ctx.launches()
+    replays0 = replays[1]
     for _ in range(args.steps):
         flush.zero_()  # L2 flush (256 MiB write) outside the timed events
         if world > 1:
@@ -377,7 +420,7 @@ def run_ours(args):
         step_ms.append(e0.elapsed_time(e1))
         if single:
             ev_steps.append({k: a.elapsed_time(b) for k, (a, b) in evs.items()})
-    launches = ctx.launches() - launches0
+    launches = ctx.launches() - launches0 + (replays[1] - replays0) * replays[0]  # graph replays count too
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -601,8 +644,12 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-reports", action="store_true", help="skip the summary/trace measurement")
+    ap.add_argument("--no-graph", action="store_true", help="multi-class workloads: launch eagerly, no CUDA graph")
     ap.add_argument("--report-rows", type=int, default=1024, help="schedules summarised in the reports line")
+    ap.add_argument("--streams", type=int, default=16, help="multi-class workloads: concurrent class streams")
     args = ap.parse_args()
+    # concurrent topology classes need more hardware work queues than the default 8
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -188,16 +188,16 @@ class TopologyClass:
 
         lg, S, N, D = self.lg, self.lp.n_sims, self.lg.n, self.lg.n_devices
         dev = f"cuda:{self.ctx.device}"
-        if "sched" not in o:
+        if "sched" not in o:  # callers may pre-place any output (e.g. flags as a view of a shared buffer)
             o["sched"] = torch.empty((S, N, 2), dtype=torch.float64, device=dev)  # (start, finish) pairs
             o["start"], o["finish"] = o["sched"][..., 0], o["sched"][..., 1]
-            o["makespan"] = torch.empty(S, dtype=torch.float64, device=dev)
-            o["busy"] = torch.empty((S, max(D, 1)), dtype=torch.float64, device=dev)
-            o["n_placed"] = torch.empty(S, dtype=torch.int32, device=dev)
-            o["flags"] = torch.empty(S, dtype=torch.int32, device=dev)
-            o["cp_len"] = torch.empty(S, dtype=torch.float64, device=dev)
-            o["cp_src"] = torch.empty(S, dtype=torch.int32, device=dev)
-            o["bad"] = torch.zeros(S, dtype=torch.int32, device=dev)
+            o.setdefault("makespan", torch.empty(S, dtype=torch.float64, device=dev))
+            o.setdefault("busy", torch.empty((S, max(D, 1)), dtype=torch.float64, device=dev))
+            o.setdefault("n_placed", torch.empty(S, dtype=torch.int32, device=dev))
+            o.setdefault("flags", torch.empty(S, dtype=torch.int32, device=dev))
+            o.setdefault("cp_len", torch.empty(S, dtype=torch.float64, device=dev))
+            o.setdefault("cp_src", torch.empty(S, dtype=torch.int32, device=dev))
+            o.setdefault("bad", torch.zeros(S, dtype=torch.int32, device=dev))
         o["layout"] = "position"
         rec = lambda name, i: ev[name][i].record() if name in ev else None  # noqa: E731
         rec("estimate", 0)
@@ -443,7 +443,7 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
 
 
 def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,
-                   fused: bool = True, streams: int = 8) -> SweepResult:
+                   fused: bool = True, streams: int = 16) -> SweepResult:
     """``sweep`` where candidate i runs ``configs[i]`` on ``graphs[graph_of[i]]`` (e.g. one graph per
     batch size).  Graphs of identical structure share a topology class (variants.py).
 
@@ -482,9 +482,11 @@ def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, kee
             tc.run(schedules=True, out=o, defer_fallback=True)
     for st in side:
         cur.wait_stream(st)
-    for (idx, tc), o in zip(built, outs):  # exact re-run of ring overflows, then their critical paths
-        if tc.fallback_if_needed(o):
-            tc.critical_path_only(o)
+    fused_flags = [o["flags"].any() for (_, tc), o in zip(built, outs) if tc.fused]
+    if fused_flags and bool(torch.stack(fused_flags).any()):  # one host check for every class
+        for (idx, tc), o in zip(built, outs):  # exact re-run of ring overflows, then their critical paths
+            if tc.fallback_if_needed(o):
+                tc.critical_path_only(o)
     for pos, ((idx, tc), o) in enumerate(zip(built, outs)):
         t_idx = torch.as_tensor(idx, dtype=torch.int64, device=dev)
         makespan.index_copy_(0, t_idx, o["makespan"])
