@@ -343,6 +343,32 @@ typedef struct {
 int64_t dfsim_trace_write(const dfsim_trace_tables *t, int64_t n_entries, const int32_t *entry_node,
                           const double *start, const double *finish, char *buf, int64_t cap);
 
+/* ---------------------------------------------------------------- graph documents (host) */
+/* parse_graph (graph.py:192-293) + the lowering's CSR / node rows for large documents, in C++.
+ * Only well-formed documents load; anything the reference warns about or rejects returns
+ * DFSIM_CONFIG with a reason, and the caller re-parses with the reference semantics. */
+typedef struct {
+    int32_t n_nodes, n_devices, n_ops, n_sigs, n_fnames, n_declared, max_indeg, n_sources;
+    int64_t n_edges;
+    const char *id_blob; const int64_t *id_off;       /* node ids in rank (code-point) order */
+    const char *op_blob; const int64_t *op_off;       /* op types, first appearance in rank order */
+    const char *dev_blob; const int64_t *dev_off;     /* node devices, sorted (the device ranks) */
+    const char *fname_blob; const int64_t *fname_off; /* feature names */
+    const int32_t *op_of; const uint8_t *kind_of;     /* per node: op index, kind 0/1/2 */
+    const int32_t *dev_of, *indeg, *succ_off, *succ_idx, *sources, *queue_off;  /* host_csr arrays */
+    const int32_t *sig_of; const int64_t *sig_off;    /* feature signature per node (first appearance) */
+    const int32_t *sig_fname; const double *sig_fval; /* signature k: names/values [sig_off[k], sig_off[k+1]) */
+    const uint8_t *comm_ok; const int64_t *comm_bytes; const int32_t *group_size;
+    const double *link_thr, *link_lat;                /* node_rows communication attributes */
+    const int64_t *node_lo, *node_hi;                 /* byte range of each node's JSON object */
+    int64_t meta_lo, meta_hi;                         /* metadata object (-1: absent) */
+    int64_t decl_lo, decl_hi;                         /* devices list (-1: absent) */
+} dfsim_document;
+
+int dfsim_document_parse(const char *text, int64_t len, void **doc_out, char *why, int64_t why_cap);
+const dfsim_document *dfsim_document_view(const void *doc);
+void dfsim_document_free(void *doc);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,7 @@ from .batch import SweepResult, TopologyClass, gather_best, sweep, sweep_variant
 from .estimate import estimate_all, estimate_batch  # noqa: F401
 from .expansion import expand_class, expand_data_parallel  # noqa: F401
 from .lowering import fit_for_grid, fit_linear, node_features  # noqa: F401
+from .document import DocumentGraph, load_graph  # noqa: F401
 from .ps import expand_parameter_server  # noqa: F401
 from .reporting import SummaryReport, render_summary_text, summarize, to_trace, trace_intervals  # noqa: F401
 from .simulator import critical_path, simulate  # noqa: F401

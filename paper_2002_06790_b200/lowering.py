@@ -55,6 +55,9 @@ def _dev_tensor(a, device, dtype=None):
 
 def host_csr(g, ids=None) -> dict:
     """Rank-ordered CSR arrays of ``g`` (host numpy; graph.py:122-135 semantics)."""
+    csr = getattr(g, "csr", None)  # document.DocumentGraph: built by the C++ loader
+    if csr is not None and (ids is None or ids is g.ids):
+        return csr
     ids = list(ids) if ids is not None else sorted(g.nodes)
     rank = {nid: i for i, nid in enumerate(ids)}
     nodes = g.nodes
@@ -405,9 +408,11 @@ class LoweredProfiles:
                 ov_key_to_id[ov_key] = len(ov_sets)
                 ov_sets.append(resolve_overrides(cfg.overrides, ids))
             self.strat_ov.append(ov_key_to_id[ov_key])
+        # document.DocumentGraph: the C++ loader already interned ops, signatures and comm rows
+        doc = getattr(g, "signatures", None) is not None and variant_rows is None and ids is g.ids
         if variant_rows is None:
-            variant_rows = [node_rows(g, ids)]
-        GV = len(variant_rows)
+            variant_rows = [] if doc else [node_rows(g, ids)]
+        GV = 1 if doc else len(variant_rows)
         self.n_gvariants = GV
         self.strat_gv = list(strat_gv) if strat_gv is not None else [0] * len(configs)
         # per node: op, kind (structural); per (variant, node): features and comm attributes
@@ -415,17 +420,28 @@ class LoweredProfiles:
         op = np.empty(N, np.int32)
         kind = np.empty(N, np.uint8)
         self.op_nodes = {}
-        for i, nid in enumerate(ids):
-            n = nodes[nid]
-            op[i] = op_ids.setdefault(n.op_type, len(op_ids))
-            self.op_nodes.setdefault(n.op_type, []).append(i)
-            kind[i] = 0 if n.kind == COMPUTE else (1 if n.kind == TRANSFER else 2)
+        if doc:
+            op_ids = {name: k for k, name in enumerate(g.op_names)}
+            op[:], kind[:] = g.op_of, g.kind_of
+            order = np.argsort(op, kind="stable")
+            bounds = np.searchsorted(op[order], np.arange(len(op_ids) + 1))
+            self.op_nodes = {name: order[bounds[k]:bounds[k + 1]].tolist() for name, k in op_ids.items()}
+        else:
+            for i, nid in enumerate(ids):
+                n = nodes[nid]
+                op[i] = op_ids.setdefault(n.op_type, len(op_ids))
+                self.op_nodes.setdefault(n.op_type, []).append(i)
+                kind[i] = 0 if n.kind == COMPUTE else (1 if n.kind == TRANSFER else 2)
         sig = np.empty((GV, N), np.int32)
         cbytes = np.zeros((GV, N), np.int64)
         cok = np.zeros((GV, N), np.uint8)
         gsize = np.zeros((GV, N), np.int32)
         lthr = np.ones((GV, N), np.float64)
         llat = np.zeros((GV, N), np.float64)
+        if doc:
+            sig_ids = {feats: k for k, feats in enumerate(g.signatures)}
+            sig[0], cok[0], cbytes[0], gsize[0] = g.sig_of, g.comm["ok"], g.comm["bytes"], g.comm["group"]
+            lthr[0], llat[0] = g.comm["thr"], g.comm["lat"]
         for gv, rows in enumerate(variant_rows):
             if len(rows) != N:
                 raise ValueError("graph variants must share the class structure")

@@ -151,6 +151,11 @@ def _doc(text: str, err):
     return doc
 
 
+_NODE_REQUIRED = ("id", "op", "kind", "device")
+_NODE_FIELDS = set(_NODE_REQUIRED) | {"attrs", "inputs", "output_shapes"}
+_DEVICE_FIELDS = {"id", "kind", "hardware", "throughput_mbps", "latency_us"}
+
+
 def parse_graph(text: str) -> DataflowGraph:
     """Read a reference graph document (graph.py:192-293 format)."""
     doc = _doc(text, GraphFormatError)
@@ -162,6 +167,10 @@ def parse_graph(text: str) -> DataflowGraph:
         warnings.warn(f"ignoring unknown graph field {key!r}", GraphFormatWarning, stacklevel=2)
     devices = []
     for i, d in enumerate(doc.get("devices", [])):
+        if not isinstance(d, dict) or "id" not in d or "kind" not in d:
+            raise GraphFormatError("device entry needs 'id' and 'kind'", location=f"devices[{i}]")
+        for key in sorted(set(d) - _DEVICE_FIELDS):  # graph.py:217-219
+            warnings.warn(f"ignoring unknown device field {key!r}", GraphFormatWarning, stacklevel=2)
         try:
             devices.append(DeviceSpec(d["id"], d["kind"], d.get("hardware", ""),
                                       d.get("throughput_mbps"), d.get("latency_us", 0.0)))
@@ -170,6 +179,13 @@ def parse_graph(text: str) -> DataflowGraph:
     nodes = []
     for i, nd in enumerate(doc.get("nodes", [])):
         loc = f"nodes[{i}]"
+        if not isinstance(nd, dict):
+            raise GraphFormatError("node entry must be an object", location=loc)
+        for fieldname in _NODE_REQUIRED:  # graph.py:230-233
+            if fieldname not in nd:
+                raise GraphFormatError(f"missing required node field {fieldname!r}", location=loc)
+        for key in sorted(set(nd) - _NODE_FIELDS):  # graph.py:234-236
+            warnings.warn(f"ignoring unknown node field {key!r}", GraphFormatWarning, stacklevel=2)
         try:
             refs = []
             for ref in nd.get("inputs", []):

@@ -87,6 +87,16 @@ class TraceTables(ctypes.Structure):
                 ("name_off", P), ("tag", P), ("tag_name", P), ("track", P), ("track_name", P)]
 
 
+class Document(ctypes.Structure):
+    _fields_ = [(n, I32) for n in ("n_nodes", "n_devices", "n_ops", "n_sigs", "n_fnames", "n_declared", "max_indeg",
+                                    "n_sources")] + [("n_edges", I64)] + [
+        (n, P) for n in ("id_blob", "id_off", "op_blob", "op_off", "dev_blob", "dev_off", "fname_blob", "fname_off",
+                         "op_of", "kind_of", "dev_of", "indeg", "succ_off", "succ_idx", "sources", "queue_off",
+                         "sig_of", "sig_off", "sig_fname", "sig_fval", "comm_ok", "comm_bytes", "group_size",
+                         "link_thr", "link_lat", "node_lo", "node_hi")] + [
+        (n, I64) for n in ("meta_lo", "meta_hi", "decl_lo", "decl_hi")]
+
+
 _SIGNATURES = {
     "dfsim_abi_version": (I32, []),
     "dfsim_ctx_create": (ctypes.c_int, [I32, P, ctypes.POINTER(P)]),
@@ -112,6 +122,9 @@ _SIGNATURES = {
     "dfsim_argmin_records": (ctypes.c_int, [P, I64, P, P]),
     "dfsim_summarize": (ctypes.c_int, [P, ctypes.POINTER(SummaryTables), I64, P, P, I64, P, I32, P, P, P]),
     "dfsim_trace_write": (I64, [ctypes.POINTER(TraceTables), I64, P, P, P, P, I64]),
+    "dfsim_document_parse": (ctypes.c_int, [ctypes.c_char_p, I64, ctypes.POINTER(P), ctypes.c_char_p, I64]),
+    "dfsim_document_view": (ctypes.POINTER(Document), [P]),
+    "dfsim_document_free": (None, [P]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

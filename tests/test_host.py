@@ -17,7 +17,7 @@ HEADER = ROOT / "include" / "dfsim_b200.h"
 
 def _header_functions():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^(?:int|int32_t|int64_t|const char \*)\s*\*?\s*(dfsim_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:const\s+)?\w+\s*\*?\s*(dfsim_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():
