@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             const double gap = active ? __ldg(a.st.op_gap + s) : 0.0;
             const int ovs = (active && a.st.override_set) ? __ldg(a.st.override_set + s) : -1;
             double2 *out = reinterpret_cast<double2 *>(a.sched) + s * N;
+            asm volatile("mov.b64 %0, %0;" : "+l"(out));  // keep the row base in a register (no per-pop s * N)
             if (active) {
                 for (int w = ll; w < a.g.n_counter_words; w += kGS) cnt[w] = __ldg(a.g.cnt_init + w);
                 if (ll < D) tails[ll] = 0;
