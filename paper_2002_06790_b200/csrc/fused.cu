@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
     const int gid = warp * 2 + half;  // candidate slot of this half-warp in the CTA
     double *region = reinterpret_cast<double *>(smem + a.table_bytes) + static_cast<size_t>(gid) * (SR + 2 * SD);
     double *spill_row = a.spill + (static_cast<int64_t>(blockIdx.x) * a.wpb * 2 + gid) * a.t.n_long;
+    asm volatile("mov.b64 %0, %0;" : "+l"(spill_row));
     const int64_t per_iter = static_cast<int64_t>(gridDim.x) * a.wpb * 2;
 
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * a.wpb * 2 + warp * 2; base < a.S; base += per_iter) {
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
         const bool live = s < a.S;
         const int64_t sr = live ? s : base;  // the idle half shadows its partner's reads
         const double *row = a.sched + 2 * sr * N;
+        asm volatile("mov.b64 %0, %0;" : "+l"(row));  // keep row bases in registers (no 64-bit re-derivation)
         auto prefetch = [&](int c) {
             const int p0 = s_goff[s_coff[c]], p1 = s_goff[s_coff[c + 1]];
             double *bs = region + SR + (c & 1) * SD;
