@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(1024) k_critical_path_wide(CpWideArgs a) {
     for (int64_t s = blockIdx.x; s < a.S; s += gridDim.x) {
         const double *st = a.start ? a.start + s * N : nullptr;
         const double *fi = a.finish + s * N;
+        asm volatile("mov.b64 %0, %0;" : "+l"(fi));  // row bases stay in registers
         double len = 0.0;
         int32_t src = 0x7fffffff;
         for (int32_t L = a.n_levels - 1; L >= 0; L--) {

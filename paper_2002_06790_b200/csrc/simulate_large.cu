@@ -94,11 +94,15 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
     double *rdur = reinterpret_cast<double *>(ws + 128);               // [D][QC]
     int32_t *rnode = reinterpret_cast<int32_t *>(rdur + static_cast<size_t>(D) * QC);  // [D][QC]
     CT *cnt = reinterpret_cast<CT *>(a.gcnt + (static_cast<int64_t>(blockIdx.x) * wpb + wib) * a.cnt_bytes);
+    asm volatile("mov.b64 %0, %0;" : "+l"(cnt));
 
     for (int64_t s = static_cast<int64_t>(blockIdx.x) * wpb + wib; s < a.S; s += static_cast<int64_t>(gridDim.x) * wpb) {
         const double *dur = a.dur + s * a.dur_stride;
         double *out_s = a.start ? a.start + s * N : nullptr;
         double *out_f = a.finish ? a.finish + s * N : nullptr;
+        asm volatile("mov.b64 %0, %0;" : "+l"(dur));  // row bases stay in registers
+        asm volatile("mov.b64 %0, %0;" : "+l"(out_s));
+        asm volatile("mov.b64 %0, %0;" : "+l"(out_f));
         for (int v = lane; v < N; v += 32) cnt[v] = static_cast<CT>(__ldg(a.indeg + v));
         if (lane < D) tails[lane] = 0;
         __syncwarp();
