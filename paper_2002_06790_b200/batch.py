@@ -14,6 +14,7 @@ per rank over NCCL.
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -22,11 +23,9 @@ from . import native
 from .errors import CycleError
 from .estimate import estimate_batch, raise_for_row
 from .expansion import ExpansionPlan
-from .lowering import LoweredGraph, LoweredProfiles, lowered
+from .lowering import LoweredGraph, LoweredProfiles, lowered, resolve_overrides
 from .model import SOURCE_TAGS, DurationEntry
 from .prepare import ClassTables
-from .lowering import resolve_overrides
-import warnings
 from .simulator import build_schedule, critical_path_arrays, simulate_arrays
 
 
