@@ -67,3 +67,49 @@ def test_headline_class_full_size_properties():
         got_s, got_f = st[i].cpu().numpy(), fi[i].cpu().numpy()
         for nid, _, s, f in entries:
             assert got_s[rank[nid]] == s and got_f[rank[nid]] == f, (i, nid)
+
+
+def _class_invariants(tc, o):
+    """Engine invariants of one topology class's schedules (see the module docstring)."""
+    import torch
+
+    lg, N = tc.lg, tc.lg.n
+    st, fi = o["start"][:, :N], o["finish"][:, :N]
+    if o.get("layout") == "position":
+        pos = torch.as_tensor(tc.tables.pos, device=st.device)
+        st, fi = st.index_select(1, pos), fi.index_select(1, pos)
+    assert bool((o["n_placed"] == N).all())
+    assert bool((fi >= st).all())
+    assert torch.equal(o["makespan"], fi.max(dim=1).values)
+    off = lg.t_succ_off[: N + 1].long()
+    idx = lg.t_succ_idx[: lg.n_edges].long()
+    src = torch.repeat_interleave(torch.arange(N, device=st.device), off[1:] - off[:-1])
+    assert bool((st[:, idx] >= fi[:, src]).all())
+    dev = lg.t_dev[:N].long()
+    for d in range(lg.n_devices):
+        nodes = torch.nonzero(dev == d).flatten()
+        s_d, order = st[:, nodes].sort(dim=1, stable=True)
+        f_d = fi[:, nodes].gather(1, order)
+        assert bool((s_d[:, 1:] >= f_d[:, :-1]).all())
+    assert bool((o["cp_len"] <= o["makespan"] * (1 + 1e-12)).all())
+
+
+@pytest.mark.parametrize("workload", ["bert-large-ps-ar", "vgg16-sweep"])
+def test_multiclass_workloads_full_size(workload):
+    """C4 (16,384 candidates, 18 classes) and C3 (10,032 candidates, 45 classes) exactly as the
+    bench builds them: per-class invariants on every schedule, oracle bit-parity on a sample."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2002_06790_b200 import sweep_variants
+
+    graphs, db, configs, graph_of = bench.build_workload(0, bench.WORKLOADS[workload][1], workload)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = sweep_variants(graphs, db, configs, graph_of, keep_schedules=True)
+    for tc, _, o in res.classes:
+        _class_invariants(tc, o)
+    ms = res.makespan
+    assert res.best_index == int(np.lexsort((np.arange(len(ms)), ms))[0])
+    for i in np.linspace(0, len(configs) - 1, 6).astype(int).tolist():
+        want = bench._run_candidate_ps_aware(graphs[graph_of[i]], db, configs[i])
+        assert res.makespan[i] == want, (workload, i)
