@@ -133,3 +133,21 @@ def test_parameter_server_sixteen_workers_vs_oracle():
         entries, ms, busy = O.simulate(gx, {k: v for k, (v, _) in table.items()})
         cp = O.critical_path(gx, {nid: f - s for nid, _, s, f in entries})
         assert res.makespan[i] == ms and res.cp_len[i] == cp[0], i
+
+
+@pytest.mark.parametrize("n", [1, 1000, 16384, 16385, 65536, 1_000_003])
+def test_argmin_first_minimum(n):
+    """K5: first minimum of (value, index) -- single-CTA and two-pass paths, ties across slices."""
+    import torch
+
+    from paper_2002_06790_b200 import native
+
+    rng = np.random.default_rng(n)
+    vals = rng.integers(0, 50, n).astype(np.float64)
+    vals[rng.integers(0, n, 5)] = -1.0  # several tying minima
+    t = torch.tensor(vals, device="cuda:0")
+    rec = torch.empty(2, dtype=torch.float64, device="cuda:0")
+    ctx = native.Context.get(0)
+    ctx.call("dfsim_argmin", n, native.ptr(t), 7, native.ptr(rec))
+    r = rec.cpu()
+    assert float(r[0]) == vals.min() and int(r[1:2].view(torch.int64)) == 7 + int(np.argmin(vals))
