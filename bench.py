@@ -382,13 +382,26 @@ def run_ours(args):
         r = gather_best(rec) if world > 1 else rec
         return r, ms_all, cp_all
 
+    stages = ("estimate", "simulate", "critical_path")
+    # stage events of the single-class step live inside the graph as external event-record
+    # nodes, so each replay times its own kernels (the roofline reads them)
+    graph_evs = {k: (torch.cuda.Event(enable_timing=True, external=True),
+                     torch.cuda.Event(enable_timing=True, external=True)) for k in stages}
+
+    cap_stream = torch.cuda.Stream(local)
+
     def capture():
         nonlocal graph
+        # per-stream device scratch: size it on the capture stream first (no allocation may
+        # happen while a stream is capturing)
+        cap_stream.wait_stream(torch.cuda.current_stream(local))
+        with torch.cuda.stream(cap_stream):
+            launch_all()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = ctx.launches()
-        with torch.cuda.graph(g):
-            launch_all()
+        with torch.cuda.graph(g, stream=cap_stream):
+            launch_all(graph_evs if single else None)
         torch.cuda.synchronize()
         replays[0] = ctx.launches() - n0
         graph = g
@@ -397,12 +410,11 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if not single and not args.no_graph:
+    if not args.no_graph:
         capture()
         step()  # one replay before timing
         torch.cuda.synchronize()
 
-    stages = ("estimate", "simulate", "critical_path")
     ev_steps, step_ms = [], []
     launches0 = ctx.launches()
     replays0 = replays[1]
@@ -419,7 +431,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         if single:
-            ev_steps.append({k: a.elapsed_time(b) for k, (a, b) in evs.items()})
+            src = graph_evs if graph is not None else evs
+            ev_steps.append({k: a.elapsed_time(b) for k, (a, b) in src.items()})
     launches = ctx.launches() - launches0 + (replays[1] - replays0) * replays[0]  # graph replays count too
     total_ms = sum(step_ms)
     if world > 1:
@@ -644,7 +657,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-reports", action="store_true", help="skip the summary/trace measurement")
-    ap.add_argument("--no-graph", action="store_true", help="multi-class workloads: launch eagerly, no CUDA graph")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--report-rows", type=int, default=1024, help="schedules summarised in the reports line")
     ap.add_argument("--streams", type=int, default=16, help="multi-class workloads: concurrent class streams")
     args = ap.parse_args()
