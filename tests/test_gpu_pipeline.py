@@ -126,3 +126,24 @@ def test_sweep_concurrent_streams_match_serial():
         if cfgs[i].sync == "allreduce":
             ms, cp, *_ = O.run_candidate(graphs[gof[i]], db, cfgs[i])
             assert (b.makespan[i], b.cp_len[i]) == (ms, cp), i
+
+
+def test_sweep_edge_cases():
+    """Empty graph, a single node, no configs: the reference's answers (cli.py:123-149)."""
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200.model import DeviceSpec, OpNode, ProfileDB, StrategyConfig, make_graph
+
+    empty = make_graph([], [])
+    res = fw.sweep(empty, ProfileDB(), [StrategyConfig(), StrategyConfig(op_gap_us=1.0)], keep_schedules=True)
+    assert list(res.makespan) == [0.0, 0.0] and list(res.cp_len) == [0.0, 0.0] and res.best_index == 0
+    s = res.schedule(0)
+    assert s.entries == [] and s.makespan_us == 0.0
+    assert fw.to_trace(s) == "[]\n"
+    one = make_graph([OpNode("a", "Op", "gpu0")], [DeviceSpec("gpu0", "Compute")])
+    cfgs = [StrategyConfig(overrides={"a": 2.5}), StrategyConfig(overrides={"a": 1.5})]
+    res = fw.sweep(one, ProfileDB(), cfgs, keep_schedules=True)
+    assert list(res.makespan) == [2.5, 1.5] and res.best_index == 1
+    rep = res.summary(1)
+    assert rep.critical_path_nodes == ["a"] and rep.critical_path_us == 1.5 and rep.top_k_ops == [("Op", 1.5, 1.0)]
+    none = fw.sweep(one, ProfileDB(), [])
+    assert none.best_index == -1 and len(none.makespan) == 0
