@@ -167,8 +167,12 @@ extern "C" int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfs
 extern "C" int dfsim_estimate_batch(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t,
                                     const dfsim_strategies *st, double *dur, uint8_t *src, int32_t *bad) {
     if (!ctx || !t || !st || !dur) return DFSIM_BAD_ARGUMENT;
-    if (n_nodes <= 0 || st->n_sims <= 0) return DFSIM_OK;
+    if (st->n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    if (n_nodes <= 0) {  // an empty graph estimates fine: bad[s] = 0 (no unresolved node)
+        if (bad) DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, sizeof(int32_t) * (size_t)st->n_sims, ctx->stream));
+        return DFSIM_OK;
+    }
     const int64_t total = st->n_sims * (int64_t)n_nodes;
     int64_t blocks = (total + 255) / 256;
     const int64_t cap = (int64_t)ctx->num_sms * 16;

@@ -160,10 +160,13 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
             auto start_idle = [&]() {
                 const int t = owner ? tails[ll] : 0;
-                if (owner && !running && static_cast<int>(head) < t) {
+                if (owner && !running && !ovf && static_cast<int>(head) < t) {
                     // a busy device only gains entries until its next pop, so checking the
-                    // occupancy before every pop catches every ring overflow
-                    ovf |= static_cast<unsigned>(t) - head > static_cast<unsigned>(QCAP);
+                    // occupancy before every pop catches every ring overflow; the device then
+                    // stops for good (no overwritten entry is ever read, so the flagged candidate
+                    // cannot corrupt its counters or loop) and the candidate is re-run exactly
+                    ovf = static_cast<unsigned>(t) - head > static_cast<unsigned>(QCAP);
+                    if (ovf) return;
                     const int v = q[ll * QSTRIDE + (head & QMASK)];
                     head++;
                     const double b = lds_f64(a_base + 8u * v);
@@ -262,7 +265,10 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 __syncwarp();
                 start_idle();
             }
-            flag = flag || group_any<kGS>(ovf, grp);
+            // evaluated by every lane: a short-circuit here would leave the groups of a warp at
+            // different warp-wide votes (a deadlock when only some groups are flagged)
+            const bool any_ovf = group_any<kGS>(ovf, grp);
+            flag = flag || any_ovf;
             const double ms = group_max_nonneg<kGS>(span, grp);
             const unsigned total = group_add_u32<kGS>(ll < D ? head : 0u, grp);  // every pop starts a node
             if (active && ll == 0) {
@@ -430,6 +436,7 @@ FusedShape fused_shape(const dfsim_sim_tables *g) {
     const size_t tail_bytes = g->n_devices <= 16 ? 64 : 128;  // 4-byte tail per device, padded
     f.warp_bytes = (tail_bytes + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * (g->qcap + 2) * 2 + 15) / 16 * 16;
     f.gs = g->n_devices <= 10 ? 10 : (g->n_devices <= 16 ? 16 : 32);
+
     // the candidate groups of one warp start on spread-out banks: 16 banks apart for two
     // groups (stride == 64 mod 128 bytes), 11 banks apart for three (== 44 mod 128)
     f.warp_bytes = (f.warp_bytes + 127) / 128 * 128 + (f.gs == 10 ? 44 : 64);

@@ -143,8 +143,9 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
         };
         auto start_idle = [&]() {
             const int t = lane < D ? tails[lane] : 0;
-            if (lane < D && !running && static_cast<int>(head) < t) {
-                ovf |= static_cast<unsigned>(t) - head > static_cast<unsigned>(QC);
+            if (lane < D && !running && !ovf && static_cast<int>(head) < t) {
+                ovf = static_cast<unsigned>(t) - head > static_cast<unsigned>(QC);
+                if (ovf) return;  // stop the device: the candidate is re-run exactly
                 const int slot = lane * QC + static_cast<int>(head & QM);
                 const int v = rnode[slot];
                 const double f = __dadd_rn(now, rdur[slot]);

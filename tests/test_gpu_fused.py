@@ -129,6 +129,24 @@ def test_fused_ring_overflow_falls_back_exactly(resnet, monkeypatch):
     assert of.get("fallback_rows"), "QCAP=2 must overflow on this graph"
 
 
+@pytest.mark.parametrize("n", [1, 2, 4, 97])
+def test_fused_overflow_in_partial_warps(resnet, monkeypatch, n):
+    """Chunks whose warps hold flagged and idle candidate groups side by side (three groups
+    per warp): every lane must reach the warp-wide votes (regression: a short-circuited vote
+    deadlocked such warps)."""
+    from paper_2002_06790_b200.batch import TopologyClass
+    from paper_2002_06790_b200.prepare import ClassTables
+
+    g, db = resnet
+    cfgs = _configs(n)
+    monkeypatch.setattr(ClassTables, "QCAP", 2)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        tf = TopologyClass(g, db, cfgs, fused=True)
+        tu = TopologyClass(g, db, cfgs, fused=False)
+    _compare(tf, tu)
+
+
 def test_fused_spot_check_against_oracle(resnet):
     from oracle import dfsim_oracle as O
     from paper_2002_06790_b200 import sweep

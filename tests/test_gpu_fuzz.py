@@ -1,0 +1,54 @@
+"""GPU: randomized parity of the batched fused path against the oracle.
+
+Random DAGs (sizes, fan-in, 1-12 devices), random strategies (hardware tag, op_gap_us,
+override sets with ties and zeros, data-parallel expansion with gradient markers); every
+candidate's schedule, makespan and critical path must equal the oracle's bit for bit."""
+
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fused_sweep_random_instances(seed):
+    import paper_2002_06790_b200 as fw
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(30, 260))
+    g = W.random_dag(n, float(rng.uniform(0.01, 0.08)), seed=100 + seed, num_devices=int(rng.integers(1, 13)))
+    db = W.dag_profiles(["hwA", "hwB"])
+    for link in W.SYNTH_LINKS:  # gpu-gpu-uni rows for the ring formula
+        W.db_insert(db, link)
+    ids = sorted(g.nodes)
+    dp = seed % 2 == 1
+    cfgs = []
+    for i in range(24):
+        ov = {}
+        if i % 3 == 0:  # literal and prefix overrides, ties and zeros
+            for nid in rng.choice(ids, size=min(4, n), replace=False).tolist():
+                ov[nid] = float(rng.choice([0.0, 1.0, 2.5, 2.5]))
+            ov[ids[0][:6] + "*"] = 3.0
+        kw = dict(hardware=("hwA", "hwB")[i % 2], op_gap_us=float(rng.choice([0.0, 0.125, 1e-3 * i])), overrides=ov)
+        if dp:
+            R = int(rng.integers(2, 5))
+            kw.update(replicas=R, device_map=tuple(f"gpu{k}" for k in range(R)),
+                      collective=CollectiveConfig("RingAnalytic", "PCIeSwitch"), gradient_markers=(ids[-1][:8] + "*",))
+        cfgs.append(StrategyConfig(**kw))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = fw.sweep(g, db, cfgs, keep_schedules=True)
+        for i, cfg in enumerate(cfgs):
+            ms, cp, entries, busy, path = O.run_candidate(g, db, cfg)
+            assert (res.makespan[i], res.cp_len[i]) == (ms, cp), (seed, i)
+            s = res.schedule(i)
+            assert [(e.node_id, e.device, e.start_us, e.finish_us) for e in s.entries] == entries, (seed, i)
+            assert res.critical_path(i) == (cp, path), (seed, i)
+    assert res.best_index == int(np.lexsort((np.arange(len(cfgs)), res.makespan))[0])
