@@ -52,3 +52,48 @@ def test_fused_sweep_random_instances(seed):
             assert [(e.node_id, e.device, e.start_us, e.finish_us) for e in s.entries] == entries, (seed, i)
             assert res.critical_path(i) == (cp, path), (seed, i)
     assert res.best_index == int(np.lexsort((np.arange(len(cfgs)), res.makespan))[0])
+
+
+@pytest.mark.parametrize("seed", range(8, 20))
+def test_fused_sweep_random_mixed(seed):
+    """Mixed classes in one sweep: plain, allreduce and parameter-server strategies, measured and
+    ring algorithms, 1-30 devices (16- and 32-lane groups), against the oracle."""
+    import paper_2002_06790_b200 as fw
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+    from paper_2002_06790_b200.ps import expand_parameter_server
+
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(20, 160))
+    g = W.random_dag(n, float(rng.uniform(0.02, 0.1)), seed=300 + seed, num_devices=int(rng.integers(1, 31)))
+    db = W.dag_profiles(["hwA"])
+    for link in W.SYNTH_LINKS:
+        W.db_insert(db, link)
+    ids = sorted(g.nodes)
+    cfgs = []
+    for i in range(18):
+        kind = i % 3
+        kw = dict(hardware="hwA", op_gap_us=float(rng.choice([0.0, 0.5])),
+                  overrides={ids[int(rng.integers(0, n))]: float(rng.choice([0.0, 2.0]))} if i % 4 == 0 else {})
+        if kind:
+            R = int(rng.integers(2, 5))
+            kw.update(replicas=R, device_map=tuple(f"gpu{k}" for k in range(R)),
+                      collective=CollectiveConfig(("RingAnalytic", "MeasuredThroughput")[i % 2], "PCIeSwitch"),
+                      gradient_markers=(ids[-1][:8] + "*",), sync=("allreduce", "parameter_server")[kind - 1])
+            if kind == 2:
+                kw["overrides"] = dict(kw["overrides"], **{"aggregate_*": 1.25})  # no PSAggregate profile
+        cfgs.append(StrategyConfig(**kw))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = fw.sweep(g, db, cfgs, keep_schedules=True)
+        for i, cfg in enumerate(cfgs):
+            if getattr(cfg, "sync", "allreduce") == "parameter_server":
+                gx = expand_parameter_server(g, cfg, db).graph
+                table = O.estimate(gx, db, cfg)
+                entries, ms, _ = O.simulate(gx, {k: v for k, (v, _) in table.items()})
+                cp = O.critical_path(gx, {nid: f - s for nid, _, s, f in entries})[0]
+            else:
+                ms, cp, entries, _, _ = O.run_candidate(g, db, cfg)
+            assert (res.makespan[i], res.cp_len[i]) == (ms, cp), (seed, i)
+            assert [(e.node_id, e.device, e.start_us, e.finish_us) for e in res.schedule(i).entries] == entries
