@@ -122,3 +122,60 @@ def test_loader_rejects_what_python_would_parse_differently():
         g = load_graph(json.dumps(d))
         assert not isinstance(g, DocumentGraph)
         assert g.nodes["x"].attrs == parse_graph(json.dumps(d)).nodes["x"].attrs or attrs.get("v") != attrs.get("v")
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_loader_random_documents(seed):
+    """Random well-formed documents (ids with escapes and non-ASCII, numeric / boolean / string /
+    nested attrs, multi-output shapes, duplicate references, link and collective devices) load
+    identically; random corruptions fall back to parse_graph's exact behaviour."""
+    import random
+
+    rng = random.Random(seed)
+    alphabet = "abcxyz_0189-./é漢\"\\ \t"
+    n = rng.randint(1, 60)
+    ids = set()
+    while len(ids) < n:
+        ids.add("".join(rng.choice(alphabet) for _ in range(rng.randint(1, 8))).replace(":", "") or "n")
+    ids = list(ids)
+    devs = [{"id": f"gpu{k}", "kind": "Compute"} for k in range(rng.randint(1, 4))]
+    devs.append({"id": "lnk", "kind": "Link", "throughput_mbps": rng.choice([10, 2.5e3]), "latency_us": rng.random()})
+    devs.append({"id": "fab", "kind": "CollectiveResource", "throughput_mbps": 1.0})
+    nodes = []
+    n_out = [rng.randint(0, 2) for _ in ids]
+    for i, nid in enumerate(ids):
+        kind = rng.choice(["Compute", "Compute", "Transfer", "Collective"])
+        dev = {"Compute": rng.choice(devs[:-2])["id"], "Transfer": "lnk", "Collective": "fab"}[kind]
+        attrs = {}
+        for k in range(rng.randint(0, 5)):
+            attrs[rng.choice(["a", "b", "flops", "k", "n", "bytes", "group", "z9", "é"])] = rng.choice(
+                [rng.randint(-5, 10 ** 6), rng.random() * 100, rng.randint(1, 9), 7, None, "s", [1, 2], {"x": 1},
+                 -0.0, True])
+        nd = {"id": nid, "op": rng.choice(["MatMul", "Add", "", "Send", "AllReduce"]), "kind": kind, "device": dev,
+              "attrs": attrs,
+              "inputs": [f"{ids[j]}:{rng.randint(0, max(1, n_out[j]) - 1) if rng.random() < 0.97 else 5}"
+                         for j in rng.sample(range(i), min(i, rng.randint(0, 3)))] if i else [],
+              "output_shapes": [{"dims": [rng.randint(0, 9) for _ in range(rng.randint(0, 3))],
+                                 "dtype_bytes": rng.choice([1, 2, 4])} for _ in range(n_out[i])]}
+        if nd["inputs"] and rng.random() < 0.2:
+            nd["inputs"].append(nd["inputs"][0])  # duplicate reference
+        nodes.append(nd)
+    doc = {"format_version": rng.choice([1, "1", "1.7"]), "metadata": {"seed": seed}, "devices": devs, "nodes": nodes}
+    text = json.dumps(doc, ensure_ascii=rng.random() < 0.5, indent=rng.choice([None, 1, 2]))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        try:
+            ref = parse_graph(text)
+        except Exception as exc:  # e.g. a slot beyond a producer's outputs, a feature-name collision
+            with pytest.raises(type(exc)):
+                load_graph(text)
+            return
+        try:
+            rows = node_rows(ref, host_csr(ref)["ids"])
+        except ValueError:
+            rows = None  # attr/feature collisions are rejected by estimate, not by parse_graph
+        got = load_graph(text)
+    if rows is None or isinstance(got, type(ref)):
+        assert list(got.nodes) == list(ref.nodes)
+        return
+    _same(text)
