@@ -8,6 +8,7 @@ import hashlib
 import json
 import warnings
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -107,3 +108,36 @@ def test_sweep_summaries_resnet_dp8_vs_oracle():
             want = O.summarize(entries, op, kinds, busy, makespan, cp, top_k=12)
             assert json.dumps(_doc(reps[i])) == json.dumps(want), i
             assert res.trace(i) == O.to_trace(entries, op, {k: s for k, (_, s) in table.items()}, busy), i
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_summarize_random_schedules_vs_oracle(seed):
+    """K6 on random schedules: link / collective devices, empty op types, zero durations, ties."""
+    import paper_2002_06790_b200 as fw
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200.model import (DeviceSpec, DurationEntry, DurationTable, OpNode, make_graph)
+
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 400))
+    devs = [DeviceSpec(f"gpu{k}", "Compute") for k in range(int(rng.integers(1, 6)))]
+    devs += [DeviceSpec(f"link{k}", "Link", "", 100.0, 0.5) for k in range(int(rng.integers(0, 3)))]
+    devs += [DeviceSpec("fabric", "CollectiveResource", "", 1.0, 0.0)] if rng.random() < 0.5 else []
+    nodes, durs = [], {}
+    for i in range(n):
+        d = devs[int(rng.integers(0, len(devs)))]
+        kind = {"Compute": "Compute", "Link": "Transfer", "CollectiveResource": "Collective"}[d.kind]
+        ins = tuple((f"v{j:04d}", 0) for j in sorted(set(rng.integers(0, i, size=int(rng.integers(0, 3))).tolist()))) if i else ()
+        nodes.append(OpNode(f"v{i:04d}", str(rng.choice(["MatMul", "Add", "", "Send"])), d.id, kind, {}, ins))
+        durs[f"v{i:04d}"] = float(rng.choice([0.0, 1.0, 2.5, rng.uniform(0, 10)]))
+    g = make_graph(nodes, devs)
+    table = DurationTable(entries={k: DurationEntry(v, "Override") for k, v in durs.items()})
+    s = fw.simulate(g, table)
+    rep = fw.summarize(s, g, top_k=int(rng.integers(0, 6)))
+    entries, ms, busy = O.simulate(g, durs)
+    cp = O.critical_path(g, {nid: f - st for nid, _, st, f in entries})
+    want = O.summarize(entries, {k: v.op_type for k, v in g.nodes.items()}, {d: sp.kind for d, sp in g.devices.items()},
+                       s.per_device_busy_us, ms, cp, top_k=len(rep.top_k_ops) if rep.top_k_ops else 0)
+    got = _doc(rep)
+    for k in ("compute_us", "comm_us", "overlap_us", "critical_path_us", "critical_path_nodes", "makespan_us"):
+        assert got[k] == want[k], (seed, k)
+    assert got["top_k_ops"] == want["top_k_ops"][: len(got["top_k_ops"])]
