@@ -36,10 +36,11 @@ enum : uint8_t { J_NULL, J_TRUE, J_FALSE, J_INT, J_FLOAT, J_STR, J_ARR, J_OBJ };
 
 struct Val {
     uint8_t t = J_NULL;
-    int64_t i = 0;      // J_INT (fits int64)
-    double d = 0.0;     // J_INT / J_FLOAT numeric value (float(int) for ints)
-    uint32_t a = 0, n = 0;  // J_STR: string pool [a, a+n); J_ARR/J_OBJ: kids [a, a+n)
-    int64_t lo = 0, hi = 0; // byte range in the text
+    uint8_t in_text = 0;    // J_STR without escapes: [a, a+n) of the document itself (no copy)
+    uint32_t a = 0, n = 0;  // J_STR: string pool / text [a, a+n); J_ARR/J_OBJ: kids [a, a+n)
+    uint32_t lo = 0, hi = 0;  // byte range in the text (documents < 4 GB)
+    int64_t i = 0;          // J_INT (fits int64)
+    double d = 0.0;         // J_INT / J_FLOAT numeric value (float(int) for ints)
 };
 
 struct Parser {
@@ -92,6 +93,17 @@ struct Parser {
     void string_into(Val &v) {
         p++;  // opening quote
         v.t = J_STR;
+        {  // fast path: no escape before the closing quote -> a view of the document
+            int64_t q = p;
+            while (q < len && s[q] != '"' && s[q] != '\\' && static_cast<unsigned char>(s[q]) >= 0x20) q++;
+            if (q < len && s[q] == '"') {
+                v.in_text = 1;
+                v.a = static_cast<uint32_t>(p);
+                v.n = static_cast<uint32_t>(q - p);
+                p = q + 1;
+                return;
+            }
+        }
         v.a = static_cast<uint32_t>(pool.size());
         while (true) {
             if (p >= len) unsupported("JSON syntax");
@@ -198,7 +210,7 @@ struct Parser {
         const uint32_t idx = static_cast<uint32_t>(vals.size());
         vals.emplace_back();
         Val v;
-        v.lo = p;
+        v.lo = static_cast<uint32_t>(p);
         const char c = peek();
         if (c == '{') {
             p++;
@@ -213,9 +225,9 @@ struct Parser {
                     const uint32_t k = static_cast<uint32_t>(vals.size());
                     vals.emplace_back();
                     Val kv;
-                    kv.lo = p;
+                    kv.lo = static_cast<uint32_t>(p);
                     string_into(kv);
-                    kv.hi = p;
+                    kv.hi = static_cast<uint32_t>(p);
                     vals[k] = kv;
                     expect(':');
                     const uint32_t val = value(depth + 1);
@@ -266,7 +278,7 @@ struct Parser {
         } else {
             number_into(v);  // NaN / Infinity literals land here and are unsupported
         }
-        v.hi = p;
+        v.hi = static_cast<uint32_t>(p);
         vals[idx] = v;
         return idx;
     }
@@ -292,7 +304,9 @@ struct Doc {
     dfsim_document view{};
 };
 
-std::string_view sv(const Parser &P, const Val &v) { return std::string_view(P.pool).substr(v.a, v.n); }
+std::string_view sv(const Parser &P, const Val &v) {
+    return v.in_text ? std::string_view(P.s + v.a, v.n) : std::string_view(P.pool).substr(v.a, v.n);
+}
 
 // object field lookup; duplicate keys are unsupported (json.loads keeps the last one)
 struct Fields {  // at most 8 known fields: no heap allocation per object
@@ -322,6 +336,45 @@ Fields fields_of(const Parser &P, const Val &obj, std::initializer_list<std::str
 }
 
 const char *kKinds[3] = {"Compute", "Transfer", "Collective"};
+
+uint64_t hash_bytes(const char *p, size_t n, uint64_t h = 1469598103934665603ull) {  // FNV-1a
+    for (size_t i = 0; i < n; i++) h = (h ^ static_cast<unsigned char>(p[i])) * 1099511628211ull;
+    return h;
+}
+
+// string_view -> index, open addressing (no per-entry allocation; the id lookups of a 10^6-node
+// document are the loader's hottest operation)
+struct IdTable {
+    std::vector<int32_t> slot;  // -1 empty, else index into keys
+    const std::vector<std::string_view> *keys = nullptr;
+    uint64_t mask = 0;
+    void build(const std::vector<std::string_view> &k, const std::vector<uint32_t> &order) {
+        keys = &k;
+        size_t cap = 16;
+        while (cap < order.size() * 2) cap <<= 1;
+        slot.assign(cap, -1);
+        mask = cap - 1;
+        for (size_t r = 0; r < order.size(); r++) {
+            const std::string_view key = k[order[r]];
+            uint64_t h = hash_bytes(key.data(), key.size()) & mask;
+            while (slot[h] >= 0) {
+                if ((*keys)[order[slot[h]]] == key) unsupported("duplicate node id");
+                h = (h + 1) & mask;
+            }
+            slot[h] = static_cast<int32_t>(r);
+        }
+        order_ = &order;
+    }
+    int32_t find(std::string_view key) const {
+        uint64_t h = hash_bytes(key.data(), key.size()) & mask;
+        while (slot[h] >= 0) {
+            if ((*keys)[(*order_)[slot[h]]] == key) return slot[h];
+            h = (h + 1) & mask;
+        }
+        return -1;
+    }
+    const std::vector<uint32_t> *order_ = nullptr;
+};
 
 void build(Doc &D, Parser &P, uint32_t root) {
     const Val &top = P.vals[root];
@@ -390,6 +443,7 @@ void build(Doc &D, Parser &P, uint32_t root) {
         const Val *obj, *attrs, *inputs, *shapes;
     };
     std::vector<NodeRef> raw(N);
+    std::vector<std::string_view> raw_ids(N);
     for (uint32_t i = 0; i < N; i++) {
         const Val &o = P.vals[P.kids[nv->a + i]];
         if (o.t != J_OBJ) unsupported("node entry");
@@ -408,17 +462,14 @@ void build(Doc &D, Parser &P, uint32_t root) {
         if (in && in->t != J_ARR) unsupported("inputs");
         if (sh && sh->t != J_ARR) unsupported("output_shapes");
         raw[i] = NodeRef{ids, sv(P, *op), sv(P, *dev), kc, &o, at, in, sh};
+        raw_ids[i] = ids;
     }
     // rank order: code-point order of ids == byte order of their UTF-8
     std::vector<uint32_t> order(N);
     for (uint32_t i = 0; i < N; i++) order[i] = i;
-    std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return raw[x].id < raw[y].id; });
-    std::unordered_map<std::string_view, int32_t> rank;
-    rank.reserve(N * 2 + 1);
-    for (uint32_t r = 0; r < N; r++) {
-        if (r > 0 && raw[order[r]].id == raw[order[r - 1]].id) unsupported("duplicate node id");
-        rank.emplace(raw[order[r]].id, static_cast<int32_t>(r));
-    }
+    std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return raw_ids[x] < raw_ids[y]; });
+    IdTable rank;  // node id -> rank
+    rank.build(raw_ids, order);
     // output shapes (dims as ints, dtype_bytes > 0), flat: node r's slot k has dims
     // dims[dim_off[shape_off[r] + k] .. dim_off[shape_off[r] + k + 1])
     std::vector<int64_t> dims_flat, dim_off{0};
@@ -460,11 +511,22 @@ void build(Doc &D, Parser &P, uint32_t root) {
     D.queue_off.assign(devs.size() + 1, 0);
     // per node, rank order
     std::vector<int32_t> prods, cons;
-    std::string key;  // signature dedup key: (name, value bits with -0.0 == 0.0) sequence
-    std::unordered_map<std::string, int32_t> sig_ids;
+    // signature dedup (tuple equality: -0.0 == 0.0): open addressing on a content hash
+    std::vector<int32_t> sig_slot(1024, -1);
+    std::vector<uint64_t> sig_hash;
     std::unordered_map<std::string, int32_t> fname_ids;
     std::vector<std::string> fnames;
-    std::vector<std::pair<std::string, double>> feats;
+    std::vector<std::pair<std::string_view, double>> feats;
+    char genbuf[8192];  // this node's generated in<i>_dim<j> names (views into it live for one node)
+    auto sig_equal = [&](int32_t sid) {
+        const int64_t b = D.sig_off[sid], e = D.sig_off[sid + 1];
+        if (e - b != static_cast<int64_t>(feats.size())) return false;
+        for (int64_t j = b; j < e; j++) {
+            const auto &f = feats[static_cast<size_t>(j - b)];
+            if (f.second != D.fval[j] || fnames[D.fname[j]] != f.first) return false;
+        }
+        return true;
+    };
     D.sig_off.push_back(0);
     for (uint32_t r = 0; r < N; r++) {
         const NodeRef &n = raw[order[r]];
@@ -488,13 +550,14 @@ void build(Doc &D, Parser &P, uint32_t root) {
         D.indeg.push_back(static_cast<int32_t>(nin));
         D.max_indeg = std::max<int32_t>(D.max_indeg, static_cast<int32_t>(nin));
         feats.clear();
+        int genlen = 0;
         if (n.attrs) {
             for (uint32_t k = 0; k < n.attrs->n; k++) {
                 const std::string_view an = sv(P, P.vals[P.kids[n.attrs->a + 2 * k]]);
                 for (uint32_t q = 0; q < k; q++)
                     if (sv(P, P.vals[P.kids[n.attrs->a + 2 * q]]) == an) unsupported("duplicate attr");
                 const Val &av = P.vals[P.kids[n.attrs->a + 2 * k + 1]];
-                if (av.t == J_INT || av.t == J_FLOAT) feats.emplace_back(std::string(an), av.d);
+                if (av.t == J_INT || av.t == J_FLOAT) feats.emplace_back(an, av.d);
             }
         }
         for (uint32_t k = 0; k < nin; k++) {
@@ -510,9 +573,8 @@ void build(Doc &D, Parser &P, uint32_t root) {
                 if (ch < '0' || ch > '9') unsupported("slot");
                 slot = slot * 10 + (ch - '0');
             }
-            const auto pr = rank.find(pid);
-            if (pr == rank.end()) unsupported("missing producer");
-            const int32_t q = pr->second;
+            const int32_t q = rank.find(pid);
+            if (q < 0) unsupported("missing producer");
             const int64_t nshapes = shape_off[q + 1] - shape_off[q];
             if (!(slot < std::max<int64_t>(1, nshapes))) unsupported("bad slot");
             prods.push_back(q);
@@ -520,7 +582,8 @@ void build(Doc &D, Parser &P, uint32_t root) {
             if (slot < nshapes) {  // node_features' in<i>_dim<j>
                 const int64_t sh = shape_off[q] + slot;
                 for (int64_t j = 0; j < dim_off[sh + 1] - dim_off[sh]; j++) {
-                    char nm[48];
+                    if (genlen + 48 > static_cast<int>(sizeof genbuf)) unsupported("too many input dims");
+                    char *nm = genbuf + genlen;
                     int len = 0;
                     auto put_uint = [&](uint64_t x) {
                         char tmp[24];
@@ -535,35 +598,54 @@ void build(Doc &D, Parser &P, uint32_t root) {
                     len += 4;
                     put_uint(static_cast<uint64_t>(j));
                     const std::string_view nv(nm, static_cast<size_t>(len));
+                    genlen += len;
                     for (auto &e : feats)
                         if (e.first == nv) unsupported("attr name collides with an input dim");
-                    feats.emplace_back(std::string(nv), static_cast<double>(dims_flat[dim_off[sh] + j]));
+                    feats.emplace_back(nv, static_cast<double>(dims_flat[dim_off[sh] + j]));
                 }
             }
         }
         std::sort(feats.begin(), feats.end(), [](auto &x, auto &y) { return x.first < y.first; });
-        key.clear();
+        uint64_t hk = 1469598103934665603ull;
         for (auto &e : feats) {
-            key += e.first;
-            key += '\0';
+            hk = hash_bytes(e.first.data(), e.first.size(), hk) * 31;
             const double v = e.second == 0.0 ? 0.0 : e.second;  // tuple equality: -0.0 == 0.0
-            key.append(reinterpret_cast<const char *>(&v), sizeof v);
+            hk = hash_bytes(reinterpret_cast<const char *>(&v), sizeof v, hk);
         }
-        auto si = sig_ids.find(key);
-        if (si == sig_ids.end()) {
-            si = sig_ids.emplace(key, static_cast<int32_t>(sig_ids.size())).first;
+        uint64_t h = hk & (sig_slot.size() - 1);
+        int32_t sid = -1;
+        while (sig_slot[h] >= 0) {
+            if (sig_hash[sig_slot[h]] == hk && sig_equal(sig_slot[h])) {
+                sid = sig_slot[h];
+                break;
+            }
+            h = (h + 1) & (sig_slot.size() - 1);
+        }
+        if (sid < 0) {
+            sid = static_cast<int32_t>(sig_hash.size());
+            sig_slot[h] = sid;
+            sig_hash.push_back(hk);
             for (auto &e : feats) {
-                auto fi = fname_ids.find(e.first);
+                auto fi = fname_ids.find(std::string(e.first));
                 if (fi == fname_ids.end()) {
-                    fi = fname_ids.emplace(e.first, static_cast<int32_t>(fnames.size())).first;
-                    fnames.push_back(e.first);
+                    fi = fname_ids.emplace(std::string(e.first), static_cast<int32_t>(fnames.size())).first;
+                    fnames.emplace_back(e.first);
                 }
                 D.fname.push_back(fi->second);
                 D.fval.push_back(e.second);  // the first-appearing values represent the signature
             }
             D.sig_off.push_back(static_cast<int64_t>(D.fname.size()));
+            if (sig_hash.size() * 2 > sig_slot.size()) {  // grow and rehash
+                std::vector<int32_t> bigger(sig_slot.size() * 2, -1);
+                for (size_t k = 0; k < sig_hash.size(); k++) {
+                    uint64_t q = sig_hash[k] & (bigger.size() - 1);
+                    while (bigger[q] >= 0) q = (q + 1) & (bigger.size() - 1);
+                    bigger[q] = static_cast<int32_t>(k);
+                }
+                sig_slot.swap(bigger);
+            }
         }
-        D.sig_of.push_back(si->second);
+        D.sig_of.push_back(sid);
         // communication attributes (node_rows: costmodel.py:347-376 inputs)
         uint8_t ok = 0;
         int64_t bytes = 0;
