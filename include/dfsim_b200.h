@@ -231,6 +231,8 @@ typedef struct {
     const int32_t *ov_off;
     const int32_t *ov_node;
     const double *ov_val;
+    int32_t max_chunk;         /* largest chunk_count (0: the capacity); CTAs are sized to it, so a
+                                  small class spread over many small chunks fills the SMs */
 } dfsim_fused_strategies;
 
 /* K2a: base[var*N+v] = estimate of node v under variant var = (graph variant, hw, algo, path) with
@@ -243,6 +245,11 @@ int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_
 /* Candidates one CTA of the fused engine holds; chunks of dfsim_fused_strategies
  * must not exceed it (0: the class does not fit the fused engine). */
 int32_t dfsim_fused_capacity(const dfsim_sim_tables *g);
+
+/* Chunk size for a class of n_sims candidates on a GPU of num_sms SMs: small classes are
+ * cut finer so their CTAs cover the SMs, never below the size at which a CTA's copy of
+ * the class tables outweighs its candidates' state; <= dfsim_fused_capacity. */
+int32_t dfsim_fused_chunk(const dfsim_sim_tables *g, int64_t n_sims, int32_t num_sms);
 
 /* K3 v2: outputs sched[S][N][2] = (start, finish) by level position (16-byte aligned);
  * flags[s] = 1 when the FIFO ring overflowed (re-run s with dfsim_simulate_batch_ex);

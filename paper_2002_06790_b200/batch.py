@@ -121,6 +121,10 @@ class TopologyClass:
         if cap <= 0:
             return
         self.chunk_capacity = cap
+        # a small class is cut into smaller chunks so that its CTAs cover the SMs (the
+        # launcher sizes CTAs to the largest chunk)
+        sms = torch.cuda.get_device_properties(self.ctx.device).multi_processor_count
+        cap = int(self.ctx.lib.dfsim_fused_chunk(native.ctypes.byref(self.tables.sim_struct), lp.n_sims, sms))
         order = np.argsort(var_of, kind="stable")
         firsts, counts, variants = [], [], []
         sorted_var = var_of[order]
@@ -138,7 +142,7 @@ class TopologyClass:
             lp.n_sims, V, native.ptr(self.base), len(firsts), native.ptr(self.f_order), native.ptr(self.f_first),
             native.ptr(self.f_count), native.ptr(self.f_var), native.ptr(s["gap"]),
             native.ptr(s["ov"]) if any(x >= 0 for x in lp.strat_ov) else native.P(0),
-            native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]))
+            native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]), max(counts, default=0))
         self.fused = True
 
     def resolve(self):
@@ -442,7 +446,7 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
 
 
 def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,
-                   fused: bool = True, streams: int = 16) -> SweepResult:
+                   fused: bool = True, streams: int = 48) -> SweepResult:
     """``sweep`` where candidate i runs ``configs[i]`` on ``graphs[graph_of[i]]`` (e.g. one graph per
     batch size).  Graphs of identical structure share a topology class (variants.py).
 

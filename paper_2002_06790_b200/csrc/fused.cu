@@ -456,6 +456,20 @@ extern "C" int32_t dfsim_fused_capacity(const dfsim_sim_tables *g) {
     return f.fits ? f.wpb * f.per_warp : 0;
 }
 
+extern "C" int32_t dfsim_fused_chunk(const dfsim_sim_tables *g, int64_t n_sims, int32_t num_sms) {
+    const int32_t cap = dfsim_fused_capacity(g);
+    if (cap <= 0 || n_sims <= 0 || num_sms <= 0) return cap;
+    const FusedShape f = fused_shape(g);
+    const int64_t pw = f.per_warp;
+    auto warps = [&](int64_t c) { return (c + pw - 1) / pw * pw; };
+    // enough chunks to cover every SM, each holding at least as many candidate bytes as its
+    // CTA's copy of the class tables (smaller chunks would trade candidates for table copies)
+    const int64_t spread = warps((n_sims + num_sms - 1) / num_sms);
+    const int64_t least = warps((int64_t)((f.graph_bytes + f.warp_bytes - 1) / f.warp_bytes));
+    int64_t c = spread > least ? spread : least;
+    return c < cap ? static_cast<int32_t>(c) : cap;
+}
+
 extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,
                                     double *sched, double *makespan, double *busy, int32_t *n_placed,
                                     int32_t *flags) {
@@ -472,8 +486,11 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     const FusedShape f = fused_shape(g);
     DFSIM_ARG_CHECK(ctx, f.fits, "class tables do not fit in shared memory");
     const size_t graph_bytes = f.graph_bytes, warp_bytes = f.warp_bytes;
-    const int gs = f.gs, wpb = f.wpb;
-    (void)warp_bytes;
+    const int gs = f.gs;
+    DFSIM_ARG_CHECK(ctx, st->max_chunk >= 0 && st->max_chunk <= f.wpb * f.per_warp, "max_chunk exceeds the capacity");
+    // CTAs hold max_chunk candidates: a class cut into small chunks runs as many small CTAs
+    // (several per SM) instead of a few full ones
+    const int wpb = st->max_chunk > 0 ? (st->max_chunk + f.per_warp - 1) / f.per_warp : f.wpb;
     FusedArgs a;
     a.g = *g;
     a.st = *st;
@@ -487,13 +504,18 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     if (rc) return rc;
     a.chunk_counter = static_cast<int32_t *>(p);
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(a.chunk_counter, 0, sizeof(int32_t), ctx->stream));
-    const size_t smem = f.smem;
-    const int grid = ctx->num_sms < st->n_chunks ? ctx->num_sms : (int)st->n_chunks;
+    const size_t smem = graph_bytes + (size_t)wpb * f.per_warp * warp_bytes;
+    const int threads = wpb * 32;
 #define DFSIM_LAUNCH_FUSED_P(GS, PK)                                                                           \
     do {                                                                                                       \
         DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<GS, PK>,                                     \
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
-        k_simulate_fused<GS, PK><<<grid, wpb * 32, smem, ctx->stream>>>(a);                                    \
+        int occ = 1;                                                                                           \
+        DFSIM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_fused<GS, PK>,      \
+                                                                          threads, smem));                    \
+        const int64_t slots = (int64_t)ctx->num_sms * (occ > 0 ? occ : 1);                                    \
+        const int grid = (int)(slots < st->n_chunks ? slots : st->n_chunks);                                   \
+        k_simulate_fused<GS, PK><<<grid, threads, smem, ctx->stream>>>(a);                                    \
     } while (0)
 #define DFSIM_LAUNCH_FUSED(GS)                                                                                 \
     do {                                                                                                       \
@@ -527,8 +549,20 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     int wpb = 32;
     while (wpb > 1 && table_bytes + wpb * per_warp > budget) wpb--;
     DFSIM_ARG_CHECK(ctx, table_bytes + wpb * per_warp <= budget, "critical-path tables do not fit in shared memory");
+    // a small batch is spread over every SM (fewer warps per CTA, several CTAs per SM), but
+    // never so thin that the per-CTA table copy outweighs the candidates' regions
+    const int64_t spread = (n_sims + 2 * (int64_t)ctx->num_sms - 1) / (2 * (int64_t)ctx->num_sms);
+    const int64_t least = (int64_t)((table_bytes + per_warp - 1) / per_warp);
+    const int64_t thin = spread > least ? spread : least;
+    if (thin < wpb) wpb = thin < 1 ? 1 : (int)thin;
+    const size_t smem = table_bytes + wpb * per_warp;
+    DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_critical_path_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 1;
+    const int threads = wpb * 32;
+    DFSIM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_critical_path_levels, threads, smem));
     const int64_t want = (n_sims + 2 * wpb - 1) / (2 * wpb);
-    const int grid = (int)(want < ctx->num_sms ? want : ctx->num_sms);
+    const int64_t slots = (int64_t)ctx->num_sms * (occ > 0 ? occ : 1);
+    const int grid = (int)(want < slots ? want : slots);
     void *p = nullptr;
     int rc = dfsim_scratch(ctx, (size_t)grid * wpb * 2 * (size_t)(t->n_long > 0 ? t->n_long : 1) * 8, &p);
     if (rc) return rc;
@@ -539,8 +573,6 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     a.spill = static_cast<double *>(p);
     a.wpb = wpb;
     a.table_bytes = (int)table_bytes;
-    const size_t smem = table_bytes + wpb * per_warp;
-    DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_critical_path_levels, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_critical_path_levels<<<grid, wpb * 32, smem, ctx->stream>>>(a);
+    k_critical_path_levels<<<grid, threads, smem, ctx->stream>>>(a);
     return dfsim_after_launch(ctx, "k_critical_path_levels");
 }

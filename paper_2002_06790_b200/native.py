@@ -68,7 +68,7 @@ class SimTables(ctypes.Structure):
 class FusedStrategies(ctypes.Structure):
     _fields_ = [("n_sims", I64), ("n_variants", I32), ("base", P), ("n_chunks", I32), ("order", P),
                 ("chunk_first", P), ("chunk_count", P), ("chunk_variant", P), ("op_gap", P), ("override_set", P),
-                ("ov_off", P), ("ov_node", P), ("ov_val", P)]
+                ("ov_off", P), ("ov_node", P), ("ov_val", P), ("max_chunk", I32)]
 
 
 class CpTables(ctypes.Structure):
@@ -118,6 +118,7 @@ _SIGNATURES = {
                                             P, P]),
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P]),
     "dfsim_fused_capacity": (I32, [ctypes.POINTER(SimTables)]),
+    "dfsim_fused_chunk": (I32, [ctypes.POINTER(SimTables), I64, I32]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),
     "dfsim_argmin_records": (ctypes.c_int, [P, I64, P, P]),
     "dfsim_summarize": (ctypes.c_int, [P, ctypes.POINTER(SummaryTables), I64, P, P, I64, P, I32, P, P, P]),
