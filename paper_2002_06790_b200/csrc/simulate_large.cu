@@ -138,7 +138,13 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
         auto load_durs = [&]() {  // second stage, one iteration after the start
 #pragma unroll
             for (int k = 0; k < kPre; k++)
-                if (k < static_cast<int>(r0.y)) pdur[k] = __ldg(dur + (succ_of(k) & 0x7ffffffu));
+                if (k < static_cast<int>(r0.y)) {
+                    const unsigned m = succ_of(k) & 0x7ffffffu;
+                    pdur[k] = __ldg(dur + m);
+                    // the counter is read when this node finishes, usually several iterations
+                    // on: bring its line into L1 now (values can still change, so no load)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(cnt + m));
+                }
             have_dur = true;
         };
         auto start_idle = [&]() {
@@ -162,6 +168,10 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                 r0 = __ldg(a.srec + 2 * static_cast<int64_t>(v));
                 r1 = __ldg(a.srec + 2 * static_cast<int64_t>(v) + 1);
                 have_dur = false;
+                if (static_cast<int>(head) < t) {  // the device's next node: its record into L1 now
+                    const int nv = rnode[lane * QC + static_cast<int>(head & QM)];
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.srec + 2 * static_cast<int64_t>(nv)));
+                }
             }
         };
 
@@ -177,18 +187,34 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                 // one device finished (the common case): it alone updates counters and rings
                 if (done) {
                     const int deg = static_cast<int>(r0.y);
-                    for (int k = 0; k < deg; k++) {
-                        unsigned e;
-                        double dd;
-                        if (k < kPre) {
-                            e = succ_of(k);
-                            dd = k == 0 ? pdur[0] : (k == 1 ? pdur[1] : (k == 2 ? pdur[2] : pdur[3]));
-                        } else {
-                            const int m = __ldg(a.succ_idx + static_cast<int>(r0.x) + k);
-                            e = static_cast<unsigned>(m) | (static_cast<unsigned>(__ldg(a.device + m)) << 27);
-                            dd = __ldg(dur + m);
+                    // the carried successors' counters are loaded together (one latency, not
+                    // deg); a repeated successor (duplicate edge) sees the earlier decrements
+                    int cpre[kPre];
+#pragma unroll
+                    for (int k = 0; k < kPre; k++)
+                        if (k < deg) cpre[k] = static_cast<int>(cnt[succ_of(k) & 0x7ffffffu]);
+#pragma unroll
+                    for (int k = 0; k < kPre; k++) {
+                        if (k < deg) {
+                            const unsigned e = succ_of(k);
+                            const int m = static_cast<int>(e & 0x7ffffffu), dv = static_cast<int>(e >> 27);
+                            int c = cpre[k];
+#pragma unroll
+                            for (int j = 0; j < k; j++) c -= (succ_of(j) & 0x7ffffffu) == static_cast<unsigned>(m);
+                            cnt[m] = static_cast<CT>(c - 1);
+                            if (c == 1) {
+                                const int p = tails[dv];
+                                tails[dv] = p + 1;
+                                rnode[dv * QC + (p & QM)] = m;
+                                rdur[dv * QC + (p & QM)] = pdur[k];
+                            }
                         }
-                        const int m = static_cast<int>(e & 0x7ffffffu), dv = static_cast<int>(e >> 27);
+                    }
+                    for (int k = kPre; k < deg; k++) {
+                        const int m = __ldg(a.succ_idx + static_cast<int>(r0.x) + k);
+                        const unsigned e = static_cast<unsigned>(m) | (static_cast<unsigned>(__ldg(a.device + m)) << 27);
+                        const double dd = __ldg(dur + m);
+                        const int dv = static_cast<int>(e >> 27);
                         const int c = static_cast<int>(cnt[m]);
                         cnt[m] = static_cast<CT>(c - 1);
                         if (c == 1) {

@@ -115,3 +115,29 @@ def test_large_engine_ring_overflow_falls_back():
     rng = np.random.default_rng(2)
     n = len(nodes)
     _check_engine(g, [rng.uniform(0.5, 3, n), np.ones(n)])
+
+
+def test_large_engine_duplicate_edges_and_wide_fanout():
+    """Repeated producers (two slots of one node: duplicate edges) and hub nodes with
+    fan-outs far beyond the kPre carried successors, on the large engine."""
+    from paper_2002_06790_b200.model import DeviceSpec, OpNode, TensorShape, make_graph
+
+    rng = np.random.default_rng(9)
+    n, D = 150_000, 6
+    shapes = (TensorShape((4,), 4), TensorShape((4,), 4))
+    nodes = []
+    for i in range(n):
+        ins = []
+        if i:
+            for _ in range(int(rng.integers(1, 4))):
+                p = int(rng.integers(max(0, i - 1500), i))
+                ins.append((f"v{p:06d}", 0))
+                if rng.random() < 0.3:
+                    ins.append((f"v{p:06d}", 1))  # the same producer again
+            if i % 97 == 0 and i % 1000:
+                ins.append((f"v{(i // 1000) * 1000:06d}", 0))  # hubs: every 1000th node
+        uniq = tuple(dict.fromkeys(ins))
+        nodes.append(OpNode(f"v{i:06d}", "Op", f"gpu{i % D}", inputs=uniq, output_shapes=shapes))
+    g = make_graph(nodes, [DeviceSpec(f"gpu{k}", "Compute") for k in range(D)])
+    rows = [rng.uniform(0.5, 30, n), np.round(rng.uniform(0, 4, n)) / 2]
+    _check_engine(g, rows)
