@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
             for (int k = 0; k < kPre; k++)
                 if (k < static_cast<int>(r0.y)) {
                     const unsigned m = succ_of(k) & 0x7ffffffu;
-                    pdur[k] = __ldg(dur + m);
+                    pdur[k] = __ldcg(dur + m);  // L2 only: L1 stays with the counters and successor records
                     // the counter is read when this node finishes, usually several iterations
                     // on: bring its line into L1 now (values can still change, so no load)
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(cnt + m));
