@@ -286,6 +286,10 @@ typedef struct {
 int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *sched,
                                double *cp_len, int32_t *cp_src);
 
+/* Candidates one CTA of dfsim_critical_path_levels holds (0: the class tables do not fit
+ * in shared memory; such a class uses the rank-layout kernels instead). */
+int32_t dfsim_critical_path_levels_capacity(const dfsim_cp_tables *t);
+
 /* ---------------------------------------------------------------- critical path (K4) */
 /* Over d = finish - start (reporting.py:128), or over d = finish when start is NULL
  * (the plain critical_path(g, durations) call).  cp_len[s]; cp_path [n_sims][N] and

@@ -118,8 +118,8 @@ class TopologyClass:
         if (st >= 253).any():
             return  # some candidate fails estimation: keep the unfused path (exact error semantics)
         cap = int(self.ctx.lib.dfsim_fused_capacity(native.ctypes.byref(self.tables.sim_struct)))
-        if cap <= 0:
-            return
+        if cap <= 0 or self.ctx.lib.dfsim_critical_path_levels_capacity(native.ctypes.byref(self.tables.cp_struct)) <= 0:
+            return  # engine or critical-path tables exceed shared memory: rank-layout kernels
         self.chunk_capacity = cap
         # a small class is cut into smaller chunks so that its CTAs cover the SMs (the
         # launcher sizes CTAs to the largest chunk)

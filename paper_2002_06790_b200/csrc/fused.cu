@@ -527,6 +527,31 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     return dfsim_after_launch(ctx, "k_simulate_fused");
 }
 
+namespace {
+// shared-memory layout of k_critical_path_levels: class tables once per CTA, then one
+// region pair (slots + two prefetch stages) per two candidates (a warp)
+struct CpShape {
+    size_t table_bytes, per_warp;
+    int wpb;  // warps that fit (0: not even one)
+};
+
+CpShape cp_shape(const dfsim_cp_tables *t) {
+    CpShape c;
+    c.table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 +
+                     (size_t)(t->n_chunks + 1) * 4 + (size_t)t->n_edges * 2 + 15) / 16 * 16;
+    // layout: (cp_meta, pinfo) pairs 8N | succ 2E | group_off 2(G+1) | chunk/spill offsets 4(NC+1) | spill list <= 2E
+    c.per_warp = 2 * ((size_t)t->slot_region + 2 * (size_t)t->stage_doubles) * 8;  // two candidates
+    const size_t budget = 227 * 1024 - 64;
+    c.wpb = 32;
+    while (c.wpb > 0 && c.table_bytes + c.wpb * c.per_warp > budget) c.wpb--;
+    return c;
+}
+}  // namespace
+
+extern "C" int32_t dfsim_critical_path_levels_capacity(const dfsim_cp_tables *t) {
+    return t ? 2 * cp_shape(t).wpb : 0;
+}
+
 extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *sched,
                                           double *cp_len, int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
@@ -540,15 +565,10 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
                     "inconsistent critical-path region layout");
     if (n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    const size_t n_spill_reads = 0;  // staged list length is read on the device; bound it by E
-    const size_t table_bytes = ((size_t)t->n_nodes * 8 + (size_t)t->n_edges * 2 + (size_t)(t->n_groups + 1) * 2 +
-                                (size_t)(t->n_chunks + 1) * 4 + (size_t)t->n_edges * 2 + n_spill_reads + 15) / 16 * 16;
-    // layout: (cp_meta, pinfo) pairs 8N | succ 2E | group_off 2(G+1) | chunk/spill offsets 4(NC+1) | spill list <= 2E
-    const size_t per_warp = 2 * ((size_t)t->slot_region + 2 * (size_t)t->stage_doubles) * 8;  // two candidates
-    const size_t budget = 227 * 1024 - 64;
-    int wpb = 32;
-    while (wpb > 1 && table_bytes + wpb * per_warp > budget) wpb--;
-    DFSIM_ARG_CHECK(ctx, table_bytes + wpb * per_warp <= budget, "critical-path tables do not fit in shared memory");
+    const CpShape shape = cp_shape(t);
+    const size_t table_bytes = shape.table_bytes, per_warp = shape.per_warp;
+    int wpb = shape.wpb;
+    DFSIM_ARG_CHECK(ctx, wpb >= 1, "critical-path tables do not fit in shared memory (dfsim_critical_path_levels_capacity)");
     // a small batch is spread over every SM (fewer warps per CTA, several CTAs per SM), but
     // never so thin that the per-CTA table copy outweighs the candidates' regions
     const int64_t spread = (n_sims + 2 * (int64_t)ctx->num_sms - 1) / (2 * (int64_t)ctx->num_sms);

@@ -117,6 +117,7 @@ _SIGNATURES = {
     "dfsim_simulate_fused": (ctypes.c_int, [P, ctypes.POINTER(SimTables), ctypes.POINTER(FusedStrategies), P, P, P,
                                             P, P]),
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P]),
+    "dfsim_critical_path_levels_capacity": (I32, [ctypes.POINTER(CpTables)]),
     "dfsim_fused_capacity": (I32, [ctypes.POINTER(SimTables)]),
     "dfsim_fused_chunk": (I32, [ctypes.POINTER(SimTables), I64, I32]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),

@@ -97,3 +97,29 @@ def test_fused_sweep_random_mixed(seed):
                 ms, cp, entries, _, _ = O.run_candidate(g, db, cfg)
             assert (res.makespan[i], res.cp_len[i]) == (ms, cp), (seed, i)
             assert [(e.node_id, e.device, e.start_us, e.finish_us) for e in res.schedule(i).entries] == entries
+
+
+def test_dense_class_beyond_critical_path_smem():
+    """A dense DAG expanded 7 ways: the class fits the engine's limits but its level-order
+    critical-path tables exceed shared memory, so the class runs on the rank-layout kernels
+    (found by the soak: seed 50280 used to raise instead)."""
+    import paper_2002_06790_b200 as fw
+    from oracle import dfsim_oracle as O
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+
+    g = W.random_dag(295, 0.14186208467922018, seed=50280, num_devices=4)
+    db = W.dag_profiles(["hwA", "hwB"])
+    for link in W.SYNTH_LINKS:
+        W.db_insert(db, link)
+    cfgs = [StrategyConfig(replicas=7, device_map=tuple(f"gpu{k}" for k in range(7)),
+                           collective=CollectiveConfig("RingAnalytic", "PCIeSwitch"),
+                           gradient_markers=("node_02*",), hardware=("hwA", "hwB")[i % 2],
+                           op_gap_us=0.125 * i) for i in range(6)]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = fw.sweep(g, db, cfgs, keep_schedules=True)
+        for i, cfg in enumerate(cfgs):
+            ms, cp, entries, _, _ = O.run_candidate(g, db, cfg)
+            assert (res.makespan[i], res.cp_len[i]) == (ms, cp), i
+            assert [(e.node_id, e.device, e.start_us, e.finish_us) for e in res.schedule(i).entries] == entries, i

@@ -159,3 +159,32 @@ def test_engine_tables_wide_counters_unpacked():
             code = int(t.cidx[p])
             width, shift, word = 2 << (code & 3), (code >> 2) & 31, code >> 7
             assert (int(t.cnt_init[word]) >> shift) & ((1 << width) - 1) == h["indeg"][v]
+
+
+def test_dense_class_exceeds_critical_path_smem():
+    """The class of tests/test_gpu_fuzz.py::test_dense_class_beyond_critical_path_smem passes
+    the engine's table limits (fused_ok) while its level-order critical-path tables exceed
+    one CTA's shared memory (the layout of csrc/fused.cu cp_shape), so that GPU test runs
+    the capacity check's fallback."""
+    import warnings
+
+    from oracle import dfsim_oracle as O
+    from oracle import native_oracle as NO
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+    from paper_2002_06790_b200.prepare import Tables
+
+    g = W.random_dag(295, 0.14186208467922018, seed=50280, num_devices=4)
+    cfg = StrategyConfig(replicas=7, device_map=tuple(f"gpu{k}" for k in range(7)),
+                         collective=CollectiveConfig("RingAnalytic", "PCIeSwitch"), gradient_markers=("node_02*",),
+                         hardware="hwA")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        gx = O.expand(g, cfg)[0]
+    c = NO.Csr(gx)
+    idx = np.asarray(c.idx)
+    t = Tables(c.n, c.n_dev, np.asarray(c.off), idx, np.asarray(c.indeg), np.asarray(c.dev))
+    assert t.fused_ok
+    table = (c.n * 8 + len(idx) * 4 + (t.n_groups + 1) * 2 + (t.n_chunks + 1) * 4 + 15) // 16 * 16
+    per_warp = 2 * (t.slot_region + 2 * t.stage_doubles) * 8
+    assert table + per_warp > 227 * 1024 - 64
