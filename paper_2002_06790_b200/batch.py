@@ -130,11 +130,9 @@ class TopologyClass:
         sorted_var = var_of[order]
         bounds = np.flatnonzero(np.diff(sorted_var)) + 1
         for a, b in zip(np.r_[0, bounds], np.r_[bounds, len(order)]):
-            k = -(-(b - a) // cap)  # chunks of this variant, sizes within one of each other
-            cuts = a + ((b - a) * np.arange(k + 1)) // k
-            for c0, c1 in zip(cuts[:-1], cuts[1:]):
-                firsts.append(int(c0))
-                counts.append(int(c1 - c0))
+            for c in range(a, b, cap):  # full chunks (whole warps), then the variant's remainder
+                firsts.append(int(c))
+                counts.append(int(min(cap, b - c)))
                 variants.append(int(sorted_var[a]))
         T = lambda x, dt: torch.as_tensor(np.asarray(x), dtype=dt, device=dev)  # noqa: E731
         self.f_order = T(order, torch.int64)
