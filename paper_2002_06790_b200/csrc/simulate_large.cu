@@ -5,13 +5,16 @@
 // event iterations (~N of them), so the design goal is the latency of one iteration,
 // not bandwidth.  Against the exact-capacity engine (simulate.cu, global mode) it
 // removes every dependent global round trip from the iteration:
-//   * FIFO rings in shared memory hold (node, duration) pairs: a pop needs no global
-//     load.  Ring occupancy is checked before every pop (a device only gains entries
-//     until its next pop); an overflowed candidate is re-run by the exact engine.
+//   * FIFO rings of node ids in shared memory (4 bytes an entry, so most of the SM's
+//     256 KB stays L1 for the counter rows).  When a device starts a node it also loads
+//     the duration of its next ring entry (whose place at the head is final), so the
+//     next pop rarely waits on memory.  Ring occupancy is checked before every pop (a
+//     device only gains entries until its next pop); an overflowed candidate is re-run
+//     by the exact engine.
 //   * A start loads the node's 32-byte successor record (range + the first kPre
-//     successors with their devices, built once per launch); the next iteration loads
-//     those successors' durations.  At finish the relax step reads registers only
-//     (longer lists fall back to direct loads).
+//     successors with their devices, built once per launch); the next iteration
+//     prefetches those successors' counter lines.  At finish the relax step loads the
+//     carried successors' counters together (longer lists fall back to direct loads).
 //   * One finishing device per iteration (the common case) relaxes alone with plain
 //     counter and ring-tail updates; ties between devices take the combining path.
 //   * Dependency counters are plain byte/short loads and stores in a global row per
@@ -91,8 +94,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
     const unsigned QM = static_cast<unsigned>(QC - 1);
     unsigned char *ws = smem + static_cast<size_t>(wib) * a.warp_smem;
     int32_t *tails = reinterpret_cast<int32_t *>(ws);                  // [32]
-    double *rdur = reinterpret_cast<double *>(ws + 128);               // [D][QC]
-    int32_t *rnode = reinterpret_cast<int32_t *>(rdur + static_cast<size_t>(D) * QC);  // [D][QC]
+    int32_t *rnode = reinterpret_cast<int32_t *>(ws + 128);            // [D][QC]
     CT *cnt = reinterpret_cast<CT *>(a.gcnt + (static_cast<int64_t>(blockIdx.x) * wpb + wib) * a.cnt_bytes);
     asm volatile("mov.b64 %0, %0;" : "+l"(cnt));
 
@@ -112,14 +114,12 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
             const bool has = i < a.n_sources;
             const int v = has ? __ldg(a.sources + i) : 0;
             const int dv = has ? __ldg(a.device + v) : 32 + lane;
-            const double dd = has ? __ldg(dur + v) : 0.0;
             const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, dv);
             const int base = has ? tails[dv] : 0;
             __syncwarp();
             if (has) {
                 const int p = base + __popc(peers & lanemask_lt());
                 rnode[dv * QC + (p & QM)] = v;
-                rdur[dv * QC + (p & QM)] = dd;
                 if ((peers & lanemask_lt()) == 0) tails[dv] = base + __popc(peers);
             }
             __syncwarp();
@@ -127,34 +127,31 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
         bool ovf = lane < D && tails[lane] > QC;
 
         unsigned head = 0;
-        bool running = false, have_dur = false;
+        bool running = false, have_pref = false;
         uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);  // successor record of the running node
-        double pdur[kPre];
+        int nx_v = -1;      // the device's next ring entry, whose duration is already in flight
+        double nx_d = 0.0;
         double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
         int placed = 0;
-#pragma unroll
-        for (int k = 0; k < kPre; k++) pdur[k] = 0.0;
         auto succ_of = [&](int k) -> unsigned { return k == 0 ? r0.z : (k == 1 ? r0.w : (k == 2 ? r1.x : r1.y)); };
-        auto load_durs = [&]() {  // second stage, one iteration after the start
+        auto prefetch_counters = [&]() {  // second stage, one iteration after the start
+            // the counters are read when this node finishes, usually several iterations on:
+            // bring their lines into L1 now (values can still change, so no loads)
 #pragma unroll
             for (int k = 0; k < kPre; k++)
-                if (k < static_cast<int>(r0.y)) {
-                    const unsigned m = succ_of(k) & 0x7ffffffu;
-                    pdur[k] = __ldcg(dur + m);  // L2 only: L1 stays with the counters and successor records
-                    // the counter is read when this node finishes, usually several iterations
-                    // on: bring its line into L1 now (values can still change, so no load)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(cnt + m));
-                }
-            have_dur = true;
+                if (k < static_cast<int>(r0.y)) asm volatile("prefetch.global.L1 [%0];" ::"l"(cnt + (succ_of(k) & 0x7ffffffu)));
+            have_pref = true;
         };
         auto start_idle = [&]() {
             const int t = lane < D ? tails[lane] : 0;
             if (lane < D && !running && !ovf && static_cast<int>(head) < t) {
                 ovf = static_cast<unsigned>(t) - head > static_cast<unsigned>(QC);
                 if (ovf) return;  // stop the device: the candidate is re-run exactly
-                const int slot = lane * QC + static_cast<int>(head & QM);
-                const int v = rnode[slot];
-                const double f = __dadd_rn(now, rdur[slot]);
+                const int v = rnode[lane * QC + static_cast<int>(head & QM)];
+                // the duration was loaded when the previous node started, unless this entry
+                // arrived (or was re-sorted to the head) since
+                const double d = v == nx_v ? nx_d : __ldcg(dur + v);
+                const double f = __dadd_rn(now, d);
                 head++;
                 if (out_s) {
                     __stcs(out_s + v, now);
@@ -167,11 +164,19 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                 placed++;
                 r0 = __ldg(a.srec + 2 * static_cast<int64_t>(v));
                 r1 = __ldg(a.srec + 2 * static_cast<int64_t>(v) + 1);
-                have_dur = false;
-                if (static_cast<int>(head) < t) {  // the device's next node: its record into L1 now
-                    const int nv = rnode[lane * QC + static_cast<int>(head & QM)];
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.srec + 2 * static_cast<int64_t>(nv)));
+                have_pref = false;
+                nx_v = -1;
+                if (static_cast<int>(head) < t) {  // the device's next node: its duration and record now
+                    nx_v = rnode[lane * QC + static_cast<int>(head & QM)];
+                    nx_d = __ldcg(dur + nx_v);  // L2 only: L1 stays with the counters and records
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.srec + 2 * static_cast<int64_t>(nx_v)));
                 }
+            } else if (lane < D && running && nx_v < 0 && static_cast<int>(head) < t) {
+                // an entry arrived while this device runs: its place at the head is final
+                // (later arrivals sort behind it), so load its duration now
+                nx_v = rnode[lane * QC + static_cast<int>(head & QM)];
+                nx_d = __ldcg(dur + nx_v);
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.srec + 2 * static_cast<int64_t>(nx_v)));
             }
         };
 
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
             now = warp_min_nonneg(running ? run_f : __longlong_as_double(0x7ff0000000000000LL));
             const bool done = running && run_f == now;
             const int seg_lo = lane < D ? tails[lane] : 0;
-            if (running && !have_dur) load_durs();
+            if (running && !have_pref) prefetch_counters();
             const unsigned dm = __ballot_sync(DFSIM_FULL_MASK, done);
             if (done) running = false;
             if ((dm & (dm - 1)) == 0) {
@@ -206,22 +211,18 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                                 const int p = tails[dv];
                                 tails[dv] = p + 1;
                                 rnode[dv * QC + (p & QM)] = m;
-                                rdur[dv * QC + (p & QM)] = pdur[k];
                             }
                         }
                     }
                     for (int k = kPre; k < deg; k++) {
                         const int m = __ldg(a.succ_idx + static_cast<int>(r0.x) + k);
-                        const unsigned e = static_cast<unsigned>(m) | (static_cast<unsigned>(__ldg(a.device + m)) << 27);
-                        const double dd = __ldg(dur + m);
-                        const int dv = static_cast<int>(e >> 27);
+                        const int dv = __ldg(a.device + m);
                         const int c = static_cast<int>(cnt[m]);
                         cnt[m] = static_cast<CT>(c - 1);
                         if (c == 1) {
                             const int p = tails[dv];
                             tails[dv] = p + 1;
                             rnode[dv * QC + (p & QM)] = m;
-                            rdur[dv * QC + (p & QM)] = dd;
                         }
                     }
                 }
@@ -235,14 +236,11 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                     const unsigned am = __ballot_sync(DFSIM_FULL_MASK, act);
                     if (act) {
                         unsigned e;
-                        double dd;
                         if (r < kPre) {
                             e = succ_of(r);
-                            dd = r == 0 ? pdur[0] : (r == 1 ? pdur[1] : (r == 2 ? pdur[2] : pdur[3]));
                         } else {
                             const int m = __ldg(a.succ_idx + static_cast<int>(r0.x) + r);
                             e = static_cast<unsigned>(m) | (static_cast<unsigned>(__ldg(a.device + m)) << 27);
-                            dd = __ldg(dur + m);
                         }
                         const int m = static_cast<int>(e & 0x7ffffffu), dv = static_cast<int>(e >> 27);
                         const unsigned grp = __match_any_sync(am, m);
@@ -253,7 +251,6 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                             if (c == k) {
                                 const int p = atomicAdd(tails + dv, 1);
                                 rnode[dv * QC + (p & QM)] = m;
-                                rdur[dv * QC + (p & QM)] = dd;
                             }
                         }
                     }
@@ -266,15 +263,12 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                 for (int i = seg_lo + 1; i < seg_hi; i++) {
                     const int xs = lane * QC + (i & QM);
                     const int x = rnode[xs];
-                    const double xd = rdur[xs];
                     int j = i - 1;
                     while (j >= seg_lo && rnode[lane * QC + (j & QM)] > x) {
                         rnode[lane * QC + ((j + 1) & QM)] = rnode[lane * QC + (j & QM)];
-                        rdur[lane * QC + ((j + 1) & QM)] = rdur[lane * QC + (j & QM)];
                         j--;
                     }
                     rnode[lane * QC + ((j + 1) & QM)] = x;
-                    rdur[lane * QC + ((j + 1) & QM)] = xd;
                 }
             }
             __syncwarp();
@@ -312,8 +306,8 @@ int dfsim_simulate_large(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, c
         return v >= 16 && (v & (v - 1)) == 0 ? v : 512;
     }();
     int qcap = kQcapMax;
-    while (qcap > 16 && 128 + static_cast<int64_t>(std::max(D, 1)) * qcap * 12 > budget) qcap >>= 1;
-    const int warp_smem = (128 + std::max(D, 1) * qcap * 12 + 15) / 16 * 16;
+    while (qcap > 16 && 128 + static_cast<int64_t>(std::max(D, 1)) * qcap * 4 > budget) qcap >>= 1;
+    const int warp_smem = (128 + std::max(D, 1) * qcap * 4 + 15) / 16 * 16;
     const int64_t want = (n_sims + wpb - 1) / wpb;
     const int grid = static_cast<int>(std::min<int64_t>(want, ctx->num_sms));
     const int64_t cnt_bytes = (static_cast<int64_t>(N) * cbytes + 127) / 128 * 128;
