@@ -12,9 +12,9 @@
 //     device only gains entries until its next pop); an overflowed candidate is re-run
 //     by the exact engine.
 //   * A start loads the node's 32-byte successor record (range + the first kPre
-//     successors with their devices, built once per launch); the next iteration
-//     prefetches those successors' counter lines.  At finish the relax step loads the
-//     carried successors' counters together (longer lists fall back to direct loads).
+//     successors with their devices, built once per launch).  At finish the relax step
+//     loads the carried successors' counters together (longer lists fall back to direct
+//     loads) and prefetches each newly ready node's duration into L2 for its pop.
 //   * One finishing device per iteration (the common case) relaxes alone with plain
 //     counter and ring-tail updates; ties between devices take the combining path.
 //   * Dependency counters are plain byte/short loads and stores in a global row per
@@ -127,21 +127,13 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
         bool ovf = lane < D && tails[lane] > QC;
 
         unsigned head = 0;
-        bool running = false, have_pref = false;
+        bool running = false;
         uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);  // successor record of the running node
         int nx_v = -1;      // the device's next ring entry, whose duration is already in flight
         double nx_d = 0.0;
         double run_f = 0.0, busy_sum = 0.0, span = 0.0, now = 0.0;
         int placed = 0;
         auto succ_of = [&](int k) -> unsigned { return k == 0 ? r0.z : (k == 1 ? r0.w : (k == 2 ? r1.x : r1.y)); };
-        auto prefetch_counters = [&]() {  // second stage, one iteration after the start
-            // the counters are read when this node finishes, usually several iterations on:
-            // bring their lines into L1 now (values can still change, so no loads)
-#pragma unroll
-            for (int k = 0; k < kPre; k++)
-                if (k < static_cast<int>(r0.y)) asm volatile("prefetch.global.L1 [%0];" ::"l"(cnt + (succ_of(k) & 0x7ffffffu)));
-            have_pref = true;
-        };
         auto start_idle = [&]() {
             const int t = lane < D ? tails[lane] : 0;
             if (lane < D && !running && !ovf && static_cast<int>(head) < t) {
@@ -164,7 +156,6 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                 placed++;
                 r0 = __ldg(a.srec + 2 * static_cast<int64_t>(v));
                 r1 = __ldg(a.srec + 2 * static_cast<int64_t>(v) + 1);
-                have_pref = false;
                 nx_v = -1;
                 if (static_cast<int>(head) < t) {  // the device's next node: its duration and record now
                     nx_v = rnode[lane * QC + static_cast<int>(head & QM)];
@@ -185,7 +176,6 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
             now = warp_min_nonneg(running ? run_f : __longlong_as_double(0x7ff0000000000000LL));
             const bool done = running && run_f == now;
             const int seg_lo = lane < D ? tails[lane] : 0;
-            if (running && !have_pref) prefetch_counters();
             const unsigned dm = __ballot_sync(DFSIM_FULL_MASK, done);
             if (done) running = false;
             if ((dm & (dm - 1)) == 0) {
@@ -211,6 +201,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                                 const int p = tails[dv];
                                 tails[dv] = p + 1;
                                 rnode[dv * QC + (p & QM)] = m;
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(dur + m));  // read at its pop
                             }
                         }
                     }
@@ -223,6 +214,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                             const int p = tails[dv];
                             tails[dv] = p + 1;
                             rnode[dv * QC + (p & QM)] = m;
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(dur + m));  // read at its pop
                         }
                     }
                 }
@@ -251,6 +243,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                             if (c == k) {
                                 const int p = atomicAdd(tails + dv, 1);
                                 rnode[dv * QC + (p & QM)] = m;
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(dur + m));  // read at its pop
                             }
                         }
                     }
