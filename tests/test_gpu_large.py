@@ -141,3 +141,27 @@ def test_large_engine_duplicate_edges_and_wide_fanout():
     g = make_graph(nodes, [DeviceSpec(f"gpu{k}", "Compute") for k in range(D)])
     rows = [rng.uniform(0.5, 30, n), np.round(rng.uniform(0, 4, n)) / 2]
     _check_engine(g, rows)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_large_engine_random_local_dags(seed):
+    """Random DAGs beyond the shared-memory engines (producers within a sliding window,
+    random devices incl. skewed loads, 1-20 devices): tie-heavy integer durations, zeros,
+    and continuous ones, against the C oracle."""
+    from paper_2002_06790_b200.model import DeviceSpec, OpNode, make_graph
+
+    rng = np.random.default_rng(100 + seed)
+    n, D = 80_000 + 20_000 * seed, int(rng.integers(1, 21))
+    win = int(rng.integers(20, 3000))
+    devs = rng.integers(0, D, n)
+    if seed == 1:
+        devs = np.where(rng.random(n) < 0.6, 0, devs)  # one device takes most of the work
+    nodes = []
+    for i in range(n):
+        k = int(rng.integers(0, 4)) if i else 0
+        ins = sorted({int(p) for p in rng.integers(max(0, i - win), i, k)}) if i else []
+        nodes.append(OpNode(f"x{i:06d}", "Op", f"gpu{devs[i]}", inputs=tuple((f"x{p:06d}", 0) for p in ins)))
+    g = make_graph(nodes, [DeviceSpec(f"gpu{d}", "Compute") for d in range(D)])
+    rows = [rng.integers(0, 4, n).astype(np.float64), rng.uniform(0.1, 9, n),
+            np.where(rng.random(n) < 0.5, 0.0, rng.integers(1, 3, n)).astype(np.float64)]
+    _check_engine(g, rows)
