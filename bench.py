@@ -96,10 +96,13 @@ def build_workload(rank: int, sims: int, workload: str = WORKLOAD):
         # layer parameter (the wgrad_* nodes) so communication overlaps the rest of the backward pass
         grid = [(R, sync, path) for R in (2, 4, 8) for sync in ("allreduce", "parameter_server")
                 for path in VGG_PATHS]
+        only = tuple(os.environ["DFSIM_C4_ONLY"].split(",")) if os.environ.get("DFSIM_C4_ONLY") else None
         for i in range(sims):
             gi = rank * sims + i
             R, sync, path = grid[gi % len(grid)]
             k = gi // len(grid)
+            if only and (str(R), sync) != only:  # measurement knob: one (workers, sync) group only
+                continue
             configs.append(StrategyConfig(replicas=R, device_map=tuple(f"gpu{j}" for j in range(R)),
                                           collective=CollectiveConfig("RingAnalytic", path),
                                           gradient_markers=("wgrad_*",), hardware=HW_TAGS[k % N_HW],

@@ -14,6 +14,7 @@ per rank over NCCL.
 
 from __future__ import annotations
 
+import os
 import warnings
 from dataclasses import dataclass, field
 
@@ -125,6 +126,8 @@ class TopologyClass:
         # launcher sizes CTAs to the largest chunk)
         sms = torch.cuda.get_device_properties(self.ctx.device).multi_processor_count
         cap = int(self.ctx.lib.dfsim_fused_chunk(native.ctypes.byref(self.tables.sim_struct), lp.n_sims, sms))
+        if os.environ.get("DFSIM_FUSED_CHUNK"):  # measurement knob: fixed chunk (clamped to the capacity)
+            cap = max(1, min(self.chunk_capacity, int(os.environ["DFSIM_FUSED_CHUNK"])))
         order = np.argsort(var_of, kind="stable")
         firsts, counts, variants = [], [], []
         sorted_var = var_of[order]
