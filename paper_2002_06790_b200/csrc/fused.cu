@@ -71,7 +71,10 @@ constexpr int kWide = 4;  // out-degree above which a finished node's successors
 // Successor entry formats: kPacked: consumer (13 bits) | device << 13 (4) | single << 17 | wide << 18 |
 // shift << 19 | word << 24; otherwise consumer (16) | device << 16 | single << 21 with the counter
 // code (word << 7 | shift << 2 | log2(width) - 1) in cidx[] in smem.
-template <int kGS, bool kPacked>
+// kBaseG: the variant's duration row is read from global memory (L1/L2: all candidates of a
+// chunk share it) instead of being staged in smem -- for classes whose smem tables would
+// otherwise leave room for only a few candidates per CTA.
+template <int kGS, bool kPacked, bool kBaseG>
 __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kPerWarp = 32 / kGS;
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     }
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.g.succ + i);
     int staged = -1;
+    const double *g_row = a.st.base;
 
     for (;;) {
         if (threadIdx.x == 0) s_chunk = atomicAdd(a.chunk_counter, 1);
@@ -119,9 +123,12 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
         const int var = __ldg(a.st.chunk_variant + c);
         if (var != staged) {
             const double *row = a.st.base + static_cast<int64_t>(var) * N;
-            for (int i = threadIdx.x; i < N; i += blockDim.x) s_base[i] = __ldg(row + s_rank[i]);
+            g_row = row;
+            if (!kBaseG) {
+                for (int i = threadIdx.x; i < N; i += blockDim.x) s_base[i] = __ldg(row + s_rank[i]);
+                __syncthreads();
+            }
             staged = var;
-            __syncthreads();
         }
         const bool active = in_group && gid < __ldg(a.st.chunk_count + c);
         if (__any_sync(DFSIM_FULL_MASK, active)) {
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     if (ovf) return;
                     const int v = q[ll * QSTRIDE + (head & QMASK)];
                     head++;
-                    const double b = lds_f64(a_base + 8u * v);
+                    const double b = kBaseG ? __ldg(g_row + lds_u16(a_rank + 2u * v)) : lds_f64(a_base + 8u * v);
                     double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
                     if (ovs >= 0) {  // override tables are by rank
                         const int vr = static_cast<int>(lds_u16(a_rank + 2u * v));
@@ -426,13 +433,17 @@ namespace {
 struct FusedShape {
     size_t graph_bytes, warp_bytes, smem;
     int gs, per_warp, wpb;
-    bool fits;
+    bool fits, base_global;
 };
 
-FusedShape fused_shape(const dfsim_sim_tables *g) {
+// Duration rows stay in smem unless that leaves fewer than this many candidates per CTA
+constexpr int kBaseGlobalBelow = 32;
+
+FusedShape fused_shape_with(const dfsim_sim_tables *g, bool base_global) {
     FusedShape f;
     const size_t N = (size_t)g->n_nodes;
-    f.graph_bytes = (N * (g->succ_packed ? 6 : 8) + (size_t)g->n_edges * 4 + 15) / 16 * 16 + N * 8;
+    f.base_global = base_global;
+    f.graph_bytes = (N * (g->succ_packed ? 6 : 8) + (size_t)g->n_edges * 4 + 15) / 16 * 16 + (base_global ? 0 : N * 8);
     const size_t tail_bytes = g->n_devices <= 16 ? 64 : 128;  // 4-byte tail per device, padded
     f.warp_bytes = (tail_bytes + (size_t)g->n_counter_words * 4 + (size_t)g->n_devices * (g->qcap + 2) * 2 + 15) / 16 * 16;
     f.gs = g->n_devices <= 10 ? 10 : (g->n_devices <= 16 ? 16 : 32);
@@ -447,6 +458,13 @@ FusedShape fused_shape(const dfsim_sim_tables *g) {
     f.smem = f.graph_bytes + (size_t)f.wpb * f.per_warp * f.warp_bytes;
     f.fits = f.smem <= budget;
     return f;
+}
+
+FusedShape fused_shape(const dfsim_sim_tables *g) {
+    const FusedShape f = fused_shape_with(g, false);
+    if (f.fits && f.wpb * f.per_warp >= kBaseGlobalBelow) return f;
+    const FusedShape h = fused_shape_with(g, true);
+    return h.fits && (!f.fits || h.wpb * h.per_warp > f.wpb * f.per_warp) ? h : f;
 }
 }  // namespace
 
@@ -506,16 +524,20 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(a.chunk_counter, 0, sizeof(int32_t), ctx->stream));
     const size_t smem = graph_bytes + (size_t)wpb * f.per_warp * warp_bytes;
     const int threads = wpb * 32;
-#define DFSIM_LAUNCH_FUSED_P(GS, PK)                                                                           \
+#define DFSIM_LAUNCH_FUSED_B(GS, PK, BG)                                                                       \
     do {                                                                                                       \
-        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<GS, PK>,                                     \
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<GS, PK, BG>,                                 \
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
         int occ = 1;                                                                                           \
-        DFSIM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_fused<GS, PK>,      \
+        DFSIM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_fused<GS, PK, BG>,  \
                                                                           threads, smem));                    \
         const int64_t slots = (int64_t)ctx->num_sms * (occ > 0 ? occ : 1);                                    \
         const int grid = (int)(slots < st->n_chunks ? slots : st->n_chunks);                                   \
-        k_simulate_fused<GS, PK><<<grid, threads, smem, ctx->stream>>>(a);                                    \
+        k_simulate_fused<GS, PK, BG><<<grid, threads, smem, ctx->stream>>>(a);                                \
+    } while (0)
+#define DFSIM_LAUNCH_FUSED_P(GS, PK)                                                                           \
+    do {                                                                                                       \
+        if (f.base_global) DFSIM_LAUNCH_FUSED_B(GS, PK, true); else DFSIM_LAUNCH_FUSED_B(GS, PK, false);       \
     } while (0)
 #define DFSIM_LAUNCH_FUSED(GS)                                                                                 \
     do {                                                                                                       \
@@ -524,6 +546,7 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     if (gs == 10) DFSIM_LAUNCH_FUSED(10); else if (gs == 16) DFSIM_LAUNCH_FUSED(16); else DFSIM_LAUNCH_FUSED(32);
 #undef DFSIM_LAUNCH_FUSED
 #undef DFSIM_LAUNCH_FUSED_P
+#undef DFSIM_LAUNCH_FUSED_B
     return dfsim_after_launch(ctx, "k_simulate_fused");
 }
 

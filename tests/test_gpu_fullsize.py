@@ -114,3 +114,37 @@ def test_multiclass_workloads_full_size(workload):
     for i in np.linspace(0, len(configs) - 1, n_check).astype(int).tolist():
         want = bench._run_candidate_ps_aware(graphs[graph_of[i]], db, configs[i])
         assert res.makespan[i] == want, (workload, i)
+
+
+def test_global_duration_row_class_matches_exact_engine():
+    """C4's R=8 parameter-server classes (N = 9,474, 25 devices) leave room for only 13
+    candidates per CTA with the duration row in smem, so the fused engine reads that row from
+    global memory instead (fused.cu kBaseG). Every schedule must equal the exact engine's and a
+    sample the oracle's."""
+    import torch
+
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2002_06790_b200.batch import TopologyClass
+
+    graphs, db, configs, _ = bench.build_workload(0, 2048, "bert-large-ps-ar")
+    configs = [c for c in configs if c.replicas == 8 and c.sync == "parameter_server"
+               and c.collective.path == "NVLink"]
+    assert len(configs) > 100
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        tc = TopologyClass(graphs[0], db, configs, 0)
+        ref = TopologyClass(graphs[0], db, configs, 0, fused=False)
+    assert tc.fused and tc.lg.n > 8192 and tc.lg.n_devices > 16
+    assert tc.chunk_capacity > 13  # the smem-row layout's capacity for this class
+    for c in (tc, ref):
+        c.expand()
+    o, r = tc.run(schedules=True), ref.run(schedules=True)
+    N = tc.lg.n
+    pos = torch.as_tensor(tc.tables.pos, device="cuda:0")
+    assert torch.equal(o["start"][:, :N].index_select(1, pos), r["start"][:, :N])
+    assert torch.equal(o["finish"][:, :N].index_select(1, pos), r["finish"][:, :N])
+    assert torch.equal(o["makespan"], r["makespan"])
+    assert torch.equal(o["cp_len"], r["cp_len"])
+    for i in (0, len(configs) // 2, len(configs) - 1):
+        assert float(o["makespan"][i]) == bench._run_candidate_ps_aware(graphs[0], db, configs[i])
