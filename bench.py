@@ -314,6 +314,8 @@ def run_ours(args):
         tc = TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], local, graphs=graphs,
                            graph_of=[graph_of[i] for i in idx])
         classes.append((tc, idx, {}))
+    if os.environ.get("DFSIM_LPT", "1") == "1":  # most work first (as sweep_variants): no long-CTA tail
+        classes.sort(key=lambda c: -c[0].lg.n * len(c[1]))
     setup_s = time.perf_counter() - t_setup
     ctx = native.Context.get(local)
     dev = f"cuda:{local}"

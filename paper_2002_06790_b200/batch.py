@@ -475,6 +475,7 @@ def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, kee
     failures = []
     built = [(idx, TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device, fused=fused,
                                  graphs=graphs, graph_of=[graph_of[i] for i in idx])) for idx in groups.values()]
+    built.sort(key=lambda b: -b[1].lg.n * len(b[0]))  # most work first: the longest CTAs must not form the tail
     outs = [{} for _ in built]
     side = [torch.cuda.Stream(ctx.device) for _ in range(min(max(streams, 1), len(built)))] if len(built) > 1 else []
     cur = torch.cuda.current_stream(ctx.device)
