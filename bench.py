@@ -664,7 +664,7 @@ def main():
     ap.add_argument("--no-reports", action="store_true", help="skip the summary/trace measurement")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--report-rows", type=int, default=1024, help="schedules summarised in the reports line")
-    ap.add_argument("--streams", type=int, default=48, help="multi-class workloads: concurrent class streams")
+    ap.add_argument("--streams", type=int, default=32, help="multi-class workloads: concurrent class streams (= CUDA_DEVICE_MAX_CONNECTIONS)")
     args = ap.parse_args()
     # concurrent topology classes need more hardware work queues than the default 8
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")

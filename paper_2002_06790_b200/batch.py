@@ -449,7 +449,7 @@ def sweep(g, db, configs, device: int | None = None, keep_schedules: bool = Fals
 
 
 def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,
-                   fused: bool = True, streams: int = 48) -> SweepResult:
+                   fused: bool = True, streams: int = 32) -> SweepResult:
     """``sweep`` where candidate i runs ``configs[i]`` on ``graphs[graph_of[i]]`` (e.g. one graph per
     batch size).  Graphs of identical structure share a topology class (variants.py).
 
