@@ -25,6 +25,11 @@
  *  - Calls are asynchronous on the context's stream unless documented otherwise.
  *    Per-simulation outcomes (cycle, unknown op) are written to caller arrays;
  *    the return value reports argument/launch problems.
+ *  - Threads: a context is not re-entrant.  Calls on one context must be
+ *    serialised by the caller (the Python binding holds a per-context lock
+ *    across dfsim_ctx_set_stream + the call); distinct contexts are independent.
+ *    Device scratch inside a context is kept per stream (internally locked), so
+ *    serialised callers on different streams never share a scratch buffer.
  *  - Status codes map 1:1 onto the reference exceptions (errors.py:6-92):
  */
 #ifndef DFSIM_B200_H
@@ -289,6 +294,49 @@ int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t
 /* Candidates one CTA of dfsim_critical_path_levels holds (0: the class tables do not fit
  * in shared memory; such a class uses the rank-layout kernels instead). */
 int32_t dfsim_critical_path_levels_capacity(const dfsim_cp_tables *t);
+
+/* K4 v3 (lane per candidate): graph.py:446-474 on finish - start over the fused engine's
+ * sched[S][N][2] pairs by level position.  Every lane of a warp is one candidate and the warp
+ * walks the class's positions in reverse (one node at a time, all lanes in step), so the
+ * class tables are read once per 32 candidates.  A node's suffix value lives in a shared-
+ * memory slot while it is read within its own or the next prefetch chunk, otherwise in a
+ * per-warp spill row [n_long][32] in global memory, prefetched with the reading chunk.
+ * Tables come from dfsim_cp_lanes_plan (host). */
+typedef struct {
+    int32_t n_nodes;
+    int32_t n_edges;
+    int32_t n_chunks;          /* prefetch chunks, in processing order (highest positions first) */
+    int32_t chunk_positions;   /* K: a chunk covers at most K positions (K <= 16) */
+    int32_t n_slots;           /* shared-memory suffix slots per candidate */
+    int32_t rmax;              /* spill values prefetched per chunk, at most */
+    int32_t n_long;            /* values kept in spill rows */
+    int32_t n_spill_list;      /* length of spill_list (= spill_off[n_chunks]) */
+    const uint32_t *rec;       /* [N][2] per position: x = successor begin | count << 24;
+                                  y = slot | has_slot << 12 | source << 13 | has_spill << 14 | spill << 15 */
+    const uint16_t *succ;      /* [E] per reading position (CSR by rec.x): row of the successor's value in
+                                  the candidate's region [slots | spill stage 0 | spill stage 1] */
+    const int32_t *bounds;     /* [n_chunks + 1]: chunk q covers positions [bounds[q+1], bounds[q]) */
+    const int32_t *spill_off;  /* [n_chunks + 1] */
+    const uint16_t *spill_list; /* spill indices prefetched with each chunk, in stage-row order */
+    const int32_t *rank_of_pos; /* [N] node rank of each position (source tie-break) */
+} dfsim_cp_lane_tables;
+
+/* Host planner of dfsim_cp_lane_tables (C++, no device work): positions 0..N-1 in a level
+ * order (every edge from a lower to a higher position), succ_off[N+1] / succ_pos[E] the
+ * successors of each position, is_source[N].  Chunks of <= K positions are cut in reverse
+ * order so that no chunk prefetches more than max(rmax_min, widest node) spill values.
+ * Output arrays are caller-allocated at their bounds: rec[2N], succ_loc[E], bounds[N+1],
+ * spill_off[N+1], spill_list[E]; info[5] = {n_chunks, n_slots, rmax, n_long, spill_list length}.
+ * Returns DFSIM_BAD_ARGUMENT when a field overflows its width (the class then keeps K4 v2). */
+int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int32_t *succ_pos, const uint8_t *is_source,
+                        int32_t K, int32_t rmax_min, uint32_t *rec, uint16_t *succ_loc, int32_t *bounds,
+                        int32_t *spill_off, uint16_t *spill_list, int32_t *info);
+
+int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int64_t n_sims, const double *sched,
+                              double *cp_len, int32_t *cp_src);
+
+/* Warps (32 candidates each) one CTA of dfsim_critical_path_lanes holds (0: does not fit). */
+int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t);
 
 /* ---------------------------------------------------------------- critical path (K4) */
 /* Over d = finish - start (reporting.py:128), or over d = finish when start is NULL

@@ -224,11 +224,14 @@ done:
     return status;
 }
 
-/* Batch driver for the CPU baseline: S independent simulations + CP lengths,
- * spread over n_threads pthreads (each owns a contiguous slice of sims). */
+/* Batch driver for the CPU baseline and the full-grid parity tests: S independent
+ * simulations + CP lengths, spread over n_threads pthreads (each owns a contiguous slice of
+ * sims).  Optional outputs (NULL: not written): start/finish [S][n], busy [S][n_dev],
+ * cp_src [S] (rank of the critical path's first node). */
 typedef struct {
     int32_t n, n_dev; const int32_t *succ_off, *succ_idx, *indeg, *dev;
-    int64_t s0, s1; const double *dur; double *makespan, *cp_len; int status;
+    int64_t s0, s1; const double *dur; double *makespan, *cp_len;
+    double *start_out, *finish_out, *busy_out; int32_t *cp_src; int status;
 } batch_arg_t;
 
 static void *batch_worker(void *p) {
@@ -242,9 +245,15 @@ static void *batch_worker(void *p) {
         int32_t np = 0, pl = 0;
         int rc = oracle_simulate(n, a->n_dev, a->succ_off, a->succ_idx, a->indeg, a->dev,
                                  a->dur + (size_t)s * (size_t)n, st, fi, busy, &a->makespan[s], NULL, &np);
+        if (a->start_out) memcpy(a->start_out + (size_t)s * (size_t)n, st, sizeof(double) * (size_t)n);
+        if (a->finish_out) memcpy(a->finish_out + (size_t)s * (size_t)n, fi, sizeof(double) * (size_t)n);
+        if (a->busy_out) memcpy(a->busy_out + (size_t)s * (size_t)a->n_dev, busy, sizeof(double) * (size_t)a->n_dev);
+        a->cp_len[s] = 0.0;
+        if (a->cp_src) a->cp_src[s] = -1;
         if (rc == 0) {
             for (int32_t v = 0; v < n; v++) fi[v] = fi[v] - st[v];
             rc = oracle_critical_path(n, a->succ_off, a->succ_idx, a->indeg, fi, &a->cp_len[s], path, &pl);
+            if (a->cp_src && pl > 0) a->cp_src[s] = path[0];
         }
         a->status |= rc;
     }
@@ -252,9 +261,10 @@ static void *batch_worker(void *p) {
     return NULL;
 }
 
-int oracle_simulate_batch(int32_t n, int32_t n_dev, const int32_t *succ_off, const int32_t *succ_idx,
-                          const int32_t *indeg, const int32_t *dev, int64_t n_sims, const double *dur,
-                          double *makespan, double *cp_len, int32_t n_threads) {
+int oracle_simulate_batch_full(int32_t n, int32_t n_dev, const int32_t *succ_off, const int32_t *succ_idx,
+                               const int32_t *indeg, const int32_t *dev, int64_t n_sims, const double *dur,
+                               double *makespan, double *cp_len, double *start_out, double *finish_out,
+                               double *busy_out, int32_t *cp_src, int32_t n_threads) {
     if (n_threads < 1) n_threads = 1;
     pthread_t tid[256];
     batch_arg_t arg[256];
@@ -262,9 +272,17 @@ int oracle_simulate_batch(int32_t n, int32_t n_dev, const int32_t *succ_off, con
     int status = 0;
     for (int t = 0; t < n_threads; t++) {
         arg[t] = (batch_arg_t){n, n_dev, succ_off, succ_idx, indeg, dev,
-                               n_sims * t / n_threads, n_sims * (t + 1) / n_threads, dur, makespan, cp_len, 0};
+                               n_sims * t / n_threads, n_sims * (t + 1) / n_threads, dur, makespan, cp_len,
+                               start_out, finish_out, busy_out, cp_src, 0};
         pthread_create(&tid[t], NULL, batch_worker, &arg[t]);
     }
     for (int t = 0; t < n_threads; t++) { pthread_join(tid[t], NULL); status |= arg[t].status; }
     return status;
+}
+
+int oracle_simulate_batch(int32_t n, int32_t n_dev, const int32_t *succ_off, const int32_t *succ_idx,
+                          const int32_t *indeg, const int32_t *dev, int64_t n_sims, const double *dur,
+                          double *makespan, double *cp_len, int32_t n_threads) {
+    return oracle_simulate_batch_full(n, n_dev, succ_off, succ_idx, indeg, dev, n_sims, dur, makespan, cp_len,
+                                      NULL, NULL, NULL, NULL, n_threads);
 }

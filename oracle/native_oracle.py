@@ -36,6 +36,8 @@ def lib():
         L.oracle_critical_path.argtypes = [ctypes.c_int32, P, P, P, P, P, P, P]
         L.oracle_simulate_batch.argtypes = [ctypes.c_int32, ctypes.c_int32, P, P, P, P, ctypes.c_int64, P, P, P,
                                             ctypes.c_int32]
+        L.oracle_simulate_batch_full.argtypes = [ctypes.c_int32, ctypes.c_int32, P, P, P, P, ctypes.c_int64, P, P,
+                                                 P, P, P, P, P, ctypes.c_int32]
         _lib = L
     return _lib
 
@@ -94,3 +96,18 @@ def simulate_batch(csr: Csr, dur: np.ndarray, threads: int | None = None):
     rc = lib().oracle_simulate_batch(csr.n, csr.n_dev, _p(csr.off), _p(csr.idx), _p(csr.indeg), _p(csr.dev), S,
                                      _p(dur), _p(ms), _p(cp), threads)
     return rc, ms, cp
+
+
+def simulate_batch_full(csr: Csr, dur: np.ndarray, threads: int | None = None):
+    """Like simulate_batch, plus every schedule: returns (status, makespan, cp_len, start, finish,
+    busy, cp_src) with start/finish [S, N] by rank, busy [S, n_dev] and cp_src [S] (path head rank)."""
+    dur = np.ascontiguousarray(dur, dtype=np.float64)
+    S, n = dur.shape[0], csr.n
+    ms, cp = np.zeros(S), np.zeros(S)
+    st, fi = np.empty((S, max(n, 1))), np.empty((S, max(n, 1)))
+    busy = np.zeros((S, max(csr.n_dev, 1)))
+    src = np.full(S, -1, np.int32)
+    threads = threads or len(os.sched_getaffinity(0))
+    rc = lib().oracle_simulate_batch_full(n, csr.n_dev, _p(csr.off), _p(csr.idx), _p(csr.indeg), _p(csr.dev), S,
+                                          _p(dur), _p(ms), _p(cp), _p(st), _p(fi), _p(busy), _p(src), threads)
+    return rc, ms, cp, st[:, :n], fi[:, :n], busy[:, : csr.n_dev], src

@@ -3,7 +3,7 @@
 Drop-in surface (same names and signatures as the reference's pkg/src/dfsim/__init__.py:6-43
 for the hot path): ``simulate``, ``critical_path``, ``estimate_all``,
 ``expand_data_parallel``, and the schedule consumers ``summarize`` / ``to_trace``;
-batched entry point: ``sweep`` (``SweepResult.summaries`` / ``.trace`` report on the
+batched entry points: ``sweep`` / ``sweep_variants`` / ``sweep_sharded`` (multi-GPU) (``SweepResult.summaries`` / ``.trace`` report on the
 schedules left in HBM).  Every compute call runs
 hand-written sm_100a kernels from ``libdfsim_b200.so`` through the C-ABI in
 ``include/dfsim_b200.h``; there is no CPU fallback.
@@ -46,6 +46,7 @@ from .model import (  # noqa: F401
     utilization,
 )
 from .batch import SweepResult, TopologyClass, gather_best, sweep, sweep_variants  # noqa: F401
+from .sharded import sweep_sharded  # noqa: F401
 from .estimate import estimate_all, estimate_batch  # noqa: F401
 from .expansion import expand_class, expand_data_parallel  # noqa: F401
 from .lowering import fit_for_grid, fit_linear, node_features  # noqa: F401

@@ -7,9 +7,9 @@ grouped into topology classes (same expanded graph: replicas, device_map,
 gradient markers, collective path -- strategy.py:202-252); each class is
 expanded once on the GPU (K1), then all of its candidates go through
 K2 estimate -> K3 simulate -> K4 critical path in single launches, and the best
-candidate is the first minimum makespan (K5).  Multi-GPU: ``sweep_sharded``
-splits the candidate list over ranks and all-gathers one 16-byte winner record
-per rank over NCCL.
+candidate is the first minimum makespan (K5).  Multi-GPU: ``sharded.sweep_sharded``
+splits the candidate list over GPUs (ranks of a process group, or devices of one
+process) and reduces one 16-byte winner record per GPU (NCCL all-gather / P2P).
 """
 
 from __future__ import annotations
@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import native
-from .errors import CycleError
+from .errors import CycleError, NativeError
 from .estimate import estimate_batch, raise_for_row
 from .expansion import ExpansionPlan
 from .lowering import LoweredGraph, LoweredProfiles, lowered, resolve_overrides
@@ -90,7 +90,7 @@ class TopologyClass:
         self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device, variant_rows, strat_gv)
         self.tables = None
         self.fused = False
-        if fused and self.lg.acyclic and 0 < self.lg.n <= 65535:
+        if fused and self.lg.acyclic and 0 < self.lg.n <= 65535 and self.lp.fused_values_ok:
             self.tables = ClassTables(self.lg)
             if self.tables.fused_ok:
                 self._prepare_variants()
@@ -119,7 +119,9 @@ class TopologyClass:
         if (st >= 253).any():
             return  # some candidate fails estimation: keep the unfused path (exact error semantics)
         cap = int(self.ctx.lib.dfsim_fused_capacity(native.ctypes.byref(self.tables.sim_struct)))
-        if cap <= 0 or self.ctx.lib.dfsim_critical_path_levels_capacity(native.ctypes.byref(self.tables.cp_struct)) <= 0:
+        cp_ok = (self.tables.lane is not None
+                 or self.ctx.lib.dfsim_critical_path_levels_capacity(native.ctypes.byref(self.tables.cp_struct)) > 0)
+        if cap <= 0 or not cp_ok:
             return  # engine or critical-path tables exceed shared memory: rank-layout kernels
         self.chunk_capacity = cap
         # a small class is cut into smaller chunks so that its CTAs cover the SMs (the
@@ -218,8 +220,7 @@ class TopologyClass:
         if not defer_fallback:
             self.fallback_if_needed(o)
         rec("critical_path", 0)
-        self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.tables.cp_struct), S,
-                      native.ptr(o["sched"]), native.ptr(o["cp_len"]), native.ptr(o["cp_src"]))
+        self.tables.critical_path(S, o["sched"], o["cp_len"], o["cp_src"])
         rec("critical_path", 1)
         return o
 
@@ -299,8 +300,7 @@ class TopologyClass:
     def critical_path_only(self, o: dict):
         """Re-run K4 on the current schedules (after a deferred fallback)."""
         if self.fused:
-            self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.tables.cp_struct), self.lp.n_sims,
-                          native.ptr(o["sched"]), native.ptr(o["cp_len"]), native.ptr(o["cp_src"]))
+            self.tables.critical_path(self.lp.n_sims, o["sched"], o["cp_len"], o["cp_src"])
         elif self.lg.acyclic and self.lg.n:
             critical_path_arrays(self.lg, o["start"], o["finish"], out=o)
 
@@ -455,6 +455,31 @@ def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, kee
 
     Classes are launched round-robin on up to ``streams`` CUDA streams (each stream has its
     own device scratch in the context), so many small classes share the GPU."""
+    result, _, failure = sweep_local(graphs, db, configs, graph_of, device, keep_schedules, fused, streams)
+    if failure is not None:
+        raise failure[1]
+    return result
+
+
+def _row_error(tc, o, row) -> Exception:
+    """The reference's exception for a failed candidate row (estimation error or cycle)."""
+    n = tc.lg.n
+    if int(o["bad"][row].item()):
+        try:
+            raise_for_row(tc.graph, tc.ids, o["dur"][row, :n].cpu().numpy(), o["src"][row, :n].cpu().numpy())
+        except Exception as e:  # noqa: BLE001 -- returned, raised by the caller
+            return e
+    st = o["start"][row, :n].cpu().numpy() if "start" in o else None
+    return CycleError(sorted(tc.ids[k] for k in np.nonzero(np.isnan(st))[0]) if st is not None else [])
+
+
+def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,
+                fused: bool = True, streams: int = 32, index_base: int = 0):
+    """The per-device body of every sweep: returns ``(result, record, failure)`` without raising.
+
+    ``record`` is K5's 16-byte winner ``(makespan, index_base + first minimum row)`` on the
+    device (for a cross-GPU reduction); ``failure`` is ``(local index, exception)`` of the first
+    failing config in list order (cli.py:132-145) or None.  ``result.best_*`` are this shard's."""
     import torch
 
     from .variants import structure_key
@@ -472,9 +497,16 @@ def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, kee
     makespan = torch.full((max(S, 1),), float("inf"), dtype=torch.float64, device=dev)
     cp_len = torch.zeros(max(S, 1), dtype=torch.float64, device=dev)
     result = SweepResult(np.zeros(0), np.zeros(0), -1, float("nan"))
-    failures = []
-    built = [(idx, TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device, fused=fused,
-                                 graphs=graphs, graph_of=[graph_of[i] for i in idx])) for idx in groups.values()]
+    failures = []  # (config index, exception)
+    built = []
+    for idx in groups.values():
+        try:
+            built.append((idx, TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device,
+                                             fused=fused, graphs=graphs, graph_of=[graph_of[i] for i in idx])))
+        except NativeError:
+            raise
+        except Exception as e:  # noqa: BLE001 -- expansion / lowering error: the class's first config fails
+            failures.append((idx[0], e))
     built.sort(key=lambda b: -b[1].lg.n * len(b[0]))  # most work first: the longest CTAs must not form the tail
     outs = [{} for _ in built]
     side = [torch.cuda.Stream(ctx.device) for _ in range(min(max(streams, 1), len(built)))] if len(built) > 1 else []
@@ -501,29 +533,25 @@ def sweep_variants(graphs, db, configs, graph_of, device: int | None = None, kee
             cp_len.index_copy_(0, t_idx, o["cp_len"])
         bad = o["bad"].cpu().numpy()
         placed = o["n_placed"].cpu().numpy()
-        for row in np.nonzero((bad > 0) | (placed != tc.lg.n))[0].tolist():
-            failures.append((idx[row], tc, o, row))
+        rows = np.nonzero((bad > 0) | (placed != tc.lg.n))[0]
+        if rows.size:  # this class's first failing row, while its schedules are still here
+            row = int(rows[0])
+            failures.append((idx[row], _row_error(tc, o, row)))
         if not keep_schedules:
             for k in ("start", "finish", "sched"):
                 o.pop(k, None)
         result.classes.append((tc, idx, o))
         for row, i in enumerate(idx):
             result._where[i] = (pos, row)
-    if failures:
-        i, tc, o, row = min(failures, key=lambda f: f[0])
-        n = tc.lg.n
-        if int(o["bad"][row].item()):
-            raise_for_row(tc.graph, tc.ids, o["dur"][row, :n].cpu().numpy(), o["src"][row, :n].cpu().numpy())
-        st = o["start"][row, :n].cpu().numpy() if "start" in o else None
-        raise CycleError(sorted(tc.ids[k] for k in np.nonzero(np.isnan(st))[0]) if st is not None else [])
+    failure = min(failures, key=lambda f: f[0]) if failures else None
     rec = torch.empty(2, dtype=torch.float64, device=dev)
-    ctx.call("dfsim_argmin", S, native.ptr(makespan), 0, native.ptr(rec))
-    r = rec.cpu()
+    ctx.call("dfsim_argmin", S, native.ptr(makespan), index_base, native.ptr(rec))
     result.makespan = makespan[:S].cpu().numpy()
     result.cp_len = cp_len[:S].cpu().numpy()
+    r = rec.cpu()
     result.best_makespan = float(r[0].item())
     result.best_index = int(r[1:2].view(torch.int64).item()) if S else -1
-    return result
+    return result, rec, failure
 
 
 def shard(total: int, rank: int, world: int) -> tuple[int, int]:

@@ -76,6 +76,7 @@ static int grow(dfsim_ctx *ctx, void **buf, size_t *have, size_t bytes, void **o
 }
 
 static dfsim_stream_scratch &entry(dfsim_ctx *ctx) {
+    std::lock_guard<std::mutex> guard(ctx->mu);
     for (auto &e : ctx->per_stream)
         if (e.stream == ctx->stream) return e;
     ctx->per_stream.emplace_back();

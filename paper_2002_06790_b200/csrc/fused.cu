@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 // a ring overflow corrupts only this candidate; it keeps running (every
                 // iteration consumes a finish event, so it terminates) and is re-run exactly
                 // enqueue(sorted(newly_ready)): sort each device's new ring segment by rank
-                if (seg_hi - seg_lo > 1) {
+                if (in_group && seg_hi - seg_lo > 1) {  // idle lanes alias group 0: never write
                     uint16_t *qd = q + ll * QSTRIDE;
                     for (int i = seg_lo + 1; i < seg_hi; i++) {
                         const uint16_t x = qd[i & QMASK];

@@ -4,8 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <deque>
+#include <mutex>
 #include <string>
-#include <vector>
 
 #include "dfsim_b200.h"
 
@@ -24,7 +25,10 @@ struct dfsim_ctx {
     cudaStream_t stream = nullptr;
     int32_t num_sms = 148;
     int64_t launches = 0;
-    std::vector<dfsim_stream_scratch> per_stream;
+    // deque: entries keep their address while other streams are added; guarded by mu (a
+    // context may be shared by threads that serialise their calls, see dfsim_b200.h)
+    std::deque<dfsim_stream_scratch> per_stream;
+    std::mutex mu;
     // pinned host staging for small synchronous results
     void *host_small = nullptr;
     std::string last_error;

@@ -163,7 +163,10 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
                 const int d = lane + 32 * k;
                 if (d < D && !running[k] && head[k] < tails[d]) {
                     const int v = q[head[k]++];
-                    const double f = __dadd_rn(now, __ldg(dur + v));
+                    // a failing row (estimate status >= 253: NaN / negative value) still terminates;
+                    // its exception is raised from the estimate status, never from this schedule
+                    const double dv = __ldg(dur + v);
+                    const double f = __dadd_rn(now, dv >= 0.0 ? dv : 0.0);
                     if (out_start) {
                         const int col = (a.pos ? __ldg(a.pos + v) : v) * ostride;
                         out_start[col] = now;

@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                 const int v = rnode[lane * QC + static_cast<int>(head & QM)];
                 // the duration was loaded when the previous node started, unless this entry
                 // arrived (or was re-sorted to the head) since
-                const double d = v == nx_v ? nx_d : __ldcg(dur + v);
+                const double d0 = v == nx_v ? nx_d : __ldcg(dur + v);
+                const double d = d0 >= 0.0 ? d0 : 0.0;  // failing rows (NaN / negative) still terminate
                 const double f = __dadd_rn(now, d);
                 head++;
                 if (out_s) {

@@ -18,6 +18,7 @@ Runs once per graph / topology class; everything per-strategy runs on the GPU.
 
 from __future__ import annotations
 
+import math
 import warnings
 
 import numpy as np
@@ -449,6 +450,11 @@ class LoweredProfiles:
                 sig[gv, i] = sig_ids.setdefault(feats, len(sig_ids))
                 cok[gv, i], cbytes[gv, i], gsize[gv, i], lthr[gv, i], llat[gv, i] = ok, b, gs, thr, lat
         self.op_ids, self.sig_ids = op_ids, sig_ids
+        # the fused engine forms durations on the fly (base + gap | override) and relies on every
+        # one being a finite non-negative double; anything else (NaN included: DurationEntry's
+        # `not x >= 0.0`, costmodel.py:78-80) must take the exact K2 path and its error
+        self.fused_values_ok = (all(math.isfinite(x) and x >= 0.0 for x in self.strat_gap)
+                                and all(math.isfinite(v) and v >= 0.0 for res in ov_sets for v in res.values()))
         # exact records for (hw, op, sig) triples present in the graph
         ekeys, emeans = [], []
         for hw, h in self.hw_ids.items():

@@ -2,9 +2,9 @@
 
 There is no fallback: if the library is missing, cannot be loaded, or no CUDA
 device is present, every entry point raises :class:`NativeError`.  ctypes drops
-the GIL for the duration of each foreign call, so independent Python threads can
-drive independent contexts concurrently (the reference's ``--jobs`` threads,
-cli.py:133-137).
+the GIL for the duration of each foreign call; a per-device :class:`Context` is
+shared by every thread and serialises its calls with a lock (see ``Context``), so
+the reference's ``--jobs`` threads (cli.py:133-137) may call the drop-in concurrently.
 """
 
 from __future__ import annotations
@@ -78,6 +78,12 @@ class CpTables(ctypes.Structure):
                 ("spill_list", P), ("max_spill_reads", I32), ("pinfo", P), ("slot_region", I32), ("stage_doubles", I32)]
 
 
+class CpLaneTables(ctypes.Structure):
+    _fields_ = [("n_nodes", I32), ("n_edges", I32), ("n_chunks", I32), ("chunk_positions", I32), ("n_slots", I32),
+                ("rmax", I32), ("n_long", I32), ("n_spill_list", I32), ("rec", P), ("succ", P), ("bounds", P),
+                ("spill_off", P), ("spill_list", P), ("rank_of_pos", P)]
+
+
 class SummaryTables(ctypes.Structure):
     _fields_ = [("n_nodes", I32), ("n_keys", I32), ("base_order", P), ("key", P), ("comm", P)]
 
@@ -118,6 +124,9 @@ _SIGNATURES = {
                                             P, P]),
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P]),
     "dfsim_critical_path_levels_capacity": (I32, [ctypes.POINTER(CpTables)]),
+    "dfsim_critical_path_lanes": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I64, P, P, P]),
+    "dfsim_critical_path_lanes_capacity": (I32, [ctypes.POINTER(CpLaneTables)]),
+    "dfsim_cp_lanes_plan": (ctypes.c_int, [I32, P, P, P, I32, I32, P, P, P, P, P, P]),
     "dfsim_fused_capacity": (I32, [ctypes.POINTER(SimTables)]),
     "dfsim_fused_chunk": (I32, [ctypes.POINTER(SimTables), I64, I32]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),
@@ -155,9 +164,17 @@ def load_library(path: Path | None = None):
 
 
 class Context:
-    """One dfsim_ctx per CUDA device; calls run on the caller's current torch stream."""
+    """One dfsim_ctx per CUDA device; calls run on the caller's current torch stream.
+
+    Thread safety (the reference allows concurrent simulations, and its CLI
+    sweeps on a thread pool, cli.py:133-137): ctypes releases the GIL during every call, so
+    ``call`` holds this context's lock across binding the caller's stream, the C call and
+    reading its error text.  Launches from several threads are thereby serialised per device
+    (they are asynchronous, so the GPU work itself still overlaps on the callers' streams);
+    device scratch belongs to (context, stream) inside the library."""
 
     _by_device: dict[int, "Context"] = {}
+    _create_lock = threading.Lock()
 
     def __init__(self, device: int):
         import torch
@@ -171,6 +188,7 @@ class Context:
             torch.cuda.init()
             self._check(self.lib.dfsim_ctx_create(device, None, ctypes.byref(handle)), "ctx_create", ctx=False)
         self.handle = handle
+        self.lock = threading.RLock()
 
     @classmethod
     def get(cls, device: int | None = None) -> "Context":
@@ -180,7 +198,10 @@ class Context:
             device = torch.cuda.current_device() if torch.cuda.is_available() else 0
         ctx = cls._by_device.get(device)
         if ctx is None:
-            ctx = cls._by_device[device] = Context(device)
+            with cls._create_lock:
+                ctx = cls._by_device.get(device)
+                if ctx is None:
+                    ctx = cls._by_device[device] = Context(device)
         return ctx
 
     def bind_stream(self):
@@ -203,8 +224,9 @@ class Context:
         raise NativeError(f"{what}: status {rc}: {msg}")
 
     def call(self, name: str, *args):
-        self.bind_stream()
-        self._check(getattr(self.lib, name)(self.handle, *args), name)
+        with self.lock:
+            self.bind_stream()
+            self._check(getattr(self.lib, name)(self.handle, *args), name)
 
 
 def ptr(t) -> P:

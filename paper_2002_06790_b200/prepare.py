@@ -126,6 +126,7 @@ class Tables:
         take = np.arange(int(off_p[-1]), dtype=np.int64) + np.repeat(off[order] - off_p[:-1], outdeg_p)
         cons = idx[take]                                         # consumer ranks
         cpos = pos[cons]
+        self.succ_off_pos, self.succ_pos = off_p, cpos           # successor positions by position
         self.meta = (off_p[:-1] & 0xFFFFFF) | (np.minimum(outdeg_p, 255) << 24)
         # packed entry: consumer position 13 | device 4 | single 1 | wide 1 | shift 5 | word 8
         self.succ_packed = (N <= 8192 and int(dev.max(initial=0)) < 16 and self.counter_bits <= 4
@@ -137,6 +138,7 @@ class Tables:
         else:  # consumer position 16 | device 5 | single 1; the counter code comes from cidx[]
             self.succ = cpos | (dev[cons] << 16) | (single[cons].astype(np.int64) << 21)
         self.cidx, self.cnt_init = code, packed
+        self.indeg_pos = deg_p
         self.eng_sources = pos[np.nonzero(indeg == 0)[0]]        # ascending ranks, as positions
 
     def _critical_path(self, N, idx, indeg, outdeg, order, pos, loff):
@@ -219,6 +221,36 @@ class Tables:
         self.cp_succ_abs = absent[np.argsort(pu, kind="stable")]
 
 
+LANE_K = int(os.environ.get("DFSIM_CP_LANE_K", 16))   # positions per K4 v3 prefetch chunk (8 or 16)
+LANE_RMAX = int(os.environ.get("DFSIM_CP_LANE_RMAX", 16))  # spill values per chunk (planner minimum)
+
+
+def lane_plan(t: Tables, K: int = LANE_K, rmax_min: int = LANE_RMAX):
+    """K4 v3 tables of a class (dfsim_cp_lanes_plan, host C++): dict of numpy arrays + sizes,
+    or None when a field overflows (the class then keeps K4 v2)."""
+    import ctypes
+
+    lib = native.load_library()
+    N, E = t.n, t.n_edges
+    off = np.ascontiguousarray(t.succ_off_pos, np.int32)
+    sp = np.ascontiguousarray(t.succ_pos if E else np.zeros(1), np.int32)
+    src = np.ascontiguousarray(t.indeg_pos == 0, np.uint8)
+    rec = np.zeros(2 * max(N, 1), np.uint32)
+    succ = np.zeros(max(E, 1), np.uint16)
+    bounds = np.zeros(N + 1, np.int32)
+    soff = np.zeros(N + 1, np.int32)
+    slist = np.zeros(max(E, 1), np.uint16)
+    info = np.zeros(5, np.int32)
+    pp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    rc = lib.dfsim_cp_lanes_plan(N, pp(off), pp(sp), pp(src), K, rmax_min, pp(rec), pp(succ), pp(bounds), pp(soff),
+                                 pp(slist), pp(info))
+    if rc != 0:
+        return None
+    nq, ns, rmax, n_long, nl = (int(x) for x in info)
+    return dict(K=K, n_chunks=nq, n_slots=ns, rmax=rmax, n_long=n_long, n_spill_list=nl, rec=rec[: 2 * N],
+                succ=succ[:E], bounds=bounds[: nq + 1], spill_off=soff[: nq + 1], spill_list=slist[:nl])
+
+
 class ClassTables(Tables):
     """Tables uploaded to the device, with the C-ABI structs of K3 v2 and K4 v2."""
 
@@ -256,6 +288,29 @@ class ClassTables(Tables):
                                          self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long, p(t["cp_spill"]),
                                          p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads, p(t["pinfo"]),
                                          self.slot_region, self.stage_doubles)
+
+        self.lane = None  # K4 v3 (lane per candidate), when its tables fit
+        if os.environ.get("DFSIM_CP_KERNEL", "lanes") == "lanes":
+            plan = lane_plan(self)
+            if plan is not None:
+                t.update(l_rec=T(plan["rec"], np.uint32), l_succ=T(plan["succ"], np.uint16),
+                         l_bounds=T(plan["bounds"], np.int32), l_soff=T(plan["spill_off"], np.int32),
+                         l_slist=T(plan["spill_list"], np.uint16))
+                st = native.CpLaneTables(lg.n, self.n_edges, plan["n_chunks"], plan["K"], plan["n_slots"],
+                                         plan["rmax"], plan["n_long"], plan["n_spill_list"], p(t["l_rec"]),
+                                         p(t["l_succ"]), p(t["l_bounds"]), p(t["l_soff"]), p(t["l_slist"]),
+                                         p(t["rank_of_pos"]))
+                if self.ctx.lib.dfsim_critical_path_lanes_capacity(native.ctypes.byref(st)) > 0:
+                    self.lane, self.lane_struct = plan, st
+
+    def critical_path(self, n_sims: int, sched, cp_len, cp_src):
+        """K4 over the fused engine's schedules: v3 (lane per candidate) when planned, else v2."""
+        if self.lane is not None:
+            self.ctx.call("dfsim_critical_path_lanes", native.ctypes.byref(self.lane_struct), n_sims,
+                          native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
+        else:
+            self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.cp_struct), n_sims,
+                          native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
 
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
         """Schedule row(s) stored by position -> node-rank order."""

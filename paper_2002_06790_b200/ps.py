@@ -19,7 +19,7 @@ the aggregations.  Link devices take the throughput and latency of the profile
 DB's ``gpu-gpu-uni`` row for the collective path (the row the reference's ring
 fallback reads, costmodel.py:334-344).  Parity of the expansion itself is
 unpinned (no reference); estimate + simulate of the emitted graph are pinned by
-the oracle in tests/test_gpu_ps.py.
+the oracle in tests/test_ps.py and tests/test_gpu_fuzz.py.
 """
 
 from __future__ import annotations

@@ -147,3 +147,47 @@ def test_sweep_edge_cases():
     assert rep.critical_path_nodes == ["a"] and rep.critical_path_us == 1.5 and rep.top_k_ops == [("Op", 1.5, 1.0)]
     none = fw.sweep(one, ProfileDB(), [])
     assert none.best_index == -1 and len(none.makespan) == 0
+
+
+def test_sweep_rejects_nan_or_negative_values_like_the_reference():
+    """A NaN op_gap_us or a negative override passes the config parser (NaN < 0 is False) but
+    not DurationEntry (costmodel.py:78-80): sweep must raise that ValueError instead of
+    running the fused engine on a NaN/negative duration (which never terminates)."""
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200 import workloads as W
+
+    g = W.layered_cnn(6)
+    db = W.planted_profiles(W.CNN_LAWS)
+    base = dict(replicas=4, device_map=("gpu0", "gpu1", "gpu2", "gpu3"), gradient_markers=("grad_conv_*",),
+                hardware="synth-hw")
+    good = fw.StrategyConfig(**base, op_gap_us=0.5)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        assert fw.TopologyClass(g, db, [good]).fused
+        for bad in (fw.StrategyConfig(**base, op_gap_us=float("nan")),
+                    fw.StrategyConfig(**base, op_gap_us=-1.0),
+                    fw.StrategyConfig(**base, overrides={"conv_1@r2": -2.0}),
+                    fw.StrategyConfig(**base, overrides={"conv_*": float("nan")})):
+            assert not fw.TopologyClass(g, db, [good, bad]).fused
+            with pytest.raises(ValueError, match="nonnegative"):
+                fw.sweep(g, db, [good, bad])
+
+
+def test_sweep_error_precedence_construction_vs_runtime():
+    """The first failing config in list order raises (cli.py:132-145), whether its class failed
+    to build (expansion ConfigError) or at run time (UnknownOpError)."""
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200.model import DeviceSpec, OpNode, ProfileDB, make_graph
+
+    g = make_graph([OpNode("a", "Mystery", "gpu0"),
+                    OpNode("t", "Send", "l0", "Transfer", {"src_device": "gpu0", "dst_device": "gpu1", "bytes": 8},
+                           inputs=(("a", 0),))],
+                   [DeviceSpec("gpu0", "Compute"), DeviceSpec("gpu1", "Compute"), DeviceSpec("l0", "Link", "", 100.0, 0.0)])
+    plain = fw.StrategyConfig()
+    bad_dp = fw.StrategyConfig(replicas=2, device_map=("gpu0", "gpu1"), gradient_markers=("t",))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        with pytest.raises(fw.UnknownOpError):
+            fw.sweep(g, ProfileDB(), [plain, bad_dp])
+        with pytest.raises(fw.ConfigError):
+            fw.sweep(g, ProfileDB(), [bad_dp, plain])
