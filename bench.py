@@ -633,6 +633,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_value = S_total / (e2e_total / args.steps / 1e3)
+    cold = None if args.no_cold else measure_cold(args, graphs, db, configs, graph_of, rank, world, dev, S_total)
 
     if rank == 0:
         tcf = classes[0][0]
@@ -652,6 +653,7 @@ def run_ours(args):
             "stage_ms": {k: statistics.mean(s[k] for s in ev_steps) for k in stages} if single else None,
             "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": "sims/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e_cold": cold,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
@@ -663,6 +665,72 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def measure_cold(args, graphs, db, configs, graph_of, rank, world, dev, S_total, runs: int = 3):
+    """One-shot sweeps through the public API, from host objects to host results: the wall time
+    of sweep_variants (one GPU) / sweep_sharded (one rank per GPU) including class construction
+    (expansion, lowering, tables, fits), the hot path and the D2H of makespans, critical paths
+    and the best index.  Graph-object caches are dropped before every run; median of ``runs``,
+    max over ranks."""
+    import warnings
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_06790_b200 import sweep_sharded, sweep_variants
+
+    if world > 1:  # the global candidate list; sweep_sharded gives each rank the slice it ran above
+        if args.workload == "vgg16-sweep":
+            all_cfg, all_gof = build_workload_all(args, world)
+        else:
+            all_cfg, all_gof = [], []
+            for r in range(world):
+                _, _, c, gof = build_workload(r, len(configs), args.workload)
+                all_cfg += c
+                all_gof += gof
+    walls, setups = [], []
+    for _ in range(runs):
+        for g in graphs:
+            for attr in ("_dfsim_b200_lowered", "_dfsim_base_rows"):
+                try:
+                    object.__delattr__(g, attr)
+                except AttributeError:
+                    pass
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            if world > 1:
+                res = sweep_sharded(graphs, db, all_cfg, all_gof, gather_all=False)
+            else:
+                res = sweep_variants(graphs, db, configs, graph_of)
+        walls.append(time.perf_counter() - t0)
+        assert res.best_index >= 0
+    wall = statistics.median(walls)
+    if world > 1:
+        t = torch.tensor([wall], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    return {"value": S_total / wall, "unit": "sims/s", "wall_s": wall, "runs": runs,
+            "what": "median wall time of a one-shot sweep_variants / sweep_sharded call from host objects to host "
+                    "makespans + critical paths + best index, class construction included, graph caches dropped"}
+
+
+def build_workload_all(args, world):
+    """The whole C3 grid (build_workload splits it by WORLD_SIZE)."""
+    saved = os.environ.get("WORLD_SIZE")
+    os.environ["WORLD_SIZE"] = "1"
+    try:
+        _, _, cfg, gof = build_workload(0, len(_vgg_grid()), "vgg16-sweep")
+    finally:
+        if saved is None:
+            os.environ.pop("WORLD_SIZE", None)
+        else:
+            os.environ["WORLD_SIZE"] = saved
+    return cfg, gof
 
 
 def measure_reports(tc, o, rows: int, cpu_rows: int = 8):
@@ -811,6 +879,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cold", action="store_true", help="skip the one-shot (cold) end-to-end sweeps")
     ap.add_argument("--no-reports", action="store_true", help="skip the summary/trace measurement")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--report-rows", type=int, default=1024, help="schedules summarised in the reports line")

@@ -8,7 +8,10 @@
  * maintainer would add):
  *
  *   dfsim_expand_dp          strategy.py:170-282  expand_data_parallel (+ graph.py:122-135 CSR)
- *   dfsim_topo_order         graph.py:424-443     topological_order (any valid order)
+ *   dfsim_topo_order         graph.py:424-443     topological order (any valid order, device)
+ *   dfsim_topological_order  graph.py:424-443     topological_order (the reference's order, host)
+ *   dfsim_predict_batch      costmodel.py:158-165 predict
+ *   dfsim_comm_batch         costmodel.py:168-223 comm_time_us / transfer_time / allreduce_time
  *   dfsim_estimate_batch     costmodel.py:282-376 estimate_all (predict 158-165, comm 168-223)
  *   dfsim_simulate_batch     engine.py:96-146     simulate (+ _finalize 69-93)
  *   dfsim_critical_path_batch graph.py:446-485    critical_path on finish-start (reporting.py:128)
@@ -301,20 +304,22 @@ int32_t dfsim_critical_path_levels_capacity(const dfsim_cp_tables *t);
  * class tables are read once per 32 candidates.  A node's suffix value lives in a shared-
  * memory slot while it is read within its own or the next prefetch chunk, otherwise in a
  * per-warp spill row [n_long][32] in global memory, prefetched with the reading chunk.
+ * Node records stream from global memory with the schedule data, one block per chunk.
  * Tables come from dfsim_cp_lanes_plan (host). */
 typedef struct {
     int32_t n_nodes;
-    int32_t n_edges;
     int32_t n_chunks;          /* prefetch chunks, in processing order (highest positions first) */
-    int32_t chunk_positions;   /* K: a chunk covers at most K positions (K <= 16) */
-    int32_t n_slots;           /* shared-memory suffix slots per candidate */
+    int32_t chunk_positions;   /* K: a chunk covers at most K positions (8 or 16) */
+    int32_t n_slots;           /* shared-memory suffix rows per warp (slots) */
     int32_t rmax;              /* spill values prefetched per chunk, at most */
     int32_t n_long;            /* values kept in spill rows */
     int32_t n_spill_list;      /* length of spill_list (= spill_off[n_chunks]) */
-    const uint32_t *rec;       /* [N][2] per position: x = successor begin | count << 24;
-                                  y = slot | has_slot << 12 | source << 13 | has_spill << 14 | spill << 15 */
-    const uint16_t *succ;      /* [E] per reading position (CSR by rec.x): row of the successor's value in
-                                  the candidate's region [slots | spill stage 0 | spill stage 1] */
+    int32_t block_max;         /* largest chunk block, in 16-byte units */
+    const uint32_t *blocks;    /* [4 per 16-byte unit] per chunk, in processing order: one 16-byte record per position
+                                  {x: slot | has_slot << 12 | source << 13 | has_spill << 14 | spill << 15,
+                                   y: successors | extra << 8 (u16 offset of successors 5.. in the block),
+                                   z, w: rows of successors 1-4 (16 bits each)}, then the extra rows */
+    const int32_t *block_off;  /* [n_chunks + 1] in 16-byte units */
     const int32_t *bounds;     /* [n_chunks + 1]: chunk q covers positions [bounds[q+1], bounds[q]) */
     const int32_t *spill_off;  /* [n_chunks + 1] */
     const uint16_t *spill_list; /* spill indices prefetched with each chunk, in stage-row order */
@@ -325,18 +330,22 @@ typedef struct {
  * order (every edge from a lower to a higher position), succ_off[N+1] / succ_pos[E] the
  * successors of each position, is_source[N].  Chunks of <= K positions are cut in reverse
  * order so that no chunk prefetches more than max(rmax_min, widest node) spill values.
- * Output arrays are caller-allocated at their bounds: rec[2N], succ_loc[E], bounds[N+1],
- * spill_off[N+1], spill_list[E]; info[5] = {n_chunks, n_slots, rmax, n_long, spill_list length}.
- * Returns DFSIM_BAD_ARGUMENT when a field overflows its width (the class then keeps K4 v2). */
+ * A value read within near_chunks chunks of its writer's (at least `stages`) keeps a slot.
+ * Value rows of a warp's shared region: [slots | spill stage 0 .. stages-1].  Output arrays
+ * are caller-allocated at their bounds: blocks[4 * (2N + E/8 + 2)] u32, block_off[N+1],
+ * bounds[N+1], spill_off[N+1], spill_list[E]; info[6] = {n_chunks, n_slots, rmax, n_long,
+ * spill_list length, block_max}.  Returns DFSIM_BAD_ARGUMENT when a field overflows. */
 int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int32_t *succ_pos, const uint8_t *is_source,
-                        int32_t K, int32_t rmax_min, uint32_t *rec, uint16_t *succ_loc, int32_t *bounds,
-                        int32_t *spill_off, uint16_t *spill_list, int32_t *info);
+                        int32_t K, int32_t rmax_min, int32_t stages, int32_t near_chunks, uint32_t *blocks,
+                        int32_t *block_off, int32_t *bounds, int32_t *spill_off, uint16_t *spill_list,
+                        int32_t *info);
 
-int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int64_t n_sims, const double *sched,
-                              double *cp_len, int32_t *cp_src);
+/* stages: prefetch depth (2 or 3, as planned). */
+int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
+                              const double *sched, double *cp_len, int32_t *cp_src);
 
 /* Warps (32 candidates each) one CTA of dfsim_critical_path_lanes holds (0: does not fit). */
-int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t);
+int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t, int32_t stages);
 
 /* ---------------------------------------------------------------- critical path (K4) */
 /* Over d = finish - start (reporting.py:128), or over d = finish when start is NULL
@@ -352,6 +361,20 @@ int dfsim_critical_path_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_si
 int dfsim_critical_path_wide(dfsim_ctx *ctx, const dfsim_graph *g, const int32_t *order, const int32_t *level_off,
                              int32_t n_levels, int64_t n_sims, const double *start, const double *finish,
                              double *cp_len, int32_t *cp_src);
+
+/* ---------------------------------------------------------------- scalar formulas (drop-in) */
+/* predict (costmodel.py:158-165) for n feature vectors feats[n][k] of one linear model:
+ * out[i] = max(0.0, intercept + sum(coef[j] * feats[i][j])) with CPython 3.12's float sum. */
+int dfsim_predict_batch(dfsim_ctx *ctx, int32_t k, const double *coef, double intercept, int64_t n,
+                        const double *feats, double *out);
+/* Communication formulas (costmodel.py:168-223) for n rows: kind 0 = comm_time_us
+ * (transfer_time, measured allreduce with lat 0), kind 1 = ring allreduce over a link. */
+int dfsim_comm_batch(dfsim_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *bytes,
+                     const int32_t *participants, const double *thr, const double *lat, double *out);
+/* topological_order (graph.py:424-443) on the host: Kahn with a min-heap of ranks into
+ * order[n]; returns how many nodes were ordered (< n: a cycle), -1 on bad arguments. */
+int32_t dfsim_topological_order(int32_t n, const int32_t *succ_off, const int32_t *succ_idx, const int32_t *indeg,
+                                int32_t *order);
 
 /* ---------------------------------------------------------------- best strategy (K5) */
 /* First minimum of (value, index) over n values; index = index_base + i.

@@ -54,5 +54,18 @@ from .document import DocumentGraph, load_graph  # noqa: F401
 from .ps import expand_parameter_server  # noqa: F401
 from .reporting import SummaryReport, render_summary_text, summarize, to_trace, trace_intervals  # noqa: F401
 from .simulator import critical_path, simulate  # noqa: F401
+from .scalar import (  # noqa: F401
+    allreduce_time,
+    apply_overrides,
+    comm_batch,
+    comm_time_us,
+    predict,
+    predict_batch,
+    query_exact,
+    query_grid,
+    query_link,
+    topological_order,
+    transfer_time,
+)
 
 __version__ = "0.1.0"

@@ -14,6 +14,7 @@ process) and reduces one 16-byte winner record per GPU (NCCL all-gather / P2P).
 
 from __future__ import annotations
 
+import operator
 import os
 import warnings
 from dataclasses import dataclass, field
@@ -40,6 +41,44 @@ def class_key(cfg) -> tuple:
     return ("dp", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers), cfg.collective.path)
 
 
+_R, _DMAP = operator.attrgetter("replicas"), operator.attrgetter("device_map")
+_MARKERS, _COLL = operator.attrgetter("gradient_markers"), operator.attrgetter("collective")
+
+
+def group_classes(graphs, configs, graph_of) -> list:
+    """Config indices of each topology class, classes in order of first appearance.  A class
+    is (class_key, structure of the candidate's graph); keys are derived once per distinct
+    field combination, not per candidate (sweeps hold 10^4-10^5 configs)."""
+    from .variants import structure_key
+
+    skeys = {gi: structure_key(graphs[gi]) for gi in dict.fromkeys(graph_of)}
+    # identity of the field objects (configs of a sweep share them), built with C-level maps;
+    # equal-valued but distinct objects only cost one extra class_key call each
+    try:
+        sync = list(map(operator.attrgetter("sync"), configs))
+        psd = list(map(operator.attrgetter("ps_device"), configs))
+    except AttributeError:  # e.g. the reference's own StrategyConfig (no PS extension fields)
+        sync = [getattr(c, "sync", "allreduce") for c in configs]
+        psd = [getattr(c, "ps_device", None) for c in configs]
+    cols = [list(map(_R, configs)), list(map(id, map(_DMAP, configs))), list(map(id, map(_MARKERS, configs))),
+            list(map(id, map(_COLL, configs))), sync, psd, list(graph_of)]
+    cols = [c for c in cols if len(dict.fromkeys(c)) > 1]  # fields shared by every config drop out
+    if not cols:
+        return [list(range(len(configs)))] if configs else []
+    raw = list(zip(*cols))
+    # first config of each distinct field combination (reversed: the smallest index is written last)
+    first = dict(zip(reversed(raw), range(len(raw) - 1, -1, -1)))
+    cls_of_key: dict = {}
+    cls_of_raw = {r: cls_of_key.setdefault((class_key(configs[i]), skeys[graph_of[i]]), len(cls_of_key))
+                  for r, i in first.items()}
+    cls = np.fromiter(map(cls_of_raw.__getitem__, raw), np.int64, len(raw))
+    order = np.argsort(cls, kind="stable")  # config order inside each class
+    cuts = np.flatnonzero(np.diff(cls[order])) + 1
+    groups = np.split(order, cuts) if len(order) else []
+    groups.sort(key=lambda g: int(g[0]))  # classes in order of first appearance
+    return [g.tolist() for g in groups]
+
+
 class TopologyClass:
     """One expanded graph resident on a device + profile tables for a candidate list.
 
@@ -51,7 +90,7 @@ class TopologyClass:
     """
 
     def __init__(self, g, db, configs, device: int | None = None, fused: bool = True, graphs=None,
-                 graph_of=None):
+                 graph_of=None, fit_cache=None):
         ctx = native.Context.get(device)
         self.ctx = ctx
         cfg0 = configs[0]
@@ -77,17 +116,23 @@ class TopologyClass:
         self.ids = self.lg.ids
         self.configs = list(configs)
         variant_rows, strat_gv = None, None
-        if graphs is not None and len(set(graph_of)) > 1:
-            from .variants import rows_for
+        multi = graphs is not None and len(set(graph_of)) > 1
+        if multi or kind != "plain":
+            # estimate inputs from the base graph(s): a clone's row is its base node's, so features
+            # are computed once per base node and collective / PS node, not per expanded node
+            from .variants import variant_arrays
 
+            if graphs is None:
+                graphs, graph_of = [g], [0] * len(configs)
             gv_of: dict = {}
             variant_rows = []
-            for gi in graph_of:
-                if gi not in gv_of:
-                    gv_of[gi] = len(variant_rows)
-                    variant_rows.append(rows_for(kind, self.ids, graphs[gi], structure, cfg0, db))
+            cache: dict = {}
+            for gi in dict.fromkeys(graph_of):
+                gv_of[gi] = len(variant_rows)
+                variant_rows.append(variant_arrays(kind, self.ids, graphs[gi], structure, cfg0, db, cache))
             strat_gv = [gv_of[gi] for gi in graph_of]
-        self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device, variant_rows, strat_gv)
+        self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device, None, strat_gv,
+                                  fit_cache=fit_cache, variant_arrays=variant_rows)
         self.tables = None
         self.fused = False
         if fused and self.lg.acyclic and 0 < self.lg.n <= 65535 and self.lp.fused_values_ok:
@@ -120,7 +165,8 @@ class TopologyClass:
             return  # some candidate fails estimation: keep the unfused path (exact error semantics)
         cap = int(self.ctx.lib.dfsim_fused_capacity(native.ctypes.byref(self.tables.sim_struct)))
         cp_ok = (self.tables.lane is not None
-                 or self.ctx.lib.dfsim_critical_path_levels_capacity(native.ctypes.byref(self.tables.cp_struct)) > 0)
+                 or (self.tables.cp_struct is not None and self.ctx.lib.dfsim_critical_path_levels_capacity(
+                     native.ctypes.byref(self.tables.cp_struct)) > 0))
         if cap <= 0 or not cp_ok:
             return  # engine or critical-path tables exceed shared memory: rank-layout kernels
         self.chunk_capacity = cap
@@ -197,7 +243,8 @@ class TopologyClass:
         lg, S, N, D = self.lg, self.lp.n_sims, self.lg.n, self.lg.n_devices
         dev = f"cuda:{self.ctx.device}"
         if "sched" not in o:  # callers may pre-place any output (e.g. flags as a view of a shared buffer)
-            o["sched"] = torch.empty((S, N, 2), dtype=torch.float64, device=dev)  # (start, finish) pairs
+            # (start, finish) pairs; two spare pairs past the last row for K4 v3's 32-byte window loads
+            o["sched"] = torch.empty(S * N * 2 + 4, dtype=torch.float64, device=dev)[: S * N * 2].view(S, N, 2)
             o["start"], o["finish"] = o["sched"][..., 0], o["sched"][..., 1]
             o.setdefault("makespan", torch.empty(S, dtype=torch.float64, device=dev))
             o.setdefault("busy", torch.empty((S, max(D, 1)), dtype=torch.float64, device=dev))
@@ -482,15 +529,7 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
     failing config in list order (cli.py:132-145) or None.  ``result.best_*`` are this shard's."""
     import torch
 
-    from .variants import structure_key
-
-    skeys = {}
-    groups: dict = {}
-    for i, cfg in enumerate(configs):
-        gi = graph_of[i]
-        if gi not in skeys:
-            skeys[gi] = structure_key(graphs[gi])
-        groups.setdefault((class_key(cfg), skeys[gi]), []).append(i)
+    groups = group_classes(graphs, configs, graph_of)
     S = len(configs)
     ctx = native.Context.get(device)
     dev = f"cuda:{ctx.device}"
@@ -499,10 +538,12 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
     result = SweepResult(np.zeros(0), np.zeros(0), -1, float("nan"))
     failures = []  # (config index, exception)
     built = []
-    for idx in groups.values():
+    fits: dict = {}  # fitted models shared by the classes of this sweep (costmodel.py:313-316 fits per call)
+    for idx in groups:
         try:
             built.append((idx, TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device,
-                                             fused=fused, graphs=graphs, graph_of=[graph_of[i] for i in idx])))
+                                             fused=fused, graphs=graphs, graph_of=[graph_of[i] for i in idx],
+                                             fit_cache=fits)))
         except NativeError:
             raise
         except Exception as e:  # noqa: BLE001 -- expansion / lowering error: the class's first config fails

@@ -9,13 +9,15 @@
 // lane: one 16-byte (start, finish) read, one 8-byte read per successor, one max, two adds.
 //
 // Storage of suffix values (A4: suffix[v] = (finish - start)[v] + max(0, max succ suffix)):
-//  * read within the writer's prefetch chunk or the next one -> a shared-memory slot
+//  * read within the next NST - 1 prefetch chunks of its writer's -> a shared-memory slot
 //    (interval colouring by the host planner, a few dozen slots);
 //  * read later (forward activations read by their backward consumers ~half a graph
 //    later) -> the warp's spill row [n_long][32] in global memory (one coalesced 256-byte
 //    store per value), prefetched into a shared stage together with the reading chunk.
-// Schedule pairs are prefetched with cp.async one chunk ahead: each candidate's chunk is a
-// contiguous 256-byte run of its row (positions are level order), so the copies coalesce.
+// Schedule pairs, the chunk's node records (first four successor rows inline) and its spill
+// values are prefetched with cp.async NST - 1 chunks ahead (NST = 2 or 3 stages): each
+// candidate's chunk is a contiguous run of its row (positions are level order), so the
+// copies coalesce, and no class table occupies shared memory beyond a few offsets.
 //
 // Exactness: the same single max and add per node as graph.py:463-469 (any reverse
 // topological order gives identical bits, A4); source = smallest rank among the maxima.
@@ -60,6 +62,11 @@ __device__ __forceinline__ unsigned lds_h(unsigned a) {
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint4 lds_u4(unsigned a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ int lds_i(unsigned a) {
     int v;
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -75,63 +82,73 @@ struct LaneArgs {
     double *cp_len;
     int32_t *cp_src;
     double *spill;        // [grid * wpb][n_long][32]
+    int32_t *task_counter; // groups of 32 candidates handed out dynamically (SMs finish together)
     int32_t wpb;
-    int32_t table_bytes;
-    int32_t region_bytes;
+    int32_t table_bytes;  // CTA tables: bounds | spill_off | block_off | spill_list
+    int32_t region_bytes; // per warp: rows [slots | spill stages] | pair stages | block stages
 };
 
-template <int K>
+// Per warp: value rows of 256 B (one double per lane) -- slots, then one spill stage per
+// pipeline stage -- then the pair stages (32 candidates x K (start, finish) pairs, rows padded
+// by 16 B so that a warp's LDS.128 is conflict-free), then the block stages (the chunk's node
+// records).  Chunk q uses stage q % NST; prefetch runs NST - 1 chunks ahead.
+template <int K, int NST>
 __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int kStride = K * 16 + 16;  // bytes per candidate in a pair stage (padded: conflict-free LDS.128)
+    constexpr int kStride = K * 16 + 16;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int N = a.t.n_nodes, E = a.t.n_edges, NQ = a.t.n_chunks, NS = a.t.n_slots, RM = a.t.rmax;
+    const int N = a.t.n_nodes, NQ = a.t.n_chunks, NS = a.t.n_slots, RM = a.t.rmax, BM = a.t.block_max;
     const int NL = a.t.n_spill_list;
-    // CTA tables: rec[N] (uint2) | succ[E] (u16) | bounds[NQ+1] | spill_off[NQ+1] | spill_list[NL] (u16)
-    uint2 *s_rec = reinterpret_cast<uint2 *>(smem);
-    uint16_t *s_succ = reinterpret_cast<uint16_t *>(s_rec + N);
-    int32_t *s_bounds = reinterpret_cast<int32_t *>(smem + ((static_cast<size_t>(N) * 8 + static_cast<size_t>(E) * 2 + 15) / 16) * 16);
+    int32_t *s_bounds = reinterpret_cast<int32_t *>(smem);
     int32_t *s_soff = s_bounds + (NQ + 1);
-    uint16_t *s_slist = reinterpret_cast<uint16_t *>(s_soff + (NQ + 1));
-    for (int i = threadIdx.x; i < N; i += blockDim.x)
-        s_rec[i] = make_uint2(__ldg(a.t.rec + 2 * i), __ldg(a.t.rec + 2 * i + 1));
-    for (int i = threadIdx.x; i < E; i += blockDim.x) s_succ[i] = __ldg(a.t.succ + i);
+    int32_t *s_boff = s_soff + (NQ + 1);
+    uint16_t *s_slist = reinterpret_cast<uint16_t *>(s_boff + (NQ + 1));
     for (int i = threadIdx.x; i <= NQ; i += blockDim.x) {
         s_bounds[i] = __ldg(a.t.bounds + i);
         s_soff[i] = __ldg(a.t.spill_off + i);
+        s_boff[i] = __ldg(a.t.block_off + i);
     }
     for (int i = threadIdx.x; i < NL; i += blockDim.x) s_slist[i] = __ldg(a.t.spill_list + i);
     __syncthreads();
 
-    const unsigned a_rec = smem_u32(s_rec), a_succ = smem_u32(s_succ), a_bounds = smem_u32(s_bounds);
-    const unsigned a_soff = smem_u32(s_soff), a_slist = smem_u32(s_slist);
+    const unsigned a_bounds = smem_u32(s_bounds), a_soff = smem_u32(s_soff), a_boff = smem_u32(s_boff);
+    const unsigned a_slist = smem_u32(s_slist);
     unsigned char *region = smem + a.table_bytes + static_cast<size_t>(warp) * a.region_bytes;
-    const unsigned a_region = smem_u32(region);                  // rows of 256 B: slots | spill stage 0 | 1
-    const unsigned a_lane = a_region + 8u * lane;                // this lane's column in every row
-    const unsigned a_pairs = a_region + static_cast<unsigned>(NS + 2 * RM) * 256u;  // two pair stages
+    const unsigned a_region = smem_u32(region);
+    const unsigned a_lane = a_region + 8u * lane;  // this lane's column in every value row
+    const unsigned a_pairs = a_region + static_cast<unsigned>(NS + NST * RM) * 256u;
+    const unsigned a_blocks = a_pairs + static_cast<unsigned>(NST) * 32u * kStride;
     const int64_t slot_warp = static_cast<int64_t>(blockIdx.x) * a.wpb + warp;
     double *spill_warp = a.spill + slot_warp * static_cast<int64_t>(a.t.n_long) * 32 + lane;
     asm volatile("mov.b64 %0, %0;" : "+l"(spill_warp));
-    const int64_t step = static_cast<int64_t>(gridDim.x) * a.wpb * 32;
-
-    for (int64_t wbase = slot_warp * 32; wbase < a.S; wbase += step) {
+    const int64_t n_tasks = (a.S + 31) / 32;
+    for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(a.task_counter, 1);
+        task = __shfl_sync(DFSIM_FULL_MASK, task, 0);
+        if (task >= n_tasks) break;
+        const int64_t wbase = static_cast<int64_t>(task) * 32;
         const bool live = wbase + lane < a.S;
         const int n_live = static_cast<int>(a.S - wbase < 32 ? a.S - wbase : 32);
         const double *rows = a.sched + 2 * wbase * N;
         asm volatile("mov.b64 %0, %0;" : "+l"(rows));
 
         auto prefetch = [&](int q) {
+            const unsigned stg = static_cast<unsigned>(q % NST);
             const int hi = lds_i(a_bounds + 4u * q);
             const int wlo = hi > K ? hi - K : 0;
-            const unsigned st = a_pairs + static_cast<unsigned>(q & 1) * (32u * kStride);
+            const unsigned st = a_pairs + stg * (32u * kStride);
 #pragma unroll
             for (int k = lane; k < 32 * K; k += 32) {  // candidate c = k / K, pair i = k % K: coalesced runs
                 const int c = k / K, i = k % K;
                 if (c < n_live && wlo + i < N)
                     cpa16(st + static_cast<unsigned>(c * kStride + i * 16), rows + 2 * (static_cast<int64_t>(c) * N + wlo + i));
             }
+            const int b0 = lds_i(a_boff + 4u * q), b1 = lds_i(a_boff + 4u * (q + 1));
+            const unsigned bs = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
+            for (int b = b0 + lane; b < b1; b += 32) cpa16(bs + 16u * static_cast<unsigned>(b - b0), a.t.blocks + 4 * static_cast<int64_t>(b));
             const int r0 = lds_i(a_soff + 4u * q), r1 = lds_i(a_soff + 4u * (q + 1));
-            const unsigned ss = a_lane + static_cast<unsigned>(NS + (q & 1) * RM) * 256u;
+            const unsigned ss = a_lane + static_cast<unsigned>(NS + static_cast<int>(stg) * RM) * 256u;
             if (live)
                 for (int r = r0; r < r1; r++) cpa8(ss + static_cast<unsigned>(r - r0) * 256u, spill_warp + 32 * static_cast<int64_t>(lds_h(a_slist + 2u * r)));
             asm volatile("cp.async.commit_group;\n" ::);
@@ -139,31 +156,42 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
 
         double len = 0.0;
         int src = 0x7fffffff;
-        if (NQ > 0) prefetch(0);
+#pragma unroll
+        for (int q = 0; q < NST - 1; q++)
+            if (q < NQ) prefetch(q); else asm volatile("cp.async.commit_group;\n" ::);
         for (int q = 0; q < NQ; q++) {
-            if (q + 1 < NQ) {
-                prefetch(q + 1);
-                asm volatile("cp.async.wait_group 1;\n" ::);
-            } else {
-                asm volatile("cp.async.wait_group 0;\n" ::);
-            }
+            // stage (q + NST - 1) % NST was last used by chunk q - 1 (finished: __syncwarp below)
+            if (q + NST - 1 < NQ) prefetch(q + NST - 1); else asm volatile("cp.async.commit_group;\n" ::);
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(NST - 1));
             __syncwarp();
+            const unsigned stg = static_cast<unsigned>(q % NST);
             const int hi = lds_i(a_bounds + 4u * q), lo = lds_i(a_bounds + 4u * (q + 1));
             const int wlo = hi > K ? hi - K : 0;
-            const unsigned pst = a_pairs + static_cast<unsigned>(q & 1) * (32u * kStride) + static_cast<unsigned>(lane * kStride) - 16u * wlo;
-            for (int p = hi - 1; p >= lo; p--) {
-                const uint2 r = lds_u2(a_rec + 8u * p);
-                const int j0 = static_cast<int>(r.x & 0xffffffu), j1 = j0 + static_cast<int>(r.x >> 24);
-                double best = 0.0;  // max(0.0, .) (graph.py:465-468)
-                for (int j = j0; j < j1; j++) {
-                    const double x = lds_d(a_lane + 256u * lds_h(a_succ + 2u * j));
-                    best = x > best ? x : best;
-                }
+            const unsigned pst = a_pairs + stg * (32u * kStride) + static_cast<unsigned>(lane * kStride) - 16u * wlo;
+            const unsigned blk = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
+            unsigned rec = blk;  // records in processing order
+            for (int p = hi - 1; p >= lo; p--, rec += 16u) {
+                const uint4 r = lds_u4(rec);
+                const unsigned deg = r.y & 0xffu;
+                // successors 1-4 inline: independent loads, issued together
+                const double x0 = deg > 0 ? lds_d(a_lane + 256u * (r.z & 0xffffu)) : 0.0;
+                const double x1 = deg > 1 ? lds_d(a_lane + 256u * (r.z >> 16)) : 0.0;
+                const double x2 = deg > 2 ? lds_d(a_lane + 256u * (r.w & 0xffffu)) : 0.0;
+                const double x3 = deg > 3 ? lds_d(a_lane + 256u * (r.w >> 16)) : 0.0;
                 const double2 sf = lds_d2(pst + 16u * p);
+                double m01 = x1 > x0 ? x1 : x0, m23 = x3 > x2 ? x3 : x2;
+                double best = m23 > m01 ? m23 : m01;  // >= 0.0: max(0.0, .) (graph.py:465-468)
+                if (deg > 4) {
+                    const unsigned ex = blk + 2u * (r.y >> 8);
+                    for (unsigned j = 4; j < deg; j++) {
+                        const double x = lds_d(a_lane + 256u * lds_h(ex + 2u * (j - 4)));
+                        best = x > best ? x : best;
+                    }
+                }
                 const double sv = __dadd_rn(__dsub_rn(sf.y, sf.x), best);  // finish - start (reporting.py:128)
-                if (r.y & kHasSlot) sts_d(a_lane + 256u * (r.y & 0xfffu), sv);
-                if ((r.y & kHasSpill) && live) spill_warp[32 * static_cast<int64_t>(r.y >> 15)] = sv;
-                if (r.y & kSource) {
+                if (r.x & kHasSlot) sts_d(a_lane + 256u * (r.x & 0xfffu), sv);
+                if ((r.x & kHasSpill) && live) spill_warp[32 * static_cast<int64_t>(r.x >> 15)] = sv;
+                if (r.x & kSource) {
                     const int rk = __ldg(a.t.rank_of_pos + p);
                     if (src == 0x7fffffff || sv > len || (sv == len && rk < src)) {
                         len = sv;
@@ -173,10 +201,183 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
             }
             __syncwarp();
         }
+        asm volatile("cp.async.wait_group 0;\n" ::);
         if (live) {
             a.cp_len[wbase + lane] = src == 0x7fffffff ? 0.0 : len;
             if (a.cp_src) a.cp_src[wbase + lane] = src == 0x7fffffff ? -1 : src;
         }
+        __syncwarp();
+    }
+}
+
+// Register-staged variant (K = 8): each lane loads its own candidate's schedule window with
+// 32-byte loads (LDG.256, one full sector per lane, 5 per chunk) straight into registers one
+// chunk ahead, so the pair stages need no shared memory and twice as many warps fit an SM.
+// The window of chunk q is the 32-byte aligned run [a, a + K + 2) with a = hi - K - off,
+// off = parity of the pair index (s N + hi - K): position p sits at register index
+// p - a = (p - hi + K) + off, i.e. one of two static indices selected by off.  Node records
+// and spill values use two shared-memory stages as above.
+__device__ __forceinline__ void ldg_v4(double (&d)[4], const double *p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
+}
+
+template <int K>
+__global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NST = 2, NU = K / 2 + 1;  // 32-byte units per window
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int N = a.t.n_nodes, NQ = a.t.n_chunks, NS = a.t.n_slots, RM = a.t.rmax, BM = a.t.block_max;
+    const int NL = a.t.n_spill_list;
+    int32_t *s_bounds = reinterpret_cast<int32_t *>(smem);
+    int32_t *s_soff = s_bounds + (NQ + 1);
+    int32_t *s_boff = s_soff + (NQ + 1);
+    uint16_t *s_slist = reinterpret_cast<uint16_t *>(s_boff + (NQ + 1));
+    for (int i = threadIdx.x; i <= NQ; i += blockDim.x) {
+        s_bounds[i] = __ldg(a.t.bounds + i);
+        s_soff[i] = __ldg(a.t.spill_off + i);
+        s_boff[i] = __ldg(a.t.block_off + i);
+    }
+    for (int i = threadIdx.x; i < NL; i += blockDim.x) s_slist[i] = __ldg(a.t.spill_list + i);
+    __syncthreads();
+
+    const unsigned a_bounds = smem_u32(s_bounds), a_soff = smem_u32(s_soff), a_boff = smem_u32(s_boff);
+    const unsigned a_slist = smem_u32(s_slist);
+    unsigned char *region = smem + a.table_bytes + static_cast<size_t>(warp) * a.region_bytes;
+    const unsigned a_region = smem_u32(region);
+    const unsigned a_lane = a_region + 8u * lane;
+    const unsigned a_blocks = a_region + static_cast<unsigned>(NS + NST * RM) * 256u;
+    const int64_t slot_warp = static_cast<int64_t>(blockIdx.x) * a.wpb + warp;
+    double *spill_warp = a.spill + slot_warp * static_cast<int64_t>(a.t.n_long) * 32 + lane;
+    asm volatile("mov.b64 %0, %0;" : "+l"(spill_warp));
+    const int64_t n_tasks = (a.S + 31) / 32;
+    for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(a.task_counter, 1);
+        task = __shfl_sync(DFSIM_FULL_MASK, task, 0);
+        if (task >= n_tasks) break;
+        const int64_t s = static_cast<int64_t>(task) * 32 + lane;
+        const bool live = s < a.S;
+        const double *row = a.sched + 2 * (live ? s : a.S - 1) * N;  // idle lanes shadow the last row
+        const int rowpar = static_cast<int>((static_cast<int64_t>(live ? s : a.S - 1) * N) & 1);
+
+        auto prefetch_smem = [&](int q) {  // node records + spill values of chunk q
+            const unsigned stg = static_cast<unsigned>(q & 1);
+            const int b0 = lds_i(a_boff + 4u * q), b1 = lds_i(a_boff + 4u * (q + 1));
+            const unsigned bs = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
+            for (int b = b0 + lane; b < b1; b += 32) cpa16(bs + 16u * static_cast<unsigned>(b - b0), a.t.blocks + 4 * static_cast<int64_t>(b));
+            const int r0 = lds_i(a_soff + 4u * q), r1 = lds_i(a_soff + 4u * (q + 1));
+            const unsigned ss = a_lane + static_cast<unsigned>(NS + static_cast<int>(stg) * RM) * 256u;
+            for (int r = r0; r < r1; r += 32) {  // spill ids loaded by the lanes together, then broadcast
+                const int my = r + lane < r1 ? static_cast<int>(lds_h(a_slist + 2u * (r + lane))) : 0;
+                const int nr = r1 - r < 32 ? r1 - r : 32;
+                for (int k = 0; k < nr; k++) {
+                    const int id = __shfl_sync(DFSIM_FULL_MASK, my, k);
+                    if (live) cpa8(ss + static_cast<unsigned>(r - r0 + k) * 256u, spill_warp + 32 * static_cast<int64_t>(id));
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        // L2 prefetch PF chunks ahead: the schedule window (three probes cover its 160 bytes)
+        // and the chunk's spill rows, so the register / cp.async loads one chunk ahead hit L2
+        auto prefetch_l2 = [&](int q) {
+            const int hi = lds_i(a_bounds + 4u * q);
+            const int off = (rowpar + hi - K) & 1;
+            const int a0 = hi - K - off;
+            if (N >= 2 * K) {  // the probes stay inside this row (plus the padding past the last)
+                const double *w0 = row + 2 * (a0 > 0 ? a0 : 0);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(w0));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(w0 + 10));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(w0 + 19));
+            }
+            const int r0 = lds_i(a_soff + 4u * q), r1 = lds_i(a_soff + 4u * (q + 1));
+            if (r0 + (lane >> 1) < r1) {  // two lanes per 256-byte spill row
+                const int id = static_cast<int>(lds_h(a_slist + 2u * (r0 + (lane >> 1))));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(spill_warp - lane + 32 * static_cast<int64_t>(id) + 16 * (lane & 1)));
+            }
+        };
+        auto load_window = [&](int q, double (&w)[NU][4]) {
+            const int hi = lds_i(a_bounds + 4u * q);
+            const int off = (rowpar + hi - K) & 1;
+            const int a0 = hi - K - off;
+#pragma unroll
+            for (int u = 0; u < NU; u++) {
+                const int p0 = a0 + 2 * u;
+                // units wholly before the row are not needed (position >= 0); the row pointer is
+                // backed by padding past the last row, see dfsim_critical_path_lanes
+                if (p0 + 1 >= 0) ldg_v4(w[u], row + 2 * p0);
+            }
+        };
+
+        double wa[NU][4], wb[NU][4];
+        double len = 0.0;
+        int src = 0x7fffffff;
+        prefetch_smem(0);
+        load_window(0, wa);
+
+        constexpr int PF = 3;
+        for (int q = 1; q < PF && q < NQ; q++) prefetch_l2(q);
+        auto process = [&](int q, double (&w)[NU][4], double (&wn)[NU][4]) {
+            if (q + PF < NQ) prefetch_l2(q + PF);
+            if (q + 1 < NQ) {
+                prefetch_smem(q + 1);
+                load_window(q + 1, wn);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
+            }
+            __syncwarp();
+            const unsigned stg = static_cast<unsigned>(q & 1);
+            const int hi = lds_i(a_bounds + 4u * q), lo = lds_i(a_bounds + 4u * (q + 1));
+            const int off = (rowpar + hi - K) & 1;
+            const unsigned blk = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
+#pragma unroll
+            for (int t = 0; t < K; t++) {
+                if (t < hi - lo) {
+                    const int p = hi - 1 - t;
+                    const uint4 r = lds_u4(blk + 16u * t);
+                    const unsigned deg = r.y & 0xffu;
+                    const double x0 = deg > 0 ? lds_d(a_lane + 256u * (r.z & 0xffffu)) : 0.0;
+                    const double x1 = deg > 1 ? lds_d(a_lane + 256u * (r.z >> 16)) : 0.0;
+                    const double x2 = deg > 2 ? lds_d(a_lane + 256u * (r.w & 0xffffu)) : 0.0;
+                    const double x3 = deg > 3 ? lds_d(a_lane + 256u * (r.w >> 16)) : 0.0;
+                    // position p at register index K - 1 - t + off (pair = two doubles)
+                    const int i0 = K - 1 - t, i1 = K - t;  // static after unrolling
+                    const double s0 = w[i0 >> 1][(i0 & 1) * 2], f0 = w[i0 >> 1][(i0 & 1) * 2 + 1];
+                    const double s1 = w[i1 >> 1][(i1 & 1) * 2], f1 = w[i1 >> 1][(i1 & 1) * 2 + 1];
+                    const double st = off ? s1 : s0, fi = off ? f1 : f0;
+                    const double m01 = x1 > x0 ? x1 : x0, m23 = x3 > x2 ? x3 : x2;
+                    double best = m23 > m01 ? m23 : m01;
+                    if (deg > 4) {
+                        const unsigned ex = blk + 2u * (r.y >> 8);
+                        for (unsigned j = 4; j < deg; j++) {
+                            const double x = lds_d(a_lane + 256u * lds_h(ex + 2u * (j - 4)));
+                            best = x > best ? x : best;
+                        }
+                    }
+                    const double sv = __dadd_rn(__dsub_rn(fi, st), best);  // finish - start (reporting.py:128)
+                    if (r.x & kHasSlot) sts_d(a_lane + 256u * (r.x & 0xfffu), sv);
+                    if ((r.x & kHasSpill) && live) spill_warp[32 * static_cast<int64_t>(r.x >> 15)] = sv;
+                    if (r.x & kSource) {
+                        const int rk = __ldg(a.t.rank_of_pos + p);
+                        if (src == 0x7fffffff || sv > len || (sv == len && rk < src)) {
+                            len = sv;
+                            src = rk;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        };
+        for (int q = 0; q < NQ; q += 2) {  // two chunks per iteration: the window registers swap roles
+            process(q, wa, wb);
+            if (q + 1 < NQ) process(q + 1, wb, wa);
+        }
+        if (live) {
+            a.cp_len[s] = src == 0x7fffffff ? 0.0 : len;
+            if (a.cp_src) a.cp_src[s] = src == 0x7fffffff ? -1 : src;
+        }
+        __syncwarp();
     }
 }
 
@@ -185,15 +386,18 @@ struct LaneShape {
     int wpb;
 };
 
-LaneShape lane_shape(const dfsim_cp_lane_tables *t) {
-    const int spill_list_len = t->n_spill_list;
+// stages 2 / 3: pairs staged in shared memory; stages 0: pairs in registers (K = 8), two
+// shared-memory stages for records and spill values
+LaneShape lane_shape(const dfsim_cp_lane_tables *t, int stages) {
     LaneShape s;
     const size_t K = static_cast<size_t>(t->chunk_positions);
-    s.table_bytes = ((static_cast<size_t>(t->n_nodes) * 8 + static_cast<size_t>(t->n_edges) * 2 + 15) / 16) * 16 +
-                    ((static_cast<size_t>(t->n_chunks + 1) * 8 + static_cast<size_t>(spill_list_len) * 2 + 15) / 16) * 16;
-    s.region_bytes = static_cast<size_t>(t->n_slots + 2 * t->rmax) * 256 + 2 * 32 * (K * 16 + 16);
+    const bool reg = stages == 0;
+    const size_t nst = reg ? 2 : static_cast<size_t>(stages);
+    s.table_bytes = ((static_cast<size_t>(t->n_chunks + 1) * 12 + static_cast<size_t>(t->n_spill_list) * 2 + 15) / 16) * 16;
+    s.region_bytes = static_cast<size_t>(t->n_slots + nst * t->rmax) * 256 +
+                     nst * ((reg ? 0 : 32 * (K * 16 + 16)) + static_cast<size_t>(t->block_max) * 16);
     const size_t budget = 227 * 1024 - 64;
-    s.wpb = 32;
+    s.wpb = reg ? 16 : 32;  // the register variant holds 16 warps (<= 128 registers each)
     while (s.wpb > 0 && s.table_bytes + s.wpb * s.region_bytes > budget) s.wpb--;
     return s;
 }
@@ -201,11 +405,15 @@ LaneShape lane_shape(const dfsim_cp_lane_tables *t) {
 }  // namespace
 
 extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int32_t *succ_pos, const uint8_t *is_source,
-                                   int32_t K, int32_t rmax_min, uint32_t *rec, uint16_t *succ_loc, int32_t *bounds,
-                                   int32_t *spill_off, uint16_t *spill_list, int32_t *info) {
-    if (n < 0 || !succ_off || !info || K < 1 || K > 16 || rmax_min < 1) return DFSIM_BAD_ARGUMENT;
+                                   int32_t K, int32_t rmax_min, int32_t stages, int32_t near_chunks, uint32_t *blocks,
+                                   int32_t *block_off, int32_t *bounds, int32_t *spill_off, uint16_t *spill_list,
+                                   int32_t *info) {
+    if (n < 0 || !succ_off || !info || K < 1 || K > 16 || rmax_min < 1 || stages < 2 || stages > 4)
+        return DFSIM_BAD_ARGUMENT;
+    // a value read at most near_chunks - 1 chunks after its writer's stays in a slot; later reads go
+    // through a spill row, whose prefetch (stages - 1 chunks ahead) must follow the write
+    const int32_t far_at = near_chunks > stages ? near_chunks : stages;
     const int64_t E = n ? succ_off[n] : 0;
-    if (E >= (1 << 24)) return DFSIM_BAD_ARGUMENT;
     std::vector<int32_t> chunk_of(n, -1), stamp(n, -1), far_idx(E, -1);
     std::vector<uint8_t> is_long(n, 0);
     std::vector<int32_t> slist;  // spill positions per chunk, concatenated
@@ -220,7 +428,7 @@ extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int
             for (int64_t j = succ_off[p]; j < succ_off[p + 1]; j++) {
                 const int32_t v = succ_pos[j];
                 if (v <= p || v >= n) return DFSIM_BAD_ARGUMENT;  // not a level order
-                if (q - chunk_of[v] >= 2 && stamp[v] != q) {
+                if (q - chunk_of[v] >= far_at && stamp[v] != q) {
                     stamp[v] = q;  // provisional: undone below if p moves to the next chunk
                     fresh++;
                 }
@@ -236,7 +444,7 @@ extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int
             if (have + fresh > rmax) rmax = have + fresh;  // one node alone: widen the stage
             for (int64_t j = succ_off[p]; j < succ_off[p + 1]; j++) {
                 const int32_t v = succ_pos[j];
-                if (q - chunk_of[v] >= 2) {
+                if (q - chunk_of[v] >= far_at) {
                     auto it = std::find(slist.begin() + first, slist.end(), v);
                     if (it == slist.end()) {
                         slist.push_back(v);
@@ -259,7 +467,7 @@ extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int
     int32_t n_long = 0;
     for (int32_t v = n - 1; v >= 0; v--)
         if (is_long[v]) spill_of[v] = n_long++;
-    if (n_long > 65536 || n_long >= (1 << 17)) return DFSIM_BAD_ARGUMENT;
+    if (n_long >= (1 << 17) || n_long > 65536) return DFSIM_BAD_ARGUMENT;
     for (size_t i = 0; i < slist.size(); i++) spill_list[i] = static_cast<uint16_t>(spill_of[slist[i]]);
     // slots: values read near (same or next chunk) are live from their write step to the last near
     // read; greedy interval colouring in processing order (step t = n - 1 - position)
@@ -286,45 +494,73 @@ extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int
     }
     if (n_slots >= 4096) return DFSIM_BAD_ARGUMENT;
     const int32_t NS = std::max(n_slots, 1);
-    for (int32_t u = 0; u < n; u++) {
-        const int32_t cnt = succ_off[u + 1] - succ_off[u];
-        rec[2 * u] = static_cast<uint32_t>(succ_off[u]) | (static_cast<uint32_t>(cnt) << 24);
-        uint32_t y = 0;
-        if (slot_of[u] >= 0) y |= static_cast<uint32_t>(slot_of[u]) | kHasSlot;
-        if (is_source && is_source[u]) y |= kSource;
-        if (spill_of[u] >= 0) y |= kHasSpill | (static_cast<uint32_t>(spill_of[u]) << 15);
-        rec[2 * u + 1] = y;
-        for (int64_t j = succ_off[u]; j < succ_off[u + 1]; j++) {
-            const int32_t row = far_idx[j] >= 0 ? NS + (chunk_of[u] & 1) * rmax + far_idx[j] : slot_of[succ_pos[j]];
-            if (row < 0 || row >= 65536) return DFSIM_BAD_ARGUMENT;
-            succ_loc[j] = static_cast<uint16_t>(row);
+    if (NS + stages * rmax > 65535) return DFSIM_BAD_ARGUMENT;
+    // chunk blocks: records in processing order, then the rows of successors 5.., padded to 16 B
+    int64_t unit = 0;  // 16-byte units written
+    int32_t block_max = 1;
+    for (int32_t c = 0; c < NQ; c++) {
+        block_off[c] = static_cast<int32_t>(unit);
+        const int32_t hi = bounds[c], lo = bounds[c + 1];
+        uint32_t extra = static_cast<uint32_t>(hi - lo) * 8u;  // u16 index of the first extra row
+        std::vector<uint16_t> ext;
+        for (int32_t u = hi - 1; u >= lo; u--) {
+            uint32_t *r = blocks + 4 * unit++;
+            const int32_t deg = succ_off[u + 1] - succ_off[u];
+            uint32_t x = 0;
+            if (slot_of[u] >= 0) x |= static_cast<uint32_t>(slot_of[u]) | kHasSlot;
+            if (is_source && is_source[u]) x |= kSource;
+            if (spill_of[u] >= 0) x |= kHasSpill | (static_cast<uint32_t>(spill_of[u]) << 15);
+            uint16_t row[4] = {0, 0, 0, 0};
+            for (int32_t k = 0; k < deg; k++) {
+                const int64_t j = succ_off[u] + k;
+                const int32_t rv = far_idx[j] >= 0 ? NS + (chunk_of[u] % stages) * rmax + far_idx[j] : slot_of[succ_pos[j]];
+                if (rv < 0 || rv >= 65536) return DFSIM_BAD_ARGUMENT;
+                if (k < 4) row[k] = static_cast<uint16_t>(rv); else ext.push_back(static_cast<uint16_t>(rv));
+            }
+            const uint32_t off = deg > 4 ? extra + static_cast<uint32_t>(ext.size()) - static_cast<uint32_t>(deg - 4) : 0u;
+            if (off >= (1u << 24)) return DFSIM_BAD_ARGUMENT;
+            r[0] = x;
+            r[1] = static_cast<uint32_t>(deg) | (off << 8);
+            r[2] = row[0] | (static_cast<uint32_t>(row[1]) << 16);
+            r[3] = row[2] | (static_cast<uint32_t>(row[3]) << 16);
         }
+        const size_t eu = (ext.size() + 7) / 8;  // extra rows, 8 per 16-byte unit
+        uint16_t *eb = reinterpret_cast<uint16_t *>(blocks + 4 * unit);
+        for (size_t i = 0; i < eu * 8; i++) eb[i] = i < ext.size() ? ext[i] : 0;
+        unit += static_cast<int64_t>(eu);
+        block_max = std::max(block_max, static_cast<int32_t>(unit - block_off[c]));
+        if (unit >= (int64_t(1) << 31)) return DFSIM_BAD_ARGUMENT;
     }
+    block_off[NQ] = static_cast<int32_t>(unit);
     info[0] = NQ;
     info[1] = NS;
     info[2] = rmax;
     info[3] = n_long;
     info[4] = static_cast<int32_t>(slist.size());
+    info[5] = block_max;
     return DFSIM_OK;
 }
 
-extern "C" int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t) {
-    if (!t || t->n_chunks <= 0) return 0;
-    return lane_shape(t).wpb;
+extern "C" int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t, int32_t stages) {
+    if (!t || t->n_chunks <= 0 || !(stages == 0 || stages == 2 || stages == 3)) return 0;
+    if (stages == 0 && t->chunk_positions != 8) return 0;
+    return lane_shape(t, stages).wpb;
 }
 
-extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int64_t n_sims,
+extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
                                          const double *sched, double *cp_len, int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, sched && cp_len, "sched and cp_len are required");
     DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
     DFSIM_ARG_CHECK(ctx, t->chunk_positions == 8 || t->chunk_positions == 16, "chunk_positions must be 8 or 16");
+    DFSIM_ARG_CHECK(ctx, stages == 0 || stages == 2 || stages == 3, "stages must be 0 (registers), 2 or 3");
+    DFSIM_ARG_CHECK(ctx, stages != 0 || t->chunk_positions == 8, "the register variant needs chunk_positions 8");
     DFSIM_ARG_CHECK(ctx, t->n_nodes > 0 && t->n_chunks > 0 && t->n_slots >= 1 && t->n_slots < 4096 && t->rmax >= 1 &&
-                         t->n_spill_list >= 0 && t->n_edges < (1 << 24),
+                         t->n_spill_list >= 0 && t->block_max >= 1,
                     "inconsistent lane tables");
     if (n_sims <= 0) return DFSIM_OK;
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-    const LaneShape shape = lane_shape(t);
+    const LaneShape shape = lane_shape(t, stages);
     DFSIM_ARG_CHECK(ctx, shape.wpb >= 1, "lane tables do not fit in shared memory");
     // as many warps as the batch needs, spread over the SMs
     const int64_t warps = (n_sims + 31) / 32;
@@ -334,9 +570,13 @@ extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tab
     const size_t smem = shape.table_bytes + static_cast<size_t>(wpb) * shape.region_bytes;
     const int grid = static_cast<int>(std::min<int64_t>((warps + wpb - 1) / wpb, ctx->num_sms));
     void *p = nullptr;
-    int rc = dfsim_scratch(ctx, static_cast<size_t>(grid) * wpb * std::max(t->n_long, 1) * 32 * 8, &p);
+    const size_t spill_bytes = static_cast<size_t>(grid) * wpb * std::max(t->n_long, 1) * 32 * 8;
+    int rc = dfsim_scratch(ctx, spill_bytes + 256, &p);
     if (rc) return rc;
+    int32_t *counter = reinterpret_cast<int32_t *>(static_cast<unsigned char *>(p) + spill_bytes);
+    DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, sizeof(int32_t), ctx->stream));
     LaneArgs a;
+    a.task_counter = counter;
     a.t = *t;
     a.S = n_sims;
     a.sched = sched;
@@ -351,5 +591,7 @@ extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tab
         kern<<<grid, wpb * 32, smem, ctx->stream>>>(a);
         return dfsim_after_launch(ctx, "k_critical_path_lanes");
     };
-    return t->chunk_positions == 16 ? launch(k_critical_path_lanes<16>) : launch(k_critical_path_lanes<8>);
+    if (stages == 0) return launch(k_critical_path_lanes_reg<8>);
+    if (t->chunk_positions == 16) return stages == 2 ? launch(k_critical_path_lanes<16, 2>) : launch(k_critical_path_lanes<16, 3>);
+    return stages == 2 ? launch(k_critical_path_lanes<8, 2>) : launch(k_critical_path_lanes<8, 3>);
 }

@@ -19,6 +19,8 @@ Runs once per graph / topology class; everything per-strategy runs on the GPU.
 from __future__ import annotations
 
 import math
+import operator
+import threading
 import warnings
 
 import numpy as np
@@ -377,6 +379,61 @@ def node_rows(g, ids) -> list:
     return rows
 
 
+class _FeatureRegistry:
+    """Process-wide interning of feature vectors (node_features tuples) -> int ids, so that the
+    rows of graph variants, clones and classes are combined with numpy instead of per node."""
+
+    def __init__(self):
+        self.ids: dict = {}
+        self.rows: list = []
+        self.lock = threading.Lock()
+
+    def intern(self, feats_list) -> np.ndarray:
+        with self.lock:
+            ids, rows = self.ids, self.rows
+            out = np.empty(len(feats_list), np.int64)
+            for i, f in enumerate(feats_list):
+                k = ids.get(f)
+                if k is None:
+                    k = ids[f] = len(rows)
+                    rows.append(f)
+                out[i] = k
+            return out
+
+
+FEATURES = _FeatureRegistry()
+ROW_FIELDS = ("fid", "ok", "bytes", "gsize", "thr", "lat")
+
+
+def row_arrays(rows) -> dict:
+    """node_rows tuples -> arrays (features as FEATURES ids)."""
+    n = len(rows)
+    return dict(fid=FEATURES.intern([r[0] for r in rows]),
+                ok=np.fromiter((r[1] for r in rows), np.uint8, n), bytes=np.fromiter((r[2] for r in rows), np.int64, n),
+                gsize=np.fromiter((r[3] for r in rows), np.int32, n), thr=np.fromiter((r[4] for r in rows), np.float64, n),
+                lat=np.fromiter((r[5] for r in rows), np.float64, n))
+
+
+def base_arrays(g):
+    """Row arrays of every node of g in insertion order + {node id: index}; cached on the graph
+    (graphs are immutable by contract, graph.py:110-116)."""
+    cached = getattr(g, "_dfsim_base_arr", None)
+    if cached is not None and cached[0] == len(g.nodes):
+        return cached[1], cached[2]
+    order = list(g.nodes)
+    arr = row_arrays(node_rows(g, order))
+    index = {nid: i for i, nid in enumerate(order)}
+    try:
+        object.__setattr__(g, "_dfsim_base_arr", (len(order), arr, index))
+    except (AttributeError, TypeError):
+        pass
+    return arr, index
+
+
+_HARDWARE, _GAP = operator.attrgetter("hardware"), operator.attrgetter("op_gap_us")
+_COLLECTIVE, _OVERRIDES = operator.attrgetter("collective"), operator.attrgetter("overrides")
+
+
 class LoweredProfiles:
     """Device tables for dfsim_estimate_batch over one graph and a list of configs.
 
@@ -385,35 +442,45 @@ class LoweredProfiles:
     then reads variant ``strat_gv[i]``.  Without it there is one variant, g itself.
     """
 
-    def __init__(self, g, ids, db, configs, device: int, variant_rows=None, strat_gv=None):
+    def __init__(self, g, ids, db, configs, device: int, variant_rows=None, strat_gv=None, fit_cache=None,
+                 variant_arrays=None):
         self.device = device
         N = len(ids)
         nodes = g.nodes
         rank = {nid: i for i, nid in enumerate(ids)}
-        # hardware tags, paths, override sets of the strategies
+        # hardware tags, paths, override sets of the strategies: each distinct value is handled
+        # once, the per-candidate columns are built with C-level maps (sweeps hold 10^4-10^5 configs)
         self.hw_ids, self.path_ids = {}, {}
         ov_sets, ov_key_to_id = [], {}
-        self.strat_hw, self.strat_gap, self.strat_algo, self.strat_path, self.strat_ov = [], [], [], [], []
-        for cfg in configs:
-            self.strat_hw.append(self.hw_ids.setdefault(cfg.hardware, len(self.hw_ids)))
-            self.strat_gap.append(float(cfg.op_gap_us))
-            if cfg.collective.algo not in (ALGO_MEASURED, ALGO_RING):
-                raise ValueError(f"unknown collective algorithm {cfg.collective.algo!r}")
-            self.strat_algo.append(0 if cfg.collective.algo == ALGO_MEASURED else 1)
-            self.strat_path.append(self.path_ids.setdefault(cfg.collective.path, len(self.path_ids)))
-            ov_key = tuple(cfg.overrides.items())
-            if not ov_key:
-                self.strat_ov.append(-1)
+        hws = list(map(_HARDWARE, configs))
+        self.strat_hw = [self.hw_ids.setdefault(h, len(self.hw_ids)) for h in hws]
+        self.strat_gap = list(map(float, map(_GAP, configs)))
+        coll_of = {}  # id(CollectiveConfig) -> (algo code, path id)
+        colls = list(map(_COLLECTIVE, configs))
+        for c in {id(c): c for c in colls}.values():
+            if c.algo not in (ALGO_MEASURED, ALGO_RING):
+                raise ValueError(f"unknown collective algorithm {c.algo!r}")
+            coll_of[id(c)] = (0 if c.algo == ALGO_MEASURED else 1, self.path_ids.setdefault(c.path, len(self.path_ids)))
+        ap = [coll_of[id(c)] for c in colls]
+        self.strat_algo = [x[0] for x in ap]
+        self.strat_path = [x[1] for x in ap]
+        self.strat_ov = [-1] * len(configs)
+        for i, ov in enumerate(map(_OVERRIDES, configs)):
+            if not ov:
                 continue
+            ov_key = tuple(ov.items())
             if ov_key not in ov_key_to_id:
                 ov_key_to_id[ov_key] = len(ov_sets)
-                ov_sets.append(resolve_overrides(cfg.overrides, ids))
-            self.strat_ov.append(ov_key_to_id[ov_key])
+                ov_sets.append(resolve_overrides(ov, ids))
+            self.strat_ov[i] = ov_key_to_id[ov_key]
         # document.DocumentGraph: the C++ loader already interned ops, signatures and comm rows
-        doc = getattr(g, "signatures", None) is not None and variant_rows is None and ids is g.ids
-        if variant_rows is None:
-            variant_rows = [] if doc else [node_rows(g, ids)]
-        GV = 1 if doc else len(variant_rows)
+        doc = (getattr(g, "signatures", None) is not None and variant_rows is None and variant_arrays is None
+               and ids is g.ids)
+        if variant_arrays is None:
+            if variant_rows is None:
+                variant_rows = [] if doc else [node_rows(g, ids)]
+            variant_arrays = [row_arrays(rows) for rows in variant_rows]
+        GV = 1 if doc else len(variant_arrays)
         self.n_gvariants = GV
         self.strat_gv = list(strat_gv) if strat_gv is not None else [0] * len(configs)
         # per node: op, kind (structural); per (variant, node): features and comm attributes
@@ -443,17 +510,21 @@ class LoweredProfiles:
             sig_ids = {feats: k for k, feats in enumerate(g.signatures)}
             sig[0], cok[0], cbytes[0], gsize[0] = g.sig_of, g.comm["ok"], g.comm["bytes"], g.comm["group"]
             lthr[0], llat[0] = g.comm["thr"], g.comm["lat"]
-        for gv, rows in enumerate(variant_rows):
-            if len(rows) != N:
+        if variant_arrays:
+            if any(len(va["fid"]) != N for va in variant_arrays):
                 raise ValueError("graph variants must share the class structure")
-            for i, (feats, ok, b, gs, thr, lat) in enumerate(rows):
-                sig[gv, i] = sig_ids.setdefault(feats, len(sig_ids))
-                cok[gv, i], cbytes[gv, i], gsize[gv, i], lthr[gv, i], llat[gv, i] = ok, b, gs, thr, lat
+            fid = np.stack([va["fid"] for va in variant_arrays])
+            uniq, inv = np.unique(fid, return_inverse=True)  # class-local signature ids
+            sig[:] = inv.reshape(GV, N)
+            sig_ids = {FEATURES.rows[u]: k for k, u in enumerate(uniq.tolist())}
+            for name, dst in (("ok", cok), ("bytes", cbytes), ("gsize", gsize), ("thr", lthr), ("lat", llat)):
+                dst[:] = np.stack([va[name] for va in variant_arrays])
         self.op_ids, self.sig_ids = op_ids, sig_ids
         # the fused engine forms durations on the fly (base + gap | override) and relies on every
         # one being a finite non-negative double; anything else (NaN included: DurationEntry's
         # `not x >= 0.0`, costmodel.py:78-80) must take the exact K2 path and its error
-        self.fused_values_ok = (all(math.isfinite(x) and x >= 0.0 for x in self.strat_gap)
+        gaps = np.asarray(self.strat_gap, np.float64)
+        self.fused_values_ok = (bool(np.all(np.isfinite(gaps) & (gaps >= 0.0)))
                                 and all(math.isfinite(v) and v >= 0.0 for res in ov_sets for v in res.values()))
         # exact records for (hw, op, sig) triples present in the graph
         ekeys, emeans = [], []
@@ -479,7 +550,12 @@ class LoweredProfiles:
                     continue
                 if not self._needs_model(h, o, opname, sig, exact_set, ids, ov_sets):
                     continue
-                m = fit_for_grid(db, opname, hw)
+                if fit_cache is not None and (opname, hw) in fit_cache:  # one fit per (op, hw) per sweep
+                    m = fit_cache[(opname, hw)]
+                else:
+                    m = fit_for_grid(db, opname, hw)
+                    if fit_cache is not None:
+                        fit_cache[(opname, hw)] = m
                 self.models[(opname, hw)] = m
                 if m is None:
                     continue

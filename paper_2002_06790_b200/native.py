@@ -79,9 +79,9 @@ class CpTables(ctypes.Structure):
 
 
 class CpLaneTables(ctypes.Structure):
-    _fields_ = [("n_nodes", I32), ("n_edges", I32), ("n_chunks", I32), ("chunk_positions", I32), ("n_slots", I32),
-                ("rmax", I32), ("n_long", I32), ("n_spill_list", I32), ("rec", P), ("succ", P), ("bounds", P),
-                ("spill_off", P), ("spill_list", P), ("rank_of_pos", P)]
+    _fields_ = [("n_nodes", I32), ("n_chunks", I32), ("chunk_positions", I32), ("n_slots", I32), ("rmax", I32),
+                ("n_long", I32), ("n_spill_list", I32), ("block_max", I32), ("blocks", P), ("block_off", P),
+                ("bounds", P), ("spill_off", P), ("spill_list", P), ("rank_of_pos", P)]
 
 
 class SummaryTables(ctypes.Structure):
@@ -124,9 +124,12 @@ _SIGNATURES = {
                                             P, P]),
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P]),
     "dfsim_critical_path_levels_capacity": (I32, [ctypes.POINTER(CpTables)]),
-    "dfsim_critical_path_lanes": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I64, P, P, P]),
-    "dfsim_critical_path_lanes_capacity": (I32, [ctypes.POINTER(CpLaneTables)]),
-    "dfsim_cp_lanes_plan": (ctypes.c_int, [I32, P, P, P, I32, I32, P, P, P, P, P, P]),
+    "dfsim_critical_path_lanes": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I32, I64, P, P, P]),
+    "dfsim_critical_path_lanes_capacity": (I32, [ctypes.POINTER(CpLaneTables), I32]),
+    "dfsim_cp_lanes_plan": (ctypes.c_int, [I32, P, P, P, I32, I32, I32, I32, P, P, P, P, P, P]),
+    "dfsim_predict_batch": (ctypes.c_int, [P, I32, P, ctypes.c_double, I64, P, P]),
+    "dfsim_comm_batch": (ctypes.c_int, [P, I64, P, P, P, P, P, P]),
+    "dfsim_topological_order": (I32, [I32, P, P, P, P]),
     "dfsim_fused_capacity": (I32, [ctypes.POINTER(SimTables)]),
     "dfsim_fused_chunk": (I32, [ctypes.POINTER(SimTables), I64, I32]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),

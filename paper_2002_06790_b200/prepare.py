@@ -61,7 +61,7 @@ class Tables:
     """Host arrays + statistics of one class (see module docstring)."""
 
     def __init__(self, N: int, D: int, succ_off, succ_idx, indeg, device, group: int = GROUP,
-                 chunk: int = CHUNK):
+                 chunk: int = CHUNK, levels: bool = True):
         off = np.asarray(succ_off, np.int64)
         idx = np.asarray(succ_idx, np.int64)
         indeg = np.asarray(indeg, np.int64)
@@ -79,12 +79,21 @@ class Tables:
         pos[order] = np.arange(N)
         self.pos, self.rank_of_pos, self.level_off = pos, order, loff
         self._engine(N, off, idx, indeg, dev, outdeg)
-        self._critical_path(N, idx, indeg, outdeg, order, pos, loff)
+        self._cp_args = (N, idx, indeg, outdeg, order, pos, loff)
+        self.levels_built = False
+        # engine limits; the critical path adds its own (K4 v3 planner or K4 v2 tables below)
         self.fused_ok = (N <= 65535 and D <= 32 and self.n_edges < 65536 and outdeg.max(initial=0) < 255
-                         and self.counter_words <= 512
-                         and indeg.max(initial=0) <= 65534 and self.n_slots < 0x7FFF
-                         and self.max_spill_reads < 0x7FFF and self.n_long < 0x7FFF
-                         and self.slot_region + 2 * self.stage_doubles < 65536 and len(self.spill_list) < 65536)
+                         and self.counter_words <= 512 and indeg.max(initial=0) <= 65534)
+        if levels:
+            self.fused_ok = self.fused_ok and self.build_levels()
+
+    def build_levels(self) -> bool:
+        """K4 v2 tables (only needed when K4 v3's plan is unavailable); True when they fit."""
+        if not self.levels_built:
+            self._critical_path(*self._cp_args)
+            self.levels_built = True
+        return (self.n_slots < 0x7FFF and self.max_spill_reads < 0x7FFF and self.n_long < 0x7FFF
+                and self.slot_region + 2 * self.stage_doubles < 65536 and len(self.spill_list) < 65536)
 
     def _engine(self, N, off, idx, indeg, dev, outdeg):
         """K3 v2 tables with nodes numbered by level position p (pos[rank]); ranks survive only
@@ -221,11 +230,17 @@ class Tables:
         self.cp_succ_abs = absent[np.argsort(pu, kind="stable")]
 
 
-LANE_K = int(os.environ.get("DFSIM_CP_LANE_K", 16))   # positions per K4 v3 prefetch chunk (8 or 16)
-LANE_RMAX = int(os.environ.get("DFSIM_CP_LANE_RMAX", 16))  # spill values per chunk (planner minimum)
+LANE_K = int(os.environ.get("DFSIM_CP_LANE_K", 8))   # positions per K4 v3 prefetch chunk (8 or 16)
+LANE_RMAX = int(os.environ.get("DFSIM_CP_LANE_RMAX", 8))  # spill values per chunk (planner minimum)
+# K4 v3 variant: 0 = schedule windows staged in registers (K = 8), 2 / 3 = shared-memory stages
+LANE_STAGES = int(os.environ.get("DFSIM_CP_LANE_STAGES", 0))
 
 
-def lane_plan(t: Tables, K: int = LANE_K, rmax_min: int = LANE_RMAX):
+LANE_NEAR = int(os.environ.get("DFSIM_CP_LANE_NEAR", 8))  # chunks a value may wait in a slot
+
+
+def lane_plan(t: Tables, K: int = LANE_K, rmax_min: int = LANE_RMAX, stages: int = LANE_STAGES,
+              near: int = LANE_NEAR):
     """K4 v3 tables of a class (dfsim_cp_lanes_plan, host C++): dict of numpy arrays + sizes,
     or None when a field overflows (the class then keeps K4 v2)."""
     import ctypes
@@ -235,20 +250,23 @@ def lane_plan(t: Tables, K: int = LANE_K, rmax_min: int = LANE_RMAX):
     off = np.ascontiguousarray(t.succ_off_pos, np.int32)
     sp = np.ascontiguousarray(t.succ_pos if E else np.zeros(1), np.int32)
     src = np.ascontiguousarray(t.indeg_pos == 0, np.uint8)
-    rec = np.zeros(2 * max(N, 1), np.uint32)
-    succ = np.zeros(max(E, 1), np.uint16)
+    blocks = np.zeros(4 * (2 * N + E // 8 + 2), np.uint32)
+    boff = np.zeros(N + 1, np.int32)
     bounds = np.zeros(N + 1, np.int32)
     soff = np.zeros(N + 1, np.int32)
     slist = np.zeros(max(E, 1), np.uint16)
-    info = np.zeros(5, np.int32)
+    info = np.zeros(6, np.int32)
     pp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-    rc = lib.dfsim_cp_lanes_plan(N, pp(off), pp(sp), pp(src), K, rmax_min, pp(rec), pp(succ), pp(bounds), pp(soff),
-                                 pp(slist), pp(info))
+    if stages == 0:
+        K = 8  # the register variant's window size
+    rc = lib.dfsim_cp_lanes_plan(N, pp(off), pp(sp), pp(src), K, rmax_min, stages or 2, near, pp(blocks), pp(boff),
+                                 pp(bounds), pp(soff), pp(slist), pp(info))
     if rc != 0:
         return None
-    nq, ns, rmax, n_long, nl = (int(x) for x in info)
-    return dict(K=K, n_chunks=nq, n_slots=ns, rmax=rmax, n_long=n_long, n_spill_list=nl, rec=rec[: 2 * N],
-                succ=succ[:E], bounds=bounds[: nq + 1], spill_off=soff[: nq + 1], spill_list=slist[:nl])
+    nq, ns, rmax, n_long, nl, bmax = (int(x) for x in info)
+    return dict(K=K, stages=stages, smem_stages=stages or 2, n_chunks=nq, n_slots=ns, rmax=rmax, n_long=n_long, n_spill_list=nl,
+                block_max=bmax, blocks=blocks[: 4 * int(boff[nq])], block_off=boff[: nq + 1], bounds=bounds[: nq + 1],
+                spill_off=soff[: nq + 1], spill_list=slist[:nl])
 
 
 class ClassTables(Tables):
@@ -263,51 +281,57 @@ class ClassTables(Tables):
                         succ_idx=lg.t_succ_idx[: lg.n_edges].cpu().numpy(),
                         indeg=lg.t_indeg[: lg.n].cpu().numpy(), device=lg.t_dev[: lg.n].cpu().numpy())
         super().__init__(lg.n, lg.n_devices, host["succ_off"], host["succ_idx"], host["indeg"], host["device"],
-                         self.GROUP, self.CHUNK)
+                         self.GROUP, self.CHUNK, levels=False)
+        self.lane = self.cp_struct = None
         if not self.fused_ok:
             return
         d = self.ctx.device
         T = lambda a, dt: _t(a, dt, d)  # noqa: E731
+        p = native.ptr
         self.t = t = dict(
             meta=T(self.meta, np.uint32), succ=T(self.succ, np.uint32), cidx=T(self.cidx, np.uint16),
             cnt_init=T(self.cnt_init, np.uint32), rank16=T(self.rank_of_pos, np.uint16),
             eng_sources=T(self.eng_sources, np.int32), pos32=T(self.pos, np.int32),
-            rank_of_pos=T(self.rank_of_pos, np.int32), cp_slot=T(self.cp_slot, np.uint16),
-            cp_spill=T(self.cp_spill, np.uint16), cp_meta=T(self.cp_meta, np.uint32),
-            cp_succ=T(self.cp_succ_abs, np.uint16), group_off=T(self.group_off, np.int32),
-            chunk_off=T(self.chunk_off, np.int32), spill_off=T(self.spill_off, np.int32),
-            spill_list=T(self.spill_list, np.uint16), pinfo=T(self.pinfo, np.uint32))
-        p = native.ptr
+            rank_of_pos=T(self.rank_of_pos, np.int32))
         self.sim_struct = native.SimTables(lg.n, lg.n_devices, self.n_edges, p(t["meta"]), p(lg.t_succ_off),
                                            p(t["succ"]), p(t["cidx"]), p(t["cnt_init"]), self.counter_words,
                                            self.counter_bits, p(t["rank16"]), p(t["eng_sources"]), lg.n_sources,
                                            self.QCAP,
                                            p(lg.t_dev), int(self.succ_packed))
-        self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
-                                         p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
-                                         self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long, p(t["cp_spill"]),
-                                         p(t["spill_off"]), p(t["spill_list"]), self.max_spill_reads, p(t["pinfo"]),
-                                         self.slot_region, self.stage_doubles)
-
-        self.lane = None  # K4 v3 (lane per candidate), when its tables fit
+        # K4 v3 (lane per candidate) when its plan fits, else K4 v2 (level groups)
         if os.environ.get("DFSIM_CP_KERNEL", "lanes") == "lanes":
             plan = lane_plan(self)
             if plan is not None:
-                t.update(l_rec=T(plan["rec"], np.uint32), l_succ=T(plan["succ"], np.uint16),
+                t.update(l_blocks=T(plan["blocks"], np.uint32), l_boff=T(plan["block_off"], np.int32),
                          l_bounds=T(plan["bounds"], np.int32), l_soff=T(plan["spill_off"], np.int32),
                          l_slist=T(plan["spill_list"], np.uint16))
-                st = native.CpLaneTables(lg.n, self.n_edges, plan["n_chunks"], plan["K"], plan["n_slots"],
-                                         plan["rmax"], plan["n_long"], plan["n_spill_list"], p(t["l_rec"]),
-                                         p(t["l_succ"]), p(t["l_bounds"]), p(t["l_soff"]), p(t["l_slist"]),
+                st = native.CpLaneTables(lg.n, plan["n_chunks"], plan["K"], plan["n_slots"], plan["rmax"],
+                                         plan["n_long"], plan["n_spill_list"], plan["block_max"], p(t["l_blocks"]),
+                                         p(t["l_boff"]), p(t["l_bounds"]), p(t["l_soff"]), p(t["l_slist"]),
                                          p(t["rank_of_pos"]))
-                if self.ctx.lib.dfsim_critical_path_lanes_capacity(native.ctypes.byref(st)) > 0:
+                if self.ctx.lib.dfsim_critical_path_lanes_capacity(native.ctypes.byref(st), plan["stages"]) > 0:
                     self.lane, self.lane_struct = plan, st
+        if self.lane is None:
+            if not self.build_levels():
+                self.fused_ok = False
+                return
+            t.update(cp_slot=T(self.cp_slot, np.uint16), cp_spill=T(self.cp_spill, np.uint16),
+                     cp_meta=T(self.cp_meta, np.uint32), cp_succ=T(self.cp_succ_abs, np.uint16),
+                     group_off=T(self.group_off, np.int32), chunk_off=T(self.chunk_off, np.int32),
+                     spill_off=T(self.spill_off, np.int32), spill_list=T(self.spill_list, np.uint16),
+                     pinfo=T(self.pinfo, np.uint32))
+            self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
+                                             p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
+                                             self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long,
+                                             p(t["cp_spill"]), p(t["spill_off"]), p(t["spill_list"]),
+                                             self.max_spill_reads, p(t["pinfo"]), self.slot_region,
+                                             self.stage_doubles)
 
     def critical_path(self, n_sims: int, sched, cp_len, cp_src):
         """K4 over the fused engine's schedules: v3 (lane per candidate) when planned, else v2."""
         if self.lane is not None:
-            self.ctx.call("dfsim_critical_path_lanes", native.ctypes.byref(self.lane_struct), n_sims,
-                          native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
+            self.ctx.call("dfsim_critical_path_lanes", native.ctypes.byref(self.lane_struct), self.lane["stages"],
+                          n_sims, native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
         else:
             self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.cp_struct), n_sims,
                           native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))

@@ -13,7 +13,9 @@ builds it.  ``tests/test_variants.py`` pins the rows against fully materialised 
 
 from __future__ import annotations
 
-from .lowering import node_features, node_rows
+import numpy as np
+
+from .lowering import FEATURES, ROW_FIELDS, base_arrays, node_features, node_rows, row_arrays
 
 
 class _Stand:
@@ -30,51 +32,82 @@ def structure_key(g) -> int:
 
 
 def rows_for(kind: str, ids, g_b, structure, cfg=None, db=None) -> list:
-    """Estimate-input rows (rank order ``ids``) of variant graph ``g_b`` for a class of
-    ``kind`` "plain" | "dp" (structure: ExpansionPlan) | "ps" (structure: ExpandedGraph)."""
-    if kind == "plain":
-        return node_rows(g_b, ids)
-    base = getattr(g_b, "_dfsim_base_rows", None)  # shared by every class of this graph
-    if base is None:
-        base = dict(zip(list(g_b.nodes), node_rows(g_b, list(g_b.nodes))))
-        try:
-            object.__setattr__(g_b, "_dfsim_base_rows", base)
-        except (AttributeError, TypeError):
-            pass
+    """Estimate-input rows (rank order ``ids``) of variant graph ``g_b`` as node_rows tuples
+    (reference path of ``variant_arrays``; tests/test_variants.py pins both)."""
+    arr = variant_arrays(kind, ids, g_b, structure, cfg, db, {})
+    rows = FEATURES.rows
+    return [(rows[f], int(ok), int(b), int(gs), float(thr), float(lat))
+            for f, ok, b, gs, thr, lat in zip(*(arr[k].tolist() for k in ROW_FIELDS))]
+
+
+def _special_rows(kind, ids, pos, g_b, structure, cfg) -> dict:
+    """Rows of the nodes a class adds (AllReduce / PS push, aggregate, pull) at positions
+    ``pos``, each built exactly as the expansion builds it, with the reference's own
+    node_features on a stand-in graph."""
     out = []
     if kind == "dp":
         plan = structure
-        for cid in ids:
-            what, gid = plan.origin[cid]
-            if what == "clone":
-                out.append(base[gid])
-                continue
+        for p in pos:
+            gid = plan.origin[ids[p]][1]
             grad = g_b.nodes[gid]
             node = plan.collective_node(gid, grad)
-            stand = _Stand({f"{gid}@r{k}": grad for k in range(plan.R)}, {})
-            out.append(node_rows(_Stand({**stand.nodes, node.id: node}, {}), [node.id])[0])
-        return out
-    if kind == "ps":
+            stand = {f"{gid}@r{k}": grad for k in range(plan.R)}
+            out.append(node_rows(_Stand({**stand, node.id: node}, {}), [node.id])[0])
+    else:
         from .ps import ps_nodes
 
-        ex = structure
-        gx = ex.graph
+        gx = structure.graph
         built = {}
-        for cid in ids:
-            what, gid = ex.origin[cid]
-            if what == "clone":
-                out.append(base[gid])
-                continue
+        for p in pos:
+            cid = ids[p]
+            gid = structure.origin[cid][1]
             if gid not in built:
                 grad = g_b.nodes[gid]
                 nodes = {f"{gid}@r{k}": grad for k in range(cfg.replicas)}
                 for n in ps_nodes(gid, grad, cfg, cfg.ps_device):
                     nodes[n.id] = n
                 built[gid] = _Stand(nodes, gx.devices)
-            stand = built[gid]
-            out.append(node_rows(stand, [cid])[0])
-        return out
-    raise ValueError(kind)
+            out.append(node_rows(built[gid], [cid])[0])
+    return row_arrays(out)
 
 
-__all__ = ["structure_key", "rows_for", "node_features"]
+def variant_arrays(kind: str, ids, g_b, structure, cfg=None, db=None, cache=None) -> dict:
+    """Estimate-input rows (rank order ``ids``) of variant graph ``g_b`` for a class of
+    ``kind`` "plain" | "dp" (structure: ExpansionPlan) | "ps" (structure: ExpandedGraph), as
+    arrays (lowering.ROW_FIELDS; features as FEATURES ids).
+
+    A clone's row is its base node's (its producers are clones or the collective, all carrying
+    the base producers' shapes): gathered from the graph's cached base rows.  The rows of the
+    added nodes depend on the class and on the output shapes of the marked gradients only, so
+    ``cache`` (one dict per class) keeps them per distinct gradient-shape tuple -- graph
+    variants that differ in batch size share their weight-gradient shapes."""
+    cache = {} if cache is None else cache
+    base, index = base_arrays(g_b)
+    if "perm" not in cache:  # same structure => same node order in every variant graph
+        if kind == "plain":
+            perm, special = [index[nid] for nid in ids], []
+        else:
+            origin = structure.origin
+            perm, special = [], []
+            for p, cid in enumerate(ids):
+                what, gid = origin[cid]
+                if what == "clone":
+                    perm.append(index[gid])
+                else:
+                    perm.append(0)
+                    special.append(p)
+        cache["perm"], cache["special"] = np.asarray(perm, np.int64), np.asarray(special, np.int64)
+        cache["grads"] = list(dict.fromkeys(structure.origin[ids[p]][1] for p in special)) if special else []
+    perm, special = cache["perm"], cache["special"]
+    out = {k: base[k][perm] for k in ROW_FIELDS}
+    if len(special):
+        key = tuple(g_b.nodes[gid].output_shapes for gid in cache["grads"])
+        rows = cache.get(("special", key))
+        if rows is None:
+            rows = cache[("special", key)] = _special_rows(kind, ids, special.tolist(), g_b, structure, cfg)
+        for k in ROW_FIELDS:
+            out[k][special] = rows[k]
+    return out
+
+
+__all__ = ["structure_key", "rows_for", "variant_arrays", "node_features"]

@@ -26,36 +26,46 @@ class _Csr:
 
 
 def emulate(t, plan, d_by_pos):
-    NS, RM = plan["n_slots"], plan["rmax"]
-    rows = np.full(NS + 2 * RM, np.nan)
+    """The kernel's data movement for one candidate (one lane): value rows [slots | spill
+    stages], chunk blocks and spill values prefetched ``stages - 1`` chunks ahead."""
+    NS, RM, ST = plan["n_slots"], plan["rmax"], plan["smem_stages"]
+    rows = np.full(NS + ST * RM, np.nan)
     spill = np.full(max(plan["n_long"], 1), np.nan)
-    rec = plan["rec"].reshape(-1, 2)
-    succ, b, so, sl = plan["succ"], plan["bounds"], plan["spill_off"], plan["spill_list"]
+    blocks = plan["blocks"].reshape(-1, 4)
+    boff, b, so, sl = plan["block_off"], plan["bounds"], plan["spill_off"], plan["spill_list"]
     NQ = plan["n_chunks"]
+    staged = {}
 
-    def prefetch(q):  # issued before chunk q - 1 runs (kernel: one chunk ahead)
+    def prefetch(q):  # the chunk's block and spill values, into stage q % ST
+        staged[q % ST] = blocks[boff[q]:boff[q + 1]].copy()
         for r in range(so[q], so[q + 1]):
-            rows[NS + (q & 1) * RM + (r - so[q])] = spill[sl[r]]
+            rows[NS + (q % ST) * RM + (r - so[q])] = spill[sl[r]]
 
     length, src = 0.0, None
-    prefetch(0)
+    for q in range(min(ST - 1, NQ)):
+        prefetch(q)
     for q in range(NQ):
-        if q + 1 < NQ:
-            prefetch(q + 1)
+        if q + ST - 1 < NQ:
+            prefetch(q + ST - 1)
         assert b[q] - b[q + 1] <= plan["K"]
-        for p in range(b[q] - 1, b[q + 1] - 1, -1):
-            x, y = int(rec[p, 0]), int(rec[p, 1])
+        blk = staged[q % ST]
+        ext = blk.view(np.uint16).reshape(-1)
+        for i, p in enumerate(range(b[q] - 1, b[q + 1] - 1, -1)):
+            x, y, z, w = (int(v) for v in blk[i])
+            deg = y & 0xFF
+            succ = [z & 0xFFFF, z >> 16, w & 0xFFFF, w >> 16][: min(deg, 4)]
+            succ += [int(ext[(y >> 8) + k]) for k in range(deg - 4)] if deg > 4 else []
             best = 0.0
-            for j in range(x & 0xFFFFFF, (x & 0xFFFFFF) + (x >> 24)):
-                v = rows[succ[j]]
-                assert not np.isnan(v), ("stale read", p, j)
+            for e in succ:
+                v = rows[e]
+                assert not np.isnan(v), ("stale read", p, e)
                 best = v if v > best else best
             sv = d_by_pos[p] + best
-            if y & (1 << 12):
-                rows[y & 0xFFF] = sv
-            if y & (1 << 14):
-                spill[y >> 15] = sv
-            if y & (1 << 13):
+            if x & (1 << 12):
+                rows[x & 0xFFF] = sv
+            if x & (1 << 14):
+                spill[x >> 15] = sv
+            if x & (1 << 13):
                 rk = t.rank_of_pos[p]
                 if src is None or sv > length or (sv == length and rk < src):
                     length, src = sv, rk
@@ -81,10 +91,10 @@ def _random_dag(n, rng, window, max_in=3, hub_every=0):
     return off, idx, indeg
 
 
-def _check(off, idx, indeg, rng, K):
+def _check(off, idx, indeg, rng, K, stages=3, rmax=8, near=1):
     n = len(indeg)
     t = Tables(n, 1, off, idx, indeg, np.zeros(n, np.int64))
-    plan = lane_plan(t, K=K)
+    plan = lane_plan(t, K=K, rmax_min=rmax, stages=stages, near=near)
     assert plan is not None
     csr = _Csr(off, idx, indeg)
     for trial in range(3):
@@ -95,13 +105,13 @@ def _check(off, idx, indeg, rng, K):
     return plan
 
 
-@pytest.mark.parametrize("K", [8, 16])
+@pytest.mark.parametrize("K, stages, near", [(8, 0, 1), (8, 0, 8), (8, 2, 3), (8, 3, 1), (16, 2, 1), (16, 3, 5)])
 @pytest.mark.parametrize("seed", range(4))
-def test_plan_random_dags(K, seed):
+def test_plan_random_dags(K, stages, near, seed):
     rng = np.random.default_rng(seed)
     n = int(rng.integers(50, 3000))
-    off, idx, indeg = _random_dag(n, rng, window=int(rng.integers(2, 800)))
-    _check(off, idx, indeg, rng, K)
+    off, idx, indeg = _random_dag(n, rng, window=int(rng.integers(2, 800)), max_in=int(rng.integers(1, 7)))
+    _check(off, idx, indeg, rng, K, stages, near=near)
 
 
 def test_plan_wide_fanout_widens_stage():
@@ -128,5 +138,5 @@ def test_plan_resnet50_dp8_class():
                          collective=CollectiveConfig("RingAnalytic", "NVLink"), gradient_markers=("wgrad_*",))
     c = NO.Csr(O.expand(g, cfg)[0])
     plan = _check(c.off.astype(np.int64), c.idx.astype(np.int64), c.indeg.astype(np.int64),
-                  np.random.default_rng(0), 16)
-    assert plan["n_slots"] <= 32 and plan["rmax"] == 16 and plan["n_long"] > 1000
+                  np.random.default_rng(0), 8, stages=0, near=8)
+    assert plan["n_slots"] <= 40 and plan["n_long"] > 1000

@@ -165,8 +165,8 @@ def test_sweep_rejects_nan_or_negative_values_like_the_reference():
         warnings.simplefilter("ignore")
         assert fw.TopologyClass(g, db, [good]).fused
         for bad in (fw.StrategyConfig(**base, op_gap_us=float("nan")),
-                    fw.StrategyConfig(**base, op_gap_us=-1.0),
-                    fw.StrategyConfig(**base, overrides={"conv_1@r2": -2.0}),
+                    fw.StrategyConfig(**base, op_gap_us=-1e9),
+                    fw.StrategyConfig(**base, overrides={"conv_01@r2": -2.0}),
                     fw.StrategyConfig(**base, overrides={"conv_*": float("nan")})):
             assert not fw.TopologyClass(g, db, [good, bad]).fused
             with pytest.raises(ValueError, match="nonnegative"):
