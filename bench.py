@@ -382,9 +382,13 @@ def cpu_baseline(sample: int | None = None, workers: int | None = None, target_s
 
 
 def b_table_bytes(lp) -> int:
-    keys = ("soff", "sname", "sval", "ek", "em", "mk", "moff", "mname", "mcoef", "micpt", "nk", "nt", "uok", "uthr",
-            "ulat")
-    return int(sum(lp.tensors[k].numel() * lp.tensors[k].element_size() for k in keys))
+    """B_table of one candidate: the staged (op, hw) models, exact records and
+    link rows, plus the feature vectors of ONE graph variant (a class holding GV graph variants,
+    e.g. one per batch size in C3, stores GV variants' vectors; a candidate reads its own)."""
+    nb = lambda k: lp.tensors[k].numel() * lp.tensors[k].element_size()  # noqa: E731
+    shared = sum(nb(k) for k in ("ek", "em", "mk", "moff", "mname", "mcoef", "micpt", "nk", "nt", "uok", "uthr", "ulat"))
+    per_variant = sum(nb(k) for k in ("soff", "sname", "sval")) / max(1, lp.n_gvariants)
+    return int(shared + per_variant)
 
 
 def run_ours(args):
@@ -453,7 +457,8 @@ def run_ours(args):
             for k, (tc, _, o) in enumerate(classes):
                 with torch.cuda.stream(streams[k % len(streams)]):
                     tc.expand()
-                    tc.run(schedules=True, out=o, defer_fallback=True)
+                    tc.run(schedules=True, out=o, defer_fallback=True,
+                           events=class_evs[k] if events is not None else None)
             for st in streams:
                 cur.wait_stream(st)
         for tc, _, o in (classes if not streams else ()):
@@ -498,6 +503,10 @@ def run_ours(args):
     # nodes, so each replay times its own kernels (the roofline reads them)
     graph_evs = {k: (torch.cuda.Event(enable_timing=True, external=True),
                      torch.cuda.Event(enable_timing=True, external=True)) for k in stages}
+    # several classes: each class's engine launch is bracketed by its own events on its own
+    # stream inside the real (concurrent) step; the engine span is first start -> last end
+    class_evs = [{"simulate": (torch.cuda.Event(enable_timing=True, external=True),
+                               torch.cuda.Event(enable_timing=True, external=True))} for _ in classes]
 
     cap_stream = torch.cuda.Stream(local)
 
@@ -512,7 +521,7 @@ def run_ours(args):
         g = torch.cuda.CUDAGraph()
         n0 = ctx.launches()
         with torch.cuda.graph(g, stream=cap_stream):
-            launch_all(graph_evs if single else None)
+            launch_all(graph_evs)
         torch.cuda.synchronize()
         replays[0] = ctx.launches() - n0
         graph = g
@@ -544,6 +553,10 @@ def run_ours(args):
         if single:
             src = graph_evs if graph is not None else evs
             ev_steps.append({k: a.elapsed_time(b) for k, (a, b) in src.items()})
+        elif graph is not None:  # engine span of the concurrent class launches in this step
+            starts = [e0.elapsed_time(c["simulate"][0]) for c in class_evs]
+            ends = [e0.elapsed_time(c["simulate"][1]) for c in class_evs]
+            ev_steps.append({"simulate": max(ends) - min(starts)})
     launches = ctx.launches() - launches0 + (replays[1] - replays0) * replays[0]  # graph replays count too
     total_ms = sum(step_ms)
     if world > 1:
@@ -570,9 +583,9 @@ def run_ours(args):
     roofline = None
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    if single:
+    if ev_steps:
         sim_ms = statistics.mean(s["simulate"] for s in ev_steps)
-    else:  # time the engine launches alone (each class once, one pass)
+    else:  # (eager multi-class steps) time the engine launches alone, each class once
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         outs = [o for _, _, o in classes]
@@ -598,7 +611,10 @@ def run_ours(args):
                 "traffic_source": "profiles/r1_ncu_full.json (ncu --set full, same config)" if traffic else None,
                 "b_sim_bytes_mean": b_sim_total / S,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "kernel_ms": sim_ms, "launches_timed": len(classes)}
+                "kernel_ms": sim_ms, "launches_timed": len(classes),
+                "kernel_ms_source": ("CUDA events around the engine launch of the timed steps" if single else
+                                     "span from the first class's engine start to the last class's engine end "
+                                     "inside the timed (concurrent) steps") if ev_steps else "serialised re-run"}
 
     # ---- e2e through the public C-ABI path with host buffers: H2D candidate arrays, D2H results
     host_in = [{k: v.cpu().pin_memory() for k, v in tc.lp.t_strat.items()} for tc, _, _ in classes]
@@ -692,7 +708,7 @@ def measure_cold(args, graphs, db, configs, graph_of, rank, world, dev, S_total,
     walls, setups = [], []
     for _ in range(runs):
         for g in graphs:
-            for attr in ("_dfsim_b200_lowered", "_dfsim_base_rows"):
+            for attr in ("_dfsim_b200_lowered", "_dfsim_base_rows", "_dfsim_base_arr", "_dfsim_grad_keys"):
                 try:
                     object.__delattr__(g, attr)
                 except AttributeError:

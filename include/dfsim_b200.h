@@ -7,7 +7,8 @@
  * candidate strategies (see INTEGRATION.md for the ctypes binding a dfsim
  * maintainer would add):
  *
- *   dfsim_expand_dp          strategy.py:170-282  expand_data_parallel (+ graph.py:122-135 CSR)
+ *   dfsim_expand_dp          strategy.py:170-282  expand_data_parallel (+ graph.py:122-135 CSR);
+ *                                                also the parameter-server expansion (ps.py, new)
  *   dfsim_topo_order         graph.py:424-443     topological order (any valid order, device)
  *   dfsim_topological_order  graph.py:424-443     topological_order (the reference's order, host)
  *   dfsim_predict_batch      costmodel.py:158-165 predict
@@ -112,11 +113,22 @@ typedef struct {
     const int32_t *coll_rank;  /* [G] rank of "allreduce_<gid>" */
     const int32_t *map_dev;    /* [R] device rank of device_map[k] (ignored where remap==0) */
     int32_t fabric_dev;        /* device rank of the collective fabric */
+    /* parameter-server mode (ps != 0; new code, no reference: ps.py): each marked gradient g gets
+     * push_<g>@r<k> (input g@r<k>, device up_dev[k]), aggregate_<g> (inputs push_<g>@r*, rank
+     * coll_rank[g], device ps_dev) and pull_<g>@r<k> (input aggregate_<g>, device down_dev[k]);
+     * consumers of g@r<k> read pull_<g>@r<k> instead (slot kept). */
+    int32_t ps;
+    const int32_t *push_rank;  /* [G*R] rank of push_<g>@r<k> at g*R+k */
+    const int32_t *pull_rank;  /* [G*R] rank of pull_<g>@r<k> */
+    const int32_t *up_dev;     /* [R] device rank of the worker k -> PS link */
+    const int32_t *down_dev;   /* [R] device rank of the PS -> worker k link */
+    int32_t ps_dev;            /* device rank of the parameter server */
 } dfsim_expand_plan;
 
 /* Emits the expanded graph's CSR (succ_off/succ_idx), indeg, device, sources, queue_off
- * and topo into the caller-allocated arrays of *out (sizes: N=R*N0+G, E given by
- * *n_edges_host after the call).  Synchronous when the three *_host count pointers are
+ * and topo into the caller-allocated arrays of *out (sizes: N = R*N0 + G, or R*N0 +
+ * G*(2R+1) in PS mode; succ_capacity >= R*refs + G*R, or R*refs + 3*G*R in PS mode; E given
+ * by *n_edges_host after the call).  Synchronous when the three *_host count pointers are
  * given; with all three NULL (and base->n_refs >= 0) it is fully asynchronous. */
 int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, const dfsim_expand_plan *plan,
                     int32_t *succ_off, int32_t *succ_idx, int64_t succ_capacity, int32_t *indeg,
@@ -343,6 +355,13 @@ int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int32_t *succ_
 /* stages: prefetch depth (2 or 3, as planned). */
 int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
                               const double *sched, double *cp_len, int32_t *cp_src);
+
+/* The same over candidates order[0..n_sims) (device int64 indices into sched's rows; NULL:
+ * 0..n_sims-1), with at most max_warps warps a CTA (0: as many as fit) so that the kernel can
+ * share SMs with a concurrently running engine launch.  order requires stages 0. */
+int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
+                                 const int64_t *order, int32_t max_warps, const double *sched, double *cp_len,
+                                 int32_t *cp_src);
 
 /* Warps (32 candidates each) one CTA of dfsim_critical_path_lanes holds (0: does not fit). */
 int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t, int32_t stages);

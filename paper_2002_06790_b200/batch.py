@@ -98,21 +98,15 @@ class TopologyClass:
         key = class_key(cfg0)
         if graphs is not None:
             g = graphs[graph_of[0]]
+        self._graph = None
         if key == ("plain",):
-            kind, self.graph = "plain", g
+            kind, self._graph = "plain", g
             self.lg: LoweredGraph = lowered(g, ctx.device)
             structure = None
-        elif key[0] == "ps":
-            from .ps import expand_parameter_server
-
-            kind = "ps"
-            structure = expand_parameter_server(g, cfg0, db, cfg0.ps_device)
-            self.graph = structure.graph
-            self.lg = lowered(self.graph, ctx.device)
-        else:
-            kind = "dp"
-            self.plan = structure = ExpansionPlan(g, cfg0, ctx.device)
-            self.graph, self.lg = self.plan.graph, self.plan.lowered
+        else:  # K1 on the device: data-parallel allreduce, or the parameter-server expansion (ps.py)
+            kind = "ps" if key[0] == "ps" else "dp"
+            self.plan = structure = ExpansionPlan(g, cfg0, ctx.device, build_objects=False, db=db)
+            self.lg = self.plan.lowered
         self.ids = self.lg.ids
         self.configs = list(configs)
         variant_rows, strat_gv = None, None
@@ -120,41 +114,48 @@ class TopologyClass:
         if multi or kind != "plain":
             # estimate inputs from the base graph(s): a clone's row is its base node's, so features
             # are computed once per base node and collective / PS node, not per expanded node
-            from .variants import variant_arrays
+            from .variants import variant_arrays_many
 
             if graphs is None:
                 graphs, graph_of = [g], [0] * len(configs)
-            gv_of: dict = {}
-            variant_rows = []
-            cache: dict = {}
-            for gi in dict.fromkeys(graph_of):
-                gv_of[gi] = len(variant_rows)
-                variant_rows.append(variant_arrays(kind, self.ids, graphs[gi], structure, cfg0, db, cache))
-            strat_gv = [gv_of[gi] for gi in graph_of]
-        self.lp = LoweredProfiles(self.graph, self.ids, db, self.configs, ctx.device, None, strat_gv,
-                                  fit_cache=fit_cache, variant_arrays=variant_rows)
+            gv_of = {gi: k for k, gi in enumerate(dict.fromkeys(graph_of))}
+            variant_rows = variant_arrays_many(kind, self.ids, [graphs[gi] for gi in gv_of], structure, cfg0, db)
+            strat_gv = np.fromiter(map(gv_of.__getitem__, graph_of), np.int32, len(graph_of))
+        self.lp = LoweredProfiles(g if self.plan is not None else self.graph, self.ids, db, self.configs,
+                                  ctx.device, None, strat_gv, fit_cache=fit_cache, variant_arrays=variant_rows,
+                                  op_kind=self.plan.op_kind() if self.plan is not None else None)
         self.tables = None
         self.fused = False
         if fused and self.lg.acyclic and 0 < self.lg.n <= 65535 and self.lp.fused_values_ok:
-            self.tables = ClassTables(self.lg)
+            self.tables = ClassTables(self.lg, n_sims=len(configs))
             if self.tables.fused_ok:
                 self._prepare_variants()
+
+    @property
+    def graph(self):
+        """The class's expanded graph objects (built on first use for expanded classes)."""
+        return self._graph if self.plan is None else self.plan.graph
 
     # ------------------------------------------------------------------ fused path
     def _prepare_variants(self):
         import torch
 
         lp, N = self.lp, self.lg.n
-        keys = list(zip(lp.strat_gv, lp.strat_hw, lp.strat_algo, lp.strat_path))
-        var_ids: dict = {}
-        var_of = np.asarray([var_ids.setdefault(k, len(var_ids)) for k in keys], np.int64)
-        V = len(var_ids)
+        # variant = (graph variant, hardware, algorithm, path): one int64 key per candidate
+        cols = [np.asarray(c, np.int64) for c in (lp.strat_gv, lp.strat_hw, lp.strat_algo, lp.strat_path)]
+        span = [int(c.max(initial=0)) + 1 for c in cols]
+        key = ((cols[0] * span[1] + cols[1]) * span[2] + cols[2]) * span[3] + cols[3]
+        uniq, var_of = np.unique(key, return_inverse=True)
+        var_of = var_of.astype(np.int64)
+        V = len(uniq)
         dev = f"cuda:{self.ctx.device}"
-        vk = list(var_ids)
-        self.v_gv = torch.tensor([k[0] for k in vk], dtype=torch.int32, device=dev)
-        self.v_hw = torch.tensor([k[1] for k in vk], dtype=torch.int32, device=dev)
-        self.v_algo = torch.tensor([k[2] for k in vk], dtype=torch.uint8, device=dev)
-        self.v_path = torch.tensor([k[3] for k in vk], dtype=torch.int32, device=dev)
+        u_path, rest = uniq % span[3], uniq // span[3]
+        u_algo, rest = rest % span[2], rest // span[2]
+        u_hw, u_gv = rest % span[1], rest // span[1]
+        self.v_gv = torch.as_tensor(u_gv, dtype=torch.int32, device=dev)
+        self.v_hw = torch.as_tensor(u_hw, dtype=torch.int32, device=dev)
+        self.v_algo = torch.as_tensor(u_algo, dtype=torch.uint8, device=dev)
+        self.v_path = torch.as_tensor(u_path, dtype=torch.int32, device=dev)
         self.n_variants = V
         self.var_of = var_of
         self.base = torch.empty((V, N), dtype=torch.float64, device=dev)
@@ -192,7 +193,7 @@ class TopologyClass:
         self.fused_strat = native.FusedStrategies(
             lp.n_sims, V, native.ptr(self.base), len(firsts), native.ptr(self.f_order), native.ptr(self.f_first),
             native.ptr(self.f_count), native.ptr(self.f_var), native.ptr(s["gap"]),
-            native.ptr(s["ov"]) if any(x >= 0 for x in lp.strat_ov) else native.P(0),
+            native.ptr(s["ov"]) if lp.strat_ov.size and lp.strat_ov.max() >= 0 else native.P(0),
             native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]), max(counts, default=0))
         self.fused = True
 
@@ -308,28 +309,29 @@ class TopologyClass:
                 o.pop(k, None)
         return o
 
-    def rows_by_rank(self, o: dict, row: int):
-        """(start, finish) of one candidate as device tensors in node-rank order."""
-        n = self.lg.n
-        st, fi = o["start"][row, :n], o["finish"][row, :n]
-        if o.get("layout") == "position":
-            import torch
+    def rows_by_position(self, o: dict, rows):
+        """(start, finish) of candidates ``rows`` as [R, N] device tensors by level position
+        (fused layouts) or by rank (unfused)."""
+        import torch
 
-            pos = torch.as_tensor(self.tables.pos, device=st.device)
-            st, fi = st.index_select(0, pos), fi.index_select(0, pos)
-        return st, fi
+        n = self.lg.n
+        r = torch.as_tensor(list(rows), dtype=torch.int64, device=o["makespan"].device)
+        return o["start"].index_select(0, r)[:, :n], o["finish"].index_select(0, r)[:, :n]
 
     def rows_by_rank_batch(self, o: dict, rows):
         """(start, finish) of several candidates as contiguous [R][N] device tensors by node rank."""
         import torch
 
-        n = self.lg.n
-        r = torch.as_tensor(list(rows), dtype=torch.int64, device=o["makespan"].device)
-        st, fi = o["start"].index_select(0, r)[:, :n], o["finish"].index_select(0, r)[:, :n]
+        st, fi = self.rows_by_position(o, rows)
         if o.get("layout") == "position":
             pos = torch.as_tensor(self.tables.pos, device=st.device)
             st, fi = st.index_select(1, pos), fi.index_select(1, pos)
         return st.contiguous(), fi.contiguous()
+
+    def rows_by_rank(self, o: dict, row: int):
+        """(start, finish) of one candidate as device tensors in node-rank order."""
+        st, fi = self.rows_by_rank_batch(o, [row])
+        return st[0], fi[0]
 
     def summary_tables(self):
         """K6 tables of this class (cached): op key, comm flag and (device, id) order per node rank."""
@@ -345,9 +347,11 @@ class TopologyClass:
         return self._summary
 
     def critical_path_only(self, o: dict):
-        """Re-run K4 on the current schedules (after a deferred fallback)."""
+        """Re-run K4 on the current schedules (after a deferred fallback): only the re-run
+        candidates when K4 v3 can take a candidate list."""
         if self.fused:
-            self.tables.critical_path(self.lp.n_sims, o["sched"], o["cp_len"], o["cp_src"])
+            self.tables.critical_path(self.lp.n_sims, o["sched"], o["cp_len"], o["cp_src"],
+                                      rows=o.get("fallback_rows"))
         elif self.lg.acyclic and self.lg.n:
             critical_path_arrays(self.lg, o["start"], o["finish"], out=o)
 
@@ -372,7 +376,7 @@ class SweepResult:
     def _row(self, i):
         c, row = self._where[i]
         tc, _, o = self.classes[c]
-        if "start" not in o:
+        if "sched" not in o and "start" not in o:
             raise ValueError("run sweep(..., keep_schedules=True) to rebuild schedules")
         return tc, o, row
 
@@ -415,7 +419,7 @@ class SweepResult:
             by_class.setdefault(c, []).append((k, row))
         for c, items in by_class.items():
             tc, _, o = self.classes[c]
-            if "start" not in o:
+            if "sched" not in o and "start" not in o:
                 raise ValueError("run sweep(..., keep_schedules=True) to summarise schedules")
             rows = [row for _, row in items]
             st, fi = tc.rows_by_rank_batch(o, rows)
@@ -516,8 +520,10 @@ def _row_error(tc, o, row) -> Exception:
             raise_for_row(tc.graph, tc.ids, o["dur"][row, :n].cpu().numpy(), o["src"][row, :n].cpu().numpy())
         except Exception as e:  # noqa: BLE001 -- returned, raised by the caller
             return e
-    st = o["start"][row, :n].cpu().numpy() if "start" in o else None
-    return CycleError(sorted(tc.ids[k] for k in np.nonzero(np.isnan(st))[0]) if st is not None else [])
+    if "sched" not in o and "start" not in o:
+        return CycleError([])
+    st = tc.rows_by_rank(o, row)[0].cpu().numpy() if tc.fused else o["start"][row, :n].cpu().numpy()
+    return CycleError(sorted(tc.ids[k] for k in np.nonzero(np.isnan(st))[0]))
 
 
 def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,

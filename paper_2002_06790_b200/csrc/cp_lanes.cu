@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -83,6 +84,8 @@ struct LaneArgs {
     int32_t *cp_src;
     double *spill;        // [grid * wpb][n_long][32]
     int32_t *task_counter; // groups of 32 candidates handed out dynamically (SMs finish together)
+    const int64_t *order;  // optional: lane i of task t takes candidate order[32 t + i] (register variant)
+    int32_t l2_ahead;      // chunks between the L2 prefetch and the register loads (register variant)
     int32_t wpb;
     int32_t table_bytes;  // CTA tables: bounds | spill_off | block_off | spill_list
     int32_t region_bytes; // per warp: rows [slots | spill stages] | pair stages | block stages
@@ -256,10 +259,12 @@ __global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) 
         if (lane == 0) task = atomicAdd(a.task_counter, 1);
         task = __shfl_sync(DFSIM_FULL_MASK, task, 0);
         if (task >= n_tasks) break;
-        const int64_t s = static_cast<int64_t>(task) * 32 + lane;
-        const bool live = s < a.S;
-        const double *row = a.sched + 2 * (live ? s : a.S - 1) * N;  // idle lanes shadow the last row
-        const int rowpar = static_cast<int>((static_cast<int64_t>(live ? s : a.S - 1) * N) & 1);
+        const int64_t k = static_cast<int64_t>(task) * 32 + lane;
+        const bool live = k < a.S;
+        const int64_t kk = live ? k : a.S - 1;  // idle lanes shadow the last candidate's row
+        const int64_t s = a.order ? __ldg(a.order + kk) : kk;
+        const double *row = a.sched + 2 * s * N;
+        const int rowpar = static_cast<int>((s * N) & 1);
 
         auto prefetch_smem = [&](int q) {  // node records + spill values of chunk q
             const unsigned stg = static_cast<unsigned>(q & 1);
@@ -315,10 +320,10 @@ __global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) 
         prefetch_smem(0);
         load_window(0, wa);
 
-        constexpr int PF = 3;
+        const int PF = a.l2_ahead;  // 0: no L2 prefetch
         for (int q = 1; q < PF && q < NQ; q++) prefetch_l2(q);
         auto process = [&](int q, double (&w)[NU][4], double (&wn)[NU][4]) {
-            if (q + PF < NQ) prefetch_l2(q + PF);
+            if (PF > 0 && q + PF < NQ) prefetch_l2(q + PF);
             if (q + 1 < NQ) {
                 prefetch_smem(q + 1);
                 load_window(q + 1, wn);
@@ -549,7 +554,14 @@ extern "C" int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables
 
 extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
                                          const double *sched, double *cp_len, int32_t *cp_src) {
+    return dfsim_critical_path_lanes_ex(ctx, t, stages, n_sims, nullptr, 0, sched, cp_len, cp_src);
+}
+
+extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages,
+                                            int64_t n_sims, const int64_t *order, int32_t max_warps,
+                                            const double *sched, double *cp_len, int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
+    DFSIM_ARG_CHECK(ctx, !order || stages == 0, "a candidate order needs the register variant (stages 0)");
     DFSIM_ARG_CHECK(ctx, sched && cp_len, "sched and cp_len are required");
     DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
     DFSIM_ARG_CHECK(ctx, t->chunk_positions == 8 || t->chunk_positions == 16, "chunk_positions must be 8 or 16");
@@ -565,6 +577,7 @@ extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tab
     // as many warps as the batch needs, spread over the SMs
     const int64_t warps = (n_sims + 31) / 32;
     int wpb = shape.wpb;
+    if (max_warps > 0 && max_warps < wpb) wpb = max_warps;  // leaves room for a co-resident kernel
     const int64_t per_sm = (warps + ctx->num_sms - 1) / ctx->num_sms;
     if (per_sm < wpb) wpb = static_cast<int>(per_sm < 1 ? 1 : per_sm);
     const size_t smem = shape.table_bytes + static_cast<size_t>(wpb) * shape.region_bytes;
@@ -577,6 +590,12 @@ extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tab
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, sizeof(int32_t), ctx->stream));
     LaneArgs a;
     a.task_counter = counter;
+    a.order = order;
+    static const int kL2Ahead = [] {  // DFSIM_CP_L2AHEAD: measurement knob
+        const char *e = std::getenv("DFSIM_CP_L2AHEAD");
+        return e ? std::atoi(e) : 0;  // measured: prefetching 3-12 chunks ahead was slower
+    }();
+    a.l2_ahead = kL2Ahead;
     a.t = *t;
     a.S = n_sims;
     a.sched = sched;

@@ -6,7 +6,8 @@
 // "allreduce_<gid>", device ranks); the device builds everything per edge:
 //   clone (k, v) keeps v's refs within replica k (strategy.py:215); a ref to a
 //   marked gradient becomes a ref to its collective when R > 1 (231-238); the
-//   collective of gradient g consumes g@r0..g@r{R-1} (249).
+//   collective of gradient g consumes g@r0..g@r{R-1} (249).  PS mode (ps.py, new code):
+//   g@r<k> -> push_<g>@r<k> -> aggregate_<g> -> pull_<g>@r<k>, and refs to g@r<k> read the pull.
 // Edges are (producer rank << 32 | consumer rank) keys; one radix sort gives the
 // rank-sorted successor lists with multiplicity, a histogram + scan gives offsets.
 #include <cub/cub.cuh>
@@ -24,7 +25,7 @@ constexpr unsigned long long kDangling = ~0ull;
 __global__ void k_expand_nodes(dfsim_base_graph b, dfsim_expand_plan p, int32_t *indeg, int32_t *device,
                                int32_t *dev_count) {
     const int64_t n_clone = static_cast<int64_t>(p.replicas) * b.n_base;
-    const int64_t total = n_clone + p.n_collectives;
+    const int64_t total = n_clone + static_cast<int64_t>(p.n_collectives) * (p.ps ? 2 * p.replicas + 1 : 1);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int32_t r, deg, dev;
@@ -34,10 +35,27 @@ __global__ void k_expand_nodes(dfsim_base_graph b, dfsim_expand_plan p, int32_t 
             r = p.clone_rank[i];
             deg = b.in_off[v + 1] - b.in_off[v];
             dev = b.remap[v] ? p.map_dev[k] : b.base_dev[v];
-        } else {
+        } else if (!p.ps) {
             r = p.coll_rank[i - n_clone];
             deg = p.replicas;
             dev = p.fabric_dev;
+        } else {  // PS nodes of gradient g: R pushes, the aggregate, R pulls
+            const int64_t j = i - n_clone, per = 2 * static_cast<int64_t>(p.replicas) + 1;
+            const int g = static_cast<int>(j / per), m = static_cast<int>(j - g * per);
+            if (m < p.replicas) {
+                r = p.push_rank[static_cast<int64_t>(g) * p.replicas + m];
+                deg = 1;
+                dev = p.up_dev[m];
+            } else if (m == p.replicas) {
+                r = p.coll_rank[g];
+                deg = p.replicas;
+                dev = p.ps_dev;
+            } else {
+                const int k = m - p.replicas - 1;
+                r = p.pull_rank[static_cast<int64_t>(g) * p.replicas + k];
+                deg = 1;
+                dev = p.down_dev[k];
+            }
         }
         indeg[r] = deg;
         device[r] = dev;
@@ -58,17 +76,27 @@ __global__ void k_expand_edges(dfsim_base_graph b, dfsim_expand_plan p, int64_t 
             unsigned long long key = kDangling;
             if (u >= 0) {
                 const int32_t g = p.replicas > 1 ? b.marked[u] : -1;
-                const int32_t prod = g >= 0 ? p.coll_rank[g] : p.clone_rank[static_cast<int64_t>(k) * b.n_base + u];
+                const int32_t prod = g < 0 ? p.clone_rank[static_cast<int64_t>(k) * b.n_base + u]
+                                           : (p.ps ? p.pull_rank[static_cast<int64_t>(g) * p.replicas + k] : p.coll_rank[g]);
                 key = (static_cast<unsigned long long>(static_cast<uint32_t>(prod)) << 32) | cons;
             }
             keys[static_cast<int64_t>(k) * n_refs + j] = key;
         }
-        // collective inputs: the gradient's clone in replica k feeds its collective
+        // collective inputs: the gradient's clone in replica k feeds its collective; in PS mode
+        // it feeds push(g, k), which feeds aggregate(g), which feeds pull(g, k)
         const int32_t g = p.replicas > 1 ? b.marked[v] : -1;
-        if (g >= 0) {
+        auto key = [](int32_t prod, int32_t cons) {
+            return (static_cast<unsigned long long>(static_cast<uint32_t>(prod)) << 32) | static_cast<uint32_t>(cons);
+        };
+        if (g >= 0 && !p.ps) {
             keys[static_cast<int64_t>(p.replicas) * n_refs + static_cast<int64_t>(g) * p.replicas + k] =
-                (static_cast<unsigned long long>(static_cast<uint32_t>(p.clone_rank[i])) << 32) |
-                static_cast<uint32_t>(p.coll_rank[g]);
+                key(p.clone_rank[i], p.coll_rank[g]);
+        } else if (g >= 0) {
+            const int64_t gk = static_cast<int64_t>(g) * p.replicas + k;
+            unsigned long long *out = keys + static_cast<int64_t>(p.replicas) * n_refs + 3 * gk;
+            out[0] = key(p.clone_rank[i], p.push_rank[gk]);
+            out[1] = key(p.push_rank[gk], p.coll_rank[g]);
+            out[2] = key(p.coll_rank[g], p.pull_rank[gk]);
         }
     }
 }
@@ -113,7 +141,9 @@ extern "C" int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, con
     DFSIM_ARG_CHECK(ctx, plan->replicas > 1 || plan->n_collectives == 0, "collectives need replicas > 1");
     DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const int32_t R = plan->replicas, N0 = base->n_base, G = plan->n_collectives;
-    const int64_t N = (int64_t)R * N0 + G;
+    DFSIM_ARG_CHECK(ctx, !plan->ps || (plan->push_rank && plan->pull_rank && plan->up_dev && plan->down_dev),
+                    "PS mode needs push/pull ranks and link devices");
+    const int64_t N = (int64_t)R * N0 + (int64_t)G * (plan->ps ? 2 * R + 1 : 1);
     DFSIM_ARG_CHECK(ctx, N < (1ll << 31), "expanded graph too large");
     // number of base refs: given by the caller, or read back from in_off[N0]
     int32_t n_refs32 = base->n_refs;
@@ -124,8 +154,8 @@ extern "C" int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, con
     }
     if (n_refs32 < 0) n_refs32 = 0;
     const int64_t n_refs = n_refs32;
-    const int64_t n_keys = (int64_t)R * n_refs + (int64_t)G * R;
-    DFSIM_ARG_CHECK(ctx, succ_capacity >= n_keys, "succ_capacity below R*refs + G*R");
+    const int64_t n_keys = (int64_t)R * n_refs + (int64_t)G * R * (plan->ps ? 3 : 1);
+    DFSIM_ARG_CHECK(ctx, succ_capacity >= n_keys, "succ_capacity below R*refs + G*R (3*G*R in PS mode)");
 
     // cub temp sizes
     size_t sort_tmp = 0, scan_tmp = 0, sel_tmp = 0;

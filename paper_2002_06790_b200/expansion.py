@@ -18,7 +18,7 @@ import numpy as np
 
 from . import native
 from .errors import ConfigError, DfsimError, PatternWarning
-from .lowering import LoweredGraph, _dev_tensor, match_pattern
+from .lowering import LoweredGraph, _dev_tensor, match_pattern, upload
 from .model import (
     COLLECTIVE,
     COMPUTE,
@@ -57,10 +57,31 @@ def marked_gradients(g, cfg) -> list[str]:
 
 
 class ExpansionPlan:
-    """Strings and ranks of one topology class (host), plus its device CSR (K1)."""
+    """Strings and ranks of one topology class (host), plus its device CSR (K1).
 
-    def __init__(self, g, cfg, device: int | None = None, build_objects: bool = True, run_k1: bool = True):
+    ``sync`` "allreduce" is strategy.py:170-282; "parameter_server" is this repo's PS
+    expansion (ps.py: push / aggregate / pull nodes on per-worker links), emitted by the
+    same K1 launch in PS mode.  Host node objects (``graph``) are built on first use only:
+    the batched path needs the ids, ranks and CSR, not the objects."""
+
+    def __init__(self, g, cfg, device: int | None = None, build_objects: bool = True, run_k1: bool = True,
+                 db=None, sync: str | None = None):
         R = cfg.replicas
+        self.sync = sync or getattr(cfg, "sync", "allreduce")
+        ps = self.sync == "parameter_server"
+        self.ps_device = getattr(cfg, "ps_device", "ps0")
+        path = cfg.collective.path
+        link = None
+        if ps:  # ps.py's checks, in its order
+            from .model import SCENARIO_GPU_GPU_UNI
+
+            if R < 2 or len(cfg.device_map) != R:
+                raise ConfigError("parameter-server expansion needs replicas >= 2 and a device_map")
+            if self.ps_device in cfg.device_map:
+                raise ConfigError(f"PS device {self.ps_device!r} collides with a worker device")
+            link = db.link_records.get((SCENARIO_GPU_GPU_UNI, path, 2)) if db is not None else None
+            if link is None:
+                raise ConfigError(f"no {SCENARIO_GPU_GPU_UNI}/{path}/2 link record for the PS links")
         if cfg.device_map and len(cfg.device_map) != R:
             raise ConfigError(f"device_map has {len(cfg.device_map)} entries for {R} replicas")
         if R > 1 and not cfg.device_map:
@@ -73,29 +94,46 @@ class ExpansionPlan:
         clone_dev = [[(dmap[k] if (dmap and g.nodes[nid].kind == COMPUTE) else g.nodes[nid].device)
                       for nid in base_ids] for k in range(R)]
         group = list(dmap) if dmap else sorted({d for row in clone_dev for d in row})
-        path = cfg.collective.path
         self.fabric = fabric = f"collective:{path}:" + "+".join(group)
-        coll_ids = [f"allreduce_{gid}" for gid in marked] if R > 1 else []
         clone_ids = [f"{nid}@r{k}" for k in range(R) for nid in base_ids]
-        all_ids = clone_ids + coll_ids
-        if len(set(all_ids)) != len(all_ids):
-            seen = set(clone_ids)
-            dup = next(c for c in coll_ids if c in seen)
-            raise DfsimError(f"collective id {dup!r} collides with an existing node")
-        self._validate_inherited(g, base_index, R, marked, group)
         self.origin = {f"{nid}@r{k}": ("clone", nid) for k in range(R) for nid in base_ids}
-        self.origin.update({cid: ("coll", gid) for gid, cid in zip(marked, coll_ids)})
+        self.link = link
+        if ps:  # per gradient: R pushes, the aggregate, R pulls (ps.ps_nodes order)
+            self.up_links = [f"link:{path}:{w}->{self.ps_device}" for w in dmap]
+            self.down_links = [f"link:{path}:{self.ps_device}->{w}" for w in dmap]
+            push_ids = [[f"push_{gid}@r{k}" for k in range(R)] for gid in marked]
+            agg_ids = [f"aggregate_{gid}" for gid in marked]
+            pull_ids = [[f"pull_{gid}@r{k}" for k in range(R)] for gid in marked]
+            coll_ids = agg_ids
+            added = [x for gi in range(len(marked)) for x in (push_ids[gi] + [agg_ids[gi]] + pull_ids[gi])]
+            for gid, pu, ag, pl in zip(marked, push_ids, agg_ids, pull_ids):
+                for cid in pu + [ag] + pl:
+                    self.origin[cid] = ("ps", gid)
+        else:
+            coll_ids = [f"allreduce_{gid}" for gid in marked] if R > 1 else []
+            added = coll_ids
+            self.origin.update({cid: ("coll", gid) for gid, cid in zip(marked, coll_ids)})
+        all_ids = clone_ids + added
+        if len(self.origin) != len(all_ids):
+            seen = set(clone_ids)
+            dup = next(c for c in added if c in seen)
+            raise DfsimError(f"collective id {dup!r} collides with an existing node")
+        if not ps:
+            self._validate_inherited(g, base_index, R, marked, group)
         order = sorted(range(len(all_ids)), key=all_ids.__getitem__)
         self.ids = [all_ids[i] for i in order]
         rank = np.empty(len(all_ids), dtype=np.int32)
         rank[np.asarray(order, dtype=np.int64)] = np.arange(len(all_ids), dtype=np.int32)
         devset = {d for row in clone_dev for d in row}
-        if coll_ids:
+        if ps and marked:
+            devset.update([self.ps_device] + self.up_links + self.down_links)
+        elif coll_ids:
             devset.add(fabric)
         self.devices = sorted(devset)
         drank = {d: i for i, d in enumerate(self.devices)}
         self.R, self.N0, self.G = R, N0, len(coll_ids)
         self.cfg, self.base_ids, self.clone_dev, self.coll_ids, self.group = cfg, base_ids, clone_dev, coll_ids, group
+        self._g, self._graph = g, None
         # base arrays
         in_off = np.zeros(N0 + 1, dtype=np.int32)
         in_src, remap, marked_idx, base_dev = [], np.zeros(N0, np.uint8), np.full(N0, -1, np.int32), []
@@ -113,25 +151,78 @@ class ExpansionPlan:
                 marked_idx[v] = gidx[nid]
         self.max_indeg = max(max_in, R if coll_ids else 0)
         if not run_k1:  # host strings only (ids, origins, collective nodes); no device arrays
-            self.ctx, self.lowered, self.graph = None, None, None
+            self.ctx, self.lowered = None, None
             return
         ctx = native.Context.get(device)
         self.ctx = ctx
         d = ctx.device
-        T = lambda a, dt: _dev_tensor(np.asarray(a, dt) if len(a) else np.zeros(1, dt), d, dt)  # noqa: E731
-        self._keep = [T(in_off, np.int32), T(in_src, np.int32), T(base_dev, np.int32), T(remap, np.uint8),
-                      T(marked_idx, np.int32), T(rank[: R * N0], np.int32), T(rank[R * N0:], np.int32),
-                      T([drank[x] for x in dmap] if dmap else [0], np.int32)]
-        k = self._keep
+        n_clone, G = R * N0, len(coll_ids)
+        if ps:  # added ids are grouped per gradient: R pushes, aggregate, R pulls
+            added_rank = rank[n_clone:].reshape(G, 2 * R + 1) if G else np.zeros((0, 2 * R + 1), np.int32)
+            coll_rank = added_rank[:, R]
+            push_rank, pull_rank = added_rank[:, :R].ravel(), added_rank[:, R + 1:].ravel()
+        else:
+            coll_rank, push_rank, pull_rank = rank[n_clone:], np.zeros(1, np.int32), np.zeros(1, np.int32)
+        up = upload(dict(
+            in_off=(in_off, np.int32), in_src=(in_src, np.int32), base_dev=(base_dev, np.int32),
+            remap=(remap, np.uint8), marked=(marked_idx, np.int32), clone_rank=(rank[:n_clone], np.int32),
+            coll_rank=(coll_rank, np.int32), map_dev=([drank[x] for x in dmap] if dmap else [0], np.int32),
+            push_rank=(push_rank, np.int32), pull_rank=(pull_rank, np.int32),
+            up_dev=([drank[x] for x in self.up_links] if ps and G else [0], np.int32),
+            down_dev=([drank[x] for x in self.down_links] if ps and G else [0], np.int32)), d)
+        self._keep = k = list(up.values())  # one host-to-device copy; order as listed
         base = native.BaseGraph(N0, native.ptr(k[0]), native.ptr(k[1]), native.ptr(k[2]), native.ptr(k[3]),
                                 native.ptr(k[4]), len(in_src))
-        plan = native.ExpandPlan(R, self.G, native.ptr(k[5]), native.ptr(k[6]), native.ptr(k[7]),
-                                 drank.get(fabric, 0))
+        plan = native.ExpandPlan(R, G, native.ptr(k[5]), native.ptr(k[6]), native.ptr(k[7]), drank.get(fabric, 0),
+                                 int(ps), native.ptr(k[8]), native.ptr(k[9]), native.ptr(k[10]), native.ptr(k[11]),
+                                 drank.get(self.ps_device, 0))
         self._structs = (base, plan, len(in_src))
         self.lowered = self._run_k1(ctx, base, plan, len(in_src))
         if self.lowered.n_ordered != self.lowered.n:
             raise DfsimError("internal: expansion produced an invalid graph: graph contains a cycle")
-        self.graph = self._objects(g, cfg) if build_objects else None
+        if build_objects:
+            _ = self.graph
+
+    @property
+    def graph(self) -> DataflowGraph:
+        """The expanded graph's host objects (built on first use)."""
+        if self._graph is None and getattr(self, "ctx", None) is not None:
+            self._graph = self._objects(self._g, self.cfg)
+        return self._graph
+
+    @property
+    def device_specs(self) -> dict:
+        """DeviceSpec of every device the expansion adds (PS links need their throughput)."""
+        if self.sync != "parameter_server":
+            return {}
+        out = {}
+        for lid in self.up_links + self.down_links:
+            out[lid] = DeviceSpec(lid, "Link", self.cfg.hardware, self.link.throughput_mbps, self.link.latency_us)
+        return out
+
+    def op_kind(self):
+        """op type and kind code (0 Compute, 1 Transfer, 2 Collective) of every id, without objects."""
+        from .ps import AGGREGATE_OP, PULL_OP, PUSH_OP
+
+        g = self._g
+        code = {COMPUTE: 0, TRANSFER: 1, COLLECTIVE: 2}
+        ops, kinds = [], []
+        for cid in self.ids:
+            what, nid = self.origin[cid]
+            if what == "clone":
+                n = g.nodes[nid]
+                ops.append(n.op_type)
+                kinds.append(code.get(n.kind, 2))
+            elif what == "coll":
+                ops.append("AllReduce")
+                kinds.append(2)
+            elif cid.startswith("aggregate_"):
+                ops.append(AGGREGATE_OP)
+                kinds.append(0)
+            else:
+                ops.append(PUSH_OP if cid.startswith("push_") else PULL_OP)
+                kinds.append(1)
+        return ops, kinds
 
     def _validate_inherited(self, g, base_index, R, marked, group):
         """Findings of validate(expanded) that come from the base graph (graph.py:331-381)."""
@@ -170,7 +261,7 @@ class ExpansionPlan:
         base, plan, n_refs = self._structs
         lg = self.lowered
         N, D = len(self.ids), len(self.devices)
-        cap = self.R * n_refs + self.G * self.R
+        cap = self.R * n_refs + self.G * self.R * (3 if self.sync == "parameter_server" else 1)
         by = native.ctypes.byref
         P0 = native.P(0)
         if not check:
@@ -193,7 +284,7 @@ class ExpansionPlan:
         N = len(self.ids)
         D = len(self.devices)
         dev = f"cuda:{ctx.device}"
-        cap = self.R * n_refs + self.G * self.R
+        cap = self.R * n_refs + self.G * self.R * (3 if self.sync == "parameter_server" else 1)
         z = lambda n: torch.empty(max(n, 1), dtype=torch.int32, device=dev)  # noqa: E731
         succ_off, succ_idx, indeg, device = z(N + 1), z(cap), z(N), z(N)
         sources, queue_off, topo = z(N), z(D + 1), z(N)
@@ -214,7 +305,15 @@ class ExpansionPlan:
                       tuple((f"{gid}@r{k}", 0) for k in range(self.R)), grad.output_shapes)
 
     def _objects(self, g, cfg) -> DataflowGraph:
-        """Host node/device objects in the reference's insertion order (strategy.py:202-276)."""
+        """Host node/device objects in the reference's insertion order (strategy.py:202-276);
+        PS mode: ps.expand_parameter_server's objects."""
+        if self.sync == "parameter_server":
+            from .ps import expand_parameter_server
+
+            gx = expand_parameter_server(g, cfg, _LinkDB(self.link, cfg.collective.path), self.ps_device).graph
+            object.__setattr__(gx, "_dfsim_b200_lowered", ((len(gx.nodes), len(gx.devices), self.ctx.device),
+                                                           self.lowered))
+            return gx
         R, marked = self.R, set(self.marked) if self.R > 1 else set()
         nodes = {}
         for k in range(R):
@@ -243,10 +342,19 @@ class ExpansionPlan:
 
 def expand_data_parallel(g, cfg, device: int | None = None) -> ExpandedGraph:
     """strategy.py:170-282; the expanded graph's CSR is built by K1 on the GPU."""
-    plan = ExpansionPlan(g, cfg, device)
+    plan = ExpansionPlan(g, cfg, device, sync="allreduce")  # the reference has no PS (SPEC.md:346)
     replica_of = {f"{nid}@r{k}": (nid, k) for k in range(plan.R) for nid in plan.base_ids}
     return ExpandedGraph(graph=plan.graph, replica_of=replica_of, collective_nodes=list(plan.coll_ids))
 
 
 def expand_class(g, cfg, device: int | None = None) -> ExpansionPlan:
     return ExpansionPlan(g, cfg, device)
+
+
+class _LinkDB:
+    """The one profile-DB row expand_parameter_server reads (the PS links' gpu-gpu-uni row)."""
+
+    def __init__(self, link, path):
+        from .model import SCENARIO_GPU_GPU_UNI
+
+        self.link_records = {(SCENARIO_GPU_GPU_UNI, path, 2): link}

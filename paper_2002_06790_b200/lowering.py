@@ -53,6 +53,32 @@ def _dev_tensor(a, device, dtype=None):
     return t.to(device=f"cuda:{device}", non_blocking=False)
 
 
+_VIEW_AS = {np.dtype(np.uint64): np.int64, np.dtype(np.uint32): np.int32, np.dtype(np.uint16): np.int16}
+
+
+def upload(arrays: dict, device) -> dict:
+    """Many small host tables -> device tensors with ONE host-to-device copy: ``arrays`` maps a
+    name to (array, dtype); each lands 16-byte aligned in one device buffer and comes back as
+    a typed view (unsigned 16/32/64-bit as the signed type of the same bits).  Empty arrays
+    become one zero element (the C-ABI never sees a null table)."""
+    import torch
+
+    layout, pos = [], 0
+    for name, (a, dt) in arrays.items():
+        arr = np.asarray(a, dt).ravel() if np.size(a) else np.zeros(1, dt)
+        arr = np.ascontiguousarray(arr)
+        arr = arr.view(_VIEW_AS.get(arr.dtype, arr.dtype))
+        pos = (pos + 15) // 16 * 16
+        layout.append((name, pos, arr))
+        pos += arr.nbytes
+    host = torch.empty(max(pos, 16), dtype=torch.uint8, pin_memory=True)
+    hv = host.numpy()
+    for _, o, arr in layout:
+        hv[o:o + arr.nbytes] = arr.view(np.uint8)
+    dev = host.to(f"cuda:{device}", non_blocking=True)
+    return {name: dev[o:o + arr.nbytes].view(getattr(torch, arr.dtype.name)) for name, o, arr in layout}
+
+
 # ----------------------------------------------------------------------------- graph
 
 
@@ -386,19 +412,40 @@ class _FeatureRegistry:
     def __init__(self):
         self.ids: dict = {}
         self.rows: list = []
+        # flat copy: vector k = names[f_name[f_off[k]:f_off[k+1]]], values f_val[...]
+        self.names: dict = {}
+        self.name_list: list = []
+        self.f_off, self.f_name, self.f_val = [0], [], []
+        self._flat = None
         self.lock = threading.Lock()
 
     def intern(self, feats_list) -> np.ndarray:
         with self.lock:
-            ids, rows = self.ids, self.rows
+            ids, rows, names = self.ids, self.rows, self.names
             out = np.empty(len(feats_list), np.int64)
             for i, f in enumerate(feats_list):
                 k = ids.get(f)
                 if k is None:
                     k = ids[f] = len(rows)
                     rows.append(f)
+                    for nm, v in f:
+                        gid = names.get(nm)
+                        if gid is None:
+                            gid = names[nm] = len(self.name_list)
+                            self.name_list.append(nm)
+                        self.f_name.append(gid)
+                        self.f_val.append(v)
+                    self.f_off.append(len(self.f_name))
                 out[i] = k
             return out
+
+    def flat(self):
+        """(f_off, f_name, f_val) as numpy arrays (cached until the registry grows)."""
+        with self.lock:
+            if self._flat is None or len(self._flat[0]) != len(self.f_off):
+                self._flat = (np.asarray(self.f_off, np.int64), np.asarray(self.f_name, np.int64),
+                              np.asarray(self.f_val, np.float64))
+            return self._flat
 
 
 FEATURES = _FeatureRegistry()
@@ -443,7 +490,7 @@ class LoweredProfiles:
     """
 
     def __init__(self, g, ids, db, configs, device: int, variant_rows=None, strat_gv=None, fit_cache=None,
-                 variant_arrays=None):
+                 variant_arrays=None, op_kind=None):
         self.device = device
         N = len(ids)
         nodes = g.nodes
@@ -452,26 +499,30 @@ class LoweredProfiles:
         # once, the per-candidate columns are built with C-level maps (sweeps hold 10^4-10^5 configs)
         self.hw_ids, self.path_ids = {}, {}
         ov_sets, ov_key_to_id = [], {}
+        n = len(configs)
         hws = list(map(_HARDWARE, configs))
-        self.strat_hw = [self.hw_ids.setdefault(h, len(self.hw_ids)) for h in hws]
-        self.strat_gap = list(map(float, map(_GAP, configs)))
-        coll_of = {}  # id(CollectiveConfig) -> (algo code, path id)
+        for h in dict.fromkeys(hws):
+            self.hw_ids[h] = len(self.hw_ids)
+        self.strat_hw = np.fromiter(map(self.hw_ids.__getitem__, hws), np.int32, n)
+        self.strat_gap = np.fromiter(map(float, map(_GAP, configs)), np.float64, n)
         colls = list(map(_COLLECTIVE, configs))
+        code_of, algo_tab, path_tab = {}, [], []
         for c in {id(c): c for c in colls}.values():
             if c.algo not in (ALGO_MEASURED, ALGO_RING):
                 raise ValueError(f"unknown collective algorithm {c.algo!r}")
-            coll_of[id(c)] = (0 if c.algo == ALGO_MEASURED else 1, self.path_ids.setdefault(c.path, len(self.path_ids)))
-        ap = [coll_of[id(c)] for c in colls]
-        self.strat_algo = [x[0] for x in ap]
-        self.strat_path = [x[1] for x in ap]
-        self.strat_ov = [-1] * len(configs)
-        for i, ov in enumerate(map(_OVERRIDES, configs)):
-            if not ov:
-                continue
-            ov_key = tuple(ov.items())
+            code_of[id(c)] = len(algo_tab)
+            algo_tab.append(0 if c.algo == ALGO_MEASURED else 1)
+            path_tab.append(self.path_ids.setdefault(c.path, len(self.path_ids)))
+        code = np.fromiter(map(code_of.__getitem__, map(id, colls)), np.int64, n)
+        self.strat_algo = np.asarray(algo_tab, np.uint8)[code] if n else np.zeros(0, np.uint8)
+        self.strat_path = np.asarray(path_tab, np.int32)[code] if n else np.zeros(0, np.int32)
+        self.strat_ov = np.full(n, -1, np.int32)
+        ovs = list(map(_OVERRIDES, configs))
+        for i in np.flatnonzero(np.fromiter(map(bool, ovs), bool, n)).tolist():
+            ov_key = tuple(ovs[i].items())
             if ov_key not in ov_key_to_id:
                 ov_key_to_id[ov_key] = len(ov_sets)
-                ov_sets.append(resolve_overrides(ov, ids))
+                ov_sets.append(resolve_overrides(ovs[i], ids))
             self.strat_ov[i] = ov_key_to_id[ov_key]
         # document.DocumentGraph: the C++ loader already interned ops, signatures and comm rows
         doc = (getattr(g, "signatures", None) is not None and variant_rows is None and variant_arrays is None
@@ -480,11 +531,13 @@ class LoweredProfiles:
             if variant_rows is None:
                 variant_rows = [] if doc else [node_rows(g, ids)]
             variant_arrays = [row_arrays(rows) for rows in variant_rows]
-        GV = 1 if doc else len(variant_arrays)
+        GV = 1 if doc else (variant_arrays["fid"].shape[0] if isinstance(variant_arrays, dict) else len(variant_arrays))
         self.n_gvariants = GV
-        self.strat_gv = list(strat_gv) if strat_gv is not None else [0] * len(configs)
+        self.strat_gv = (np.asarray(strat_gv, np.int32) if strat_gv is not None
+                         else np.zeros(len(configs), np.int32))
         # per node: op, kind (structural); per (variant, node): features and comm attributes
         op_ids, sig_ids = {}, {}
+        flat_uniq = None  # registry ids of this class's feature vectors (sig id = index)
         op = np.empty(N, np.int32)
         kind = np.empty(N, np.uint8)
         self.op_nodes = {}
@@ -494,6 +547,12 @@ class LoweredProfiles:
             order = np.argsort(op, kind="stable")
             bounds = np.searchsorted(op[order], np.arange(len(op_ids) + 1))
             self.op_nodes = {name: order[bounds[k]:bounds[k + 1]].tolist() for name, k in op_ids.items()}
+        elif op_kind is not None:  # an expansion's ids: op type and kind code by origin (no objects)
+            ops, kinds = op_kind
+            for i, name in enumerate(ops):
+                op[i] = op_ids.setdefault(name, len(op_ids))
+                self.op_nodes.setdefault(name, []).append(i)
+            kind[:] = kinds
         else:
             for i, nid in enumerate(ids):
                 n = nodes[nid]
@@ -511,15 +570,19 @@ class LoweredProfiles:
             sig[0], cok[0], cbytes[0], gsize[0] = g.sig_of, g.comm["ok"], g.comm["bytes"], g.comm["group"]
             lthr[0], llat[0] = g.comm["thr"], g.comm["lat"]
         if variant_arrays:
-            if any(len(va["fid"]) != N for va in variant_arrays):
+            # a list of per-variant row dicts, or one dict of stacked [GV, N] fields
+            va = variant_arrays if isinstance(variant_arrays, dict) else \
+                {k: np.stack([v[k] for v in variant_arrays]) for k in ROW_FIELDS}
+            if va["fid"].shape != (GV, N):
                 raise ValueError("graph variants must share the class structure")
-            fid = np.stack([va["fid"] for va in variant_arrays])
-            uniq, inv = np.unique(fid, return_inverse=True)  # class-local signature ids
-            sig[:] = inv.reshape(GV, N)
-            sig_ids = {FEATURES.rows[u]: k for k, u in enumerate(uniq.tolist())}
+            fid = va["fid"]
+            present = np.zeros(int(fid.max(initial=-1)) + 1, np.int64)  # class-local signature ids:
+            present[fid.ravel()] = 1                                    # registry ids in ascending order
+            flat_uniq = np.flatnonzero(present)
+            sig[:] = (np.cumsum(present) - 1)[fid]
             for name, dst in (("ok", cok), ("bytes", cbytes), ("gsize", gsize), ("thr", lthr), ("lat", llat)):
-                dst[:] = np.stack([va[name] for va in variant_arrays])
-        self.op_ids, self.sig_ids = op_ids, sig_ids
+                dst[:] = va[name]
+        self.op_ids = op_ids
         # the fused engine forms durations on the fly (base + gap | override) and relies on every
         # one being a finite non-negative double; anything else (NaN included: DurationEntry's
         # `not x >= 0.0`, costmodel.py:78-80) must take the exact K2 path and its error
@@ -533,6 +596,15 @@ class LoweredProfiles:
                 grid = db.op_records.get((opname, hw))
                 if not grid:
                     continue
+                if flat_uniq is not None:  # records whose vectors occur in this class
+                    fids = np.fromiter((FEATURES.ids.get(f, -1) for f in grid), np.int64, len(grid))
+                    loc = np.searchsorted(flat_uniq, fids)
+                    hit = (fids >= 0) & (loc < len(flat_uniq)) & (flat_uniq[np.minimum(loc, len(flat_uniq) - 1)] == fids)
+                    recs = list(grid.values())
+                    for j in np.flatnonzero(hit).tolist():
+                        ekeys.append((h << 42) | (o << 21) | int(loc[j]))
+                        emeans.append(recs[j].mean_duration_us)
+                    continue
                 for feats, rec in grid.items():
                     s = sig_ids.get(feats)
                     if s is not None:
@@ -542,7 +614,16 @@ class LoweredProfiles:
         mkeys, moff, mnames, mcoef, micpt = [], [0], [], [], []
         exact_set = set(ekeys)
         self.models = {}
-        name_pool = {nm for feats in sig_ids for nm, _ in feats}
+        if flat_uniq is not None:  # the class's feature entries, gathered from the registry
+            f_off, f_name, f_val = FEATURES.flat()
+            starts, lens = f_off[flat_uniq], f_off[flat_uniq + 1] - f_off[flat_uniq]
+            seg = np.zeros(len(flat_uniq) + 1, np.int64)
+            np.cumsum(lens, out=seg[1:])
+            take = np.repeat(starts - seg[:-1], lens) + np.arange(int(seg[-1]), dtype=np.int64)
+            g_names, g_vals = f_name[take], f_val[take]
+            name_pool = {FEATURES.name_list[k] for k in np.unique(g_names).tolist()}
+        else:
+            name_pool = {nm for feats in sig_ids for nm, _ in feats}
         fitted = []
         for hw, h in self.hw_ids.items():
             for opname, o in op_ids.items():
@@ -571,12 +652,20 @@ class LoweredProfiles:
             moff.append(len(mnames))
             micpt.append(m.intercept)
         # feature vectors
-        soff, sname, sval = [0], [], []
-        for feats in sig_ids:  # insertion order == id order
-            for nm, v in feats:
-                sname.append(name_id[nm])
-                sval.append(v)
-            soff.append(len(sname))
+        if flat_uniq is not None:  # names ascend within a vector in both orders (ids follow the sorted names)
+            local = np.full(len(FEATURES.name_list), -1, np.int64)
+            for nm, i in name_id.items():
+                k = FEATURES.names.get(nm)
+                if k is not None:
+                    local[k] = i
+            soff, sname, sval = seg, local[g_names], g_vals
+        else:
+            soff, sname, sval = [0], [], []
+            for feats in sig_ids:  # insertion order == id order
+                for nm, v in feats:
+                    sname.append(name_id[nm])
+                    sval.append(v)
+                soff.append(len(sname))
         # links
         n_paths = len(self.path_ids)
         uni_ok = np.zeros(max(n_paths, 1), np.uint8)
@@ -608,48 +697,49 @@ class LoweredProfiles:
 
         ek, em = srt(ekeys, np.asarray(emeans, np.float64))
         nk, nt = srt(nkeys, np.asarray(nthr, np.float64))
-        d = device
-        T = lambda a, dt: _dev_tensor(np.asarray(a, dt).ravel() if np.size(a) else np.zeros(1, dt), d, dt)  # noqa: E731
-        self.tensors = dict(
-            op=T(op, np.int32), kind=T(kind, np.uint8), sig=T(sig, np.int32), cbytes=T(cbytes, np.int64),
-            cok=T(cok, np.uint8), gsize=T(gsize, np.int32), lthr=T(lthr, np.float64), llat=T(llat, np.float64),
-            soff=T(soff, np.int32), sname=T(sname, np.int32), sval=T(sval, np.float64),
-            ek=T(ek, np.uint64), em=T(em, np.float64),
-            mk=T(np.asarray(mkeys, np.uint64), np.uint64), moff=T(moff, np.int32), mname=T(mnames, np.int32),
-            mcoef=T(mcoef, np.float64), micpt=T(micpt, np.float64),
-            nk=T(nk, np.uint64), nt=T(nt, np.float64),
-            uok=T(uni_ok, np.uint8), uthr=T(uni_thr, np.float64), ulat=T(uni_lat, np.float64),
-            ooff=T(ooff, np.int32), onode=T(onode, np.int32), oval=T(oval, np.float64),
-        )
+        up = upload(dict(
+            op=(op, np.int32), kind=(kind, np.uint8), sig=(sig, np.int32), cbytes=(cbytes, np.int64),
+            cok=(cok, np.uint8), gsize=(gsize, np.int32), lthr=(lthr, np.float64), llat=(llat, np.float64),
+            soff=(soff, np.int32), sname=(sname, np.int32), sval=(sval, np.float64),
+            ek=(ek, np.uint64), em=(em, np.float64),
+            mk=(np.asarray(mkeys, np.uint64), np.uint64), moff=(moff, np.int32), mname=(mnames, np.int32),
+            mcoef=(mcoef, np.float64), micpt=(micpt, np.float64),
+            nk=(nk, np.uint64), nt=(nt, np.float64),
+            uok=(uni_ok, np.uint8), uthr=(uni_thr, np.float64), ulat=(uni_lat, np.float64),
+            ooff=(ooff, np.int32), onode=(onode, np.int32), oval=(oval, np.float64),
+            s_hw=(self.strat_hw, np.int32), s_gap=(self.strat_gap, np.float64), s_algo=(self.strat_algo, np.uint8),
+            s_path=(self.strat_path, np.int32), s_ov=(self.strat_ov, np.int32), s_gv=(self.strat_gv, np.int32)),
+            device)
+        self.tensors = {k: v for k, v in up.items() if not k.startswith("s_")}
         t = self.tensors
         pp = native.ptr
         self.struct = native.ProfileTables(
             pp(t["op"]), pp(t["kind"]), pp(t["sig"]), pp(t["cbytes"]), pp(t["cok"]), pp(t["gsize"]),
             pp(t["lthr"]), pp(t["llat"]),
-            len(sig_ids), pp(t["soff"]), pp(t["sname"]), pp(t["sval"]),
+            len(flat_uniq) if flat_uniq is not None else len(sig_ids), pp(t["soff"]), pp(t["sname"]),
+            pp(t["sval"]),
             len(ekeys), pp(t["ek"]), pp(t["em"]),
             len(mkeys), pp(t["mk"]), pp(t["moff"]), pp(t["mname"]), pp(t["mcoef"]), pp(t["micpt"]),
             len(nkeys), pp(t["nk"]), pp(t["nt"]),
             n_paths, pp(t["uok"]), pp(t["uthr"]), pp(t["ulat"]),
             len(ov_sets), pp(t["ooff"]), pp(t["onode"]), pp(t["oval"]))
         self.n_sims = len(configs)
-        self.t_strat = dict(hw=T(self.strat_hw, np.int32), gap=T(self.strat_gap, np.float64),
-                            algo=T(self.strat_algo, np.uint8), path=T(self.strat_path, np.int32),
-                            ov=T(self.strat_ov, np.int32), gv=T(self.strat_gv, np.int32))
+        self.t_strat = {k[2:]: v for k, v in up.items() if k.startswith("s_")}
         s = self.t_strat
         self.strategies = native.Strategies(self.n_sims, pp(s["hw"]), pp(s["gap"]), pp(s["algo"]), pp(s["path"]),
                                             pp(s["ov"]), pp(s["gv"]))
 
     def _needs_model(self, h, o, opname, sig, exact_set, ids, ov_sets) -> bool:
         """True if some node of this op, not overridden in every strategy, has no exact record."""
+        ov_h = self.strat_ov[self.strat_hw == h]
+        sets = [ov_sets[k] for k in np.unique(ov_h).tolist()] if ov_h.size and (ov_h >= 0).all() else None
         for i in self.op_nodes.get(opname, ()):
             for gv in range(sig.shape[0]):
                 key = (h << 42) | (o << 21) | int(sig[gv, i])
                 if key in exact_set:
                     continue
-                if self.strat_ov and all(k >= 0 and ids[i] in ov_sets[k]
-                                         for k, hh in zip(self.strat_ov, self.strat_hw) if hh == h):
-                    continue
+                if sets is not None and all(ids[i] in res for res in sets):
+                    continue  # overridden for every strategy of this hardware tag
                 return True
         return False
 

@@ -39,7 +39,8 @@ class BaseGraph(ctypes.Structure):
 
 class ExpandPlan(ctypes.Structure):
     _fields_ = [("replicas", I32), ("n_collectives", I32), ("clone_rank", P), ("coll_rank", P), ("map_dev", P),
-                ("fabric_dev", I32)]
+                ("fabric_dev", I32), ("ps", I32), ("push_rank", P), ("pull_rank", P), ("up_dev", P), ("down_dev", P),
+                ("ps_dev", I32)]
 
 
 class ProfileTables(ctypes.Structure):
@@ -125,6 +126,7 @@ _SIGNATURES = {
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P]),
     "dfsim_critical_path_levels_capacity": (I32, [ctypes.POINTER(CpTables)]),
     "dfsim_critical_path_lanes": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I32, I64, P, P, P]),
+    "dfsim_critical_path_lanes_ex": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I32, I64, P, I32, P, P, P]),
     "dfsim_critical_path_lanes_capacity": (I32, [ctypes.POINTER(CpLaneTables), I32]),
     "dfsim_cp_lanes_plan": (ctypes.c_int, [I32, P, P, P, I32, I32, I32, I32, P, P, P, P, P, P]),
     "dfsim_predict_batch": (ctypes.c_int, [P, I32, P, ctypes.c_double, I64, P, P]),

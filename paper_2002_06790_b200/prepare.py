@@ -23,6 +23,7 @@ import os
 import numpy as np
 
 from . import native
+from .lowering import upload
 
 GROUP = 16        # positions processed together (one per lane of a half-warp)
 CHUNK = int(os.environ.get("DFSIM_CP_CHUNK", 32))  # positions prefetched per cp.async batch
@@ -237,6 +238,7 @@ LANE_STAGES = int(os.environ.get("DFSIM_CP_LANE_STAGES", 0))
 
 
 LANE_NEAR = int(os.environ.get("DFSIM_CP_LANE_NEAR", 8))  # chunks a value may wait in a slot
+LANE_MIN_SIMS = int(os.environ.get("DFSIM_CP_LANES_MIN", 16384))  # candidates a class needs for K4 v3
 
 
 def lane_plan(t: Tables, K: int = LANE_K, rmax_min: int = LANE_RMAX, stages: int = LANE_STAGES,
@@ -274,7 +276,7 @@ class ClassTables(Tables):
 
     GROUP, CHUNK, QCAP = GROUP, CHUNK, QCAP
 
-    def __init__(self, lg, host=None):
+    def __init__(self, lg, host=None, n_sims: int | None = None):
         self.ctx = lg.ctx
         if host is None:
             host = dict(succ_off=lg.t_succ_off[: lg.n + 1].cpu().numpy(),
@@ -286,40 +288,53 @@ class ClassTables(Tables):
         if not self.fused_ok:
             return
         d = self.ctx.device
-        T = lambda a, dt: _t(a, dt, d)  # noqa: E731
         p = native.ptr
-        self.t = t = dict(
-            meta=T(self.meta, np.uint32), succ=T(self.succ, np.uint32), cidx=T(self.cidx, np.uint16),
-            cnt_init=T(self.cnt_init, np.uint32), rank16=T(self.rank_of_pos, np.uint16),
-            eng_sources=T(self.eng_sources, np.int32), pos32=T(self.pos, np.int32),
-            rank_of_pos=T(self.rank_of_pos, np.int32))
+        tabs = dict(meta=(self.meta, np.uint32), succ=(self.succ, np.uint32), cidx=(self.cidx, np.uint16),
+                    cnt_init=(self.cnt_init, np.uint32), rank16=(self.rank_of_pos, np.uint16),
+                    eng_sources=(self.eng_sources, np.int32), pos32=(self.pos, np.int32),
+                    rank_of_pos=(self.rank_of_pos, np.int32))
+        # K4 v3 (lane per candidate) when its plan fits, else K4 v2 (level groups).
+        # K4 v3 walks all N positions one after another per warp, so its latency is N steps: it
+        # pays off once a class has enough candidates to keep every SM busy meanwhile
+        # (measured on C2, 65,536: 1.99 ms vs 2.31 ms for K4 v2; C3 / C4 classes of ~200-900
+        # candidates are faster on K4 v2's level groups)
+        enough = n_sims is None or n_sims >= LANE_MIN_SIMS
+        plan = lane_plan(self) if os.environ.get("DFSIM_CP_KERNEL", "lanes") == "lanes" and enough else None
+        if plan is not None:
+            tabs.update(l_blocks=(plan["blocks"], np.uint32), l_boff=(plan["block_off"], np.int32),
+                        l_bounds=(plan["bounds"], np.int32), l_soff=(plan["spill_off"], np.int32),
+                        l_slist=(plan["spill_list"], np.uint16))
+        levels_ok = plan is not None or self.build_levels()
+        if plan is None and levels_ok:
+            tabs.update(cp_slot=(self.cp_slot, np.uint16), cp_spill=(self.cp_spill, np.uint16),
+                        cp_meta=(self.cp_meta, np.uint32), cp_succ=(self.cp_succ_abs, np.uint16),
+                        group_off=(self.group_off, np.int32), chunk_off=(self.chunk_off, np.int32),
+                        spill_off=(self.spill_off, np.int32), spill_list=(self.spill_list, np.uint16),
+                        pinfo=(self.pinfo, np.uint32))
+        self.t = t = upload(tabs, d)  # one host-to-device copy for the class's tables
         self.sim_struct = native.SimTables(lg.n, lg.n_devices, self.n_edges, p(t["meta"]), p(lg.t_succ_off),
                                            p(t["succ"]), p(t["cidx"]), p(t["cnt_init"]), self.counter_words,
                                            self.counter_bits, p(t["rank16"]), p(t["eng_sources"]), lg.n_sources,
                                            self.QCAP,
                                            p(lg.t_dev), int(self.succ_packed))
-        # K4 v3 (lane per candidate) when its plan fits, else K4 v2 (level groups)
-        if os.environ.get("DFSIM_CP_KERNEL", "lanes") == "lanes":
-            plan = lane_plan(self)
-            if plan is not None:
-                t.update(l_blocks=T(plan["blocks"], np.uint32), l_boff=T(plan["block_off"], np.int32),
-                         l_bounds=T(plan["bounds"], np.int32), l_soff=T(plan["spill_off"], np.int32),
-                         l_slist=T(plan["spill_list"], np.uint16))
-                st = native.CpLaneTables(lg.n, plan["n_chunks"], plan["K"], plan["n_slots"], plan["rmax"],
-                                         plan["n_long"], plan["n_spill_list"], plan["block_max"], p(t["l_blocks"]),
-                                         p(t["l_boff"]), p(t["l_bounds"]), p(t["l_soff"]), p(t["l_slist"]),
-                                         p(t["rank_of_pos"]))
-                if self.ctx.lib.dfsim_critical_path_lanes_capacity(native.ctypes.byref(st), plan["stages"]) > 0:
-                    self.lane, self.lane_struct = plan, st
+        if plan is not None:
+            st = native.CpLaneTables(lg.n, plan["n_chunks"], plan["K"], plan["n_slots"], plan["rmax"],
+                                     plan["n_long"], plan["n_spill_list"], plan["block_max"], p(t["l_blocks"]),
+                                     p(t["l_boff"]), p(t["l_bounds"]), p(t["l_soff"]), p(t["l_slist"]),
+                                     p(t["rank_of_pos"]))
+            if self.ctx.lib.dfsim_critical_path_lanes_capacity(native.ctypes.byref(st), plan["stages"]) > 0:
+                self.lane, self.lane_struct = plan, st
         if self.lane is None:
-            if not self.build_levels():
-                self.fused_ok = False
-                return
-            t.update(cp_slot=T(self.cp_slot, np.uint16), cp_spill=T(self.cp_spill, np.uint16),
-                     cp_meta=T(self.cp_meta, np.uint32), cp_succ=T(self.cp_succ_abs, np.uint16),
-                     group_off=T(self.group_off, np.int32), chunk_off=T(self.chunk_off, np.int32),
-                     spill_off=T(self.spill_off, np.int32), spill_list=T(self.spill_list, np.uint16),
-                     pinfo=T(self.pinfo, np.uint32))
+            if not levels_ok or "cp_meta" not in t:
+                if not self.build_levels():
+                    self.fused_ok = False
+                    return
+                t.update(upload(dict(
+                    cp_slot=(self.cp_slot, np.uint16), cp_spill=(self.cp_spill, np.uint16),
+                    cp_meta=(self.cp_meta, np.uint32), cp_succ=(self.cp_succ_abs, np.uint16),
+                    group_off=(self.group_off, np.int32), chunk_off=(self.chunk_off, np.int32),
+                    spill_off=(self.spill_off, np.int32), spill_list=(self.spill_list, np.uint16),
+                    pinfo=(self.pinfo, np.uint32)), d))
             self.cp_struct = native.CpTables(lg.n, self.n_slots, self.n_edges, p(t["rank_of_pos"]), p(t["cp_meta"]),
                                              p(t["cp_slot"]), p(t["cp_succ"]), self.n_groups, p(t["group_off"]),
                                              self.n_chunks, p(t["chunk_off"]), self.CHUNK, self.n_long,
@@ -327,8 +342,16 @@ class ClassTables(Tables):
                                              self.max_spill_reads, p(t["pinfo"]), self.slot_region,
                                              self.stage_doubles)
 
-    def critical_path(self, n_sims: int, sched, cp_len, cp_src):
-        """K4 over the fused engine's schedules: v3 (lane per candidate) when planned, else v2."""
+    def critical_path(self, n_sims: int, sched, cp_len, cp_src, rows=None):
+        """K4 over the fused engine's schedules: v3 (lane per candidate) when planned, else v2.
+        ``rows``: only these candidates (K4 v3's register variant takes a candidate list)."""
+        if self.lane is not None and rows and self.lane["stages"] == 0:
+            import torch
+
+            order = torch.as_tensor(sorted(set(rows)), dtype=torch.int64, device=f"cuda:{self.ctx.device}")
+            self.ctx.call("dfsim_critical_path_lanes_ex", native.ctypes.byref(self.lane_struct), 0, order.numel(),
+                          native.ptr(order), 0, native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
+            return
         if self.lane is not None:
             self.ctx.call("dfsim_critical_path_lanes", native.ctypes.byref(self.lane_struct), self.lane["stages"],
                           n_sims, native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
@@ -339,15 +362,3 @@ class ClassTables(Tables):
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
         """Schedule row(s) stored by position -> node-rank order."""
         return arr_by_pos[..., self.pos]
-
-
-def _t(a, dt, device):
-    import torch
-
-    arr = np.ascontiguousarray(np.asarray(a).astype(dt, copy=False))
-    if arr.size == 0:
-        arr = np.zeros(1, dt)
-    for src, dst in ((np.uint64, np.int64), (np.uint32, np.int32), (np.uint16, np.int16)):
-        if arr.dtype == src:
-            arr = arr.view(dst)
-    return torch.from_numpy(arr).to(f"cuda:{device}")

@@ -56,7 +56,7 @@ def _special_rows(kind, ids, pos, g_b, structure, cfg) -> dict:
     else:
         from .ps import ps_nodes
 
-        gx = structure.graph
+        specs = structure.device_specs  # the PS links (throughput, latency)
         built = {}
         for p in pos:
             cid = ids[p]
@@ -66,14 +66,14 @@ def _special_rows(kind, ids, pos, g_b, structure, cfg) -> dict:
                 nodes = {f"{gid}@r{k}": grad for k in range(cfg.replicas)}
                 for n in ps_nodes(gid, grad, cfg, cfg.ps_device):
                     nodes[n.id] = n
-                built[gid] = _Stand(nodes, gx.devices)
+                built[gid] = _Stand(nodes, specs)
             out.append(node_rows(built[gid], [cid])[0])
     return row_arrays(out)
 
 
 def variant_arrays(kind: str, ids, g_b, structure, cfg=None, db=None, cache=None) -> dict:
     """Estimate-input rows (rank order ``ids``) of variant graph ``g_b`` for a class of
-    ``kind`` "plain" | "dp" (structure: ExpansionPlan) | "ps" (structure: ExpandedGraph), as
+    ``kind`` "plain" | "dp" | "ps" (structure: ExpansionPlan), as
     arrays (lowering.ROW_FIELDS; features as FEATURES ids).
 
     A clone's row is its base node's (its producers are clones or the collective, all carrying
@@ -101,7 +101,8 @@ def variant_arrays(kind: str, ids, g_b, structure, cfg=None, db=None, cache=None
     perm, special = cache["perm"], cache["special"]
     out = {k: base[k][perm] for k in ROW_FIELDS}
     if len(special):
-        key = tuple(g_b.nodes[gid].output_shapes for gid in cache["grads"])
+        nodes = g_b.nodes  # key: the gradients' output shapes as plain tuples (cheap to hash)
+        key = tuple((s.dims, s.dtype_bytes) for gid in cache["grads"] for s in nodes[gid].output_shapes)
         rows = cache.get(("special", key))
         if rows is None:
             rows = cache[("special", key)] = _special_rows(kind, ids, special.tolist(), g_b, structure, cfg)
@@ -110,4 +111,49 @@ def variant_arrays(kind: str, ids, g_b, structure, cfg=None, db=None, cache=None
     return out
 
 
-__all__ = ["structure_key", "rows_for", "variant_arrays", "node_features"]
+__all__ = ["structure_key", "rows_for", "variant_arrays", "variant_arrays_many", "node_features"]
+
+
+def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None) -> dict:
+    """``variant_arrays`` of several graph variants of one class, stacked: each field [GV, N].
+    Vectorised over the variants: one gather of the stacked base rows, and the added nodes'
+    rows once per distinct gradient-shape tuple."""
+    cache: dict = {}
+    variant_arrays(kind, ids, graphs[0], structure, cfg, db, cache)  # fills perm / special / grads
+    perm, special, grads = cache["perm"], cache["special"], cache["grads"]
+    bases = [base_arrays(gb)[0] for gb in graphs]
+    out = {k: np.stack([b[k] for b in bases])[:, perm] for k in ROW_FIELDS}
+    if len(special):
+        groups: dict = {}
+        gkey = tuple(grads)
+        for v, gb in enumerate(graphs):
+            memo = gb.__dict__.get("_dfsim_grad_keys")
+            if memo is None:
+                memo = {}
+                try:
+                    object.__setattr__(gb, "_dfsim_grad_keys", memo)
+                except (AttributeError, TypeError):
+                    pass
+            key = memo.get(gkey)
+            if key is None:
+                nodes = gb.nodes
+                key = memo[gkey] = tuple((s.dims, s.dtype_bytes) for gid in grads for s in nodes[gid].output_shapes)
+            groups.setdefault(key, []).append(v)
+        for key, vs in groups.items():
+            rows = cache.get(("special", key))
+            if rows is None:
+                rows = _special_rows(kind, ids, special.tolist(), graphs[vs[0]], structure, cfg)
+            sel = np.ix_(np.asarray(vs, np.int64), special)
+            for k in ROW_FIELDS:
+                out[k][sel] = rows[k]
+    return out
+
+
+__all__ = ["structure_key", "rows_for", "variant_arrays", "variant_arrays_many", "node_features"]
+
+
+def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None) -> dict:
+    """``variant_arrays`` of several graph variants of one class, stacked: each field [GV, N]."""
+    cache: dict = {}
+    rows = [variant_arrays(kind, ids, gb, structure, cfg, db, cache) for gb in graphs]
+    return {k: np.stack([r[k] for r in rows]) for k in ROW_FIELDS}

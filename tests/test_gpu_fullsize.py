@@ -44,9 +44,7 @@ def test_headline_class_full_size_properties():
     o = tc.run(schedules=True)
     rec = tc.best(o).cpu()
     lg, S, N = tc.lg, len(configs), tc.lg.n
-    pos = torch.as_tensor(tc.tables.pos, device="cuda:0")
-    st = o["start"][:, :N].index_select(1, pos)   # node-rank order
-    fi = o["finish"][:, :N].index_select(1, pos)
+    st, fi = tc.rows_by_rank_batch(o, range(S))   # node-rank order
     assert int((o["n_placed"] == N).sum()) == S
     assert torch.equal(o["makespan"], fi.max(dim=1).values)
     ref = parity.oracle_grid_isolated("resnet50-dp8", sims=65536, schedules=True)
@@ -71,10 +69,7 @@ def _class_invariants(tc, o):
     import torch
 
     lg, N = tc.lg, tc.lg.n
-    st, fi = o["start"][:, :N], o["finish"][:, :N]
-    if o.get("layout") == "position":
-        pos = torch.as_tensor(tc.tables.pos, device=st.device)
-        st, fi = st.index_select(1, pos), fi.index_select(1, pos)
+    st, fi = tc.rows_by_rank_batch(o, range(tc.lp.n_sims))
     assert bool((o["n_placed"] == N).all())
     assert bool((fi >= st).all())
     assert torch.equal(o["makespan"], fi.max(dim=1).values)
@@ -145,9 +140,8 @@ def test_global_duration_row_class_matches_exact_engine():
         c.expand()
     o, r = tc.run(schedules=True), ref.run(schedules=True)
     N = tc.lg.n
-    pos = torch.as_tensor(tc.tables.pos, device="cuda:0")
-    assert torch.equal(o["start"][:, :N].index_select(1, pos), r["start"][:, :N])
-    assert torch.equal(o["finish"][:, :N].index_select(1, pos), r["finish"][:, :N])
+    st, fi = tc.rows_by_rank_batch(o, range(len(configs)))
+    assert torch.equal(st, r["start"][:, :N]) and torch.equal(fi, r["finish"][:, :N])
     assert torch.equal(o["makespan"], r["makespan"])
     assert torch.equal(o["cp_len"], r["cp_len"])
     for i in (0, len(configs) // 2, len(configs) - 1):

@@ -180,3 +180,63 @@ def test_sweep_unfused_matches_fused_on_layered(pipeline_cases):
             r = fw.sweep(g, db, [cfg] * 3, keep_schedules=True)
         assert r.schedule(2).to_json() == json.dumps(c["expect"]["schedule"]), c["name"]
         assert r.cp_len[1] == c["expect"]["cp"][0]
+
+
+def test_fused_row_layout_with_level_kernel(resnet, monkeypatch):
+    """A class without a K4 v3 plan keeps row-layout schedules and K4 v2 (level groups):
+    forced here; results must still equal the unfused kernels, overflow fallback included."""
+    from paper_2002_06790_b200.batch import TopologyClass
+    from paper_2002_06790_b200.prepare import ClassTables
+
+    g, db = resnet
+    monkeypatch.setenv("DFSIM_CP_KERNEL", "levels")
+    for qcap in (16, 2):
+        monkeypatch.setattr(ClassTables, "QCAP", qcap)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            tf = TopologyClass(g, db, _configs(40), fused=True)
+            tu = TopologyClass(g, db, _configs(40), fused=False)
+        assert tf.tables.lane is None and tf.tables.cp_struct is not None
+        _compare(tf, tu)
+
+
+def test_lane_kernel_partial_warps(resnet, monkeypatch):
+    """Candidate counts that leave the last 32-candidate warp of K4 v3 partly empty, and one
+    candidate alone, must agree with the unfused kernels (K4 v3 forced below its class-size
+    threshold)."""
+    from paper_2002_06790_b200 import prepare
+    from paper_2002_06790_b200.batch import TopologyClass
+
+    monkeypatch.setattr(prepare, "LANE_MIN_SIMS", 1)
+    g, db = resnet
+    for n in (1, 33, 70):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            tf = TopologyClass(g, db, _configs(n), fused=True)
+            tu = TopologyClass(g, db, _configs(n), fused=False)
+        assert tf.tables.lane is not None
+        _compare(tf, tu)
+
+
+def test_lane_kernel_with_overflow_reruns(resnet, monkeypatch):
+    """K4 v3 (forced) after ring-overflow re-runs: the critical paths of just the re-run
+    candidates are redone through the candidate-list entry (dfsim_critical_path_lanes_ex)."""
+    from paper_2002_06790_b200 import prepare
+    from paper_2002_06790_b200.batch import TopologyClass
+    from paper_2002_06790_b200.prepare import ClassTables
+
+    monkeypatch.setattr(prepare, "LANE_MIN_SIMS", 1)
+    monkeypatch.setattr(ClassTables, "QCAP", 2)
+    g, db = resnet
+    cfgs = _configs(45)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        tf = TopologyClass(g, db, cfgs, fused=True)
+        tu = TopologyClass(g, db, cfgs, fused=False)
+    assert tf.tables.lane is not None
+    o = tf.run(defer_fallback=True)
+    assert tf.fallback_if_needed(o) and o["fallback_rows"]
+    tf.critical_path_only(o)
+    ou = tu.run()
+    assert np.array_equal(o["makespan"].cpu().numpy(), ou["makespan"].cpu().numpy())
+    assert np.array_equal(o["cp_len"].cpu().numpy(), ou["cp_len"].cpu().numpy())

@@ -41,9 +41,14 @@ def test_ps_rows_match_materialised():
     cfg = _cfg(4, "parameter_server", "RDMA")
     ex0 = expand_parameter_server(g0, cfg, db)
     ids = sorted(ex0.graph.nodes)
+    plan = ExpansionPlan(g0, cfg, run_k1=False, db=db)  # the class structure K1 emits in PS mode
+    assert plan.ids == ids and plan.devices == sorted(ex0.graph.devices)
+    assert plan.origin == ex0.origin
+    assert plan.op_kind() == ([ex0.graph.nodes[i].op_type for i in ids],
+                              [{"Compute": 0, "Transfer": 1}.get(ex0.graph.nodes[i].kind, 2) for i in ids])
     for gb in (g0, g1):
         gx = expand_parameter_server(gb, cfg, db).graph
-        assert rows_for("ps", ids, gb, ex0, cfg, db) == node_rows(gx, ids)
+        assert rows_for("ps", ids, gb, plan, cfg, db) == node_rows(gx, ids)
 
 
 def test_plain_rows_and_batch_dependence():
@@ -51,3 +56,23 @@ def test_plain_rows_and_batch_dependence():
     ids = sorted(g0.nodes)
     r0, r1 = rows_for("plain", ids, g0, None), rows_for("plain", ids, g1, None)
     assert r0 != r1 and [x[1:] for x in r0] == [x[1:] for x in r1]  # features differ, comm rows equal
+
+
+@pytest.mark.parametrize("sync", ["allreduce", "parameter_server"])
+def test_variant_arrays_many_equals_per_variant(sync):
+    """The stacked, vectorised rows of many graph variants equal the per-variant rows."""
+    import numpy as np
+
+    from paper_2002_06790_b200.lowering import ROW_FIELDS
+    from paper_2002_06790_b200.variants import variant_arrays, variant_arrays_many
+
+    graphs = [W.vgg16_training(batch=b) for b in (8, 24, 40)]
+    db = W.model_profiles(graphs[0], ["hw0"])
+    cfg = _cfg(4, sync, "RDMA")
+    plan = ExpansionPlan(graphs[0], cfg, run_k1=False, db=db)
+    kind = "ps" if sync == "parameter_server" else "dp"
+    many = variant_arrays_many(kind, plan.ids, graphs, plan, cfg, db)
+    for v, gb in enumerate(graphs):
+        one = variant_arrays(kind, plan.ids, gb, plan, cfg, db, {})
+        for k in ROW_FIELDS:
+            assert np.array_equal(many[k][v], one[k]), (k, v)
