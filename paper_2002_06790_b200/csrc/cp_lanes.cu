@@ -225,7 +225,7 @@ __device__ __forceinline__ void ldg_v4(double (&d)[4], const double *p) {
                  : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
 }
 
-template <int K>
+template <int K, bool kPingPong>
 __global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NST = 2, NU = K / 2 + 1;  // 32-byte units per window
@@ -355,7 +355,8 @@ __global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) 
                     double best = m23 > m01 ? m23 : m01;
                     if (deg > 4) {
                         const unsigned ex = blk + 2u * (r.y >> 8);
-                        for (unsigned j = 4; j < deg; j++) {
+#pragma unroll 1
+                        for (unsigned j = 4; j < deg; j++) {  // rare (wide fan-outs): kept compact
                             const double x = lds_d(a_lane + 256u * lds_h(ex + 2u * (j - 4)));
                             best = x > best ? x : best;
                         }
@@ -374,9 +375,19 @@ __global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) 
             }
             __syncwarp();
         };
-        for (int q = 0; q < NQ; q += 2) {  // two chunks per iteration: the window registers swap roles
-            process(q, wa, wb);
-            if (q + 1 < NQ) process(q + 1, wb, wa);
+        if constexpr (kPingPong) {
+            for (int q = 0; q < NQ; q += 2) {  // two chunks per iteration: the window registers swap roles
+                process(q, wa, wb);
+                if (q + 1 < NQ) process(q + 1, wb, wa);
+            }
+        } else {
+            for (int q = 0; q < NQ; q++) {  // one copy of the chunk body (half the code)
+                process(q, wa, wb);
+#pragma unroll
+                for (int u = 0; u < NU; u++)
+#pragma unroll
+                    for (int e = 0; e < 4; e++) wa[u][e] = wb[u][e];
+            }
         }
         if (live) {
             a.cp_len[s] = src == 0x7fffffff ? 0.0 : len;
@@ -610,7 +621,11 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
         kern<<<grid, wpb * 32, smem, ctx->stream>>>(a);
         return dfsim_after_launch(ctx, "k_critical_path_lanes");
     };
-    if (stages == 0) return launch(k_critical_path_lanes_reg<8>);
+    static const bool kPP = [] {  // DFSIM_CP_PINGPONG=0: single chunk body (measurement knob)
+        const char *e = std::getenv("DFSIM_CP_PINGPONG");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (stages == 0) return kPP ? launch(k_critical_path_lanes_reg<8, true>) : launch(k_critical_path_lanes_reg<8, false>);
     if (t->chunk_positions == 16) return stages == 2 ? launch(k_critical_path_lanes<16, 2>) : launch(k_critical_path_lanes<16, 3>);
     return stages == 2 ? launch(k_critical_path_lanes<8, 2>) : launch(k_critical_path_lanes<8, 3>);
 }
