@@ -394,6 +394,20 @@ int dfsim_comm_batch(dfsim_ctx *ctx, int64_t n, const uint8_t *kind, const int64
  * order[n]; returns how many nodes were ordered (< n: a cycle), -1 on bad arguments. */
 int32_t dfsim_topological_order(int32_t n, const int32_t *succ_off, const int32_t *succ_idx, const int32_t *indeg,
                                 int32_t *order);
+/* Host planning of a topology class (csrc/levels.cpp; no reference counterpart: table layout).
+ * dfsim_level_order: Kahn waves (each sorted by rank) into order[n], level[n] and
+ * level_off[n + 1]; returns the number of levels, -1 for a cycle, -2 on bad arguments. */
+int32_t dfsim_level_order(int32_t n, const int32_t *succ_off, const int32_t *succ_idx, const int32_t *indeg,
+                          int32_t *order, int32_t *level, int32_t *level_off);
+/* dfsim_cp_levels_plan: the K4 v2 tables (CpTables) from the rank CSR and the level order.
+ * Capacities: group_off / chunk_off / spill_off n + 1, slot_of_pos / spill_of_pos / cp_meta /
+ * pinfo n, spill_list / cp_succ / cp_succ_abs n_edges.  info[8] = n_groups, n_chunks, n_slots,
+ * n_long, max_spill_reads, n_spill_list, slot_region, stage_doubles.  0 on success. */
+int32_t dfsim_cp_levels_plan(int32_t n, const int32_t *succ_off, const int32_t *succ_idx, const int32_t *indeg,
+                             const int32_t *order, const int32_t *level_off, int32_t n_levels, int32_t group,
+                             int32_t chunk, int32_t *group_off, int32_t *chunk_off, int32_t *slot_of_pos,
+                             int32_t *spill_of_pos, int32_t *spill_off, int32_t *spill_list, int32_t *cp_succ,
+                             int32_t *cp_succ_abs, uint32_t *cp_meta, uint32_t *pinfo, int32_t *info);
 
 /* ---------------------------------------------------------------- best strategy (K5) */
 /* First minimum of (value, index) over n values; index = index_base + i.

@@ -132,6 +132,8 @@ _SIGNATURES = {
     "dfsim_predict_batch": (ctypes.c_int, [P, I32, P, ctypes.c_double, I64, P, P]),
     "dfsim_comm_batch": (ctypes.c_int, [P, I64, P, P, P, P, P, P]),
     "dfsim_topological_order": (I32, [I32, P, P, P, P]),
+    "dfsim_level_order": (I32, [I32, P, P, P, P, P, P]),
+    "dfsim_cp_levels_plan": (I32, [I32, P, P, P, P, P, I32, I32, I32] + [P] * 11),
     "dfsim_fused_capacity": (I32, [ctypes.POINTER(SimTables)]),
     "dfsim_fused_chunk": (I32, [ctypes.POINTER(SimTables), I64, I32]),
     "dfsim_argmin": (ctypes.c_int, [P, I64, P, I64, P]),

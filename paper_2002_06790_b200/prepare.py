@@ -30,32 +30,24 @@ CHUNK = int(os.environ.get("DFSIM_CP_CHUNK", 32))  # positions prefetched per cp
 QCAP = 16         # per-device FIFO ring capacity of the fused engine (overflow -> exact engine)
 
 
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
 def level_order(n: int, succ_off: np.ndarray, succ_idx: np.ndarray, indeg: np.ndarray):
-    """Kahn waves with numpy: returns (order, level_of_rank, level_offsets) or None on a cycle."""
-    left = indeg.astype(np.int64).copy()
-    frontier = np.nonzero(left == 0)[0]
-    order, offsets = [], [0]
-    level = np.full(n, -1, dtype=np.int64)
-    lv = 0
-    while frontier.size:
-        frontier = np.sort(frontier)
-        order.append(frontier)
-        level[frontier] = lv
-        offsets.append(offsets[-1] + frontier.size)
-        starts, ends = succ_off[frontier], succ_off[frontier + 1]
-        cnt = ends - starts
-        if cnt.sum() == 0:
-            break
-        eidx = np.repeat(ends - cnt.cumsum(), cnt) + np.arange(cnt.sum())
-        targets = succ_idx[eidx]
-        np.subtract.at(left, targets, 1)
-        cand = np.unique(targets)
-        frontier = cand[left[cand] == 0]
-        lv += 1
-    order = np.concatenate(order) if order else np.zeros(0, np.int64)
-    if order.size != n:
+    """Kahn waves (dfsim_level_order, host C++): (order, level_of_rank, level_offsets) as int64
+    arrays, or None on a cycle."""
+    lib = native.load_library()
+    off, idx, deg = _i32(succ_off), _i32(succ_idx if len(succ_idx) else np.zeros(1)), _i32(indeg)
+    order, level, loff = (np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.int32),
+                          np.zeros(n + 1, np.int32))
+    pp = lambda a: a.ctypes.data_as(native.P)  # noqa: E731
+    nl = lib.dfsim_level_order(n, pp(off), pp(idx), pp(deg), pp(order), pp(level), pp(loff))
+    if nl == -2:
+        raise ValueError("level_order: bad graph arrays")
+    if nl < 0:
         return None
-    return order, level, np.asarray(offsets, dtype=np.int64)
+    return order[:n].astype(np.int64), level[:n].astype(np.int64), loff[: nl + 1].astype(np.int64)
 
 
 class Tables:
@@ -152,83 +144,30 @@ class Tables:
         self.eng_sources = pos[np.nonzero(indeg == 0)[0]]        # ascending ranks, as positions
 
     def _critical_path(self, N, idx, indeg, outdeg, order, pos, loff):
-        goff = [0]
-        for lv in range(loff.size - 1):
-            a, b = int(loff[lv]), int(loff[lv + 1])
-            for p in range(a, b, self.group):
-                goff.append(min(b, p + self.group))
-        goff = np.asarray(goff, np.int64)
-        coff, start = [0], 0
-        for gi in range(1, goff.size):
-            if goff[gi] - goff[start] > self.chunk:
-                coff.append(gi - 1)
-                start = gi - 1
-        if coff[-1] != goff.size - 1:
-            coff.append(goff.size - 1)
-        coff = np.asarray(coff, np.int64)
-        n_groups, n_chunks = goff.size - 1, coff.size - 1
-        group_of_pos = np.repeat(np.arange(n_groups), np.diff(goff))
-        chunk_of_pos = np.repeat(np.arange(n_chunks), np.diff(coff))[group_of_pos]
-        step_of_pos = (n_groups - 1) - group_of_pos                  # reverse processing order
-        src_of_edge = np.repeat(np.arange(N), outdeg)
-        pu, pv = pos[src_of_edge], pos[idx]                          # reader u, written value v
-        near = chunk_of_pos[pu] >= chunk_of_pos[pv] - 1
-        far = ~near
-        last_near = np.full(N, -1, np.int64)
-        np.maximum.at(last_near, pv[near], step_of_pos[pu[near]])
-        slot_of_pos = np.full(N, 0xFFFF, np.int64)
-        free, nslots, release = [], 0, {}
-        for g in range(n_groups - 1, -1, -1):
-            step = (n_groups - 1) - g
-            free.extend(release.pop(step - 1, ()))
-            for p in range(int(goff[g]), int(goff[g + 1])):
-                if last_near[p] < 0:
-                    continue
-                if free:
-                    sl = free.pop()
-                else:
-                    sl, nslots = nslots, nslots + 1
-                slot_of_pos[p] = sl
-                release.setdefault(int(last_near[p]), []).append(sl)
-        spill_flag = np.zeros(N, bool)
-        spill_flag[pv[far]] = True
-        spill_of_pos = np.full(N, 0xFFFF, np.int64)
-        spill_of_pos[spill_flag] = np.arange(int(spill_flag.sum()))
-        far_chunk, far_k = chunk_of_pos[pu[far]], spill_of_pos[pv[far]]
-        pairs = np.unique(np.stack([far_chunk, far_k], 1), axis=0) if far.any() else np.zeros((0, 2), np.int64)
-        soff = np.zeros(n_chunks + 1, np.int64)
-        if len(pairs):
-            np.add.at(soff, pairs[:, 0] + 1, 1)
-        soff = np.cumsum(soff)
-        bufidx = {(c_, k_): i_ - int(soff[c_]) for i_, (c_, k_) in enumerate(pairs.tolist())}
-        ent = np.where(near, slot_of_pos[pv], 0)
-        if far.any():
-            ent[far] = [0x8000 | bufidx[(c_, k_)] for c_, k_ in zip(far_chunk.tolist(), far_k.tolist())]
-        cp_succ = ent[np.argsort(pu, kind="stable")]               # CSR by reading position
-        cp_off = np.zeros(N + 1, np.int64)
-        cp_off[1:] = np.cumsum(outdeg[order])
-        src_flag = (indeg[order] == 0).astype(np.int64)
-        self.cp_meta = (cp_off[:-1] & 0xFFFF) | (np.minimum(outdeg[order], 255) << 16) | (src_flag << 24)
-        self.cp_slot, self.cp_spill, self.cp_succ = slot_of_pos, spill_of_pos, cp_succ
-        has_slot = slot_of_pos != 0xFFFF
-        self.pinfo = ((np.where(has_slot, slot_of_pos, 0) & 0x7FFF) | (has_slot.astype(np.int64) << 15)
-                      | ((np.where(spill_flag, spill_of_pos, 0) & 0x7FFF) << 16) | (spill_flag.astype(np.int64) << 31))
-        self.group_off, self.chunk_off, self.spill_off = goff, coff, soff
-        self.spill_list = pairs[:, 1] if len(pairs) else np.zeros(0, np.int64)
-        self.n_groups, self.n_chunks = n_groups, n_chunks
-        self.n_slots, self.n_long = nslots, int(spill_flag.sum())
-        self.max_spill_reads = int(np.diff(soff).max(initial=0))
-        # per-candidate shared region (doubles): [slots | stage 0 | stage 1], stage = start K | finish K | spill R;
-        # successor entries become absolute indices into it (the reader's chunk parity picks the stage)
-        self.slot_region = (max(nslots, 1) + 1) // 2 * 2
-        self.stage_doubles = (2 * self.chunk + self.max_spill_reads + 1) // 2 * 2
-        reader_chunk = chunk_of_pos[pu]
-        absent = np.where(near, slot_of_pos[pv], 0)
-        if far.any():
-            absent[far] = [self.slot_region + (c_ & 1) * self.stage_doubles + 2 * self.chunk + bufidx[(c_, k_)]
-                           for c_, k_ in zip(far_chunk.tolist(), far_k.tolist())]
-        del reader_chunk
-        self.cp_succ_abs = absent[np.argsort(pu, kind="stable")]
+        """K4 v2 tables (dfsim_cp_levels_plan, host C++; layout in the module docstring)."""
+        lib = native.load_library()
+        E = int(outdeg.sum())
+        off = np.zeros(N + 1, np.int32)
+        np.cumsum(outdeg, out=off[1:])
+        z = lambda k, dt=np.int32: np.zeros(max(k, 1), dt)  # noqa: E731
+        goff, coff, soff = z(N + 1), z(N + 1), z(N + 1)
+        slot, spill, meta, pinfo = z(N), z(N), z(N, np.uint32), z(N, np.uint32)
+        slist, succ, succ_abs, info = z(E), z(E), z(E), z(8)
+        pp = lambda a: a.ctypes.data_as(native.P)  # noqa: E731
+        rc = lib.dfsim_cp_levels_plan(N, pp(off), pp(_i32(idx) if E else z(1)), pp(_i32(indeg)), pp(_i32(order)),
+                                      pp(_i32(loff)), len(loff) - 1, self.group, self.chunk, pp(goff), pp(coff),
+                                      pp(slot), pp(spill), pp(soff), pp(slist), pp(succ), pp(succ_abs), pp(meta),
+                                      pp(pinfo), pp(info))
+        if rc != 0:
+            raise ValueError(f"dfsim_cp_levels_plan failed ({rc})")
+        ng, nc, nslots, n_long, max_reads, nl, region, stage = (int(x) for x in info)
+        self.cp_meta, self.cp_slot, self.cp_spill = meta[:N].astype(np.int64), slot[:N], spill[:N]
+        self.cp_succ, self.cp_succ_abs, self.pinfo = succ[:E], succ_abs[:E], pinfo[:N].astype(np.int64)
+        self.group_off, self.chunk_off, self.spill_off = goff[: ng + 1], coff[: nc + 1], soff[: nc + 1]
+        self.spill_list = slist[:nl]
+        self.n_groups, self.n_chunks = ng, nc
+        self.n_slots, self.n_long, self.max_spill_reads = nslots, n_long, max_reads
+        self.slot_region, self.stage_doubles = region, stage
 
 
 LANE_K = int(os.environ.get("DFSIM_CP_LANE_K", 8))   # positions per K4 v3 prefetch chunk (8 or 16)
