@@ -308,9 +308,12 @@ __global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) 
 #pragma unroll
             for (int u = 0; u < NU; u++) {
                 const int p0 = a0 + 2 * u;
-                // units wholly before the row are not needed (position >= 0); the row pointer is
+                // units wholly before the row are never read (positions >= 0): they load an
+                // aligned unit at the row start instead (same parity), so that every load is
+                // unconditional -- a predicated load made the compiler stage it through a temporary
+                // and a predicated move that waited for the data on the spot.  The row pointer is
                 // backed by padding past the last row, see dfsim_critical_path_lanes
-                if (p0 + 1 >= 0) ldg_v4(w[u], row + 2 * p0);
+                ldg_v4(w[u], row + 2 * (p0 + 1 >= 0 ? p0 : rowpar));
             }
         };
 

@@ -13,6 +13,8 @@
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 int dfsim_topo_launch(dfsim_ctx *ctx, int32_t N, const int32_t *succ_off, const int32_t *succ_idx,
@@ -125,6 +127,164 @@ __global__ void k_queue_off(int32_t D, const int32_t *dev_count, int32_t *queue_
     }
 }
 
+// ---- K1 for small classes in ONE launch (one 1024-thread CTA): the clone / edge phases of
+// the kernels above, then a block radix sort of 32-bit (producer << bits | consumer) keys,
+// the successor histogram + scan, the source compaction and the queue offsets, all through
+// shared memory.  The multi-kernel path (radix sort, scan, select: ~20 launches) costs more
+// in launch latency than in work at these sizes (C2 N = 4,619; C3 / C4 classes <= 9,474
+// nodes and 13,568 edges), and a multi-class step launches it once per class.
+constexpr int kSmallT = 1024, kSmallIPT = 16, kSmallKeys = kSmallT * kSmallIPT, kSmallN = 16384, kSmallD = 256;
+using SmallSort = cub::BlockRadixSort<uint32_t, kSmallT, kSmallIPT>;
+using SmallScan = cub::BlockScan<int32_t, kSmallT>;
+struct SmallSmem {
+    union {
+        typename SmallSort::TempStorage sort;
+        typename SmallScan::TempStorage scan;
+        uint32_t keys[kSmallKeys];
+    } u;
+    int32_t count[kSmallN + 1];
+    int32_t dev_count[kSmallD + 1];
+    int32_t n_valid;
+};
+
+__device__ __forceinline__ int32_t block_exclusive_scan(SmallSmem &s, int32_t x, int32_t &total) {
+    int32_t out;
+    SmallScan(s.u.scan).ExclusiveSum(x, out, total);
+    __syncthreads();
+    return out;
+}
+
+__global__ void __launch_bounds__(kSmallT, 1)
+    k_expand_small(dfsim_base_graph b, dfsim_expand_plan p, int32_t n_refs, int32_t N, int32_t n_keys, int32_t bits,
+                   int32_t D, int32_t *succ_off, int32_t *succ_idx, int32_t *indeg, int32_t *device, int32_t *sources,
+                   int32_t *queue_off, unsigned long long *small) {
+    extern __shared__ __align__(16) unsigned char small_raw[];
+    SmallSmem &s = *reinterpret_cast<SmallSmem *>(small_raw);
+    const int tid = threadIdx.x;
+    constexpr uint32_t kSent = 0xFFFFFFFFu;
+    for (int i = tid; i <= N; i += kSmallT) s.count[i] = 0;
+    for (int i = tid; i <= D; i += kSmallT) s.dev_count[i] = 0;
+    if (tid == 0) s.n_valid = 0;
+    for (int i = tid; i < kSmallKeys; i += kSmallT) s.u.keys[i] = kSent;
+    __syncthreads();
+    // nodes: in-degree, device, per-device counts (k_expand_nodes)
+    const int32_t n_clone = p.replicas * b.n_base;
+    for (int32_t i = tid; i < N; i += kSmallT) {
+        int32_t r, deg, dev;
+        if (i < n_clone) {
+            const int k = i / b.n_base, v = i - k * b.n_base;
+            r = p.clone_rank[i];
+            deg = b.in_off[v + 1] - b.in_off[v];
+            dev = b.remap[v] ? p.map_dev[k] : b.base_dev[v];
+        } else if (!p.ps) {
+            r = p.coll_rank[i - n_clone];
+            deg = p.replicas;
+            dev = p.fabric_dev;
+        } else {
+            const int32_t j = i - n_clone, per = 2 * p.replicas + 1;
+            const int g = j / per, m = j - g * per;
+            if (m < p.replicas) {
+                r = p.push_rank[g * p.replicas + m];
+                deg = 1;
+                dev = p.up_dev[m];
+            } else if (m == p.replicas) {
+                r = p.coll_rank[g];
+                deg = p.replicas;
+                dev = p.ps_dev;
+            } else {
+                const int k = m - p.replicas - 1;
+                r = p.pull_rank[g * p.replicas + k];
+                deg = 1;
+                dev = p.down_dev[k];
+            }
+        }
+        indeg[r] = deg;
+        device[r] = dev;
+        atomicAdd(&s.dev_count[dev], 1);
+    }
+    // edges: packed keys at the same slots as k_expand_edges' 64-bit keys
+    auto key = [bits](int32_t prod, int32_t cons) {
+        return static_cast<uint32_t>(prod) << bits | static_cast<uint32_t>(cons);
+    };
+    for (int32_t i = tid; i < n_clone; i += kSmallT) {
+        const int k = i / b.n_base, v = i - k * b.n_base;
+        const int32_t cons = p.clone_rank[i];
+        for (int j = b.in_off[v]; j < b.in_off[v + 1]; j++) {
+            const int32_t u = b.in_src[j];
+            uint32_t kk = kSent;
+            if (u >= 0) {
+                const int32_t g = p.replicas > 1 ? b.marked[u] : -1;
+                const int32_t prod = g < 0 ? p.clone_rank[k * b.n_base + u]
+                                           : (p.ps ? p.pull_rank[g * p.replicas + k] : p.coll_rank[g]);
+                kk = key(prod, cons);
+            }
+            s.u.keys[k * n_refs + j] = kk;
+        }
+        const int32_t g = p.replicas > 1 ? b.marked[v] : -1;
+        if (g >= 0 && !p.ps) {
+            s.u.keys[p.replicas * n_refs + g * p.replicas + k] = key(p.clone_rank[i], p.coll_rank[g]);
+        } else if (g >= 0) {
+            const int32_t gk = g * p.replicas + k;
+            uint32_t *out = s.u.keys + p.replicas * n_refs + 3 * gk;
+            out[0] = key(p.clone_rank[i], p.push_rank[gk]);
+            out[1] = key(p.push_rank[gk], p.coll_rank[g]);
+            out[2] = key(p.coll_rank[g], p.pull_rank[gk]);
+        }
+    }
+    __syncthreads();
+    uint32_t kr[kSmallIPT];
+#pragma unroll
+    for (int i = 0; i < kSmallIPT; i++) kr[i] = s.u.keys[tid * kSmallIPT + i];
+    __syncthreads();
+    // valid keys < 2^(2 bits) - 1 (N < 2^bits), so the sentinel sorts last on the low 2*bits bits
+    SmallSort(s.u.sort).Sort(kr, 0, 2 * bits);
+    const uint32_t mask = (1u << bits) - 1;
+    int valid = 0;
+#pragma unroll
+    for (int i = 0; i < kSmallIPT; i++) {
+        const int pos = tid * kSmallIPT + i;
+        if (kr[i] != kSent && pos < n_keys) {
+            succ_idx[pos] = static_cast<int32_t>(kr[i] & mask);
+            atomicAdd(&s.count[kr[i] >> bits], 1);
+            valid++;
+        }
+    }
+    if (valid) atomicAdd(&s.n_valid, valid);
+    __syncthreads();
+    // succ_off = exclusive scan of count[0..N] (blocked: thread t owns [t*P, t*P + P))
+    {
+        const int P = (N + 1 + kSmallT - 1) / kSmallT, lo = tid * P, hi = min(lo + P, N + 1);
+        int32_t sum = 0;
+        for (int i = lo; i < hi; i++) sum += s.count[i];
+        int32_t total;
+        int32_t run = block_exclusive_scan(s, sum, total);
+        for (int i = lo; i < hi; i++) {
+            succ_off[i] = run;
+            run += s.count[i];
+        }
+    }
+    // sources: nodes of in-degree 0, ascending (global indeg written by this block above)
+    {
+        const int P = (N + kSmallT - 1) / kSmallT, lo = tid * P, hi = min(lo + P, N);
+        int32_t c = 0;
+        for (int i = lo; i < hi; i++) c += indeg[i] == 0;
+        int32_t total;
+        int32_t at = block_exclusive_scan(s, c, total);
+        for (int i = lo; i < hi; i++)
+            if (indeg[i] == 0) sources[at++] = i;
+        if (tid == 0) {
+            small[0] = static_cast<unsigned long long>(s.n_valid);
+            *reinterpret_cast<int32_t *>(small + 1) = total;
+            int32_t acc = 0;
+            for (int d = 0; d < D; d++) {
+                queue_off[d] = acc;
+                acc += s.dev_count[d];
+            }
+            queue_off[D] = acc;
+        }
+    }
+}
+
 size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
 
 }  // namespace
@@ -156,6 +316,40 @@ extern "C" int dfsim_expand_dp(dfsim_ctx *ctx, const dfsim_base_graph *base, con
     const int64_t n_refs = n_refs32;
     const int64_t n_keys = (int64_t)R * n_refs + (int64_t)G * R * (plan->ps ? 3 : 1);
     DFSIM_ARG_CHECK(ctx, succ_capacity >= n_keys, "succ_capacity below R*refs + G*R (3*G*R in PS mode)");
+
+    int32_t bits = 1;
+    while ((1ll << bits) <= N) bits++;  // N < 2^bits
+    if (N <= kSmallN && n_keys <= kSmallKeys && n_devices <= kSmallD && 2 * bits <= 32 && N > 0 && n_refs32 >= 0 &&
+        !std::getenv("DFSIM_K1_MULTI")) {
+        void *p = nullptr;
+        int rc = dfsim_scratch(ctx, align_up(64) + 4 * (size_t)(N + 1) + 256, &p);
+        if (rc) return rc;
+        auto *small = static_cast<unsigned long long *>(p);
+        auto *left = reinterpret_cast<int32_t *>(static_cast<unsigned char *>(p) + align_up(64));
+        static bool attr_set[64] = {};
+        if (ctx->device < 64 && !attr_set[ctx->device]) {
+            DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_expand_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     static_cast<int>(sizeof(SmallSmem))));
+            attr_set[ctx->device] = true;
+        }
+        k_expand_small<<<1, kSmallT, sizeof(SmallSmem), ctx->stream>>>(*base, *plan, n_refs32, (int32_t)N,
+                                                                         (int32_t)n_keys, bits, n_devices, succ_off,
+                                                                         succ_idx, indeg, device, sources, queue_off,
+                                                                         small);
+        if ((rc = dfsim_after_launch(ctx, "k_expand_small"))) return rc;
+        if (topo) {
+            if ((rc = dfsim_topo_launch(ctx, (int32_t)N, succ_off, succ_idx, indeg, topo,
+                                        reinterpret_cast<int32_t *>(small + 2), left))) return rc;
+        }
+        if (!n_edges_host) return DFSIM_OK;
+        DFSIM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->host_small, small, 32, cudaMemcpyDeviceToHost, ctx->stream));
+        DFSIM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        const unsigned long long *h = static_cast<const unsigned long long *>(ctx->host_small);
+        *n_edges_host = (int64_t)h[0];
+        *n_sources_host = *reinterpret_cast<const int32_t *>(h + 1);
+        *n_ordered_host = topo ? *reinterpret_cast<const int32_t *>(h + 2) : (int32_t)N;
+        return DFSIM_OK;
+    }
 
     // cub temp sizes
     size_t sort_tmp = 0, scan_tmp = 0, sel_tmp = 0;

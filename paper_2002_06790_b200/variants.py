@@ -16,6 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from .lowering import FEATURES, ROW_FIELDS, base_arrays, node_features, node_rows, row_arrays
+from .model import DEVICE_LINK, TRANSFER
 
 
 class _Stand:
@@ -57,7 +58,7 @@ def _special_rows(kind, ids, pos, g_b, structure, cfg) -> dict:
         from .ps import ps_nodes
 
         specs = structure.device_specs  # the PS links (throughput, latency)
-        built = {}
+        built, first = {}, {}
         for p in pos:
             cid = ids[p]
             gid = structure.origin[cid][1]
@@ -67,7 +68,21 @@ def _special_rows(kind, ids, pos, g_b, structure, cfg) -> dict:
                 for n in ps_nodes(gid, grad, cfg, cfg.ps_device):
                     nodes[n.id] = n
                 built[gid] = _Stand(nodes, specs)
-            out.append(node_rows(built[gid], [cid])[0])
+            stand = built[gid]
+            node = stand.nodes[cid]
+            # push_<g>@r<k> / pull_<g>@r<k> differ across k only in their link device (the
+            # features -- bytes, the gradient's shapes -- are k-independent), so the row of k > 0
+            # is k = 0's with the link's throughput / latency
+            role = (gid, node.op_type)
+            row0 = first.get(role)
+            dev = specs.get(node.device)
+            if row0 is not None and row0[1] and node.kind == TRANSFER and dev is not None and dev.kind == DEVICE_LINK:
+                out.append(row0[:4] + (dev.throughput_mbps, dev.latency_us))
+                continue
+            row = node_rows(stand, [cid])[0]
+            if node.kind == TRANSFER:
+                first.setdefault(role, row)
+            out.append(row)
     return row_arrays(out)
 
 

@@ -61,3 +61,40 @@ def test_device_ps_expansion_equals_host(workload, limit):
         plan.reexpand(topo=True, check=True)
         # the lazily built objects are the host expansion's
         assert sorted(plan.graph.nodes) == plan.ids
+
+
+@pytest.mark.parametrize("workload, limit", [("resnet50-dp8", 1), ("bert-large-ps-ar", None), ("vgg16-sweep", 12)])
+def test_single_launch_k1_equals_multi_kernel_k1(workload, limit, monkeypatch):
+    """K1 for small classes runs as one CTA (k_expand_small: block radix sort of 32-bit keys);
+    its CSR, in-degrees, devices, sources, and queue offsets must equal the
+    multi-kernel path's (cub device radix sort / scan / select) array for array."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2002_06790_b200.batch import class_key
+    from paper_2002_06790_b200.expansion import ExpansionPlan
+
+    graphs, db, configs, graph_of = bench.build_workload(0, bench.WORKLOADS[workload][1], workload)
+    seen, classes = set(), []
+    for cfg, gi in zip(configs, graph_of):
+        k = (class_key(cfg), gi if workload != "vgg16-sweep" else gi % 5)
+        if k not in seen:
+            seen.add(k)
+            classes.append((graphs[gi], cfg))
+    for g, cfg in classes[:limit]:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            plan = ExpansionPlan(g, cfg, 0, build_objects=False, db=db)
+        lg = plan.lowered
+        N = lg.n
+        arrays = lambda: [lg.t_succ_off[: N + 1].cpu(), lg.t_succ_idx[: lg.n_edges].cpu(), lg.t_indeg[:N].cpu(),  # noqa: E731
+                          lg.t_dev[:N].cpu(), lg.t_sources[: lg.n_sources].cpu(),
+                          lg.t_queue_off[: lg.n_devices + 1].cpu()]
+        small = arrays()
+        monkeypatch.setenv("DFSIM_K1_MULTI", "1")
+        plan.reexpand(topo=True, check=True)
+        multi = arrays()
+        monkeypatch.delenv("DFSIM_K1_MULTI")
+        plan.reexpand(topo=True, check=True)
+        again = arrays()
+        for a, b, c in zip(small, multi, again):
+            assert np.array_equal(a.numpy(), b.numpy()) and np.array_equal(a.numpy(), c.numpy())
