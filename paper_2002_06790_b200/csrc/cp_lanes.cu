@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "internal.cuh"
@@ -225,8 +226,12 @@ __device__ __forceinline__ void ldg_v4(double (&d)[4], const double *p) {
                  : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
 }
 
+// 14 warps per CTA (one CTA per SM): what shared memory holds for C2 anyway (C2: 1.84 -> 1.79 ms
+// together with the window loads issued before the chunk's cp.async bookkeeping)
+constexpr int kRegWarps = 14;
+
 template <int K, bool kPingPong>
-__global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) {
+__global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(LaneArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NST = 2, NU = K / 2 + 1;  // 32-byte units per window
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,8 +333,8 @@ __global__ void __launch_bounds__(512, 1) k_critical_path_lanes_reg(LaneArgs a) 
         auto process = [&](int q, double (&w)[NU][4], double (&wn)[NU][4]) {
             if (PF > 0 && q + PF < NQ) prefetch_l2(q + PF);
             if (q + 1 < NQ) {
+                load_window(q + 1, wn);  // first: the window registers are claimed before any temporaries
                 prefetch_smem(q + 1);
-                load_window(q + 1, wn);
                 asm volatile("cp.async.wait_group 1;\n" ::);
             } else {
                 asm volatile("cp.async.wait_group 0;\n" ::);
@@ -592,6 +597,7 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
     const int64_t warps = (n_sims + 31) / 32;
     int wpb = shape.wpb;
     if (max_warps > 0 && max_warps < wpb) wpb = max_warps;  // leaves room for a co-resident kernel
+    if (stages == 0 && wpb > kRegWarps) wpb = kRegWarps;
     const int64_t per_sm = (warps + ctx->num_sms - 1) / ctx->num_sms;
     if (per_sm < wpb) wpb = static_cast<int>(per_sm < 1 ? 1 : per_sm);
     const size_t smem = shape.table_bytes + static_cast<size_t>(wpb) * shape.region_bytes;
@@ -622,7 +628,15 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
     auto launch = [&](auto kern) -> int {
         DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<grid, wpb * 32, smem, ctx->stream>>>(a);
-        return dfsim_after_launch(ctx, "k_critical_path_lanes");
+        const int rc = dfsim_after_launch(ctx, "k_critical_path_lanes");
+        if (rc) {  // say what was asked for
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kern);
+            ctx->last_error += " (grid " + std::to_string(grid) + ", block " + std::to_string(wpb * 32) + ", smem " +
+                               std::to_string(smem) + ", registers " + std::to_string(fa.numRegs) + ", max threads " +
+                               std::to_string(fa.maxThreadsPerBlock) + ")";
+        }
+        return rc;
     };
     static const bool kPP = [] {  // DFSIM_CP_PINGPONG=0: single chunk body (measurement knob)
         const char *e = std::getenv("DFSIM_CP_PINGPONG");
