@@ -111,14 +111,17 @@ def build_workload(rank: int, sims: int, workload: str = WORKLOAD):
         return graphs, db, configs, graph_of
     dmap = tuple(f"gpu{i}" for i in range(8))
     coll = CollectiveConfig("RingAnalytic", "NVLink")
+    # measurement knob (not the headline): every K-th C2 candidate carries manual overrides
+    ov_every = int(os.environ.get("DFSIM_BENCH_OVERRIDES", 0))
     for i in range(sims):
         gi = rank * sims + i  # global candidate index
         hw, gap = HW_TAGS[gi % N_HW], 1e-3 * (gi // N_HW)
         if workload == "dag1m":
             configs.append(StrategyConfig(hardware=hw, op_gap_us=gap))
         else:
+            ov = ({"l2_b0_conv1@r*": 50.0 + gi % 7, "fc@r0": 20.0} if ov_every and gi % ov_every == 0 else {})
             configs.append(StrategyConfig(replicas=8, device_map=dmap, collective=coll, gradient_markers=("wgrad_*",),
-                                          hardware=hw, op_gap_us=gap))
+                                          hardware=hw, op_gap_us=gap, overrides=ov))
         graph_of.append(0)
     return graphs, db, configs, graph_of
 

@@ -253,6 +253,8 @@ typedef struct {
     const double *ov_val;
     int32_t max_chunk;         /* largest chunk_count (0: the capacity); CTAs are sized to it, so a
                                   small class spread over many small chunks fills the SMs */
+    const uint32_t *ov_any;    /* [(N + 31) / 32] bit per node rank: in some override set (NULL: search
+                                  every popped node of a candidate with overrides) */
 } dfsim_fused_strategies;
 
 /* K2a: base[var*N+v] = estimate of node v under variant var = (graph variant, hw, algo, path) with
@@ -261,6 +263,14 @@ typedef struct {
 int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t, int32_t n_variants,
                            const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path,
                            const int32_t *var_gv, double *base, uint8_t *status);
+
+/* Rows of (variant, override set) combinations for the fused engine: out[c][r] = base[combo_variant[c]][r],
+ * with the override values of set combo_set[c] (-1: none) stamped in at their ranks (sign clear:
+ * an override replaces the estimate, costmodel.py:302-304).  Candidates then need no override
+ * lookup in the engine (dfsim_fused_strategies.override_set = NULL). */
+int dfsim_override_rows(dfsim_ctx *ctx, int32_t n_nodes, int32_t n_combos, const double *base,
+                        const int32_t *combo_variant, const int32_t *combo_set, const int32_t *ov_off,
+                        const int32_t *ov_node, const double *ov_val, double *out);
 
 /* Candidates one CTA of the fused engine holds; chunks of dfsim_fused_strategies
  * must not exceed it (0: the class does not fit the fused engine). */

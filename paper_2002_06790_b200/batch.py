@@ -177,9 +177,26 @@ class TopologyClass:
         cap = int(self.ctx.lib.dfsim_fused_chunk(native.ctypes.byref(self.tables.sim_struct), lp.n_sims, sms))
         if os.environ.get("DFSIM_FUSED_CHUNK"):  # measurement knob: fixed chunk (clamped to the capacity)
             cap = max(1, min(self.chunk_capacity, int(os.environ["DFSIM_FUSED_CHUNK"])))
-        order = np.argsort(var_of, kind="stable")
+        # candidates with manual overrides: when the (variant, override set) combinations are few
+        # enough to fill warps (>= 32 candidates each on average), each gets its own duration row
+        # (dfsim_override_rows) and the engine never searches an override table; otherwise
+        # the engine looks overrides up per popped node (skipping nodes in no set)
+        row_of, self.combo = var_of, None
+        ovs = np.asarray(lp.strat_ov, np.int64)
+        if ovs.size and ovs.max() >= 0:
+            n_sets = int(ovs.max()) + 1
+            ck = var_of * (n_sets + 1) + (ovs + 1)
+            cuniq, combo_of = np.unique(ck, return_inverse=True)
+            C = len(cuniq)
+            if C * 32 <= lp.n_sims and C * N * 8 <= (1 << 30) and not os.environ.get("DFSIM_OV_SEARCH_ALL"):
+                self.combo = (torch.as_tensor(cuniq // (n_sets + 1), dtype=torch.int32, device=dev),
+                              torch.as_tensor(cuniq % (n_sets + 1) - 1, dtype=torch.int32, device=dev),
+                              torch.empty((C, N), dtype=torch.float64, device=dev))
+                row_of = combo_of.astype(np.int64)
+                self.resolve()
+        order = np.argsort(row_of, kind="stable")
         firsts, counts, variants = [], [], []
-        sorted_var = var_of[order]
+        sorted_var = row_of[order]
         bounds = np.flatnonzero(np.diff(sorted_var)) + 1
         for a, b in zip(np.r_[0, bounds], np.r_[bounds, len(order)]):
             for c in range(a, b, cap):  # full chunks (whole warps), then the variant's remainder
@@ -190,18 +207,27 @@ class TopologyClass:
         self.f_order = T(order, torch.int64)
         self.f_first, self.f_count, self.f_var = T(firsts, torch.int32), T(counts, torch.int32), T(variants, torch.int32)
         t, s = lp.tensors, lp.t_strat
+        rows = self.combo[2] if self.combo is not None else self.base
         self.fused_strat = native.FusedStrategies(
-            lp.n_sims, V, native.ptr(self.base), len(firsts), native.ptr(self.f_order), native.ptr(self.f_first),
+            lp.n_sims, rows.shape[0], native.ptr(rows), len(firsts), native.ptr(self.f_order), native.ptr(self.f_first),
             native.ptr(self.f_count), native.ptr(self.f_var), native.ptr(s["gap"]),
-            native.ptr(s["ov"]) if lp.strat_ov.size and lp.strat_ov.max() >= 0 else native.P(0),
-            native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]), max(counts, default=0))
+            native.ptr(s["ov"]) if self.combo is None and lp.strat_ov.size and lp.strat_ov.max() >= 0 else native.P(0),
+            native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]), max(counts, default=0),
+            native.P(0) if os.environ.get("DFSIM_OV_SEARCH_ALL") else native.ptr(t["oany"]))
         self.fused = True
 
     def resolve(self):
-        """K2a: estimate every node once per (hardware, algorithm, path) variant."""
+        """K2a: estimate every node once per (hardware, algorithm, path) variant (and stamp the
+        override sets into the (variant, set) rows when the class uses them)."""
         self.ctx.call("dfsim_resolve_variants", self.lg.n, native.ctypes.byref(self.lp.struct), self.n_variants,
                       native.ptr(self.v_hw), native.ptr(self.v_algo), native.ptr(self.v_path),
                       native.ptr(self.v_gv), native.ptr(self.base), native.ptr(self.status))
+        if getattr(self, "combo", None) is not None:
+            c_var, c_set, rows = self.combo
+            t = self.lp.tensors
+            self.ctx.call("dfsim_override_rows", self.lg.n, rows.shape[0], native.ptr(self.base), native.ptr(c_var),
+                          native.ptr(c_set), native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]),
+                          native.ptr(rows))
 
     def fallback_if_needed(self, o) -> bool:
         """Re-run ring-overflow candidates on the exact engine (host sync on the flags).

@@ -148,7 +148,47 @@ __global__ void __launch_bounds__(256) k_resolve_variants(int32_t N, dfsim_profi
     }
 }
 
+// rows of (variant, override set) combinations: the variant's K2a row with the set's override
+// values stamped in (costmodel.py:302-304 -- an override replaces the estimate, no op_gap), so
+// the fused engine reads every duration from one row and never searches an override table
+__global__ void __launch_bounds__(256) k_override_rows(int32_t N, int32_t C, const double *base, const int32_t *c_var,
+                                                       const int32_t *c_set, const int32_t *ov_off,
+                                                       const int32_t *ov_node, const double *ov_val, double *out) {
+    const int64_t total = static_cast<int64_t>(C) * N;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i / N);
+        const int r = static_cast<int>(i - static_cast<int64_t>(c) * N);
+        double b = __ldg(base + static_cast<int64_t>(__ldg(c_var + c)) * N + r);
+        const int s = __ldg(c_set + c);
+        if (s >= 0) {
+            int lo = __ldg(ov_off + s), hi = __ldg(ov_off + s + 1);
+            const int end = hi;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(ov_node + mid) < r) lo = mid + 1; else hi = mid;
+            }
+            if (lo < end && __ldg(ov_node + lo) == r) b = __ldg(ov_val + lo);  // finite, >= 0: sign clear
+        }
+        out[i] = b;
+    }
+}
+
 }  // namespace
+
+extern "C" int dfsim_override_rows(dfsim_ctx *ctx, int32_t n_nodes, int32_t n_combos, const double *base,
+                                   const int32_t *combo_variant, const int32_t *combo_set, const int32_t *ov_off,
+                                   const int32_t *ov_node, const double *ov_val, double *out) {
+    if (!ctx || !base || !combo_variant || !combo_set || !out) return DFSIM_BAD_ARGUMENT;
+    if (n_nodes <= 0 || n_combos <= 0) return DFSIM_OK;
+    DFSIM_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const int64_t total = (int64_t)n_combos * n_nodes;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)ctx->num_sms * 16) blocks = (int64_t)ctx->num_sms * 16;
+    k_override_rows<<<(unsigned)blocks, 256, 0, ctx->stream>>>(n_nodes, n_combos, base, combo_variant, combo_set,
+                                                              ov_off, ov_node, ov_val, out);
+    return dfsim_after_launch(ctx, "k_override_rows");
+}
 
 extern "C" int dfsim_resolve_variants(dfsim_ctx *ctx, int32_t n_nodes, const dfsim_profile_tables *t, int32_t n_variants,
                                       const int32_t *var_hw, const uint8_t *var_algo, const int32_t *var_path,

@@ -178,8 +178,9 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     head++;
                     const double b = kBaseG ? __ldg(g_row + lds_u16(a_rank + 2u * v)) : lds_f64(a_base + 8u * v);
                     double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
-                    if (ovs >= 0) {  // override tables are by rank
-                        const int vr = static_cast<int>(lds_u16(a_rank + 2u * v));
+                    const int vr = ovs >= 0 ? static_cast<int>(lds_u16(a_rank + 2u * v)) : 0;
+                    if (ovs >= 0 && (!a.st.ov_any || ((__ldg(a.st.ov_any + (vr >> 5)) >> (vr & 31)) & 1u))) {
+                        // override tables are by rank; nodes in no set skip the search
                         int lo = __ldg(a.st.ov_off + ovs), hi = __ldg(a.st.ov_off + ovs + 1);
                         const int end = hi;
                         while (lo < hi) {

@@ -440,11 +440,17 @@ class _FeatureRegistry:
             return out
 
     def flat(self):
-        """(f_off, f_name, f_val) as numpy arrays (cached until the registry grows)."""
+        """(f_off, f_name, f_val) as numpy arrays; when the registry has grown, only the new
+        entries are converted and appended (sweeps intern class after class)."""
         with self.lock:
-            if self._flat is None or len(self._flat[0]) != len(self.f_off):
-                self._flat = (np.asarray(self.f_off, np.int64), np.asarray(self.f_name, np.int64),
-                              np.asarray(self.f_val, np.float64))
+            if self._flat is None:
+                self._flat = (np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0, np.float64))
+            off, name, val = self._flat
+            if len(off) != len(self.f_off):
+                k, m = len(off), len(name)
+                self._flat = (np.concatenate([off, np.asarray(self.f_off[k:], np.int64)]),
+                              np.concatenate([name, np.asarray(self.f_name[m:], np.int64)]),
+                              np.concatenate([val, np.asarray(self.f_val[m:], np.float64)]))
             return self._flat
 
 
@@ -687,6 +693,11 @@ class LoweredProfiles:
             onode.extend(p for p, _ in pairs)
             oval.extend(v for _, v in pairs)
             ooff.append(len(onode))
+        # one bit per node rank: in some override set (the fused engine skips the set's search otherwise)
+        oany = np.zeros((N + 31) // 32 + 1, np.uint32)
+        if onode:
+            hit = np.unique(np.asarray(onode, np.int64))
+            np.bitwise_or.at(oany, hit >> 5, (np.uint32(1) << (hit & 31).astype(np.uint32)))
 
         def srt(keys, *vals):
             if not keys:
@@ -706,7 +717,7 @@ class LoweredProfiles:
             mcoef=(mcoef, np.float64), micpt=(micpt, np.float64),
             nk=(nk, np.uint64), nt=(nt, np.float64),
             uok=(uni_ok, np.uint8), uthr=(uni_thr, np.float64), ulat=(uni_lat, np.float64),
-            ooff=(ooff, np.int32), onode=(onode, np.int32), oval=(oval, np.float64),
+            ooff=(ooff, np.int32), onode=(onode, np.int32), oval=(oval, np.float64), oany=(oany, np.uint32),
             s_hw=(self.strat_hw, np.int32), s_gap=(self.strat_gap, np.float64), s_algo=(self.strat_algo, np.uint8),
             s_path=(self.strat_path, np.int32), s_ov=(self.strat_ov, np.int32), s_gv=(self.strat_gv, np.int32)),
             device)

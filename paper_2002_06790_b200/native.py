@@ -69,7 +69,7 @@ class SimTables(ctypes.Structure):
 class FusedStrategies(ctypes.Structure):
     _fields_ = [("n_sims", I64), ("n_variants", I32), ("base", P), ("n_chunks", I32), ("order", P),
                 ("chunk_first", P), ("chunk_count", P), ("chunk_variant", P), ("op_gap", P), ("override_set", P),
-                ("ov_off", P), ("ov_node", P), ("ov_val", P), ("max_chunk", I32)]
+                ("ov_off", P), ("ov_node", P), ("ov_val", P), ("max_chunk", I32), ("ov_any", P)]
 
 
 class CpTables(ctypes.Structure):
@@ -121,6 +121,7 @@ _SIGNATURES = {
     "dfsim_critical_path_wide": (ctypes.c_int, [P, ctypes.POINTER(Graph), P, P, I32, I64, P, P, P, P]),
     "dfsim_simulate_batch_ex": (ctypes.c_int, [P, ctypes.POINTER(Graph), I64, P, I64, P, P, P, P, P, P, P, I32]),
     "dfsim_resolve_variants": (ctypes.c_int, [P, I32, ctypes.POINTER(ProfileTables), I32, P, P, P, P, P, P]),
+    "dfsim_override_rows": (ctypes.c_int, [P, I32, I32, P, P, P, P, P, P, P]),
     "dfsim_simulate_fused": (ctypes.c_int, [P, ctypes.POINTER(SimTables), ctypes.POINTER(FusedStrategies), P, P, P,
                                             P, P]),
     "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P]),

@@ -26,10 +26,26 @@ class _Stand:
         self.nodes, self.devices = nodes, devices
 
 
-def structure_key(g) -> int:
-    """Hash of everything that shapes a topology class (not attrs or shapes)."""
-    return hash((tuple((nid, n.kind, n.device, n.op_type, n.inputs) for nid, n in g.nodes.items()),
-                 tuple(sorted((d.id, d.kind) for d in g.devices.values()))))
+class StructureKey:
+    """Everything that shapes a topology class (ids, kinds, devices, op types, inputs; not
+    attrs or shapes), compared exactly: the hash is computed once, and equal hashes are
+    confirmed on the full tuples, so two structures never share a class by a hash collision."""
+
+    __slots__ = ("t", "h")
+
+    def __init__(self, t):
+        self.t, self.h = t, hash(t)
+
+    def __hash__(self):
+        return self.h
+
+    def __eq__(self, other):
+        return self is other or (isinstance(other, StructureKey) and self.h == other.h and self.t == other.t)
+
+
+def structure_key(g) -> StructureKey:
+    return StructureKey((tuple((nid, n.kind, n.device, n.op_type, n.inputs) for nid, n in g.nodes.items()),
+                         tuple(sorted((d.id, d.kind) for d in g.devices.values()))))
 
 
 def rows_for(kind: str, ids, g_b, structure, cfg=None, db=None) -> list:
@@ -126,7 +142,7 @@ def variant_arrays(kind: str, ids, g_b, structure, cfg=None, db=None, cache=None
     return out
 
 
-__all__ = ["structure_key", "rows_for", "variant_arrays", "variant_arrays_many", "node_features"]
+__all__ = ["StructureKey", "structure_key", "rows_for", "variant_arrays", "variant_arrays_many", "node_features"]
 
 
 def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None) -> dict:
@@ -163,12 +179,3 @@ def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None) ->
                 out[k][sel] = rows[k]
     return out
 
-
-__all__ = ["structure_key", "rows_for", "variant_arrays", "variant_arrays_many", "node_features"]
-
-
-def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None) -> dict:
-    """``variant_arrays`` of several graph variants of one class, stacked: each field [GV, N]."""
-    cache: dict = {}
-    rows = [variant_arrays(kind, ids, gb, structure, cfg, db, cache) for gb in graphs]
-    return {k: np.stack([r[k] for r in rows]) for k in ROW_FIELDS}

@@ -22,7 +22,7 @@ def _configs(n, overrides_every=5):
     dmap = tuple(f"gpu{i}" for i in range(8))
     out = []
     for i in range(n):
-        ov = {"wgrad_l1_*": 3.25, "l2_b0_conv1@r3": 0.0} if i % overrides_every == 3 else {}
+        ov = {"wgrad_l1_*": 3.25, "l2_b0_conv1@r3": 0.0} if i % overrides_every == min(3, overrides_every - 1) else {}
         algo = "RingAnalytic" if i % 3 else "MeasuredThroughput"
         out.append(StrategyConfig(replicas=8, device_map=dmap, collective=CollectiveConfig(algo, "NVLink"),
                                   gradient_markers=("wgrad_*",), hardware=f"hw{i % 4}", op_gap_us=1e-3 * (i // 4),
@@ -67,6 +67,26 @@ def test_fused_equals_unfused_resnet_dp8(resnet):
     assert not of.get("fallback_rows")
     src = of["cp_src"].cpu().numpy()
     assert (src >= 0).all()
+
+
+@pytest.mark.parametrize("search_all", [False, True])
+def test_fused_override_rows_equal_unfused(resnet, monkeypatch, search_all):
+    """Overrides in the fused engine, both ways: few (variant, override set) combinations get
+    their own duration rows (dfsim_override_rows: no lookup in the engine), otherwise the
+    engine searches the set per popped node (skipping nodes in no set).  Both must equal the
+    unfused kernels bit for bit (costmodel.py:302-304: an override replaces the estimate)."""
+    from paper_2002_06790_b200.batch import TopologyClass
+
+    if search_all:
+        monkeypatch.setenv("DFSIM_OV_SEARCH_ALL", "1")
+    g, db = resnet
+    cfgs = _configs(256, overrides_every=2)  # 4 hw x 2 algos x {none, one set}: 16 combinations
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        tf = TopologyClass(g, db, cfgs, fused=True)
+        tu = TopologyClass(g, db, cfgs, fused=False)
+    assert (tf.combo is None) == search_all
+    _compare(tf, tu)
 
 
 def test_reexpand_async_reproduces_first_expansion(resnet):

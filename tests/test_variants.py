@@ -76,3 +76,16 @@ def test_variant_arrays_many_equals_per_variant(sync):
         one = variant_arrays(kind, plan.ids, gb, plan, cfg, db, {})
         for k in ROW_FIELDS:
             assert np.array_equal(many[k][v], one[k]), (k, v)
+
+
+def test_structure_key_equality_is_exact():
+    """Topology classes group by the exact structure: a forced hash collision between two
+    different structures must not merge them."""
+    from paper_2002_06790_b200.variants import StructureKey, structure_key
+
+    g1, g2 = W.vgg16_training(batch=8), W.vgg16_training(batch=16)
+    k1, k2 = structure_key(g1), structure_key(g2)
+    assert k1 == k2 and hash(k1) == hash(k2)  # batch size changes shapes, not structure
+    a, b = StructureKey(("x",)), StructureKey(("y",))
+    b.h = a.h  # collide
+    assert a != b and len({a: 0, b: 1}) == 2
