@@ -53,6 +53,8 @@ extern "C" {
 #define DFSIM_CUDA 5             /* device / launch failure */
 #define DFSIM_BAD_ARGUMENT 6     /* ValueError-class argument problems */
 #define DFSIM_NEGATIVE_DURATION 7 /* DurationEntry(<0 or NaN) -> ValueError */
+#define DFSIM_CHECK_FAILED 8      /* checked build only (libdfsim_b200_checked.so): a device-side bounds
+                                     check of a launch failed; last_error names the kernel and check bits */
 
 /* per-(sim,node) duration source tags written by dfsim_estimate_batch */
 #define DFSIM_SRC_OVERRIDE 0

@@ -18,6 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdfsim_b200.so"
+LIB_CHECKED = PKG / "libdfsim_b200_checked.so"  # -DDFSIM_CHECKED: device-side bounds checks (internal.cuh)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -33,21 +34,22 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
-def needs_build() -> bool:
-    if not LIB.exists():
+def needs_build(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    mtime = LIB.stat().st_mtime
+    mtime = lib.stat().st_mtime
     deps = sources() + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "dfsim_b200.h"]
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
-        return LIB
-    objdir = ROOT / "build" / "obj"
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not needs_build(lib):
+        return lib
+    objdir = ROOT / "build" / ("obj_checked" if checked else "obj")
     objdir.mkdir(parents=True, exist_ok=True)
     flags = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
-                    "-I", str(ROOT / "include"), "-I", str(CSRC)]
+                    "-I", str(ROOT / "include"), "-I", str(CSRC)] + (["-DDFSIM_CHECKED"] if checked else [])
     if verbose:
         flags += ["-Xptxas", "-v"]
     objs = []
@@ -66,12 +68,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             failed.append(src.name)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"], check=True)
-    tmp.replace(LIB)
-    return LIB
+    tmp.replace(lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

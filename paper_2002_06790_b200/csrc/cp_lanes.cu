@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
             }
             const int b0 = lds_i(a_boff + 4u * q), b1 = lds_i(a_boff + 4u * (q + 1));
             const unsigned bs = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
+            DFSIM_CHECK(b1 - b0 <= BM, 8);
             for (int b = b0 + lane; b < b1; b += 32) cpa16(bs + 16u * static_cast<unsigned>(b - b0), a.t.blocks + 4 * static_cast<int64_t>(b));
             const int r0 = lds_i(a_soff + 4u * q), r1 = lds_i(a_soff + 4u * (q + 1));
             const unsigned ss = a_lane + static_cast<unsigned>(NS + static_cast<int>(stg) * RM) * 256u;
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
             const unsigned stg = static_cast<unsigned>(q & 1);
             const int b0 = lds_i(a_boff + 4u * q), b1 = lds_i(a_boff + 4u * (q + 1));
             const unsigned bs = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
+            DFSIM_CHECK(b1 - b0 <= BM, 8);
             for (int b = b0 + lane; b < b1; b += 32) cpa16(bs + 16u * static_cast<unsigned>(b - b0), a.t.blocks + 4 * static_cast<int64_t>(b));
             const int r0 = lds_i(a_soff + 4u * q), r1 = lds_i(a_soff + 4u * (q + 1));
             const unsigned ss = a_lane + static_cast<unsigned>(NS + static_cast<int>(stg) * RM) * 256u;
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
                 const int nr = r1 - r < 32 ? r1 - r : 32;
                 for (int k = 0; k < nr; k++) {
                     const int id = __shfl_sync(DFSIM_FULL_MASK, my, k);
+                    DFSIM_CHECK(id < a.t.n_long && r - r0 + k < RM, 7);
                     if (live) cpa8(ss + static_cast<unsigned>(r - r0 + k) * 256u, spill_warp + 32 * static_cast<int64_t>(id));
                 }
             }
@@ -348,8 +351,16 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
             for (int t = 0; t < K; t++) {
                 if (t < hi - lo) {
                     const int p = hi - 1 - t;
+                    DFSIM_CHECK(t < BM && p >= 0 && p < N, 8);
                     const uint4 r = lds_u4(blk + 16u * t);
                     const unsigned deg = r.y & 0xffu;
+                    DFSIM_CHECK((deg < 1 || (r.z & 0xffffu) < static_cast<unsigned>(NS + NST * RM)) &&
+                                    (deg < 2 || (r.z >> 16) < static_cast<unsigned>(NS + NST * RM)) &&
+                                    (deg < 3 || (r.w & 0xffffu) < static_cast<unsigned>(NS + NST * RM)) &&
+                                    (deg < 4 || (r.w >> 16) < static_cast<unsigned>(NS + NST * RM)),
+                                6);
+                    DFSIM_CHECK(!(r.x & kHasSlot) || (r.x & 0xfffu) < static_cast<unsigned>(NS), 5);
+                    DFSIM_CHECK(!(r.x & kHasSpill) || (r.x >> 15) < static_cast<unsigned>(a.t.n_long), 7);
                     const double x0 = deg > 0 ? lds_d(a_lane + 256u * (r.z & 0xffffu)) : 0.0;
                     const double x1 = deg > 1 ? lds_d(a_lane + 256u * (r.z >> 16)) : 0.0;
                     const double x2 = deg > 2 ? lds_d(a_lane + 256u * (r.w & 0xffffu)) : 0.0;
@@ -365,6 +376,8 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
                         const unsigned ex = blk + 2u * (r.y >> 8);
 #pragma unroll 1
                         for (unsigned j = 4; j < deg; j++) {  // rare (wide fan-outs): kept compact
+                            DFSIM_CHECK((r.y >> 8) + (j - 4) < 8u * static_cast<unsigned>(BM), 8);
+                            DFSIM_CHECK(lds_h(ex + 2u * (j - 4)) < static_cast<unsigned>(NS + NST * RM), 6);
                             const double x = lds_d(a_lane + 256u * lds_h(ex + 2u * (j - 4)));
                             best = x > best ? x : best;
                         }

@@ -51,7 +51,7 @@ extern "C" const char *dfsim_ctx_last_error(const dfsim_ctx *ctx) {
     return ctx ? ctx->last_error.c_str() : "null context";
 }
 
-int dfsim_after_launch(dfsim_ctx *ctx, const char *what) {
+int dfsim_after_launch_base(dfsim_ctx *ctx, const char *what) {
     ctx->launches++;
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) {

@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(kSmallT, 1)
         atomicAdd(&s.dev_count[dev], 1);
     }
     // edges: packed keys at the same slots as k_expand_edges' 64-bit keys
-    auto key = [bits](int32_t prod, int32_t cons) {
+    auto key = [bits, N](int32_t prod, int32_t cons) {
+        DFSIM_CHECK(prod >= 0 && prod < N && cons >= 0 && cons < N, 13);
         return static_cast<uint32_t>(prod) << bits | static_cast<uint32_t>(cons);
     };
     for (int32_t i = tid; i < n_clone; i += kSmallT) {
@@ -218,6 +219,7 @@ __global__ void __launch_bounds__(kSmallT, 1)
                                            : (p.ps ? p.pull_rank[g * p.replicas + k] : p.coll_rank[g]);
                 kk = key(prod, cons);
             }
+            DFSIM_CHECK(k * n_refs + j < n_keys, 13);
             s.u.keys[k * n_refs + j] = kk;
         }
         const int32_t g = p.replicas > 1 ? b.marked[v] : -1;

@@ -38,7 +38,9 @@ struct FusedArgs {
 };
 
 // Decrement the counter field (width mask at bit `shift` of cnt[word]); true when it reaches zero.
-__device__ __forceinline__ bool counter_dec(unsigned *cnt, unsigned word, unsigned shift, unsigned mask) {
+__device__ __forceinline__ bool counter_dec(unsigned *cnt, unsigned word, unsigned shift, unsigned mask,
+                                            unsigned n_words) {
+    DFSIM_CHECK(word < n_words && shift < 32u, 2);
     const unsigned old = atomicSub(cnt + word, 1u << shift);
     return ((old >> shift) & mask) == 1u;
 }
@@ -89,6 +91,8 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     const int QCAP = a.g.qcap;
     const int QSTRIDE = QCAP + 2;  // u16 entries: 17-word stride keeps the 16 lanes' rings on distinct banks
     const unsigned QMASK = static_cast<unsigned>(QCAP - 1);
+    const unsigned n_cw = static_cast<unsigned>(a.g.n_counter_words);  // checked builds only
+    (void)n_cw;
 
     // CTA-shared tables
     uint32_t *s_meta = reinterpret_cast<uint32_t *>(smem);
@@ -148,7 +152,9 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 const int i = b + ll;
                 const bool has = active && i < a.g.n_sources;
                 const int v = has ? __ldg(a.g.sources + i) : 0;
+                DFSIM_CHECK(v >= 0 && v < N, 3);
                 const int dv = has ? __ldg(a.g.device + s_rank[v]) : 0;
+                DFSIM_CHECK(dv >= 0 && dv < D, 1);
                 const unsigned peers = __match_any_sync(DFSIM_FULL_MASK, has ? dv + 32 * grp : 1024 + lane);
                 const int base = has ? tails[dv] : 0;
                 __syncwarp();
@@ -175,6 +181,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     ovf = static_cast<unsigned>(t) - head > static_cast<unsigned>(QCAP);
                     if (ovf) return;
                     const int v = q[ll * QSTRIDE + (head & QMASK)];
+                    DFSIM_CHECK(v < N, 3);
                     head++;
                     const double b = kBaseG ? __ldg(g_row + lds_u16(a_rank + 2u * v)) : lds_f64(a_base + 8u * v);
                     double dur = signbit(b) ? __dadd_rn(-b, gap) : b;
@@ -209,9 +216,11 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                 int j0 = 0, deg = 0;
                 if (done) {
                     running = false;
+                    DFSIM_CHECK(run_v >= 0 && run_v < N, 0);
                     const uint32_t meta = lds_u32(a_meta + 4u * run_v);
                     j0 = static_cast<int>(meta & 0xffffffu);
                     deg = static_cast<int>(meta >> 24);  // < 255 in the fused engine (prepare.Tables)
+                    DFSIM_CHECK(j0 + deg <= E, 0);
                 }
                 auto relax = [&](int j) {
                     const uint32_t e = lds_u32(a_succ + 4u * j);
@@ -220,7 +229,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     if constexpr (kPacked) {
                         m = static_cast<int>(e & 0x1fffu);
                         dv = static_cast<int>((e >> 13) & 15u);
-                        ready = ((e >> 17) & 1u) || counter_dec(cnt, e >> 24, (e >> 19) & 31u, (e >> 18) & 1u ? 15u : 3u);
+                        ready = ((e >> 17) & 1u) || counter_dec(cnt, e >> 24, (e >> 19) & 31u, (e >> 18) & 1u ? 15u : 3u, n_cw);
                     } else {
                         m = static_cast<int>(e & 0xffffu);
                         dv = static_cast<int>((e >> 16) & 31u);
@@ -228,9 +237,10 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                             ready = true;
                         } else {
                             const unsigned code = lds_u16(a_cidx + 2u * m);
-                            ready = counter_dec(cnt, code >> 7, (code >> 2) & 31u, (1u << (2u << (code & 3u))) - 1u);
+                            ready = counter_dec(cnt, code >> 7, (code >> 2) & 31u, (1u << (2u << (code & 3u))) - 1u, n_cw);
                         }
                     }
+                    DFSIM_CHECK(m >= 0 && m < N && dv >= 0 && dv < D, 1);
                     if (ready) {
                         const int p = atomicAdd(tails + dv, 1);
                         q[dv * QSTRIDE + (p & QMASK)] = static_cast<uint16_t>(m);
@@ -361,7 +371,10 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
             double *bs = region + SR + (c & 1) * SD;
             for (int p = p0 + ll; p < p1; p += 16) cp_async16(bs + 2 * (p - p0), row + 2 * p);
             const int r0 = s_soff[c], r1 = s_soff[c + 1];
-            for (int r = r0 + ll; r < r1; r += 16) cp_async8(bs + 2 * K + (r - r0), spill_row + s_slist[r]);
+            for (int r = r0 + ll; r < r1; r += 16) {
+                DFSIM_CHECK(s_slist[r] < a.t.n_long && 2 * K + (r - r0) < SD, 11);
+                cp_async8(bs + 2 * K + (r - r0), spill_row + s_slist[r]);
+            }
             asm volatile("cp.async.commit_group;\n" ::);
         };
         double len = 0.0;
@@ -390,12 +403,16 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
                     const uint32_t m = pm.x, info = pm.y;
                     const int j0 = static_cast<int>(m & 0xffffu), j1 = j0 + static_cast<int>((m >> 16) & 0xffu);
                     double best = 0.0;  // max(0.0, .) (graph.py:465-468)
+                    DFSIM_CHECK(j1 <= E, 10);
                     for (int j = j0; j < j1; j++) {
+                        DFSIM_CHECK(s_succ[j] < SR + 2 * SD, 10);
                         const double x = region[s_succ[j]];
                         best = x > best ? x : best;
                     }
                     const double2 sf = bs[p - p0];
                     const double sv = __dadd_rn(__dsub_rn(sf.y, sf.x), best);  // finish - start (reporting.py:128)
+                    DFSIM_CHECK(!(info & 0x8000u) || (info & 0x7fffu) < static_cast<unsigned>(SR), 11);
+                    DFSIM_CHECK(!(info >> 31) || ((info >> 16) & 0x7fffu) < static_cast<unsigned>(a.t.n_long), 11);
                     if (info & 0x8000u) region[info & 0x7fffu] = sv;
                     if (live && (info >> 31)) spill_row[(info >> 16) & 0x7fffu] = sv;
                     if ((m >> 24) & 1u) {

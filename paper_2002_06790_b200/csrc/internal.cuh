@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <deque>
 #include <mutex>
 #include <string>
@@ -55,7 +56,45 @@ struct dfsim_ctx {
     } while (0)
 
 // After a kernel launch: count it and surface launch-configuration errors.
-int dfsim_after_launch(dfsim_ctx *ctx, const char *what);
+int dfsim_after_launch_base(dfsim_ctx *ctx, const char *what);
+
+// Checked builds (libdfsim_b200_checked.so, -DDFSIM_CHECKED; the pool has no compute-sanitizer):
+// DFSIM_CHECK(cond, bit) guards an index the kernels derive from table data.  A failed check
+// sets `bit` in this translation unit's check word -- no trap, the launch completes -- and the
+// launch's dfsim_after_launch synchronises, reads and clears the word and returns
+// DFSIM_CHECK_FAILED.  In the product build both are no-ops.
+#ifdef DFSIM_CHECKED
+static __device__ unsigned int dfsim_check_word;
+#define DFSIM_CHECK(cond, bit)                                                            \
+    do {                                                                                  \
+        if (!(cond)) atomicOr(&dfsim_check_word, 1u << (bit));                            \
+    } while (0)
+static inline int dfsim_after_launch(dfsim_ctx *ctx, const char *what) {
+    int rc = dfsim_after_launch_base(ctx, what);
+    if (rc) return rc;
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    unsigned v = 0;
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&v, dfsim_check_word, sizeof v);
+    if (e != cudaSuccess) {
+        ctx->last_error = std::string(what) + ": " + cudaGetErrorString(e);
+        return DFSIM_CUDA;
+    }
+    if (v) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(dfsim_check_word, &z, sizeof z);
+        char buf[32];
+        snprintf(buf, sizeof buf, "0x%x", v);
+        ctx->last_error = std::string(what) + ": device bounds check failed (bits " + buf + ")";
+        return DFSIM_CHECK_FAILED;
+    }
+    return DFSIM_OK;
+}
+#else
+#define DFSIM_CHECK(cond, bit) \
+    do {                       \
+    } while (0)
+static inline int dfsim_after_launch(dfsim_ctx *ctx, const char *what) { return dfsim_after_launch_base(ctx, what); }
+#endif
 // Grow ctx->scratch to at least `bytes` (stream-ordered: synchronises the stream first).
 int dfsim_scratch(dfsim_ctx *ctx, size_t bytes, void **out);
 // Grow ctx->aux (same rules); independent of ctx->scratch.

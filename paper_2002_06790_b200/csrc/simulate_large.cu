@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                         if (k < deg) {
                             const unsigned e = succ_of(k);
                             const int m = static_cast<int>(e & 0x7ffffffu), dv = static_cast<int>(e >> 27);
+                            DFSIM_CHECK(m < N && dv < D && cpre[k] >= 1, 12);  // a released node's counter was >= 1
                             int c = cpre[k];
 #pragma unroll
                             for (int j = 0; j < k; j++) c -= (succ_of(j) & 0x7ffffffu) == static_cast<unsigned>(m);
@@ -208,7 +209,9 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                     }
                     for (int k = kPre; k < deg; k++) {
                         const int m = __ldg(a.succ_idx + static_cast<int>(r0.x) + k);
+                        DFSIM_CHECK(m >= 0 && m < N, 12);
                         const int dv = __ldg(a.device + m);
+                        DFSIM_CHECK(dv >= 0 && dv < D, 12);
                         const int c = static_cast<int>(cnt[m]);
                         cnt[m] = static_cast<CT>(c - 1);
                         if (c == 1) {
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(256) k_simulate_large(LargeArgs a) {
                             e = static_cast<unsigned>(m) | (static_cast<unsigned>(__ldg(a.device + m)) << 27);
                         }
                         const int m = static_cast<int>(e & 0x7ffffffu), dv = static_cast<int>(e >> 27);
+                        DFSIM_CHECK(m < N && dv < D, 12);
                         const unsigned grp = __match_any_sync(am, m);
                         if ((grp & lanemask_lt()) == 0) {
                             const int k = __popc(grp);

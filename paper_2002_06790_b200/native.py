@@ -10,17 +10,21 @@ the reference's ``--jobs`` threads (cli.py:133-137) may call the drop-in concurr
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .errors import (
     STATUS_BAD_ARGUMENT,
+    STATUS_CHECK_FAILED,
     STATUS_CUDA,
     STATUS_OK,
     NativeError,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "libdfsim_b200.so"
+# DFSIM_LIB=checked loads the bounds-checked build (tests / profiles/sanitize_run.py only)
+LIB_PATH = Path(__file__).resolve().parent / (
+    "libdfsim_b200_checked.so" if os.environ.get("DFSIM_LIB") == "checked" else "libdfsim_b200.so")
 
 P = ctypes.c_void_p
 I32, I64, U8 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint8
@@ -229,6 +233,8 @@ class Context:
             raise ValueError(f"{what}: {msg}")
         if rc == STATUS_CUDA:
             raise NativeError(f"{what}: CUDA failure: {msg}")
+        if rc == STATUS_CHECK_FAILED:
+            raise NativeError(f"{what}: {msg}")
         raise NativeError(f"{what}: status {rc}: {msg}")
 
     def call(self, name: str, *args):

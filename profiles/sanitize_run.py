@@ -1,5 +1,7 @@
-"""Small workload touching every kernel of libdfsim_b200.so, for compute-sanitizer.
+"""Small workload touching every kernel of libdfsim_b200.so, for compute-sanitizer -- or, on a
+pool without it, for the bounds-checked build:
 
+    DFSIM_LIB=checked python profiles/sanitize_run.py      (tests/test_gpu_checked.py)
     compute-sanitizer --tool racecheck python profiles/sanitize_run.py   (memcheck, synccheck alike)
 
 Covers: K1 expand (+ re-expansion), K2 estimate, K2a resolve, K3 v1 exact engine, K3 v2 fused
@@ -32,6 +34,9 @@ def main():
 
     warnings.simplefilter("ignore")
     torch.cuda.set_device(0)
+    from paper_2002_06790_b200 import native
+
+    print(f"library: {native.LIB_PATH.name}", flush=True)
     from paper_2002_06790_b200 import prepare
 
     prepare.LANE_MIN_SIMS = 1  # K4 v3 on these small classes too
