@@ -604,14 +604,15 @@ def run_ours(args):
         sim_ms = a.elapsed_time(b)
     achieved = b_sim_total / (sim_ms / 1e3) / 1e9
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
-    prof = ROOT / "profiles" / "r1_ncu_full.json"
+    profs = sorted((ROOT / "profiles").glob("r*_ncu_full.json"))  # the latest round's capture
+    prof = profs[-1] if profs else ROOT / "profiles" / "r1_ncu_full.json"
     if prof.exists() and args.workload == "resnet50-dp8" and S == 65536:
         for k in json.loads(prof.read_text()):
             if kernel_name in k.get("Kernel Name", ""):
                 traffic = k["dram_bytes_per_launch"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kernel_name,
-                "traffic_source": "profiles/r1_ncu_full.json (ncu --set full, same config)" if traffic else None,
+                "traffic_source": f"profiles/{prof.name} (ncu --set full, same config)" if traffic else None,
                 "b_sim_bytes_mean": b_sim_total / S,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "kernel_ms": sim_ms, "launches_timed": len(classes),
