@@ -51,7 +51,10 @@ def group_classes(graphs, configs, graph_of) -> list:
     field combination, not per candidate (sweeps hold 10^4-10^5 configs)."""
     from .variants import structure_key
 
-    skeys = {gi: structure_key(graphs[gi]) for gi in dict.fromkeys(graph_of)}
+    # structures interned to small ints: equal structures compare in full once here, not at
+    # every class-key lookup below
+    canon: dict = {}
+    skeys = {gi: canon.setdefault(structure_key(graphs[gi]), len(canon)) for gi in dict.fromkeys(graph_of)}
     # identity of the field objects (configs of a sweep share them), built with C-level maps;
     # equal-valued but distinct objects only cost one extra class_key call each
     try:

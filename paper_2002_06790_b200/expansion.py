@@ -96,7 +96,7 @@ class ExpansionPlan:
         group = list(dmap) if dmap else sorted({d for row in clone_dev for d in row})
         self.fabric = fabric = f"collective:{path}:" + "+".join(group)
         clone_ids = [f"{nid}@r{k}" for k in range(R) for nid in base_ids]
-        self.origin = {f"{nid}@r{k}": ("clone", nid) for k in range(R) for nid in base_ids}
+        self.origin = dict(zip(clone_ids, [("clone", nid) for nid in base_ids] * R))
         self.link = link
         if ps:  # per gradient: R pushes, the aggregate, R pulls (ps.ps_nodes order)
             self.up_links = [f"link:{path}:{w}->{self.ps_device}" for w in dmap]
@@ -121,6 +121,7 @@ class ExpansionPlan:
         if not ps:
             self._validate_inherited(g, base_index, R, marked, group)
         order = sorted(range(len(all_ids)), key=all_ids.__getitem__)
+        self._order = order
         self.ids = [all_ids[i] for i in order]
         rank = np.empty(len(all_ids), dtype=np.int32)
         rank[np.asarray(order, dtype=np.int64)] = np.arange(len(all_ids), dtype=np.int32)
@@ -201,31 +202,31 @@ class ExpansionPlan:
         return out
 
     def op_kind(self):
-        """op type and kind code (0 Compute, 1 Transfer, 2 Collective) of every id, without objects."""
+        """op type and kind code (0 Compute, 1 Transfer, 2 Collective) of every id, without objects:
+        the base nodes' once, repeated per replica, the added nodes' by construction (ps.ps_nodes /
+        collective_node), then permuted into rank order."""
         from .ps import AGGREGATE_OP, PULL_OP, PUSH_OP
 
-        g = self._g
         code = {COMPUTE: 0, TRANSFER: 1, COLLECTIVE: 2}
-        ops, kinds = [], []
-        for cid in self.ids:
-            what, nid = self.origin[cid]
-            if what == "clone":
-                n = g.nodes[nid]
-                ops.append(n.op_type)
-                kinds.append(code.get(n.kind, 2))
-            elif what == "coll":
-                ops.append("AllReduce")
-                kinds.append(2)
-            elif cid.startswith("aggregate_"):
-                ops.append(AGGREGATE_OP)
-                kinds.append(0)
-            else:
-                ops.append(PUSH_OP if cid.startswith("push_") else PULL_OP)
-                kinds.append(1)
-        return ops, kinds
+        base = [self._g.nodes[nid] for nid in self.base_ids]
+        ops = [n.op_type for n in base] * self.R
+        kinds = [code.get(n.kind, 2) for n in base] * self.R
+        if self.sync == "parameter_server":
+            per = [PUSH_OP] * self.R + [AGGREGATE_OP] + [PULL_OP] * self.R
+            ops += per * self.G
+            kinds += ([1] * self.R + [0] + [1] * self.R) * self.G
+        else:
+            ops += ["AllReduce"] * self.G
+            kinds += [2] * self.G
+        order = self._order
+        return [ops[i] for i in order], [kinds[i] for i in order]
 
     def _validate_inherited(self, g, base_index, R, marked, group):
-        """Findings of validate(expanded) that come from the base graph (graph.py:331-381)."""
+        """Findings of validate(expanded) that come from the base graph (graph.py:331-381).
+        Every replica clones the same nodes, so one pass decides validity; the findings are
+        only spelled out (per replica, in the reference's order) when there are some."""
+        if self._inherited_ok(g):
+            return
         findings = []
         for k in range(R):
             for nid, node in g.nodes.items():
@@ -252,6 +253,24 @@ class ExpansionPlan:
                     break
         if findings:
             raise DfsimError("internal: expansion produced an invalid graph: " + "; ".join(findings[:5]))
+
+    @staticmethod
+    def _inherited_ok(g) -> bool:
+        nodes = g.nodes
+        for node in nodes.values():
+            for pid, slot in node.inputs:
+                prod = nodes.get(pid)
+                if prod is None or not 0 <= slot < max(1, len(prod.output_shapes)):
+                    return False
+            if node.kind == COLLECTIVE:
+                grp = node.attrs.get("group")
+                if not isinstance(grp, (list, tuple)) or len(grp) < 2 or not _positive_number(node.attrs.get("bytes")):
+                    return False
+            elif node.kind == TRANSFER:
+                src, dst = node.attrs.get("src_device"), node.attrs.get("dst_device")
+                if src is None or dst is None or src == dst or not _positive_number(node.attrs.get("bytes")):
+                    return False
+        return True
 
     def reexpand(self, topo: bool = True, check: bool = False) -> None:
         """Run K1 again into the same device arrays (timed per-class device work).

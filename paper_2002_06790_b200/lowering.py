@@ -278,26 +278,33 @@ def raise_topo_cycle(g, lg: LoweredGraph):
 # ----------------------------------------------------------------------------- profiles
 
 
+_IN_KEY: dict = {}  # (input, dim) -> "in{i}_dim{j}", built once
+
+
+def _in_key(i: int, j: int) -> str:
+    k = _IN_KEY.get((i, j))
+    if k is None:
+        k = _IN_KEY[(i, j)] = f"in{i}_dim{j}"
+    return k
+
+
 def node_features(g, node) -> tuple:
     """costmodel.py:226-246: numeric non-bool attrs + producer dims, sorted by name."""
-    feats = {}
-    for name, value in node.attrs.items():
-        if isinstance(value, bool) or not isinstance(value, (int, float)):
-            continue
-        feats[name] = float(value)
+    feats = {name: float(value) for name, value in node.attrs.items()
+             if type(value) in (int, float) or (not isinstance(value, bool) and isinstance(value, (int, float)))}
+    nodes = g.nodes
     for i, (pid, slot) in enumerate(node.inputs):
-        producer = g.nodes.get(pid)
+        producer = nodes.get(pid)
         if producer is None or slot >= len(producer.output_shapes):
             continue
         for j, dim in enumerate(producer.output_shapes[slot].dims):
-            key = f"in{i}_dim{j}"
+            key = _in_key(i, j)
             if key in feats:
                 raise ValueError(f"node {node.id!r}: attr name collides with {key!r}")
             feats[key] = float(dim)
     out = tuple(sorted(feats.items()))
-    for _, v in out:  # OpSignature's finiteness check (profiledb.py:45-47)
-        if v != v or v in (float("inf"), float("-inf")):
-            raise ValueError(f"non-finite feature value in {out}")
+    if not all(math.isfinite(v) for _, v in out):  # OpSignature's finiteness check (profiledb.py:45-47)
+        raise ValueError(f"non-finite feature value in {out}")
     return out
 
 
@@ -553,18 +560,19 @@ class LoweredProfiles:
             order = np.argsort(op, kind="stable")
             bounds = np.searchsorted(op[order], np.arange(len(op_ids) + 1))
             self.op_nodes = {name: order[bounds[k]:bounds[k + 1]].tolist() for name, k in op_ids.items()}
-        elif op_kind is not None:  # an expansion's ids: op type and kind code by origin (no objects)
-            ops, kinds = op_kind
-            for i, name in enumerate(ops):
-                op[i] = op_ids.setdefault(name, len(op_ids))
-                self.op_nodes.setdefault(name, []).append(i)
+        else:  # op ids in order of first appearance, node lists ascending (one stable sort)
+            if op_kind is not None:  # an expansion's ids: op type and kind code by origin (no objects)
+                ops, kinds = op_kind
+            else:
+                objs = [nodes[nid] for nid in ids]
+                ops = [n.op_type for n in objs]
+                kinds = [0 if n.kind == COMPUTE else (1 if n.kind == TRANSFER else 2) for n in objs]
+            op_ids = {name: k for k, name in enumerate(dict.fromkeys(ops))}
+            op[:] = np.fromiter(map(op_ids.__getitem__, ops), np.int32, N)
             kind[:] = kinds
-        else:
-            for i, nid in enumerate(ids):
-                n = nodes[nid]
-                op[i] = op_ids.setdefault(n.op_type, len(op_ids))
-                self.op_nodes.setdefault(n.op_type, []).append(i)
-                kind[i] = 0 if n.kind == COMPUTE else (1 if n.kind == TRANSFER else 2)
+            order = np.argsort(op, kind="stable")
+            bounds = np.searchsorted(op[order], np.arange(len(op_ids) + 1))
+            self.op_nodes = {name: order[bounds[k]:bounds[k + 1]] for name, k in op_ids.items()}
         sig = np.empty((GV, N), np.int32)
         cbytes = np.zeros((GV, N), np.int64)
         cok = np.zeros((GV, N), np.uint8)
@@ -618,7 +626,7 @@ class LoweredProfiles:
                         emeans.append(rec.mean_duration_us)
         # fitted models where some node could need one (the reference fits lazily, costmodel.py:313-316)
         mkeys, moff, mnames, mcoef, micpt = [], [0], [], [], []
-        exact_set = set(ekeys)
+        exact_keys = np.unique(np.asarray(ekeys, np.uint64))
         self.models = {}
         if flat_uniq is not None:  # the class's feature entries, gathered from the registry
             f_off, f_name, f_val = FEATURES.flat()
@@ -635,7 +643,7 @@ class LoweredProfiles:
             for opname, o in op_ids.items():
                 if not db.op_records.get((opname, hw)):
                     continue
-                if not self._needs_model(h, o, opname, sig, exact_set, ids, ov_sets):
+                if not self._needs_model(h, o, opname, sig, exact_keys, ids, ov_sets):
                     continue
                 if fit_cache is not None and (opname, hw) in fit_cache:  # one fit per (op, hw) per sweep
                     m = fit_cache[(opname, hw)]
@@ -740,19 +748,22 @@ class LoweredProfiles:
         self.strategies = native.Strategies(self.n_sims, pp(s["hw"]), pp(s["gap"]), pp(s["algo"]), pp(s["path"]),
                                             pp(s["ov"]), pp(s["gv"]))
 
-    def _needs_model(self, h, o, opname, sig, exact_set, ids, ov_sets) -> bool:
-        """True if some node of this op, not overridden in every strategy, has no exact record."""
+    def _needs_model(self, h, o, opname, sig, exact_keys, ids, ov_sets) -> bool:
+        """True if some node of this op, not overridden in every strategy, has no exact record
+        (exact_keys: the class's sorted exact-record keys)."""
+        idx = np.asarray(self.op_nodes.get(opname, ()), np.int64)
+        if idx.size == 0:
+            return False
+        keys = ((np.uint64(h) << np.uint64(42)) | (np.uint64(o) << np.uint64(21))
+                | sig[:, idx].astype(np.uint64))                       # [GV, n]
+        missing = ~np.isin(keys, exact_keys).all(axis=0)               # some variant lacks a record
+        if not missing.any():
+            return False
         ov_h = self.strat_ov[self.strat_hw == h]
-        sets = [ov_sets[k] for k in np.unique(ov_h).tolist()] if ov_h.size and (ov_h >= 0).all() else None
-        for i in self.op_nodes.get(opname, ()):
-            for gv in range(sig.shape[0]):
-                key = (h << 42) | (o << 21) | int(sig[gv, i])
-                if key in exact_set:
-                    continue
-                if sets is not None and all(ids[i] in res for res in sets):
-                    continue  # overridden for every strategy of this hardware tag
-                return True
-        return False
+        if ov_h.size and (ov_h >= 0).all():  # overridden for every strategy of this hardware tag?
+            sets = [ov_sets[k] for k in np.unique(ov_h).tolist()]
+            return any(not all(ids[i] in res for res in sets) for i in idx[missing].tolist())
+        return True
 
 
 def _i64(b: int) -> int:

@@ -1,5 +1,7 @@
-"""Host setup (class construction) profile of the bench workloads: wall time per workload and
-the top cProfile entries.  python profiles/setup_profile.py [workload ...]"""
+"""Host setup (class construction) profile of the bench workloads: the one-shot
+``sweep_variants`` call with the graphs' caches dropped (as bench.py's e2e_cold), after two
+warm-up calls (library, context and the CUDA caching allocator warm); wall time per workload,
+then the top cProfile entries by own time.  python profiles/setup_profile.py [workload ...]"""
 
 from __future__ import annotations
 
@@ -14,6 +16,14 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
+CACHES = ("_dfsim_b200_lowered", "_dfsim_base_rows", "_dfsim_base_arr", "_dfsim_grad_keys")
+
+
+def _drop(graphs):
+    for g in graphs:
+        for k in CACHES:
+            g.__dict__.pop(k, None)
+
 
 def main(names):
     import torch
@@ -26,17 +36,23 @@ def main(names):
         graphs, db, configs, graph_of = bench.build_workload(0, bench.WORKLOADS[wl][1], wl)
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
-            sweep_variants(graphs, db, configs[:8], graph_of[:8])  # warm the library / context
-            torch.cuda.synchronize()
+            walls = []
+            for _ in range(3):
+                _drop(graphs)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = sweep_variants(graphs, db, configs, graph_of)
+                torch.cuda.synchronize()
+                walls.append(time.perf_counter() - t0)
+            _drop(graphs)
             pr = cProfile.Profile()
-            t0 = time.perf_counter()
             pr.enable()
-            res = sweep_variants(graphs, db, configs, graph_of)
+            sweep_variants(graphs, db, configs, graph_of)
+            torch.cuda.synchronize()
             pr.disable()
-            wall = time.perf_counter() - t0
         out = io.StringIO()
-        pstats.Stats(pr, stream=out).sort_stats("cumulative").print_stats(45)
-        print(f"== {wl}: cold sweep_variants {wall:.3f} s for {len(configs)} candidates "
+        pstats.Stats(pr, stream=out).sort_stats("tottime").print_stats(30)
+        print(f"== {wl}: one-shot sweep_variants {[round(w, 3) for w in walls]} s for {len(configs)} candidates "
               f"({len(res.classes)} classes, best {res.best_index})")
         print(out.getvalue())
 
