@@ -77,6 +77,10 @@ __device__ __forceinline__ int lds_i(unsigned a) {
 
 constexpr unsigned kHasSlot = 1u << 12, kSource = 1u << 13, kHasSpill = 1u << 14;
 
+// a_lane + 256 * (16-bit row field lo / hi of w): one byte permute moves the field to bytes 1-2
+__device__ __forceinline__ unsigned row_lo(unsigned a_lane, unsigned w) { return a_lane + __byte_perm(w, 0u, 0x4104); }
+__device__ __forceinline__ unsigned row_hi(unsigned a_lane, unsigned w) { return a_lane + __byte_perm(w, 0u, 0x4324); }
+
 struct LaneArgs {
     dfsim_cp_lane_tables t;
     int64_t S;
@@ -120,8 +124,11 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
     unsigned char *region = smem + a.table_bytes + static_cast<size_t>(warp) * a.region_bytes;
     const unsigned a_region = smem_u32(region);
     const unsigned a_lane = a_region + 8u * lane;  // this lane's column in every value row
-    const unsigned a_pairs = a_region + static_cast<unsigned>(NS + NST * RM) * 256u;
+    const unsigned a_zero = a_region + static_cast<unsigned>(NS + NST * RM) * 256u;  // row of 0.0 (never written)
+    const unsigned a_pairs = a_zero + 256u;
     const unsigned a_blocks = a_pairs + static_cast<unsigned>(NST) * 32u * kStride;
+    sts_d(a_zero + 8u * lane, 0.0);
+    __syncwarp();
     const int64_t slot_warp = static_cast<int64_t>(blockIdx.x) * a.wpb + warp;
     double *spill_warp = a.spill + slot_warp * static_cast<int64_t>(a.t.n_long) * 32 + lane;
     asm volatile("mov.b64 %0, %0;" : "+l"(spill_warp));
@@ -178,11 +185,9 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
             for (int p = hi - 1; p >= lo; p--, rec += 16u) {
                 const uint4 r = lds_u4(rec);
                 const unsigned deg = r.y & 0xffu;
-                // successors 1-4 inline: independent loads, issued together
-                const double x0 = deg > 0 ? lds_d(a_lane + 256u * (r.z & 0xffffu)) : 0.0;
-                const double x1 = deg > 1 ? lds_d(a_lane + 256u * (r.z >> 16)) : 0.0;
-                const double x2 = deg > 2 ? lds_d(a_lane + 256u * (r.w & 0xffffu)) : 0.0;
-                const double x3 = deg > 3 ? lds_d(a_lane + 256u * (r.w >> 16)) : 0.0;
+                // successors 1-4 inline (unused ones name the zero row): four independent loads
+                const double x0 = lds_d(row_lo(a_lane, r.z)), x1 = lds_d(row_hi(a_lane, r.z));
+                const double x2 = lds_d(row_lo(a_lane, r.w)), x3 = lds_d(row_hi(a_lane, r.w));
                 const double2 sf = lds_d2(pst + 16u * p);
                 double m01 = x1 > x0 ? x1 : x0, m23 = x3 > x2 ? x3 : x2;
                 double best = m23 > m01 ? m23 : m01;  // >= 0.0: max(0.0, .) (graph.py:465-468)
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
                 }
                 const double sv = __dadd_rn(__dsub_rn(sf.y, sf.x), best);  // finish - start (reporting.py:128)
                 if (r.x & kHasSlot) sts_d(a_lane + 256u * (r.x & 0xfffu), sv);
-                if ((r.x & kHasSpill) && live) spill_warp[32 * static_cast<int64_t>(r.x >> 15)] = sv;
+                if (r.x & kHasSpill) spill_warp[32 * static_cast<int64_t>(r.x >> 15)] = sv;
                 if (r.x & kSource) {
                     const int rk = __ldg(a.t.rank_of_pos + p);
                     if (src == 0x7fffffff || sv > len || (sv == len && rk < src)) {
@@ -255,7 +260,10 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
     unsigned char *region = smem + a.table_bytes + static_cast<size_t>(warp) * a.region_bytes;
     const unsigned a_region = smem_u32(region);
     const unsigned a_lane = a_region + 8u * lane;
-    const unsigned a_blocks = a_region + static_cast<unsigned>(NS + NST * RM) * 256u;
+    const unsigned a_zero = a_region + static_cast<unsigned>(NS + NST * RM) * 256u;  // row of 0.0 (never written)
+    const unsigned a_blocks = a_zero + 256u;
+    sts_d(a_zero + 8u * lane, 0.0);
+    __syncwarp();
     const int64_t slot_warp = static_cast<int64_t>(blockIdx.x) * a.wpb + warp;
     double *spill_warp = a.spill + slot_warp * static_cast<int64_t>(a.t.n_long) * 32 + lane;
     asm volatile("mov.b64 %0, %0;" : "+l"(spill_warp));
@@ -354,17 +362,15 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
                     DFSIM_CHECK(t < BM && p >= 0 && p < N, 8);
                     const uint4 r = lds_u4(blk + 16u * t);
                     const unsigned deg = r.y & 0xffu;
-                    DFSIM_CHECK((deg < 1 || (r.z & 0xffffu) < static_cast<unsigned>(NS + NST * RM)) &&
-                                    (deg < 2 || (r.z >> 16) < static_cast<unsigned>(NS + NST * RM)) &&
-                                    (deg < 3 || (r.w & 0xffffu) < static_cast<unsigned>(NS + NST * RM)) &&
-                                    (deg < 4 || (r.w >> 16) < static_cast<unsigned>(NS + NST * RM)),
-                                6);
+                    DFSIM_CHECK((r.z & 0xffffu) <= static_cast<unsigned>(NS + NST * RM) &&
+                                    (r.z >> 16) <= static_cast<unsigned>(NS + NST * RM) &&
+                                    (r.w & 0xffffu) <= static_cast<unsigned>(NS + NST * RM) &&
+                                    (r.w >> 16) <= static_cast<unsigned>(NS + NST * RM),
+                                6);  // row NS + NST * RM: the zero row
                     DFSIM_CHECK(!(r.x & kHasSlot) || (r.x & 0xfffu) < static_cast<unsigned>(NS), 5);
                     DFSIM_CHECK(!(r.x & kHasSpill) || (r.x >> 15) < static_cast<unsigned>(a.t.n_long), 7);
-                    const double x0 = deg > 0 ? lds_d(a_lane + 256u * (r.z & 0xffffu)) : 0.0;
-                    const double x1 = deg > 1 ? lds_d(a_lane + 256u * (r.z >> 16)) : 0.0;
-                    const double x2 = deg > 2 ? lds_d(a_lane + 256u * (r.w & 0xffffu)) : 0.0;
-                    const double x3 = deg > 3 ? lds_d(a_lane + 256u * (r.w >> 16)) : 0.0;
+                    const double x0 = lds_d(row_lo(a_lane, r.z)), x1 = lds_d(row_hi(a_lane, r.z));
+                    const double x2 = lds_d(row_lo(a_lane, r.w)), x3 = lds_d(row_hi(a_lane, r.w));
                     // position p at register index K - 1 - t + off (pair = two doubles)
                     const int i0 = K - 1 - t, i1 = K - t;  // static after unrolling
                     const double s0 = w[i0 >> 1][(i0 & 1) * 2], f0 = w[i0 >> 1][(i0 & 1) * 2 + 1];
@@ -384,7 +390,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
                     }
                     const double sv = __dadd_rn(__dsub_rn(fi, st), best);  // finish - start (reporting.py:128)
                     if (r.x & kHasSlot) sts_d(a_lane + 256u * (r.x & 0xfffu), sv);
-                    if ((r.x & kHasSpill) && live) spill_warp[32 * static_cast<int64_t>(r.x >> 15)] = sv;
+                    if (r.x & kHasSpill) spill_warp[32 * static_cast<int64_t>(r.x >> 15)] = sv;
                     if (r.x & kSource) {
                         const int rk = __ldg(a.t.rank_of_pos + p);
                         if (src == 0x7fffffff || sv > len || (sv == len && rk < src)) {
@@ -431,7 +437,7 @@ LaneShape lane_shape(const dfsim_cp_lane_tables *t, int stages) {
     const bool reg = stages == 0;
     const size_t nst = reg ? 2 : static_cast<size_t>(stages);
     s.table_bytes = ((static_cast<size_t>(t->n_chunks + 1) * 12 + static_cast<size_t>(t->n_spill_list) * 2 + 15) / 16) * 16;
-    s.region_bytes = static_cast<size_t>(t->n_slots + nst * t->rmax) * 256 +
+    s.region_bytes = static_cast<size_t>(t->n_slots + nst * t->rmax + 1) * 256 +  // + the zero row
                      nst * ((reg ? 0 : 32 * (K * 16 + 16)) + static_cast<size_t>(t->block_max) * 16);
     const size_t budget = 227 * 1024 - 64;
     s.wpb = reg ? 16 : 32;  // the register variant holds 16 warps (<= 128 registers each)
@@ -531,7 +537,7 @@ extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int
     }
     if (n_slots >= 4096) return DFSIM_BAD_ARGUMENT;
     const int32_t NS = std::max(n_slots, 1);
-    if (NS + stages * rmax > 65535) return DFSIM_BAD_ARGUMENT;
+    if (NS + stages * rmax + 1 > 65535) return DFSIM_BAD_ARGUMENT;
     // chunk blocks: records in processing order, then the rows of successors 5.., padded to 16 B
     int64_t unit = 0;  // 16-byte units written
     int32_t block_max = 1;
@@ -547,7 +553,10 @@ extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int
             if (slot_of[u] >= 0) x |= static_cast<uint32_t>(slot_of[u]) | kHasSlot;
             if (is_source && is_source[u]) x |= kSource;
             if (spill_of[u] >= 0) x |= kHasSpill | (static_cast<uint32_t>(spill_of[u]) << 15);
-            uint16_t row[4] = {0, 0, 0, 0};
+            // unused fields name the warp's zero row (after the slots and spill stages): the kernels
+            // load all four without branching, and max(0.0, .) comes for free (graph.py:465-468)
+            const uint16_t zr = static_cast<uint16_t>(NS + stages * rmax);
+            uint16_t row[4] = {zr, zr, zr, zr};
             for (int32_t k = 0; k < deg; k++) {
                 const int64_t j = succ_off[u] + k;
                 const int32_t rv = far_idx[j] >= 0 ? NS + (chunk_of[u] % stages) * rmax + far_idx[j] : slot_of[succ_pos[j]];
