@@ -614,6 +614,9 @@ def run_ours(args):
                 "traffic": traffic, "kernel": kernel_name,
                 "traffic_source": f"profiles/{prof.name} (ncu --set full, same config)" if traffic else None,
                 "b_sim_bytes_mean": b_sim_total / S,
+                # the whole step against the same contract bytes (north star: >= 50% of the HBM roofline)
+                "step_achieved": b_sim_total / (ms_per_step / 1e3) / 1e9,
+                "step_frac": b_sim_total / (ms_per_step / 1e3) / 1e9 / peak,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "kernel_ms": sim_ms, "launches_timed": len(classes),
                 "kernel_ms_source": ("CUDA events around the engine launch of the timed steps" if single else
