@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                     run_v = v;
                     run_f = f;
                     busy_sum = __dadd_rn(busy_sum, __dsub_rn(f, now));
-                    if (f > span) span = f;
+                    span = f;  // a device's finishes never decrease (dur >= 0 here): its last one is its max
                 }
             };
             start_idle();
