@@ -399,8 +399,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2002_06790_b200 import native
-    from paper_2002_06790_b200.batch import TopologyClass, class_key, gather_best
-    from paper_2002_06790_b200.variants import structure_key
+    from paper_2002_06790_b200.batch import TopologyClass, gather_best, group_classes
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -415,15 +414,8 @@ def run_ours(args):
     S = len(configs)
     index_base = rank * S if args.workload != "vgg16-sweep" else len(_vgg_grid()) * rank // world
     t_setup = time.perf_counter()
-    groups: dict = {}
-    skeys = {}
-    for i, cfg in enumerate(configs):
-        gi = graph_of[i]
-        if gi not in skeys:
-            skeys[gi] = structure_key(graphs[gi])
-        groups.setdefault((class_key(cfg), skeys[gi]), []).append(i)
     classes = []
-    for idx in groups.values():
+    for idx in group_classes(graphs, configs, graph_of, db):  # the library's topology classes
         tc = TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], local, graphs=graphs,
                            graph_of=[graph_of[i] for i in idx])
         classes.append((tc, idx, {}))

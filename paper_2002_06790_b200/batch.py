@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import native
-from .errors import CycleError, NativeError
+from .errors import CycleError, DfsimError, NativeError
 from .estimate import estimate_batch, raise_for_row
 from .expansion import ExpansionPlan
 from .lowering import LoweredGraph, LoweredProfiles, lowered, resolve_overrides
@@ -32,23 +32,27 @@ from .simulator import build_schedule, critical_path_arrays, simulate_arrays
 
 
 def class_key(cfg) -> tuple:
-    """Candidates with equal keys share one expanded graph (cli.py:83 decides expansion)."""
+    """Candidates with equal keys share one expanded graph structure (cli.py:83 decides
+    expansion).  The collective path is not part of the key: it names the devices an expansion
+    adds and sets the PS links' attributes, but not the ids, the CSR or the device ranks --
+    group_classes checks that per path (expansion.path_roles)."""
     if getattr(cfg, "sync", "allreduce") == "parameter_server":
-        return ("ps", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers), cfg.collective.path,
-                cfg.ps_device)
+        return ("ps", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers), cfg.ps_device)
     if not (cfg.replicas > 1 or cfg.device_map):
         return ("plain",)
-    return ("dp", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers), cfg.collective.path)
+    return ("dp", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers))
 
 
 _R, _DMAP = operator.attrgetter("replicas"), operator.attrgetter("device_map")
 _MARKERS, _COLL = operator.attrgetter("gradient_markers"), operator.attrgetter("collective")
 
 
-def group_classes(graphs, configs, graph_of) -> list:
+def group_classes(graphs, configs, graph_of, db=None) -> list:
     """Config indices of each topology class, classes in order of first appearance.  A class
-    is (class_key, structure of the candidate's graph); keys are derived once per distinct
-    field combination, not per candidate (sweeps hold 10^4-10^5 configs)."""
+    is (class_key, structure of the candidate's graph, device roles of the expansion); keys
+    are derived once per distinct field combination, not per candidate (sweeps hold 10^4-10^5
+    configs)."""
+    from .expansion import path_roles
     from .variants import structure_key
 
     # structures interned to small ints: equal structures compare in full once here, not at
@@ -72,8 +76,19 @@ def group_classes(graphs, configs, graph_of) -> list:
     # first config of each distinct field combination (reversed: the smallest index is written last)
     first = dict(zip(reversed(raw), range(len(raw) - 1, -1, -1)))
     cls_of_key: dict = {}
-    cls_of_raw = {r: cls_of_key.setdefault((class_key(configs[i]), skeys[graph_of[i]]), len(cls_of_key))
-                  for r, i in first.items()}
+    roles: dict = {}
+
+    def key_of(i):
+        cfg, gi = configs[i], graph_of[i]
+        k = class_key(cfg)
+        if k == ("plain",):
+            return k, skeys[gi], None
+        rk = (k, skeys[gi], cfg.collective.path)  # graph variants of one structure share their roles
+        if rk not in roles:  # None (expansion would fail): a class of its own per path
+            roles[rk] = path_roles(graphs[gi], cfg, db) or ("\x00fails", cfg.collective.path)
+        return k, skeys[gi], roles[rk]
+
+    cls_of_raw = {r: cls_of_key.setdefault(key_of(i), len(cls_of_key)) for r, i in first.items()}
     cls = np.fromiter(map(cls_of_raw.__getitem__, raw), np.int64, len(raw))
     order = np.argsort(cls, kind="stable")  # config order inside each class
     cuts = np.flatnonzero(np.diff(cls[order])) + 1
@@ -114,6 +129,8 @@ class TopologyClass:
         self.configs = list(configs)
         variant_rows, strat_gv = None, None
         multi = graphs is not None and len(set(graph_of)) > 1
+        self._db = db
+        self._path_objects = {}  # path -> (graph objects, device names) of the other paths in the class
         if multi or kind != "plain":
             # estimate inputs from the base graph(s): a clone's row is its base node's, so features
             # are computed once per base node and collective / PS node, not per expanded node
@@ -121,9 +138,18 @@ class TopologyClass:
 
             if graphs is None:
                 graphs, graph_of = [g], [0] * len(configs)
-            gv_of = {gi: k for k, gi in enumerate(dict.fromkeys(graph_of))}
-            variant_rows = variant_arrays_many(kind, self.ids, [graphs[gi] for gi in gv_of], structure, cfg0, db)
-            strat_gv = np.fromiter(map(gv_of.__getitem__, graph_of), np.int32, len(graph_of))
+            if kind == "ps":  # the PS links' attributes depend on the path: a variant per (graph, path)
+                paths = [c.collective.path for c in configs]
+                vkeys = list(zip(graph_of, paths))
+            else:
+                vkeys = list(graph_of)
+            gv_of = {vk: k for k, vk in enumerate(dict.fromkeys(vkeys))}
+            first_cfg = {}
+            for vk, c in zip(vkeys, configs):
+                first_cfg.setdefault(vk, c)
+            variant_rows = variant_arrays_many(kind, self.ids, [graphs[vk[0] if kind == "ps" else vk] for vk in gv_of],
+                                               structure, cfg0, db, cfgs=[first_cfg[vk] for vk in gv_of])
+            strat_gv = np.fromiter(map(gv_of.__getitem__, vkeys), np.int32, len(vkeys))
         self.lp = LoweredProfiles(g if self.plan is not None else self.graph, self.ids, db, self.configs,
                                   ctx.device, None, strat_gv, fit_cache=fit_cache, variant_arrays=variant_rows,
                                   op_kind=self.plan.op_kind() if self.plan is not None else None)
@@ -138,6 +164,24 @@ class TopologyClass:
     def graph(self):
         """The class's expanded graph objects (built on first use for expanded classes)."""
         return self._graph if self.plan is None else self.plan.graph
+
+    def objects_for(self, row: int):
+        """(graph objects, device names by rank) of candidate ``row``: the class's own for its
+        first config's collective path; for another path of the class (group_classes), the
+        host objects of that path's expansion (same ids and ranks, its own device names)."""
+        path = self.configs[row].collective.path if self.plan is not None else None
+        if self.plan is None or path == self.plan.cfg.collective.path:
+            return self.graph, self.lg.devices
+        got = self._path_objects.get(path)
+        if got is None:
+            cfg = self.configs[row]
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                plan = ExpansionPlan(self.plan._g, cfg, run_k1=False, build_objects=False, db=self._db)
+            if plan.ids != self.ids or len(plan.devices) != len(self.lg.devices):
+                raise DfsimError("internal: paths of one topology class expand differently")
+            got = self._path_objects[path] = (plan.graph, plan.devices)
+        return got
 
     # ------------------------------------------------------------------ fused path
     def _prepare_variants(self):
@@ -414,9 +458,10 @@ class SweepResult:
         tc, o, row = self._row(i)
         st, fi = tc.rows_by_rank(o, row)
         entries = self._entries(tc, o, row)
-        return build_schedule(tc.graph, tc.lg, st.cpu().numpy(), fi.cpu().numpy(),
+        g, devices = tc.objects_for(row)
+        return build_schedule(g, tc.lg, st.cpu().numpy(), fi.cpu().numpy(),
                               float(o["makespan"][row].item()), o["busy"][row, : tc.lg.n_devices].cpu().numpy(),
-                              entries)
+                              entries, devices=devices)
 
     def _entries(self, tc, o, row):
         """Duration source tags of one candidate (the fused path keeps per-variant tags)."""
@@ -455,26 +500,27 @@ class SweepResult:
             tables = tc.summary_tables()
             order, key_total, key_first, sums = run_summary(tc.ctx, tables, st, fi)
             p = critical_path_arrays(tc.lg, st, fi, paths=True) if tc.lg.n else None
-            g, lg = tc.graph, tc.lg
-            kinds = {d: spec.kind for d, spec in g.devices.items()}
-            extra = [d for d in lg.devices if d not in g.devices]
+            lg = tc.lg
             kt, kf, sm = key_total.cpu().numpy(), key_first.cpu().numpy(), sums.cpu().numpy()
             ms = o["makespan"].cpu().numpy()
             busy_rows = o["busy"].cpu().numpy()
-            order_h = order.cpu().numpy() if extra else None
+            order_h = order.cpu().numpy()
             cp_len = p["cp_len"].cpu().numpy() if p else None
             cp_path = p["cp_path"].cpu().numpy() if p else None
             cp_plen = p["cp_path_len"].cpu().numpy() if p else None
             dev_of = lg.device_of_rank()
             for j, (k, row) in enumerate(items):
+                g, devices = tc.objects_for(row)
+                kinds = {d: spec.kind for d, spec in g.devices.items()}
+                extra = [d for d in devices if d not in g.devices]
                 busy = {d: 0.0 for d in g.devices}
-                rank_busy = {lg.devices[r]: float(busy_rows[row, r]) for r in range(lg.n_devices)}
+                rank_busy = {devices[r]: float(busy_rows[row, r]) for r in range(lg.n_devices)}
                 for d in g.devices:
                     if d in rank_busy:
                         busy[d] = rank_busy[d]
                 if extra:  # devices outside g.devices join in entry order (engine.py:90-92)
                     for v in order_h[j, : lg.n].tolist():
-                        d = lg.devices[dev_of[v]]
+                        d = devices[dev_of[v]]
                         if d not in busy:
                             busy[d] = rank_busy[d]
                 makespan = float(ms[row])
@@ -497,18 +543,19 @@ class SweepResult:
         tc, o, row = self._row(i)
         st, fi = tc.rows_by_rank_batch(o, [row])
         order, _, _, _ = run_summary(tc.ctx, tc.summary_tables(), st, fi)
-        g, lg = tc.graph, tc.lg
-        busy_keys = set(g.devices) | set(lg.devices)
-        tracks = sorted(busy_keys)
-        tid = {d: k for k, d in enumerate(tracks)}
-        dev_of = lg.device_of_rank()
-        if getattr(tc, "_trace_tables", None) is None:
-            tc._trace_tables = TraceTables(tc.ids, [g.nodes[nid].op_type or nid for nid in tc.ids],
-                                           np.zeros(lg.n, np.uint8), [tid[lg.devices[d]] for d in dev_of], tracks)
+        lg = tc.lg
+        g, devices = tc.objects_for(row)
+        cache = tc.__dict__.setdefault("_trace_tables", {})  # per collective path (device names)
+        tt = cache.get(id(devices))
+        if tt is None:
+            tracks = sorted(set(g.devices) | set(devices))
+            tid = {d: k for k, d in enumerate(tracks)}
+            tt = cache[id(devices)] = TraceTables(tc.ids, [g.nodes[nid].op_type or nid for nid in tc.ids],
+                                                  np.zeros(lg.n, np.uint8),
+                                                  [tid[devices[d]] for d in lg.device_of_rank()], tracks)
         src = self._entries(tc, o, row)
         tags = np.fromiter((SOURCE_TAGS.index(src[nid].source) for nid in tc.ids), dtype=np.uint8, count=lg.n)
-        return tc._trace_tables.write(order.cpu().numpy()[0, : lg.n], st.cpu().numpy()[0], fi.cpu().numpy()[0],
-                                      tags=tags)
+        return tt.write(order.cpu().numpy()[0, : lg.n], st.cpu().numpy()[0], fi.cpu().numpy()[0], tags=tags)
 
     def critical_path(self, i: int):
         tc, o, row = self._row(i)
@@ -564,7 +611,7 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
     failing config in list order (cli.py:132-145) or None.  ``result.best_*`` are this shard's."""
     import torch
 
-    groups = group_classes(graphs, configs, graph_of)
+    groups = group_classes(graphs, configs, graph_of, db)
     S = len(configs)
     ctx = native.Context.get(device)
     dev = f"cuda:{ctx.device}"

@@ -187,7 +187,7 @@ class ExpansionPlan:
     @property
     def graph(self) -> DataflowGraph:
         """The expanded graph's host objects (built on first use)."""
-        if self._graph is None and getattr(self, "ctx", None) is not None:
+        if self._graph is None and getattr(self, "_g", None) is not None:
             self._graph = self._objects(self._g, self.cfg)
         return self._graph
 
@@ -196,10 +196,8 @@ class ExpansionPlan:
         """DeviceSpec of every device the expansion adds (PS links need their throughput)."""
         if self.sync != "parameter_server":
             return {}
-        out = {}
-        for lid in self.up_links + self.down_links:
-            out[lid] = DeviceSpec(lid, "Link", self.cfg.hardware, self.link.throughput_mbps, self.link.latency_us)
-        return out
+        return {lid: DeviceSpec(lid, "Link", self.cfg.hardware, self.link.throughput_mbps, self.link.latency_us)
+                for lid in self.up_links + self.down_links}
 
     def op_kind(self):
         """op type and kind code (0 Compute, 1 Transfer, 2 Collective) of every id, without objects:
@@ -330,8 +328,9 @@ class ExpansionPlan:
             from .ps import expand_parameter_server
 
             gx = expand_parameter_server(g, cfg, _LinkDB(self.link, cfg.collective.path), self.ps_device).graph
-            object.__setattr__(gx, "_dfsim_b200_lowered", ((len(gx.nodes), len(gx.devices), self.ctx.device),
-                                                           self.lowered))
+            if self.lowered is not None:
+                object.__setattr__(gx, "_dfsim_b200_lowered", ((len(gx.nodes), len(gx.devices), self.ctx.device),
+                                                               self.lowered))
             return gx
         R, marked = self.R, set(self.marked) if self.R > 1 else set()
         nodes = {}
@@ -355,7 +354,9 @@ class ExpansionPlan:
         meta = dict(g.metadata)
         meta["replicas"] = R
         gx = DataflowGraph(nodes=nodes, devices=devices, metadata=meta)
-        object.__setattr__(gx, "_dfsim_b200_lowered", ((len(nodes), len(devices), self.ctx.device), self.lowered))
+        if self.lowered is not None:
+            object.__setattr__(gx, "_dfsim_b200_lowered", ((len(nodes), len(devices), self.ctx.device),
+                                                           self.lowered))
         return gx
 
 
@@ -368,6 +369,65 @@ def expand_data_parallel(g, cfg, device: int | None = None) -> ExpandedGraph:
 
 def expand_class(g, cfg, device: int | None = None) -> ExpansionPlan:
     return ExpansionPlan(g, cfg, device)
+
+
+def path_roles(g, cfg, db=None):
+    """The sorted device list an expansion of ``g`` under ``cfg`` produces, with the devices it
+    adds written with the collective path as a placeholder (ExpansionPlan's device logic).
+
+    Configs of one path-free class key whose roles agree expand to the same ids, CSR and device
+    ranks for every path: only the added devices' names and the PS links' attributes depend on
+    the path, so they share one topology class (batch.group_classes).  None when the expansion
+    would fail -- such configs keep a class of their own, whose construction raises the
+    reference's error."""
+    from .model import SCENARIO_GPU_GPU_UNI
+
+    try:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            marked = marked_gradients(g, cfg)
+    except DfsimError:
+        return None
+    R, dmap, path = cfg.replicas, tuple(cfg.device_map), cfg.collective.path
+    ps = getattr(cfg, "sync", "allreduce") == "parameter_server"
+    psd = getattr(cfg, "ps_device", "ps0")
+    base, compute = set(), False
+    for n in g.nodes.values():
+        if dmap and n.kind == COMPUTE:
+            compute = True
+        else:
+            base.add(n.device)
+    if compute:
+        base.update(dmap)
+    added = {}
+    if ps:
+        if R < 2 or len(dmap) != R or psd in dmap:
+            return None
+        if db is None or db.link_records.get((SCENARIO_GPU_GPU_UNI, path, 2)) is None:
+            return None
+        if marked:
+            added[psd] = psd
+            for w in dmap:
+                added[f"link:{path}:{w}->{psd}"] = f"link:\x00:{w}->{psd}"
+                added[f"link:{path}:{psd}->{w}"] = f"link:\x00:{psd}->{w}"
+    elif R > 1 and marked:
+        group = list(dmap) if dmap else sorted(base)
+        added[f"collective:{path}:" + "+".join(group)] = "collective:\x00:" + "+".join(group)
+    return tuple(added.get(d, d) for d in sorted(base | set(added)))
+
+
+def ps_link_specs(cfg, db, ps_device: str) -> dict:
+    """DeviceSpec of the PS links an expansion under ``cfg`` adds (ps.py: the path's
+    gpu-gpu-uni row gives every link's throughput and latency)."""
+    from .model import SCENARIO_GPU_GPU_UNI
+
+    path = cfg.collective.path
+    link = db.link_records[(SCENARIO_GPU_GPU_UNI, path, 2)]
+    out = {}
+    for lid in ([f"link:{path}:{w}->{ps_device}" for w in cfg.device_map]
+                + [f"link:{path}:{ps_device}->{w}" for w in cfg.device_map]):
+        out[lid] = DeviceSpec(lid, "Link", cfg.hardware, link.throughput_mbps, link.latency_us)
+    return out
 
 
 class _LinkDB:

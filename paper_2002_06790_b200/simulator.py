@@ -105,11 +105,13 @@ def simulate(g, durations, device: int | None = None) -> Schedule:
                           o["busy"][0, : lg.n_devices].cpu().numpy(), entries)
 
 
-def build_schedule(g, lg: LoweredGraph, start, finish, makespan, busy_by_rank, entries=None) -> Schedule:
-    """Schedule object from kernel outputs; entries ordered (start, device, id) (engine.py:88)."""
+def build_schedule(g, lg: LoweredGraph, start, finish, makespan, busy_by_rank, entries=None,
+                   devices=None) -> Schedule:
+    """Schedule object from kernel outputs; entries ordered (start, device, id) (engine.py:88).
+    ``devices``: names by device rank when they differ from lg's (another collective path)."""
     dev = lg.device_of_rank()
     order = np.lexsort((np.arange(lg.n), dev, start)) if lg.n else np.zeros(0, np.int64)
-    ids, devices = lg.ids, lg.devices
+    ids, devices = lg.ids, (lg.devices if devices is None else devices)
     out = []
     for i in order.tolist():
         nid = ids[i]

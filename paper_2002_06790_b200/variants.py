@@ -57,7 +57,7 @@ def rows_for(kind: str, ids, g_b, structure, cfg=None, db=None) -> list:
             for f, ok, b, gs, thr, lat in zip(*(arr[k].tolist() for k in ROW_FIELDS))]
 
 
-def _special_rows(kind, ids, pos, g_b, structure, cfg) -> dict:
+def _special_rows(kind, ids, pos, g_b, structure, cfg, db=None) -> dict:
     """Rows of the nodes a class adds (AllReduce / PS push, aggregate, pull) at positions
     ``pos``, each built exactly as the expansion builds it, with the reference's own
     node_features on a stand-in graph."""
@@ -71,9 +71,11 @@ def _special_rows(kind, ids, pos, g_b, structure, cfg) -> dict:
             stand = {f"{gid}@r{k}": grad for k in range(plan.R)}
             out.append(node_rows(_Stand({**stand, node.id: node}, {}), [node.id])[0])
     else:
+        from .expansion import ps_link_specs
         from .ps import ps_nodes
 
-        specs = structure.device_specs  # the PS links (throughput, latency)
+        # the PS links (throughput, latency) of this config's collective path
+        specs = ps_link_specs(cfg, db, cfg.ps_device) if db is not None else structure.device_specs
         built, first = {}, {}
         for p in pos:
             cid = ids[p]
@@ -136,7 +138,7 @@ def variant_arrays(kind: str, ids, g_b, structure, cfg=None, db=None, cache=None
         key = tuple((s.dims, s.dtype_bytes) for gid in cache["grads"] for s in nodes[gid].output_shapes)
         rows = cache.get(("special", key))
         if rows is None:
-            rows = cache[("special", key)] = _special_rows(kind, ids, special.tolist(), g_b, structure, cfg)
+            rows = cache[("special", key)] = _special_rows(kind, ids, special.tolist(), g_b, structure, cfg, db)
         for k in ROW_FIELDS:
             out[k][special] = rows[k]
     return out
@@ -145,10 +147,11 @@ def variant_arrays(kind: str, ids, g_b, structure, cfg=None, db=None, cache=None
 __all__ = ["StructureKey", "structure_key", "rows_for", "variant_arrays", "variant_arrays_many", "node_features"]
 
 
-def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None) -> dict:
+def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None, cfgs=None) -> dict:
     """``variant_arrays`` of several graph variants of one class, stacked: each field [GV, N].
     Vectorised over the variants: one gather of the stacked base rows, and the added nodes'
-    rows once per distinct gradient-shape tuple."""
+    rows once per distinct gradient-shape tuple (and, for PS classes, collective path:
+    ``cfgs[v]`` is variant v's config, whose path sets the PS links' attributes)."""
     cache: dict = {}
     variant_arrays(kind, ids, graphs[0], structure, cfg, db, cache)  # fills perm / special / grads
     perm, special, grads = cache["perm"], cache["special"], cache["grads"]
@@ -169,11 +172,14 @@ def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None) ->
             if key is None:
                 nodes = gb.nodes
                 key = memo[gkey] = tuple((s.dims, s.dtype_bytes) for gid in grads for s in nodes[gid].output_shapes)
-            groups.setdefault(key, []).append(v)
-        for key, vs in groups.items():
-            rows = cache.get(("special", key))
+            vcfg = cfgs[v] if cfgs is not None else cfg
+            groups.setdefault((key, vcfg.collective.path if kind == "ps" else None), []).append(v)
+        for (key, _), vs in groups.items():
+            vcfg = cfgs[vs[0]] if cfgs is not None else cfg
+            same = kind != "ps" or vcfg.collective.path == cfg.collective.path
+            rows = cache.get(("special", key)) if same else None
             if rows is None:
-                rows = _special_rows(kind, ids, special.tolist(), graphs[vs[0]], structure, cfg)
+                rows = _special_rows(kind, ids, special.tolist(), graphs[vs[0]], structure, vcfg, db)
             sel = np.ix_(np.asarray(vs, np.int64), special)
             for k in ROW_FIELDS:
                 out[k][sel] = rows[k]

@@ -112,7 +112,8 @@ def test_multiclass_workloads_full_size(workload):
     for tc, idx, o in res.classes:  # per-device busy of every candidate
         busy = o["busy"][:, : tc.lg.n_devices].cpu().numpy()
         for row, i in enumerate(idx):
-            assert [busy[row, d] for d in range(tc.lg.n_devices)] == [ref["busy"][i][d] for d in tc.lg.devices]
+            names = tc.objects_for(row)[1]  # device names of this candidate's collective path
+            assert [busy[row, d] for d in range(tc.lg.n_devices)] == [ref["busy"][i][d] for d in names]
 
 
 def test_global_duration_row_class_matches_exact_engine():

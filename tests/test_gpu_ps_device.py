@@ -26,7 +26,7 @@ def _ps_classes(workload, limit=None):
     for cfg, gi in zip(configs, graph_of):
         if getattr(cfg, "sync", "") != "parameter_server":
             continue
-        k = (class_key(cfg), gi if workload != "vgg16-sweep" else gi % 7)
+        k = (class_key(cfg), cfg.collective.path, gi if workload != "vgg16-sweep" else gi % 7)
         if k in seen:
             continue
         seen.add(k)
@@ -76,7 +76,7 @@ def test_single_launch_k1_equals_multi_kernel_k1(workload, limit, monkeypatch):
     graphs, db, configs, graph_of = bench.build_workload(0, bench.WORKLOADS[workload][1], workload)
     seen, classes = set(), []
     for cfg, gi in zip(configs, graph_of):
-        k = (class_key(cfg), gi if workload != "vgg16-sweep" else gi % 5)
+        k = (class_key(cfg), cfg.collective.path, gi if workload != "vgg16-sweep" else gi % 5)
         if k not in seen:
             seen.add(k)
             classes.append((graphs[gi], cfg))
