@@ -437,6 +437,23 @@ class TopologyClass:
         return rec
 
 
+class _Where:
+    """config index -> (class position, row) over two arrays (sweeps hold 10^4-10^5 configs)."""
+
+    def __init__(self, cls, row):
+        self.cls, self.row = cls, row
+
+    def __getitem__(self, i):
+        c = int(self.cls[i])
+        if c < 0:
+            raise KeyError(i)
+        return c, int(self.row[i])
+
+    def items(self):
+        for i in np.flatnonzero(self.cls >= 0).tolist():
+            yield i, (int(self.cls[i]), int(self.row[i]))
+
+
 @dataclass
 class SweepResult:
     makespan: np.ndarray
@@ -619,6 +636,8 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
     cp_len = torch.zeros(max(S, 1), dtype=torch.float64, device=dev)
     result = SweepResult(np.zeros(0), np.zeros(0), -1, float("nan"))
     failures = []  # (config index, exception)
+    where_cls, where_row = np.full(S, -1, np.int32), np.zeros(S, np.int32)
+    result._where = _Where(where_cls, where_row)
     built = []
     fits: dict = {}  # fitted models shared by the classes of this sweep (costmodel.py:313-316 fits per call)
     for idx in groups:
@@ -664,8 +683,9 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
             for k in ("start", "finish", "sched"):
                 o.pop(k, None)
         result.classes.append((tc, idx, o))
-        for row, i in enumerate(idx):
-            result._where[i] = (pos, row)
+        ia = np.asarray(idx, np.int64)
+        where_cls[ia] = pos
+        where_row[ia] = np.arange(len(idx), dtype=np.int32)
     failure = min(failures, key=lambda f: f[0]) if failures else None
     rec = torch.empty(2, dtype=torch.float64, device=dev)
     ctx.call("dfsim_argmin", S, native.ptr(makespan), index_base, native.ptr(rec))

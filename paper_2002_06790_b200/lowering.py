@@ -640,10 +640,9 @@ class LoweredProfiles:
             name_pool = {nm for feats in sig_ids for nm, _ in feats}
         fitted = []
         for hw, h in self.hw_ids.items():
+            need = self._ops_needing_models(h, op, sig, exact_keys, ids, ov_sets)
             for opname, o in op_ids.items():
-                if not db.op_records.get((opname, hw)):
-                    continue
-                if not self._needs_model(h, o, opname, sig, exact_keys, ids, ov_sets):
+                if o not in need or not db.op_records.get((opname, hw)):
                     continue
                 if fit_cache is not None and (opname, hw) in fit_cache:  # one fit per (op, hw) per sweep
                     m = fit_cache[(opname, hw)]
@@ -748,22 +747,20 @@ class LoweredProfiles:
         self.strategies = native.Strategies(self.n_sims, pp(s["hw"]), pp(s["gap"]), pp(s["algo"]), pp(s["path"]),
                                             pp(s["ov"]), pp(s["gv"]))
 
-    def _needs_model(self, h, o, opname, sig, exact_keys, ids, ov_sets) -> bool:
-        """True if some node of this op, not overridden in every strategy, has no exact record
-        (exact_keys: the class's sorted exact-record keys)."""
-        idx = np.asarray(self.op_nodes.get(opname, ()), np.int64)
-        if idx.size == 0:
-            return False
-        keys = ((np.uint64(h) << np.uint64(42)) | (np.uint64(o) << np.uint64(21))
-                | sig[:, idx].astype(np.uint64))                       # [GV, n]
-        missing = ~np.isin(keys, exact_keys).all(axis=0)               # some variant lacks a record
-        if not missing.any():
-            return False
+    def _ops_needing_models(self, h, op, sig, exact_keys, ids, ov_sets) -> set:
+        """Op ids (of hardware tag h) with some node that has no exact record in some graph
+        variant and is not overridden in every strategy of this tag: one vectorised pass over
+        all nodes instead of one per (op, tag)."""
+        keys = ((np.uint64(h) << np.uint64(42)) | (op.astype(np.uint64) << np.uint64(21))
+                | sig.astype(np.uint64))                                 # [GV, N]
+        missing = np.flatnonzero(~np.isin(keys, exact_keys).all(axis=0))
+        if missing.size == 0:
+            return set()
         ov_h = self.strat_ov[self.strat_hw == h]
-        if ov_h.size and (ov_h >= 0).all():  # overridden for every strategy of this hardware tag?
+        if ov_h.size and (ov_h >= 0).all():  # nodes overridden for every strategy of this tag need nothing
             sets = [ov_sets[k] for k in np.unique(ov_h).tolist()]
-            return any(not all(ids[i] in res for res in sets) for i in idx[missing].tolist())
-        return True
+            missing = np.asarray([i for i in missing.tolist() if not all(ids[i] in res for res in sets)], np.int64)
+        return set(np.unique(op[missing]).tolist()) if missing.size else set()
 
 
 def _i64(b: int) -> int:
