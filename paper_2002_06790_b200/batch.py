@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import operator
 import os
+import threading
 import warnings
 from dataclasses import dataclass, field
 
@@ -619,6 +620,23 @@ def _row_error(tc, o, row) -> Exception:
     return CycleError(sorted(tc.ids[k] for k in np.nonzero(np.isnan(st))[0]))
 
 
+_STREAMS: dict = {}
+_STREAMS_LOCK = threading.Lock()
+
+
+def _side_streams(device: int, n: int) -> list:
+    """n class streams of ``device``, the same ones on every call: PyTorch caches freed device
+    blocks per stream and the library keeps device scratch per (context, stream), so fresh
+    streams per sweep would allocate afresh every time (and grow the scratch list)."""
+    import torch
+
+    with _STREAMS_LOCK:
+        have = _STREAMS.setdefault(device, [])
+        while len(have) < n:
+            have.append(torch.cuda.Stream(device))
+        return have[:n]
+
+
 def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_schedules: bool = False,
                 fused: bool = True, streams: int = 32, index_base: int = 0):
     """The per-device body of every sweep: returns ``(result, record, failure)`` without raising.
@@ -651,7 +669,7 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
             failures.append((idx[0], e))
     built.sort(key=lambda b: -b[1].lg.n * len(b[0]))  # most work first: the longest CTAs must not form the tail
     outs = [{} for _ in built]
-    side = [torch.cuda.Stream(ctx.device) for _ in range(min(max(streams, 1), len(built)))] if len(built) > 1 else []
+    side = _side_streams(ctx.device, min(max(streams, 1), len(built))) if len(built) > 1 else []
     cur = torch.cuda.current_stream(ctx.device)
     for st in side:
         st.wait_stream(cur)
