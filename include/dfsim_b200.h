@@ -207,8 +207,9 @@ int dfsim_simulate_batch(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, c
 
 /* Exact engine with remapped outputs (the fused engine's overflow fallback):
  * row s of dur is simulated and written to output row out_rows[s] (or s when
- * NULL), node v at column pos[v] (or v when NULL).  interleaved != 0: start points at
- * [rows][N] (start, finish) pairs (the fused layout) and finish is ignored. */
+ * NULL), node v at column pos[v] (or v when NULL).  interleaved 1: start points at
+ * [rows][N] (start, finish) pairs and finish is ignored; 2: the same pairs in the fused
+ * engine's tiled layout (see dfsim_simulate_fused). */
 int dfsim_simulate_batch_ex(dfsim_ctx *ctx, const dfsim_graph *g, int64_t n_sims, const double *dur,
                             int64_t dur_stride, double *start, double *finish, double *makespan, double *busy,
                             int32_t *n_placed, const int32_t *pos, const int64_t *out_rows, int32_t interleaved);
@@ -257,6 +258,7 @@ typedef struct {
                                   small class spread over many small chunks fills the SMs */
     const uint32_t *ov_any;    /* [(N + 31) / 32] bit per node rank: in some override set (NULL: search
                                   every popped node of a candidate with overrides) */
+    int32_t sched_tiled;       /* 1: the tiled schedule layout (for K4 v3); 0: rows sched[S][N][2] (K4 v2) */
 } dfsim_fused_strategies;
 
 /* K2a: base[var*N+v] = estimate of node v under variant var = (graph variant, hw, algo, path) with
@@ -283,7 +285,12 @@ int32_t dfsim_fused_capacity(const dfsim_sim_tables *g);
  * the class tables outweighs its candidates' state; <= dfsim_fused_capacity. */
 int32_t dfsim_fused_chunk(const dfsim_sim_tables *g, int64_t n_sims, int32_t num_sms);
 
-/* K3 v2: outputs sched[S][N][2] = (start, finish) by level position (16-byte aligned);
+/* K3 v2: outputs (start, finish) pairs by level position.  st->sched_tiled = 1 (classes on K4 v3):
+ * in 32-candidate tiles -- the candidate at position k of st->order (its "slot"), node position p
+ * at pair ((k / 32) * N + p) * 32 + k % 32 of sched (room for ceil(S / 32) * 32 slots); the
+ * candidates of one chunk are neighbours, so a tile's writes meet in L2.  0 (K4 v2): rows,
+ * candidate s at pairs [s * N, s * N + N).  16-byte aligned.  A warp of K4 v3 (lane = candidate) thus reads one
+ * contiguous 512-byte run per position; a schedule row is a stride-32 gather;
  * flags[s] = 1 when the FIFO ring overflowed (re-run s with dfsim_simulate_batch_ex);
  * n_placed[s] = -1 then. */
 int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, const dfsim_fused_strategies *st,
@@ -313,17 +320,18 @@ typedef struct {
     int32_t stage_doubles;     /* doubles per prefetch stage: (start, finish) x K | spill values R */
 } dfsim_cp_tables;
 
-/* K4 v2: critical-path length and its start node per candidate over the fused
- * engine's sched[S][N][2] (start, finish) pairs stored by level position. */
-int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *sched,
-                               double *cp_len, int32_t *cp_src);
+/* K4 v2: critical-path length and its start node per candidate over the fused engine's
+ * (start, finish) pairs in the rows layout (dfsim_simulate_fused, sched_tiled = 0); row k holds
+ * candidate cand_of_slot[k] (NULL: k), whose cp_len / cp_src are written. */
+int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims,
+                               const int64_t *cand_of_slot, const double *sched, double *cp_len, int32_t *cp_src);
 
 /* Candidates one CTA of dfsim_critical_path_levels holds (0: the class tables do not fit
  * in shared memory; such a class uses the rank-layout kernels instead). */
 int32_t dfsim_critical_path_levels_capacity(const dfsim_cp_tables *t);
 
 /* K4 v3 (lane per candidate): graph.py:446-474 on finish - start over the fused engine's
- * sched[S][N][2] pairs by level position.  Every lane of a warp is one candidate and the warp
+ * tiled (start, finish) pairs (dfsim_simulate_fused).  Every lane of a warp is one candidate and the warp
  * walks the class's positions in reverse (one node at a time, all lanes in step), so the
  * class tables are read once per 32 candidates.  A node's suffix value lives in a shared-
  * memory slot while it is read within its own or the next prefetch chunk, otherwise in a
@@ -366,14 +374,16 @@ int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int32_t *succ_
 
 /* stages: prefetch depth (2 or 3, as planned). */
 int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
-                              const double *sched, double *cp_len, int32_t *cp_src);
+                              const int64_t *cand_of_slot, const double *sched, double *cp_len, int32_t *cp_src);
 
-/* The same over candidates order[0..n_sims) (device int64 indices into sched's rows; NULL:
- * 0..n_sims-1), with at most max_warps warps a CTA (0: as many as fit) so that the kernel can
- * share SMs with a concurrently running engine launch.  order requires stages 0. */
+/* Schedules are read at their slots in the fused engine's tiled layout; the candidate of slot
+ * k is cand_of_slot[k] (the engine's candidate order; NULL: k), and cp_len / cp_src are written
+ * at the candidate.  _ex: only the slots slots[0..n_sims) (device int64; NULL: 0..n_sims-1),
+ * with at most max_warps warps a CTA (0: as many as fit) so that the kernel can share SMs with
+ * a concurrently running engine launch.  slots requires stages 0. */
 int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
-                                 const int64_t *order, int32_t max_warps, const double *sched, double *cp_len,
-                                 int32_t *cp_src);
+                                 const int64_t *slots, const int64_t *cand_of_slot, int32_t max_warps,
+                                 const double *sched, double *cp_len, int32_t *cp_src);
 
 /* Warps (32 candidates each) one CTA of dfsim_critical_path_lanes holds (0: does not fit). */
 int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t, int32_t stages);

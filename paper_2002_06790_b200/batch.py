@@ -252,7 +252,12 @@ class TopologyClass:
                 counts.append(int(min(cap, b - c)))
                 variants.append(int(sorted_var[a]))
         T = lambda x, dt: torch.as_tensor(np.asarray(x), dtype=dt, device=dev)  # noqa: E731
-        self.f_order = T(order, torch.int64)
+        self.f_order = T(order, torch.int64)  # slot k of the tiled schedules holds candidate order[k]
+        # K4 v3 (lane = candidate) reads tiles of 32 candidates, one coalesced run per position;
+        # K4 v2 (a half-warp per candidate, consecutive positions) reads rows
+        self.tiled = self.tables.lane is not None
+        self.slot_of = np.empty(len(order), np.int64)
+        self.slot_of[order] = np.arange(len(order))
         self.f_first, self.f_count, self.f_var = T(firsts, torch.int32), T(counts, torch.int32), T(variants, torch.int32)
         t, s = lp.tensors, lp.t_strat
         rows = self.combo[2] if self.combo is not None else self.base
@@ -261,7 +266,7 @@ class TopologyClass:
             native.ptr(self.f_count), native.ptr(self.f_var), native.ptr(s["gap"]),
             native.ptr(s["ov"]) if self.combo is None and lp.strat_ov.size and lp.strat_ov.max() >= 0 else native.P(0),
             native.ptr(t["ooff"]), native.ptr(t["onode"]), native.ptr(t["oval"]), max(counts, default=0),
-            native.P(0) if os.environ.get("DFSIM_OV_SEARCH_ALL") else native.ptr(t["oany"]))
+            native.P(0) if os.environ.get("DFSIM_OV_SEARCH_ALL") else native.ptr(t["oany"]), int(self.tiled))
         self.fused = True
 
     def resolve(self):
@@ -306,10 +311,25 @@ class TopologyClass:
         bad = torch.empty(len(rows), dtype=torch.int32, device=dev)
         self.ctx.call("dfsim_estimate_batch", N, native.ctypes.byref(self.lp.struct), native.ctypes.byref(strat),
                       native.ptr(dur), native.ptr(src), native.ptr(bad))
-        self.ctx.call("dfsim_simulate_batch_ex", native.ctypes.byref(self.lg.struct), len(rows), native.ptr(dur), N,
-                      native.ptr(o["sched"]), native.P(0), native.ptr(o["makespan"]),
-                      native.ptr(o["busy"]), native.ptr(o["n_placed"]), native.ptr(self.tables.t["pos32"]),
-                      native.ptr(idx), 1)
+        # the exact engine writes the re-run rows' pairs by position into a scratch block, then
+        # they go to the candidates' slots of the tiled schedule (a rare path)
+        R = len(rows)
+        pairs = torch.empty((R, N, 2), dtype=torch.float64, device=dev)
+        D = o["busy"].shape[1]
+        ms, busy, placed = (torch.empty(R, dtype=torch.float64, device=dev),
+                            torch.empty((R, D), dtype=torch.float64, device=dev),
+                            torch.empty(R, dtype=torch.int32, device=dev))
+        self.ctx.call("dfsim_simulate_batch_ex", native.ctypes.byref(self.lg.struct), R, native.ptr(dur), N,
+                      native.ptr(pairs), native.P(0), native.ptr(ms), native.ptr(busy), native.ptr(placed),
+                      native.ptr(self.tables.t["pos32"]), native.P(0), 1)
+        if self.tiled:
+            slots = torch.as_tensor(self.slot_of[np.asarray(rows, np.int64)], dtype=torch.int64, device=dev)
+            o["sched"][slots // 32, :N, slots % 32, :] = pairs
+        else:
+            o["sched"][idx] = pairs
+        o["makespan"][idx] = ms
+        o["busy"][idx] = busy
+        o["n_placed"][idx] = placed
         o.setdefault("fallback_rows", []).extend(int(r) for r in rows)
 
     def run_fused(self, o: dict, ev: dict, paths: bool = False, defer_fallback: bool = False):
@@ -318,9 +338,9 @@ class TopologyClass:
         lg, S, N, D = self.lg, self.lp.n_sims, self.lg.n, self.lg.n_devices
         dev = f"cuda:{self.ctx.device}"
         if "sched" not in o:  # callers may pre-place any output (e.g. flags as a view of a shared buffer)
-            # (start, finish) pairs; two spare pairs past the last row for K4 v3's 32-byte window loads
-            o["sched"] = torch.empty(S * N * 2 + 4, dtype=torch.float64, device=dev)[: S * N * 2].view(S, N, 2)
-            o["start"], o["finish"] = o["sched"][..., 0], o["sched"][..., 1]
+            # (start, finish) pairs by position: 32-candidate tiles (K4 v3) or rows (dfsim_simulate_fused)
+            o["sched"] = (torch.empty(((S + 31) // 32, N, 32, 2), dtype=torch.float64, device=dev) if self.tiled
+                          else torch.empty((S, N, 2), dtype=torch.float64, device=dev))
             o.setdefault("makespan", torch.empty(S, dtype=torch.float64, device=dev))
             o.setdefault("busy", torch.empty((S, max(D, 1)), dtype=torch.float64, device=dev))
             o.setdefault("n_placed", torch.empty(S, dtype=torch.int32, device=dev))
@@ -342,7 +362,7 @@ class TopologyClass:
         if not defer_fallback:
             self.fallback_if_needed(o)
         rec("critical_path", 0)
-        self.tables.critical_path(S, o["sched"], o["cp_len"], o["cp_src"])
+        self.tables.critical_path(S, o["sched"], o["cp_len"], o["cp_src"], self.f_order if self.tiled else None)
         rec("critical_path", 1)
         return o
 
@@ -385,11 +405,18 @@ class TopologyClass:
 
     def rows_by_position(self, o: dict, rows):
         """(start, finish) of candidates ``rows`` as [R, N] device tensors by level position
-        (fused layouts) or by rank (unfused)."""
+        (fused layouts: gathered from the 32-candidate tiles) or by rank (unfused)."""
         import torch
 
         n = self.lg.n
         r = torch.as_tensor(list(rows), dtype=torch.int64, device=o["makespan"].device)
+        if o.get("layout") == "position" and self.tiled:  # the candidates' slots in the engine's tiles
+            k = torch.as_tensor(self.slot_of[np.asarray(list(rows), np.int64)], device=r.device)
+            pairs = o["sched"][k // 32, :, k % 32, :]  # [R, N, 2]
+            return pairs[:, :n, 0], pairs[:, :n, 1]
+        if o.get("layout") == "position":
+            pairs = o["sched"].index_select(0, r)
+            return pairs[:, :n, 0], pairs[:, :n, 1]
         return o["start"].index_select(0, r)[:, :n], o["finish"].index_select(0, r)[:, :n]
 
     def rows_by_rank_batch(self, o: dict, rows):
@@ -424,8 +451,11 @@ class TopologyClass:
         """Re-run K4 on the current schedules (after a deferred fallback): only the re-run
         candidates when K4 v3 can take a candidate list."""
         if self.fused:
+            rows = o.get("fallback_rows")
             self.tables.critical_path(self.lp.n_sims, o["sched"], o["cp_len"], o["cp_src"],
-                                      rows=o.get("fallback_rows"))
+                                      self.f_order if self.tiled else None,
+                                      slots=(self.slot_of if self.tiled else np.arange(self.lp.n_sims))[
+                                          np.asarray(rows, np.int64)] if rows else None)
         elif self.lg.acyclic and self.lg.n:
             critical_path_arrays(self.lg, o["start"], o["finish"], out=o)
 

@@ -89,8 +89,8 @@ struct LaneArgs {
     int32_t *cp_src;
     double *spill;        // [grid * wpb][n_long][32]
     int32_t *task_counter; // groups of 32 candidates handed out dynamically (SMs finish together)
-    const int64_t *order;  // optional: lane i of task t takes candidate order[32 t + i] (register variant)
-    int32_t l2_ahead;      // chunks between the L2 prefetch and the register loads (register variant)
+    const int64_t *slots;  // optional: lane i of task t takes schedule slot slots[32 t + i] (register variant)
+    const int64_t *cand;   // optional: candidate of each schedule slot (outputs go to cp_len[cand[slot]])
     int32_t wpb;
     int32_t table_bytes;  // CTA tables: bounds | spill_off | block_off | spill_list
     int32_t region_bytes; // per warp: rows [slots | spill stages] | pair stages | block stages
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
         const int64_t wbase = static_cast<int64_t>(task) * 32;
         const bool live = wbase + lane < a.S;
         const int n_live = static_cast<int>(a.S - wbase < 32 ? a.S - wbase : 32);
-        const double *rows = a.sched + 2 * wbase * N;
+        const double *rows = a.sched + 2 * wbase * N;  // the warp's tile: pair p * 32 + c (c = candidate)
         asm volatile("mov.b64 %0, %0;" : "+l"(rows));
 
         auto prefetch = [&](int q) {
@@ -150,10 +150,10 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
             const int wlo = hi > K ? hi - K : 0;
             const unsigned st = a_pairs + stg * (32u * kStride);
 #pragma unroll
-            for (int k = lane; k < 32 * K; k += 32) {  // candidate c = k / K, pair i = k % K: coalesced runs
-                const int c = k / K, i = k % K;
+            for (int k = lane; k < 32 * K; k += 32) {  // pair i = k / 32 of candidate c = k % 32: coalesced runs
+                const int c = k % 32, i = k / 32;
                 if (c < n_live && wlo + i < N)
-                    cpa16(st + static_cast<unsigned>(c * kStride + i * 16), rows + 2 * (static_cast<int64_t>(c) * N + wlo + i));
+                    cpa16(st + static_cast<unsigned>(c * kStride + i * 16), rows + 2 * (static_cast<int64_t>(wlo + i) * 32 + c));
             }
             const int b0 = lds_i(a_boff + 4u * q), b1 = lds_i(a_boff + 4u * (q + 1));
             const unsigned bs = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
@@ -213,33 +213,31 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
         }
         asm volatile("cp.async.wait_group 0;\n" ::);
         if (live) {
-            a.cp_len[wbase + lane] = src == 0x7fffffff ? 0.0 : len;
-            if (a.cp_src) a.cp_src[wbase + lane] = src == 0x7fffffff ? -1 : src;
+            const int64_t cand = a.cand ? __ldg(a.cand + wbase + lane) : wbase + lane;
+            a.cp_len[cand] = src == 0x7fffffff ? 0.0 : len;
+            if (a.cp_src) a.cp_src[cand] = src == 0x7fffffff ? -1 : src;
         }
         __syncwarp();
     }
 }
 
-// Register-staged variant (K = 8): each lane loads its own candidate's schedule window with
-// 32-byte loads (LDG.256, one full sector per lane, 5 per chunk) straight into registers one
-// chunk ahead, so the pair stages need no shared memory and twice as many warps fit an SM.
-// The window of chunk q is the 32-byte aligned run [a, a + K + 2) with a = hi - K - off,
-// off = parity of the pair index (s N + hi - K): position p sits at register index
-// p - a = (p - hi + K) + off, i.e. one of two static indices selected by off.  Node records
-// and spill values use two shared-memory stages as above.
-__device__ __forceinline__ void ldg_v4(double (&d)[4], const double *p) {
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
-                 : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]) : "l"(p));
+// Register-staged variant (K = 8): each lane loads its own candidate's 8 (start, finish)
+// pairs of the next chunk straight into registers, one chunk ahead, so the pair stages need no
+// shared memory and twice as many warps fit an SM.  Schedules are tiled by 32 candidates
+// (position-major inside a tile, see dfsim_b200.h): position p of a warp's 32 candidates is one
+// contiguous 512-byte run, so each of the 8 loads per chunk is a fully coalesced LDG.128.  Node
+// records and spill values use two shared-memory stages as above.
+__device__ __forceinline__ void ldg_pair(double (&d)[2], const double *p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(d[0]), "=d"(d[1]) : "l"(p));
 }
 
-// 14 warps per CTA (one CTA per SM): what shared memory holds for C2 anyway (C2: 1.84 -> 1.79 ms
-// together with the window loads issued before the chunk's cp.async bookkeeping)
+// 14 warps per CTA (one CTA per SM): what shared memory holds for C2 anyway
 constexpr int kRegWarps = 14;
 
-template <int K, bool kPingPong>
+template <int K>
 __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(LaneArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int NST = 2, NU = K / 2 + 1;  // 32-byte units per window
+    constexpr int NST = 2;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int N = a.t.n_nodes, NQ = a.t.n_chunks, NS = a.t.n_slots, RM = a.t.rmax, BM = a.t.block_max;
     const int NL = a.t.n_spill_list;
@@ -276,9 +274,11 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
         const int64_t k = static_cast<int64_t>(task) * 32 + lane;
         const bool live = k < a.S;
         const int64_t kk = live ? k : a.S - 1;  // idle lanes shadow the last candidate's row
-        const int64_t s = a.order ? __ldg(a.order + kk) : kk;
-        const double *row = a.sched + 2 * s * N;
-        const int rowpar = static_cast<int>((s * N) & 1);
+        const int64_t slot = a.slots ? __ldg(a.slots + kk) : kk;
+        const int64_t s = a.cand ? __ldg(a.cand + slot) : slot;  // the candidate (outputs)
+        // slot k, position p: pair ((k / 32) N + p) 32 + k % 32
+        const double *col = a.sched + 2 * ((slot >> 5) * static_cast<int64_t>(N) * 32 + (slot & 31));
+        asm volatile("mov.b64 %0, %0;" : "+l"(col));
 
         auto prefetch_smem = [&](int q) {  // node records + spill values of chunk q
             const unsigned stg = static_cast<unsigned>(q & 1);
@@ -299,50 +299,23 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
             }
             asm volatile("cp.async.commit_group;\n" ::);
         };
-        // L2 prefetch PF chunks ahead: the schedule window (three probes cover its 160 bytes)
-        // and the chunk's spill rows, so the register / cp.async loads one chunk ahead hit L2
-        auto prefetch_l2 = [&](int q) {
+        // window of chunk q: positions hi - K .. hi - 1 at register index p - (hi - K); positions
+        // below 0 (the first chunk) are never read and load position 0 instead
+        auto load_window = [&](int q, double (&w)[K][2]) {
             const int hi = lds_i(a_bounds + 4u * q);
-            const int off = (rowpar + hi - K) & 1;
-            const int a0 = hi - K - off;
-            if (N >= 2 * K) {  // the probes stay inside this row (plus the padding past the last)
-                const double *w0 = row + 2 * (a0 > 0 ? a0 : 0);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(w0));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(w0 + 10));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(w0 + 19));
-            }
-            const int r0 = lds_i(a_soff + 4u * q), r1 = lds_i(a_soff + 4u * (q + 1));
-            if (r0 + (lane >> 1) < r1) {  // two lanes per 256-byte spill row
-                const int id = static_cast<int>(lds_h(a_slist + 2u * (r0 + (lane >> 1))));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(spill_warp - lane + 32 * static_cast<int64_t>(id) + 16 * (lane & 1)));
-            }
-        };
-        auto load_window = [&](int q, double (&w)[NU][4]) {
-            const int hi = lds_i(a_bounds + 4u * q);
-            const int off = (rowpar + hi - K) & 1;
-            const int a0 = hi - K - off;
 #pragma unroll
-            for (int u = 0; u < NU; u++) {
-                const int p0 = a0 + 2 * u;
-                // units wholly before the row are never read (positions >= 0): they load an
-                // aligned unit at the row start instead (same parity), so that every load is
-                // unconditional -- a predicated load made the compiler stage it through a temporary
-                // and a predicated move that waited for the data on the spot.  The row pointer is
-                // backed by padding past the last row, see dfsim_critical_path_lanes
-                ldg_v4(w[u], row + 2 * (p0 + 1 >= 0 ? p0 : rowpar));
+            for (int i = 0; i < K; i++) {
+                const int p = hi - K + i;
+                ldg_pair(w[i], col + 64 * static_cast<int64_t>(p >= 0 ? p : 0));
             }
         };
 
-        double wa[NU][4], wb[NU][4];
+        double wa[K][2], wb[K][2];
         double len = 0.0;
         int src = 0x7fffffff;
         prefetch_smem(0);
         load_window(0, wa);
-
-        const int PF = a.l2_ahead;  // 0: no L2 prefetch
-        for (int q = 1; q < PF && q < NQ; q++) prefetch_l2(q);
-        auto process = [&](int q, double (&w)[NU][4], double (&wn)[NU][4]) {
-            if (PF > 0 && q + PF < NQ) prefetch_l2(q + PF);
+        auto process = [&](int q, double (&w)[K][2], double (&wn)[K][2]) {
             if (q + 1 < NQ) {
                 load_window(q + 1, wn);  // first: the window registers are claimed before any temporaries
                 prefetch_smem(q + 1);
@@ -353,7 +326,6 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
             __syncwarp();
             const unsigned stg = static_cast<unsigned>(q & 1);
             const int hi = lds_i(a_bounds + 4u * q), lo = lds_i(a_bounds + 4u * (q + 1));
-            const int off = (rowpar + hi - K) & 1;
             const unsigned blk = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
 #pragma unroll
             for (int t = 0; t < K; t++) {
@@ -371,11 +343,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
                     DFSIM_CHECK(!(r.x & kHasSpill) || (r.x >> 15) < static_cast<unsigned>(a.t.n_long), 7);
                     const double x0 = lds_d(row_lo(a_lane, r.z)), x1 = lds_d(row_hi(a_lane, r.z));
                     const double x2 = lds_d(row_lo(a_lane, r.w)), x3 = lds_d(row_hi(a_lane, r.w));
-                    // position p at register index K - 1 - t + off (pair = two doubles)
-                    const int i0 = K - 1 - t, i1 = K - t;  // static after unrolling
-                    const double s0 = w[i0 >> 1][(i0 & 1) * 2], f0 = w[i0 >> 1][(i0 & 1) * 2 + 1];
-                    const double s1 = w[i1 >> 1][(i1 & 1) * 2], f1 = w[i1 >> 1][(i1 & 1) * 2 + 1];
-                    const double st = off ? s1 : s0, fi = off ? f1 : f0;
+                    const double st = w[K - 1 - t][0], fi = w[K - 1 - t][1];  // position hi - 1 - t
                     const double m01 = x1 > x0 ? x1 : x0, m23 = x3 > x2 ? x3 : x2;
                     double best = m23 > m01 ? m23 : m01;
                     if (deg > 4) {
@@ -402,19 +370,9 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) k_critical_path_lanes_reg(L
             }
             __syncwarp();
         };
-        if constexpr (kPingPong) {
-            for (int q = 0; q < NQ; q += 2) {  // two chunks per iteration: the window registers swap roles
-                process(q, wa, wb);
-                if (q + 1 < NQ) process(q + 1, wb, wa);
-            }
-        } else {
-            for (int q = 0; q < NQ; q++) {  // one copy of the chunk body (half the code)
-                process(q, wa, wb);
-#pragma unroll
-                for (int u = 0; u < NU; u++)
-#pragma unroll
-                    for (int e = 0; e < 4; e++) wa[u][e] = wb[u][e];
-            }
+        for (int q = 0; q < NQ; q += 2) {  // two chunks per iteration: the window registers swap roles
+            process(q, wa, wb);
+            if (q + 1 < NQ) process(q + 1, wb, wa);
         }
         if (live) {
             a.cp_len[s] = src == 0x7fffffff ? 0.0 : len;
@@ -594,15 +552,16 @@ extern "C" int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables
 }
 
 extern "C" int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
-                                         const double *sched, double *cp_len, int32_t *cp_src) {
-    return dfsim_critical_path_lanes_ex(ctx, t, stages, n_sims, nullptr, 0, sched, cp_len, cp_src);
+                                         const int64_t *cand_of_slot, const double *sched, double *cp_len,
+                                         int32_t *cp_src) {
+    return dfsim_critical_path_lanes_ex(ctx, t, stages, n_sims, nullptr, cand_of_slot, 0, sched, cp_len, cp_src);
 }
 
 extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages,
-                                            int64_t n_sims, const int64_t *order, int32_t max_warps,
-                                            const double *sched, double *cp_len, int32_t *cp_src) {
+                                            int64_t n_sims, const int64_t *slots, const int64_t *cand_of_slot,
+                                            int32_t max_warps, const double *sched, double *cp_len, int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
-    DFSIM_ARG_CHECK(ctx, !order || stages == 0, "a candidate order needs the register variant (stages 0)");
+    DFSIM_ARG_CHECK(ctx, !slots || stages == 0, "a slot list needs the register variant (stages 0)");
     DFSIM_ARG_CHECK(ctx, sched && cp_len, "sched and cp_len are required");
     DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
     DFSIM_ARG_CHECK(ctx, t->chunk_positions == 8 || t->chunk_positions == 16, "chunk_positions must be 8 or 16");
@@ -632,12 +591,8 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(counter, 0, sizeof(int32_t), ctx->stream));
     LaneArgs a;
     a.task_counter = counter;
-    a.order = order;
-    static const int kL2Ahead = [] {  // DFSIM_CP_L2AHEAD: measurement knob
-        const char *e = std::getenv("DFSIM_CP_L2AHEAD");
-        return e ? std::atoi(e) : 0;  // measured: prefetching 3-12 chunks ahead was slower
-    }();
-    a.l2_ahead = kL2Ahead;
+    a.slots = slots;
+    a.cand = cand_of_slot;
     a.t = *t;
     a.S = n_sims;
     a.sched = sched;
@@ -660,11 +615,7 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
         }
         return rc;
     };
-    static const bool kPP = [] {  // DFSIM_CP_PINGPONG=0: single chunk body (measurement knob)
-        const char *e = std::getenv("DFSIM_CP_PINGPONG");
-        return !e || std::atoi(e) != 0;
-    }();
-    if (stages == 0) return kPP ? launch(k_critical_path_lanes_reg<8, true>) : launch(k_critical_path_lanes_reg<8, false>);
+    if (stages == 0) return launch(k_critical_path_lanes_reg<8>);
     if (t->chunk_positions == 16) return stages == 2 ? launch(k_critical_path_lanes<16, 2>) : launch(k_critical_path_lanes<16, 3>);
     return stages == 2 ? launch(k_critical_path_lanes<8, 2>) : launch(k_critical_path_lanes<8, 3>);
 }

@@ -139,7 +139,13 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             const int64_t s = active ? __ldg(a.st.order + __ldg(a.st.chunk_first + c) + gid) : 0;
             const double gap = active ? __ldg(a.st.op_gap + s) : 0.0;
             const int ovs = (active && a.st.override_set) ? __ldg(a.st.override_set + s) : -1;
-            double2 *out = reinterpret_cast<double2 *>(a.sched) + s * N;
+            // tiled schedule (dfsim_b200.h): slot k = the candidate's position in the engine's
+            // order (candidates of one chunk are neighbours), pair ((k / 32) N + v) 32 + k % 32;
+            // row layout: pair s N + v
+            const int64_t k_slot = active ? static_cast<int64_t>(__ldg(a.st.chunk_first + c)) + gid : 0;
+            double2 *out = reinterpret_cast<double2 *>(a.sched) +
+                           (a.st.sched_tiled ? (k_slot >> 5) * N * 32 + (k_slot & 31) : s * N);
+            const int ostride = a.st.sched_tiled ? 32 : 1;
             asm volatile("mov.b64 %0, %0;" : "+l"(out));  // keep the row base in a register (no per-pop s * N)
             if (active) {
                 for (int w = ll; w < a.g.n_counter_words; w += kGS) cnt[w] = __ldg(a.g.cnt_init + w);
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
                         if (lo < end && __ldg(a.st.ov_node + lo) == vr) dur = __ldg(a.st.ov_val + lo);
                     }
                     const double f = __dadd_rn(now, dur);
-                    out[v] = make_double2(now, f);
+                    out[ostride * v] = make_double2(now, f);
                     running = true;
                     run_v = v;
                     run_f = f;
@@ -310,6 +316,7 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
 struct CpLevelArgs {
     dfsim_cp_tables t;
     int64_t S;
+    const int64_t *cand;  // optional: candidate of each schedule slot (outputs go to cp_len[cand[slot]])
     const double *sched;  // [S][N] (start, finish) pairs by level position
     double *cp_len;
     int32_t *cp_src;
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
         const int64_t s = base + half;
         const bool live = s < a.S;
         const int64_t sr = live ? s : base;  // the idle half shadows its partner's reads
-        const double *row = a.sched + 2 * sr * N;
+        const double *row = a.sched + 2 * sr * N;  // row layout (classes on K4 v2)
         asm volatile("mov.b64 %0, %0;" : "+l"(row));  // keep row bases in registers (no 64-bit re-derivation)
         auto prefetch = [&](int c) {
             const int p0 = s_goff[s_coff[c]], p1 = s_goff[s_coff[c + 1]];
@@ -438,8 +445,9 @@ __global__ void __launch_bounds__(1024, 1) k_critical_path_levels(CpLevelArgs a)
             }
         }
         if (live && ll == 0) {
-            a.cp_len[s] = src == 0x7fffffff ? 0.0 : len;
-            if (a.cp_src) a.cp_src[s] = src == 0x7fffffff ? -1 : src;
+            const int64_t cand = a.cand ? __ldg(a.cand + s) : s;  // s is the schedule slot
+            a.cp_len[cand] = src == 0x7fffffff ? 0.0 : len;
+            if (a.cp_src) a.cp_src[cand] = src == 0x7fffffff ? -1 : src;
         }
         __syncwarp();
     }
@@ -593,8 +601,9 @@ extern "C" int32_t dfsim_critical_path_levels_capacity(const dfsim_cp_tables *t)
     return t ? 2 * cp_shape(t).wpb : 0;
 }
 
-extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims, const double *sched,
-                                          double *cp_len, int32_t *cp_src) {
+extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables *t, int64_t n_sims,
+                                          const int64_t *cand_of_slot, const double *sched, double *cp_len,
+                                          int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
     DFSIM_ARG_CHECK(ctx, sched && cp_len, "sched and cp_len are required");
     DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
@@ -630,6 +639,7 @@ extern "C" int dfsim_critical_path_levels(dfsim_ctx *ctx, const dfsim_cp_tables 
     CpLevelArgs a;
     a.t = *t;
     a.S = n_sims;
+    a.cand = cand_of_slot;
     a.sched = sched; a.cp_len = cp_len; a.cp_src = cp_src;
     a.spill = static_cast<double *>(p);
     a.wpb = wpb;

@@ -114,9 +114,12 @@ __global__ void __launch_bounds__(256) k_simulate(SimArgs a) {
         if (a.redo && !a.redo[s]) continue;
         const double *dur = a.dur + s * a.dur_stride;
         const int64_t row = a.out_rows ? a.out_rows[s] : s;
-        double *out_start = a.start ? a.start + row * N * (a.interleaved ? 2 : 1) : nullptr;
+        // interleaved 1: (start, finish) pairs by row; 2: pairs in 32-candidate tiles (fused layout)
+        double *out_start = !a.start ? nullptr
+                            : a.interleaved == 2 ? a.start + 2 * ((row >> 5) * N * 32 + (row & 31))
+                                                 : a.start + row * N * (a.interleaved ? 2 : 1);
         double *out_finish = a.interleaved ? (out_start ? out_start + 1 : nullptr) : (a.finish ? a.finish + row * N : nullptr);
-        const int ostride = a.interleaved ? 2 : 1;
+        const int ostride = a.interleaved == 2 ? 64 : a.interleaved ? 2 : 1;
 
         Counter<kBits>::init(cnt, a.cnt_words, a.indeg, N, lane);
         int head[kV];

@@ -73,7 +73,8 @@ class SimTables(ctypes.Structure):
 class FusedStrategies(ctypes.Structure):
     _fields_ = [("n_sims", I64), ("n_variants", I32), ("base", P), ("n_chunks", I32), ("order", P),
                 ("chunk_first", P), ("chunk_count", P), ("chunk_variant", P), ("op_gap", P), ("override_set", P),
-                ("ov_off", P), ("ov_node", P), ("ov_val", P), ("max_chunk", I32), ("ov_any", P)]
+                ("ov_off", P), ("ov_node", P), ("ov_val", P), ("max_chunk", I32), ("ov_any", P),
+                ("sched_tiled", I32)]
 
 
 class CpTables(ctypes.Structure):
@@ -128,10 +129,10 @@ _SIGNATURES = {
     "dfsim_override_rows": (ctypes.c_int, [P, I32, I32, P, P, P, P, P, P, P]),
     "dfsim_simulate_fused": (ctypes.c_int, [P, ctypes.POINTER(SimTables), ctypes.POINTER(FusedStrategies), P, P, P,
                                             P, P]),
-    "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P]),
+    "dfsim_critical_path_levels": (ctypes.c_int, [P, ctypes.POINTER(CpTables), I64, P, P, P, P]),
     "dfsim_critical_path_levels_capacity": (I32, [ctypes.POINTER(CpTables)]),
-    "dfsim_critical_path_lanes": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I32, I64, P, P, P]),
-    "dfsim_critical_path_lanes_ex": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I32, I64, P, I32, P, P, P]),
+    "dfsim_critical_path_lanes": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I32, I64, P, P, P, P]),
+    "dfsim_critical_path_lanes_ex": (ctypes.c_int, [P, ctypes.POINTER(CpLaneTables), I32, I64, P, P, I32, P, P, P]),
     "dfsim_critical_path_lanes_capacity": (I32, [ctypes.POINTER(CpLaneTables), I32]),
     "dfsim_cp_lanes_plan": (ctypes.c_int, [I32, P, P, P, I32, I32, I32, I32, P, P, P, P, P, P]),
     "dfsim_predict_batch": (ctypes.c_int, [P, I32, P, ctypes.c_double, I64, P, P]),

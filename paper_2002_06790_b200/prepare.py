@@ -281,21 +281,24 @@ class ClassTables(Tables):
                                              self.max_spill_reads, p(t["pinfo"]), self.slot_region,
                                              self.stage_doubles)
 
-    def critical_path(self, n_sims: int, sched, cp_len, cp_src, rows=None):
-        """K4 over the fused engine's schedules: v3 (lane per candidate) when planned, else v2.
-        ``rows``: only these candidates (K4 v3's register variant takes a candidate list)."""
-        if self.lane is not None and rows and self.lane["stages"] == 0:
+    def critical_path(self, n_sims: int, sched, cp_len, cp_src, cand_of_slot, slots=None):
+        """K4 over the fused engine's tiled schedules: v3 (lane per candidate) when planned, else
+        v2; slot k holds candidate ``cand_of_slot[k]`` (device int64: the engine's order).
+        ``slots``: only these schedule slots (K4 v3's register variant takes a slot list)."""
+        c = native.ptr(cand_of_slot) if cand_of_slot is not None else native.P(0)
+        if self.lane is not None and slots is not None and len(slots) and self.lane["stages"] == 0:
             import torch
 
-            order = torch.as_tensor(sorted(set(rows)), dtype=torch.int64, device=f"cuda:{self.ctx.device}")
-            self.ctx.call("dfsim_critical_path_lanes_ex", native.ctypes.byref(self.lane_struct), 0, order.numel(),
-                          native.ptr(order), 0, native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
+            sl = torch.as_tensor(sorted(set(int(x) for x in slots)), dtype=torch.int64,
+                                 device=f"cuda:{self.ctx.device}")
+            self.ctx.call("dfsim_critical_path_lanes_ex", native.ctypes.byref(self.lane_struct), 0, sl.numel(),
+                          native.ptr(sl), c, 0, native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
             return
         if self.lane is not None:
             self.ctx.call("dfsim_critical_path_lanes", native.ctypes.byref(self.lane_struct), self.lane["stages"],
-                          n_sims, native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
+                          n_sims, c, native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
         else:
-            self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.cp_struct), n_sims,
+            self.ctx.call("dfsim_critical_path_levels", native.ctypes.byref(self.cp_struct), n_sims, c,
                           native.ptr(sched), native.ptr(cp_len), native.ptr(cp_src))
 
     def output_to_rank(self, arr_by_pos: np.ndarray) -> np.ndarray:
