@@ -76,7 +76,7 @@ constexpr int kWide = 4;  // out-degree above which a finished node's successors
 // kBaseG: the variant's duration row is read from global memory (L1/L2: all candidates of a
 // chunk share it) instead of being staged in smem -- for classes whose smem tables would
 // otherwise leave room for only a few candidates per CTA.
-template <int kGS, bool kPacked, bool kBaseG>
+template <int kGS, bool kPacked, bool kBaseG, bool kTiled>
 __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kPerWarp = 32 / kGS;
@@ -143,9 +143,8 @@ __global__ void __launch_bounds__(1024, 1) k_simulate_fused(FusedArgs a) {
             // order (candidates of one chunk are neighbours), pair ((k / 32) N + v) 32 + k % 32;
             // row layout: pair s N + v
             const int64_t k_slot = active ? static_cast<int64_t>(__ldg(a.st.chunk_first + c)) + gid : 0;
-            double2 *out = reinterpret_cast<double2 *>(a.sched) +
-                           (a.st.sched_tiled ? (k_slot >> 5) * N * 32 + (k_slot & 31) : s * N);
-            const int ostride = a.st.sched_tiled ? 32 : 1;
+            double2 *out = reinterpret_cast<double2 *>(a.sched) + (kTiled ? (k_slot >> 5) * N * 32 + (k_slot & 31) : s * N);
+            constexpr int ostride = kTiled ? 32 : 1;
             asm volatile("mov.b64 %0, %0;" : "+l"(out));  // keep the row base in a register (no per-pop s * N)
             if (active) {
                 for (int w = ll; w < a.g.n_counter_words; w += kGS) cnt[w] = __ldg(a.g.cnt_init + w);
@@ -550,16 +549,20 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
     DFSIM_CUDA_TRY(ctx, cudaMemsetAsync(a.chunk_counter, 0, sizeof(int32_t), ctx->stream));
     const size_t smem = graph_bytes + (size_t)wpb * f.per_warp * warp_bytes;
     const int threads = wpb * 32;
-#define DFSIM_LAUNCH_FUSED_B(GS, PK, BG)                                                                       \
+#define DFSIM_LAUNCH_FUSED_T(GS, PK, BG, TL)                                                                   \
     do {                                                                                                       \
-        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<GS, PK, BG>,                                 \
+        DFSIM_CUDA_TRY(ctx, cudaFuncSetAttribute(k_simulate_fused<GS, PK, BG, TL>,                             \
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
         int occ = 1;                                                                                           \
-        DFSIM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_fused<GS, PK, BG>,  \
+        DFSIM_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_simulate_fused<GS, PK, BG, TL>, \
                                                                           threads, smem));                    \
         const int64_t slots = (int64_t)ctx->num_sms * (occ > 0 ? occ : 1);                                    \
         const int grid = (int)(slots < st->n_chunks ? slots : st->n_chunks);                                   \
-        k_simulate_fused<GS, PK, BG><<<grid, threads, smem, ctx->stream>>>(a);                                \
+        k_simulate_fused<GS, PK, BG, TL><<<grid, threads, smem, ctx->stream>>>(a);                            \
+    } while (0)
+#define DFSIM_LAUNCH_FUSED_B(GS, PK, BG)                                                                       \
+    do {                                                                                                       \
+        if (st->sched_tiled) DFSIM_LAUNCH_FUSED_T(GS, PK, BG, true); else DFSIM_LAUNCH_FUSED_T(GS, PK, BG, false); \
     } while (0)
 #define DFSIM_LAUNCH_FUSED_P(GS, PK)                                                                           \
     do {                                                                                                       \
@@ -573,6 +576,7 @@ extern "C" int dfsim_simulate_fused(dfsim_ctx *ctx, const dfsim_sim_tables *g, c
 #undef DFSIM_LAUNCH_FUSED
 #undef DFSIM_LAUNCH_FUSED_P
 #undef DFSIM_LAUNCH_FUSED_B
+#undef DFSIM_LAUNCH_FUSED_T
     return dfsim_after_launch(ctx, "k_simulate_fused");
 }
 
