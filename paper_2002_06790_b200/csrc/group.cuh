@@ -57,8 +57,11 @@ static __device__ __forceinline__ unsigned group_add_u32(unsigned x, int grp) {
 
 template <int kGS>
 static __device__ __forceinline__ unsigned group_bits(unsigned b, int grp) {
-    if constexpr (kGS == 32) return b;
-    return (b >> (grp * kGS)) & ((1u << kGS) - 1u);
+    if constexpr (kGS == 32) {
+        return b;
+    } else {
+        return (b >> (grp * kGS)) & ((1u << kGS) - 1u);
+    }
 }
 
 template <int kGS>
