@@ -45,7 +45,7 @@ def class_key(cfg) -> tuple:
 
 
 _R, _DMAP = operator.attrgetter("replicas"), operator.attrgetter("device_map")
-_MARKERS, _COLL = operator.attrgetter("gradient_markers"), operator.attrgetter("collective")
+_MARKERS, _PATH = operator.attrgetter("gradient_markers"), operator.attrgetter("collective.path")
 
 
 def group_classes(graphs, configs, graph_of, db=None) -> list:
@@ -60,16 +60,16 @@ def group_classes(graphs, configs, graph_of, db=None) -> list:
     # every class-key lookup below
     canon: dict = {}
     skeys = {gi: canon.setdefault(structure_key(graphs[gi]), len(canon)) for gi in dict.fromkeys(graph_of)}
-    # identity of the field objects (configs of a sweep share them), built with C-level maps;
-    # equal-valued but distinct objects only cost one extra class_key call each
     try:
         sync = list(map(operator.attrgetter("sync"), configs))
         psd = list(map(operator.attrgetter("ps_device"), configs))
     except AttributeError:  # e.g. the reference's own StrategyConfig (no PS extension fields)
         sync = [getattr(c, "sync", "allreduce") for c in configs]
         psd = [getattr(c, "ps_device", None) for c in configs]
-    cols = [list(map(_R, configs)), list(map(id, map(_DMAP, configs))), list(map(id, map(_MARKERS, configs))),
-            list(map(id, map(_COLL, configs))), sync, psd, list(graph_of)]
+    # field values (tuples of strings hash cheaply; sweeps often build per-candidate objects,
+    # so object identities would make every config its own combination)
+    cols = [list(map(_R, configs)), list(map(tuple, map(_DMAP, configs))), list(map(tuple, map(_MARKERS, configs))),
+            list(map(_PATH, configs)), sync, psd, list(graph_of)]
     cols = [c for c in cols if len(dict.fromkeys(c)) > 1]  # fields shared by every config drop out
     if not cols:
         return [list(range(len(configs)))] if configs else []

@@ -492,6 +492,7 @@ def base_arrays(g):
 
 _HARDWARE, _GAP = operator.attrgetter("hardware"), operator.attrgetter("op_gap_us")
 _COLLECTIVE, _OVERRIDES = operator.attrgetter("collective"), operator.attrgetter("overrides")
+_ALGO, _PATH = operator.attrgetter("collective.algo"), operator.attrgetter("collective.path")
 
 
 class LoweredProfiles:
@@ -518,17 +519,18 @@ class LoweredProfiles:
             self.hw_ids[h] = len(self.hw_ids)
         self.strat_hw = np.fromiter(map(self.hw_ids.__getitem__, hws), np.int32, n)
         self.strat_gap = np.fromiter(map(float, map(_GAP, configs)), np.float64, n)
-        colls = list(map(_COLLECTIVE, configs))
-        code_of, algo_tab, path_tab = {}, [], []
-        for c in {id(c): c for c in colls}.values():
-            if c.algo not in (ALGO_MEASURED, ALGO_RING):
-                raise ValueError(f"unknown collective algorithm {c.algo!r}")
-            code_of[id(c)] = len(algo_tab)
-            algo_tab.append(0 if c.algo == ALGO_MEASURED else 1)
-            path_tab.append(self.path_ids.setdefault(c.path, len(self.path_ids)))
-        code = np.fromiter(map(code_of.__getitem__, map(id, colls)), np.int64, n)
-        self.strat_algo = np.asarray(algo_tab, np.uint8)[code] if n else np.zeros(0, np.uint8)
-        self.strat_path = np.asarray(path_tab, np.int32)[code] if n else np.zeros(0, np.int32)
+        # collective algorithm and path by value (sweeps often build a config object per candidate)
+        algos = list(map(_ALGO, configs))
+        paths = list(map(_PATH, configs))
+        algo_code = {}
+        for al in dict.fromkeys(algos):
+            if al not in (ALGO_MEASURED, ALGO_RING):
+                raise ValueError(f"unknown collective algorithm {al!r}")
+            algo_code[al] = 0 if al == ALGO_MEASURED else 1
+        for pth in dict.fromkeys(paths):
+            self.path_ids[pth] = len(self.path_ids)
+        self.strat_algo = np.fromiter(map(algo_code.__getitem__, algos), np.uint8, n)
+        self.strat_path = np.fromiter(map(self.path_ids.__getitem__, paths), np.int32, n)
         self.strat_ov = np.full(n, -1, np.int32)
         ovs = list(map(_OVERRIDES, configs))
         for i in np.flatnonzero(np.fromiter(map(bool, ovs), bool, n)).tolist():

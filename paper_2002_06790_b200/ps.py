@@ -87,21 +87,33 @@ def expand_parameter_server(g, cfg, db, ps_device: str = "ps0") -> ExpandedGraph
     return ex
 
 
-def ps_nodes(gid, grad, cfg, ps_device: str) -> list:
-    """push_<g>@r<k>, aggregate_<g>, pull_<g>@r<k> for one marked gradient (module docstring)."""
-    R, path = cfg.replicas, cfg.collective.path
+def ps_link_ids(cfg, ps_device: str) -> tuple[list, list]:
+    """(uplink ids, downlink ids) of the PS links, one per worker in device_map order."""
+    path = cfg.collective.path
+    return ([f"link:{path}:{w}->{ps_device}" for w in cfg.device_map],
+            [f"link:{path}:{ps_device}->{w}" for w in cfg.device_map])
+
+
+def ps_nodes(gid, grad, cfg, ps_device: str, replicas=None) -> list:
+    """push_<g>@r<k>, aggregate_<g>, pull_<g>@r<k> for one marked gradient (module docstring);
+    ``replicas``: only these workers' push / pull nodes (the aggregate always)."""
+    R = cfg.replicas
+    ks = range(R) if replicas is None else replicas
+    up, down = ps_link_ids(cfg, ps_device)
     nbytes = grad.output_shapes[0].byte_size()
     out = []
-    for k, w in enumerate(cfg.device_map):
-        out.append(OpNode(f"push_{gid}@r{k}", PUSH_OP, f"link:{path}:{w}->{ps_device}", TRANSFER,
+    for k in ks:
+        w = cfg.device_map[k]
+        out.append(OpNode(f"push_{gid}@r{k}", PUSH_OP, up[k], TRANSFER,
                           {"src_device": w, "dst_device": ps_device, "bytes": nbytes},
                           ((f"{gid}@r{k}", 0),), grad.output_shapes))
     aid = f"aggregate_{gid}"
     out.append(OpNode(aid, AGGREGATE_OP, ps_device, COMPUTE,
                       {"replicas": R, "bytes": nbytes, "mflops": round(R * nbytes / 4 / 1e6, 6)},
                       tuple((f"push_{gid}@r{k}", 0) for k in range(R)), grad.output_shapes))
-    for k, w in enumerate(cfg.device_map):
-        out.append(OpNode(f"pull_{gid}@r{k}", PULL_OP, f"link:{path}:{ps_device}->{w}", TRANSFER,
+    for k in ks:
+        w = cfg.device_map[k]
+        out.append(OpNode(f"pull_{gid}@r{k}", PULL_OP, down[k], TRANSFER,
                           {"src_device": ps_device, "dst_device": w, "bytes": nbytes},
                           ((aid, 0),), grad.output_shapes))
     return out

@@ -74,32 +74,41 @@ def _special_rows(kind, ids, pos, g_b, structure, cfg, db=None) -> dict:
         from .expansion import ps_link_specs
         from .ps import ps_nodes
 
+        from .ps import ps_link_ids
+
         # the PS links (throughput, latency) of this config's collective path
         specs = ps_link_specs(cfg, db, cfg.ps_device) if db is not None else structure.device_specs
-        built, first = {}, {}
+        up, down = ps_link_ids(cfg, cfg.ps_device)
+        R = cfg.replicas
+        rows0 = {}
         for p in pos:
             cid = ids[p]
             gid = structure.origin[cid][1]
-            if gid not in built:
+            if gid not in rows0:
+                # push_<g>@r<k> / pull_<g>@r<k> differ across k only in their link device (the
+                # features -- bytes, the gradient's shapes -- are k-independent): worker 0's nodes
+                # and the aggregate are built as the expansion builds them, the other workers' rows
+                # are worker 0's with their own link's throughput / latency
                 grad = g_b.nodes[gid]
-                nodes = {f"{gid}@r{k}": grad for k in range(cfg.replicas)}
-                for n in ps_nodes(gid, grad, cfg, cfg.ps_device):
-                    nodes[n.id] = n
-                built[gid] = _Stand(nodes, specs)
-            stand = built[gid]
-            node = stand.nodes[cid]
-            # push_<g>@r<k> / pull_<g>@r<k> differ across k only in their link device (the
-            # features -- bytes, the gradient's shapes -- are k-independent), so the row of k > 0
-            # is k = 0's with the link's throughput / latency
-            role = (gid, node.op_type)
-            row0 = first.get(role)
-            dev = specs.get(node.device)
-            if row0 is not None and row0[1] and node.kind == TRANSFER and dev is not None and dev.kind == DEVICE_LINK:
-                out.append(row0[:4] + (dev.throughput_mbps, dev.latency_us))
+                push0, agg, pull0 = ps_nodes(gid, grad, cfg, cfg.ps_device, replicas=(0,))
+                nodes = {f"{gid}@r{k}": grad for k in range(R)}
+                nodes.update({f"push_{gid}@r{k}": grad for k in range(R)})  # the aggregate's inputs: shapes only
+                nodes.update({push0.id: push0, agg.id: agg, pull0.id: pull0})
+                stand = _Stand(nodes, specs)
+                rows0[gid] = ({n.id: node_rows(stand, [n.id])[0] for n in (push0, agg, pull0)}, stand)
+            r0, stand = rows0[gid]
+            if cid.startswith("aggregate_"):
+                out.append(r0[cid])
                 continue
-            row = node_rows(stand, [cid])[0]
-            if node.kind == TRANSFER:
-                first.setdefault(role, row)
+            push = cid.startswith("push_")
+            k = int(cid.rsplit("@r", 1)[1])
+            row = r0[f"push_{gid}@r0" if push else f"pull_{gid}@r0"]
+            dev = specs.get((up if push else down)[k])
+            if row[1] and dev is not None and dev.kind == DEVICE_LINK:
+                row = row[:4] + (dev.throughput_mbps, dev.latency_us)
+            elif k:  # a link without a Link spec: the row as node_rows gives it for this node
+                node = ps_nodes(gid, g_b.nodes[gid], cfg, cfg.ps_device, replicas=(k,))[0 if push else 2]
+                row = node_rows(_Stand({**stand.nodes, node.id: node}, specs), [cid])[0]
             out.append(row)
     return row_arrays(out)
 
