@@ -48,6 +48,16 @@ _R, _DMAP = operator.attrgetter("replicas"), operator.attrgetter("device_map")
 _MARKERS, _PATH = operator.attrgetter("gradient_markers"), operator.attrgetter("collective.path")
 
 
+def _value_codes(objs, key) -> list:
+    """Small int per object, equal for equal ``key(obj)``: objects are deduplicated by identity
+    first (sweeps usually share them), so each distinct object is keyed only once."""
+    objs = list(objs)
+    by_id = dict(zip(map(id, objs), objs))
+    codes: dict = {}
+    code_of = {i: codes.setdefault(key(o), len(codes)) for i, o in by_id.items()}
+    return list(map(code_of.__getitem__, map(id, objs)))
+
+
 def group_classes(graphs, configs, graph_of, db=None) -> list:
     """Config indices of each topology class, classes in order of first appearance.  A class
     is (class_key, structure of the candidate's graph, device roles of the expansion); keys
@@ -68,8 +78,8 @@ def group_classes(graphs, configs, graph_of, db=None) -> list:
         psd = [getattr(c, "ps_device", None) for c in configs]
     # field values (tuples of strings hash cheaply; sweeps often build per-candidate objects,
     # so object identities would make every config its own combination)
-    cols = [list(map(_R, configs)), list(map(tuple, map(_DMAP, configs))), list(map(tuple, map(_MARKERS, configs))),
-            list(map(_PATH, configs)), sync, psd, list(graph_of)]
+    cols = [list(map(_R, configs)), _value_codes(map(_DMAP, configs), tuple),
+            _value_codes(map(_MARKERS, configs), tuple), list(map(_PATH, configs)), sync, psd, list(graph_of)]
     cols = [c for c in cols if len(dict.fromkeys(c)) > 1]  # fields shared by every config drop out
     if not cols:
         return [list(range(len(configs)))] if configs else []
@@ -145,9 +155,8 @@ class TopologyClass:
             else:
                 vkeys = list(graph_of)
             gv_of = {vk: k for k, vk in enumerate(dict.fromkeys(vkeys))}
-            first_cfg = {}
-            for vk, c in zip(vkeys, configs):
-                first_cfg.setdefault(vk, c)
+            first_i = dict(zip(reversed(vkeys), range(len(vkeys) - 1, -1, -1)))  # first config of each key
+            first_cfg = {vk: configs[i] for vk, i in first_i.items()}
             variant_rows = variant_arrays_many(kind, self.ids, [graphs[vk[0] if kind == "ps" else vk] for vk in gv_of],
                                                structure, cfg0, db, cfgs=[first_cfg[vk] for vk in gv_of])
             strat_gv = np.fromiter(map(gv_of.__getitem__, vkeys), np.int32, len(vkeys))
