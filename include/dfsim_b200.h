@@ -341,7 +341,7 @@ int32_t dfsim_critical_path_levels_capacity(const dfsim_cp_tables *t);
 typedef struct {
     int32_t n_nodes;
     int32_t n_chunks;          /* prefetch chunks, in processing order (highest positions first) */
-    int32_t chunk_positions;   /* K: a chunk covers at most K positions (8 or 16) */
+    int32_t chunk_positions;   /* K: a chunk covers at most K positions (8: the register window) */
     int32_t n_slots;           /* shared-memory suffix rows per warp (slots) */
     int32_t rmax;              /* spill values prefetched per chunk, at most */
     int32_t n_long;            /* values kept in spill rows */
@@ -372,7 +372,7 @@ int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int32_t *succ_
                         int32_t *block_off, int32_t *bounds, int32_t *spill_off, uint16_t *spill_list,
                         int32_t *info);
 
-/* stages: prefetch depth (2 or 3, as planned). */
+/* stages: must be 0 (the register-window kernel; the tables are planned with 2 smem stages). */
 int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
                               const int64_t *cand_of_slot, const double *sched, double *cp_len, int32_t *cp_src);
 
@@ -380,7 +380,7 @@ int dfsim_critical_path_lanes(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int
  * k is cand_of_slot[k] (the engine's candidate order; NULL: k), and cp_len / cp_src are written
  * at the candidate.  _ex: only the slots slots[0..n_sims) (device int64; NULL: 0..n_sims-1),
  * with at most max_warps warps a CTA (0: as many as fit) so that the kernel can share SMs with
- * a concurrently running engine launch.  slots requires stages 0. */
+ * a concurrently running engine launch. */
 int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_tables *t, int32_t stages, int64_t n_sims,
                                  const int64_t *slots, const int64_t *cand_of_slot, int32_t max_warps,
                                  const double *sched, double *cp_len, int32_t *cp_src);

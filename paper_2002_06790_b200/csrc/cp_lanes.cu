@@ -89,137 +89,12 @@ struct LaneArgs {
     int32_t *cp_src;
     double *spill;        // [grid * wpb][n_long][32]
     int32_t *task_counter; // groups of 32 candidates handed out dynamically (SMs finish together)
-    const int64_t *slots;  // optional: lane i of task t takes schedule slot slots[32 t + i] (register variant)
+    const int64_t *slots;  // optional: lane i of task t takes schedule slot slots[32 t + i]
     const int64_t *cand;   // optional: candidate of each schedule slot (outputs go to cp_len[cand[slot]])
     int32_t wpb;
     int32_t table_bytes;  // CTA tables: bounds | spill_off | block_off | spill_list
-    int32_t region_bytes; // per warp: rows [slots | spill stages] | pair stages | block stages
+    int32_t region_bytes; // per warp: rows [slots | spill stages | zero row] | block stages
 };
-
-// Per warp: value rows of 256 B (one double per lane) -- slots, then one spill stage per
-// pipeline stage -- then the pair stages (32 candidates x K (start, finish) pairs, rows padded
-// by 16 B so that a warp's LDS.128 is conflict-free), then the block stages (the chunk's node
-// records).  Chunk q uses stage q % NST; prefetch runs NST - 1 chunks ahead.
-template <int K, int NST>
-__global__ void __launch_bounds__(1024, 1) k_critical_path_lanes(LaneArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int kStride = K * 16 + 16;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int N = a.t.n_nodes, NQ = a.t.n_chunks, NS = a.t.n_slots, RM = a.t.rmax, BM = a.t.block_max;
-    const int NL = a.t.n_spill_list;
-    int32_t *s_bounds = reinterpret_cast<int32_t *>(smem);
-    int32_t *s_soff = s_bounds + (NQ + 1);
-    int32_t *s_boff = s_soff + (NQ + 1);
-    uint16_t *s_slist = reinterpret_cast<uint16_t *>(s_boff + (NQ + 1));
-    for (int i = threadIdx.x; i <= NQ; i += blockDim.x) {
-        s_bounds[i] = __ldg(a.t.bounds + i);
-        s_soff[i] = __ldg(a.t.spill_off + i);
-        s_boff[i] = __ldg(a.t.block_off + i);
-    }
-    for (int i = threadIdx.x; i < NL; i += blockDim.x) s_slist[i] = __ldg(a.t.spill_list + i);
-    __syncthreads();
-
-    const unsigned a_bounds = smem_u32(s_bounds), a_soff = smem_u32(s_soff), a_boff = smem_u32(s_boff);
-    const unsigned a_slist = smem_u32(s_slist);
-    unsigned char *region = smem + a.table_bytes + static_cast<size_t>(warp) * a.region_bytes;
-    const unsigned a_region = smem_u32(region);
-    const unsigned a_lane = a_region + 8u * lane;  // this lane's column in every value row
-    const unsigned a_zero = a_region + static_cast<unsigned>(NS + NST * RM) * 256u;  // row of 0.0 (never written)
-    const unsigned a_pairs = a_zero + 256u;
-    const unsigned a_blocks = a_pairs + static_cast<unsigned>(NST) * 32u * kStride;
-    sts_d(a_zero + 8u * lane, 0.0);
-    __syncwarp();
-    const int64_t slot_warp = static_cast<int64_t>(blockIdx.x) * a.wpb + warp;
-    double *spill_warp = a.spill + slot_warp * static_cast<int64_t>(a.t.n_long) * 32 + lane;
-    asm volatile("mov.b64 %0, %0;" : "+l"(spill_warp));
-    const int64_t n_tasks = (a.S + 31) / 32;
-    for (;;) {
-        int task = 0;
-        if (lane == 0) task = atomicAdd(a.task_counter, 1);
-        task = __shfl_sync(DFSIM_FULL_MASK, task, 0);
-        if (task >= n_tasks) break;
-        const int64_t wbase = static_cast<int64_t>(task) * 32;
-        const bool live = wbase + lane < a.S;
-        const int n_live = static_cast<int>(a.S - wbase < 32 ? a.S - wbase : 32);
-        const double *rows = a.sched + 2 * wbase * N;  // the warp's tile: pair p * 32 + c (c = candidate)
-        asm volatile("mov.b64 %0, %0;" : "+l"(rows));
-
-        auto prefetch = [&](int q) {
-            const unsigned stg = static_cast<unsigned>(q % NST);
-            const int hi = lds_i(a_bounds + 4u * q);
-            const int wlo = hi > K ? hi - K : 0;
-            const unsigned st = a_pairs + stg * (32u * kStride);
-#pragma unroll
-            for (int k = lane; k < 32 * K; k += 32) {  // pair i = k / 32 of candidate c = k % 32: coalesced runs
-                const int c = k % 32, i = k / 32;
-                if (c < n_live && wlo + i < N)
-                    cpa16(st + static_cast<unsigned>(c * kStride + i * 16), rows + 2 * (static_cast<int64_t>(wlo + i) * 32 + c));
-            }
-            const int b0 = lds_i(a_boff + 4u * q), b1 = lds_i(a_boff + 4u * (q + 1));
-            const unsigned bs = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
-            DFSIM_CHECK(b1 - b0 <= BM, 8);
-            for (int b = b0 + lane; b < b1; b += 32) cpa16(bs + 16u * static_cast<unsigned>(b - b0), a.t.blocks + 4 * static_cast<int64_t>(b));
-            const int r0 = lds_i(a_soff + 4u * q), r1 = lds_i(a_soff + 4u * (q + 1));
-            const unsigned ss = a_lane + static_cast<unsigned>(NS + static_cast<int>(stg) * RM) * 256u;
-            if (live)
-                for (int r = r0; r < r1; r++) cpa8(ss + static_cast<unsigned>(r - r0) * 256u, spill_warp + 32 * static_cast<int64_t>(lds_h(a_slist + 2u * r)));
-            asm volatile("cp.async.commit_group;\n" ::);
-        };
-
-        double len = 0.0;
-        int src = 0x7fffffff;
-#pragma unroll
-        for (int q = 0; q < NST - 1; q++)
-            if (q < NQ) prefetch(q); else asm volatile("cp.async.commit_group;\n" ::);
-        for (int q = 0; q < NQ; q++) {
-            // stage (q + NST - 1) % NST was last used by chunk q - 1 (finished: __syncwarp below)
-            if (q + NST - 1 < NQ) prefetch(q + NST - 1); else asm volatile("cp.async.commit_group;\n" ::);
-            asm volatile("cp.async.wait_group %0;\n" ::"n"(NST - 1));
-            __syncwarp();
-            const unsigned stg = static_cast<unsigned>(q % NST);
-            const int hi = lds_i(a_bounds + 4u * q), lo = lds_i(a_bounds + 4u * (q + 1));
-            const int wlo = hi > K ? hi - K : 0;
-            const unsigned pst = a_pairs + stg * (32u * kStride) + static_cast<unsigned>(lane * kStride) - 16u * wlo;
-            const unsigned blk = a_blocks + stg * static_cast<unsigned>(BM) * 16u;
-            unsigned rec = blk;  // records in processing order
-            for (int p = hi - 1; p >= lo; p--, rec += 16u) {
-                const uint4 r = lds_u4(rec);
-                const unsigned deg = r.y & 0xffu;
-                // successors 1-4 inline (unused ones name the zero row): four independent loads
-                const double x0 = lds_d(row_lo(a_lane, r.z)), x1 = lds_d(row_hi(a_lane, r.z));
-                const double x2 = lds_d(row_lo(a_lane, r.w)), x3 = lds_d(row_hi(a_lane, r.w));
-                const double2 sf = lds_d2(pst + 16u * p);
-                double m01 = x1 > x0 ? x1 : x0, m23 = x3 > x2 ? x3 : x2;
-                double best = m23 > m01 ? m23 : m01;  // >= 0.0: max(0.0, .) (graph.py:465-468)
-                if (deg > 4) {
-                    const unsigned ex = blk + 2u * (r.y >> 8);
-                    for (unsigned j = 4; j < deg; j++) {
-                        const double x = lds_d(a_lane + 256u * lds_h(ex + 2u * (j - 4)));
-                        best = x > best ? x : best;
-                    }
-                }
-                const double sv = __dadd_rn(__dsub_rn(sf.y, sf.x), best);  // finish - start (reporting.py:128)
-                if (r.x & kHasSlot) sts_d(a_lane + 256u * (r.x & 0xfffu), sv);
-                if (r.x & kHasSpill) spill_warp[32 * static_cast<int64_t>(r.x >> 15)] = sv;
-                if (r.x & kSource) {
-                    const int rk = __ldg(a.t.rank_of_pos + p);
-                    if (src == 0x7fffffff || sv > len || (sv == len && rk < src)) {
-                        len = sv;
-                        src = rk;
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        asm volatile("cp.async.wait_group 0;\n" ::);
-        if (live) {
-            const int64_t cand = a.cand ? __ldg(a.cand + wbase + lane) : wbase + lane;
-            a.cp_len[cand] = src == 0x7fffffff ? 0.0 : len;
-            if (a.cp_src) a.cp_src[cand] = src == 0x7fffffff ? -1 : src;
-        }
-        __syncwarp();
-    }
-}
 
 // Register-staged variant (K = 8): each lane loads its own candidate's 8 (start, finish)
 // pairs of the next chunk straight into registers, one chunk ahead, so the pair stages need no
@@ -389,16 +264,14 @@ struct LaneShape {
 
 // stages 2 / 3: pairs staged in shared memory; stages 0: pairs in registers (K = 8), two
 // shared-memory stages for records and spill values
-LaneShape lane_shape(const dfsim_cp_lane_tables *t, int stages) {
+LaneShape lane_shape(const dfsim_cp_lane_tables *t, int /*stages: 0*/) {
     LaneShape s;
-    const size_t K = static_cast<size_t>(t->chunk_positions);
-    const bool reg = stages == 0;
-    const size_t nst = reg ? 2 : static_cast<size_t>(stages);
+    const size_t nst = 2;  // shared-memory stages of node records and spill values
     s.table_bytes = ((static_cast<size_t>(t->n_chunks + 1) * 12 + static_cast<size_t>(t->n_spill_list) * 2 + 15) / 16) * 16;
     s.region_bytes = static_cast<size_t>(t->n_slots + nst * t->rmax + 1) * 256 +  // + the zero row
-                     nst * ((reg ? 0 : 32 * (K * 16 + 16)) + static_cast<size_t>(t->block_max) * 16);
+                     nst * static_cast<size_t>(t->block_max) * 16;
     const size_t budget = 227 * 1024 - 64;
-    s.wpb = reg ? 16 : 32;  // the register variant holds 16 warps (<= 128 registers each)
+    s.wpb = kRegWarps;
     while (s.wpb > 0 && s.table_bytes + s.wpb * s.region_bytes > budget) s.wpb--;
     return s;
 }
@@ -546,8 +419,7 @@ extern "C" int dfsim_cp_lanes_plan(int32_t n, const int32_t *succ_off, const int
 }
 
 extern "C" int32_t dfsim_critical_path_lanes_capacity(const dfsim_cp_lane_tables *t, int32_t stages) {
-    if (!t || t->n_chunks <= 0 || !(stages == 0 || stages == 2 || stages == 3)) return 0;
-    if (stages == 0 && t->chunk_positions != 8) return 0;
+    if (!t || t->n_chunks <= 0 || stages != 0 || t->chunk_positions != 8) return 0;
     return lane_shape(t, stages).wpb;
 }
 
@@ -561,12 +433,9 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
                                             int64_t n_sims, const int64_t *slots, const int64_t *cand_of_slot,
                                             int32_t max_warps, const double *sched, double *cp_len, int32_t *cp_src) {
     if (!ctx || !t) return DFSIM_BAD_ARGUMENT;
-    DFSIM_ARG_CHECK(ctx, !slots || stages == 0, "a slot list needs the register variant (stages 0)");
     DFSIM_ARG_CHECK(ctx, sched && cp_len, "sched and cp_len are required");
     DFSIM_ARG_CHECK(ctx, (reinterpret_cast<uintptr_t>(sched) & 15) == 0, "sched must be 16-byte aligned");
-    DFSIM_ARG_CHECK(ctx, t->chunk_positions == 8 || t->chunk_positions == 16, "chunk_positions must be 8 or 16");
-    DFSIM_ARG_CHECK(ctx, stages == 0 || stages == 2 || stages == 3, "stages must be 0 (registers), 2 or 3");
-    DFSIM_ARG_CHECK(ctx, stages != 0 || t->chunk_positions == 8, "the register variant needs chunk_positions 8");
+    DFSIM_ARG_CHECK(ctx, stages == 0 && t->chunk_positions == 8, "stages 0 (register windows) with chunk_positions 8");
     DFSIM_ARG_CHECK(ctx, t->n_nodes > 0 && t->n_chunks > 0 && t->n_slots >= 1 && t->n_slots < 4096 && t->rmax >= 1 &&
                          t->n_spill_list >= 0 && t->block_max >= 1,
                     "inconsistent lane tables");
@@ -578,7 +447,6 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
     const int64_t warps = (n_sims + 31) / 32;
     int wpb = shape.wpb;
     if (max_warps > 0 && max_warps < wpb) wpb = max_warps;  // leaves room for a co-resident kernel
-    if (stages == 0 && wpb > kRegWarps) wpb = kRegWarps;
     const int64_t per_sm = (warps + ctx->num_sms - 1) / ctx->num_sms;
     if (per_sm < wpb) wpb = static_cast<int>(per_sm < 1 ? 1 : per_sm);
     const size_t smem = shape.table_bytes + static_cast<size_t>(wpb) * shape.region_bytes;
@@ -615,7 +483,5 @@ extern "C" int dfsim_critical_path_lanes_ex(dfsim_ctx *ctx, const dfsim_cp_lane_
         }
         return rc;
     };
-    if (stages == 0) return launch(k_critical_path_lanes_reg<8>);
-    if (t->chunk_positions == 16) return stages == 2 ? launch(k_critical_path_lanes<16, 2>) : launch(k_critical_path_lanes<16, 3>);
-    return stages == 2 ? launch(k_critical_path_lanes<8, 2>) : launch(k_critical_path_lanes<8, 3>);
+    return launch(k_critical_path_lanes_reg<8>);
 }

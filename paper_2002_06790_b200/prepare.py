@@ -170,10 +170,9 @@ class Tables:
         self.slot_region, self.stage_doubles = region, stage
 
 
-LANE_K = int(os.environ.get("DFSIM_CP_LANE_K", 8))   # positions per K4 v3 prefetch chunk (8 or 16)
+LANE_K = 8  # positions per K4 v3 chunk (its register window)
 LANE_RMAX = int(os.environ.get("DFSIM_CP_LANE_RMAX", 8))  # spill values per chunk (planner minimum)
-# K4 v3 variant: 0 = schedule windows staged in registers (K = 8), 2 / 3 = shared-memory stages
-LANE_STAGES = int(os.environ.get("DFSIM_CP_LANE_STAGES", 0))
+LANE_STAGES = 0  # K4 v3 launch variant: register windows (the planner models 2 smem stages)
 
 
 LANE_NEAR = int(os.environ.get("DFSIM_CP_LANE_NEAR", 12))  # chunks a value may wait in a slot (C2: 8 -> 12, CP 1.290 -> 1.280 ms; 14 drops a warp)
