@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .lowering import FEATURES, ROW_FIELDS, base_arrays, node_features, node_rows, row_arrays
+from .lowering import FEATURES, ROW_FIELDS, _i64, base_arrays, node_features, node_rows, row_arrays
 from .model import DEVICE_LINK, TRANSFER
 
 
@@ -192,5 +192,59 @@ def variant_arrays_many(kind: str, ids, graphs, structure, cfg=None, db=None, cf
             sel = np.ix_(np.asarray(vs, np.int64), special)
             for k in ROW_FIELDS:
                 out[k][sel] = rows[k]
+    if kind != "plain":
+        _respec_transfers(out, ids, graphs, structure, [cfgs[v] if cfgs is not None else cfg
+                                                        for v in range(len(graphs))], db)
     return out
+
+
+def _replaced_devices(structure, cfg, db) -> dict:
+    """Devices whose spec an expansion under ``cfg`` writes over the base graph's: the
+    allreduce fabric (a Collective spec, strategy.py:263-271) when there are collectives; the
+    PS device (Compute) and the PS links (the path's Link spec, ps.py)."""
+    from .expansion import ps_link_specs
+    from .model import DEVICE_COLLECTIVE, DEVICE_COMPUTE, DeviceSpec
+
+    path = cfg.collective.path
+    if getattr(cfg, "sync", "allreduce") == "parameter_server":
+        out = ps_link_specs(cfg, db, structure.ps_device)
+        out[structure.ps_device] = DeviceSpec(structure.ps_device, DEVICE_COMPUTE, cfg.hardware)
+        return out
+    if not structure.coll_ids:
+        return {}
+    fabric = f"collective:{path}:" + "+".join(structure.group)
+    return {fabric: DeviceSpec(fabric, DEVICE_COLLECTIVE, cfg.hardware, 1.0, 0.0)}
+
+
+def _respec_transfers(out, ids, graphs, structure, cfgs, db):
+    """A base transfer on a device the expansion replaces (a device literally named like the
+    fabric, a PS link or the PS device) is estimated against the replacing spec, as the
+    reference estimates the expanded graph (costmodel.py:354-359): its clones' rows are
+    rewritten.  Such a collision is class-uniform (expansion.path_roles splits the path off),
+    so this is a no-op for every class of a normal sweep."""
+    g0 = graphs[0]
+    tdevs = {n.device for n in g0.nodes.values() if n.kind == TRANSFER}
+    if not tdevs:
+        return
+    pos_of = None
+    for v, (gb, cfg) in enumerate(zip(graphs, cfgs)):
+        specs = {d: sp for d, sp in _replaced_devices(structure, cfg, db).items() if d in tdevs}
+        if not specs:
+            continue
+        if pos_of is None:
+            pos_of = {}
+            for p, cid in enumerate(ids):
+                what, gid = structure.origin[cid]
+                n = g0.nodes[gid] if what == "clone" else None
+                if n is not None and n.kind == TRANSFER and n.device in tdevs:
+                    pos_of.setdefault(n.device, []).append((p, gid))
+        for d, spec in specs.items():
+            for p, gid in pos_of.get(d, ()):
+                b = gb.nodes[gid].attrs.get("bytes")
+                link = spec.kind == DEVICE_LINK and isinstance(b, int)
+                out["ok"][v, p] = 1 if link else 0
+                out["bytes"][v, p] = _i64(b) if link else 0
+                out["gsize"][v, p] = 0
+                out["thr"][v, p] = spec.throughput_mbps if link else 1.0
+                out["lat"][v, p] = spec.latency_us if link else 0.0
 

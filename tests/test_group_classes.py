@@ -22,26 +22,34 @@ def _graphs():
     from paper_2002_06790_b200.model import DEVICE_LINK, TRANSFER, DeviceSpec, OpNode
 
     g0, g1, g2 = W.layered_cnn(4), W.layered_cnn(4, batch=64), W.layered_cnn(6)
-    # g0 plus a transfer on a link literally named like the NVLink allreduce device of gpu0+gpu1
-    clash = "collective:NVLink:gpu0+gpu1"
-    g3 = dataclasses.replace(g0, nodes=dict(g0.nodes), devices=dict(g0.devices))
     first = sorted(g0.nodes)[0]
-    g3.nodes["xfer_in"] = OpNode("xfer_in", "Copy", clash, kind=TRANSFER, inputs=((first, 0),))
-    g3.devices[clash] = DeviceSpec(clash, DEVICE_LINK, "", 1000.0, 1.0)
-    return [g0, g1, g2, g3]
+
+    def with_link(name):  # g0 plus a transfer on a link device called ``name``
+        g = dataclasses.replace(g0, nodes=dict(g0.nodes), devices=dict(g0.devices))
+        g.nodes["xfer_in"] = OpNode("xfer_in", "Copy", name, kind=TRANSFER, inputs=((first, 0),),
+                                    attrs={"src_device": "gpu0", "dst_device": "host0", "bytes": 4096})
+        g.devices[name] = DeviceSpec(name, DEVICE_LINK, "", 1000.0, 1.0)
+        return g
+
+    # named like: the NVLink allreduce fabric of gpu0+gpu1 (g3), the NVLink PS up-link of gpu0
+    # (g4), the PS device (g5) -- an expansion replaces the spec of each
+    return [g0, g1, g2, with_link("collective:NVLink:gpu0+gpu1"), with_link("link:NVLink:gpu0->ps0"),
+            with_link("ps0")]
 
 
 def _configs():
     from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
 
     out = [(StrategyConfig(hardware="synth-hw"), 0)]
-    for gi in range(4):
+    for gi in range(6):
         for R in (2, 3):
             for sync in ("allreduce", "parameter_server"):
                 for path in PATHS:
                     cfg = StrategyConfig(replicas=R, device_map=tuple(f"gpu{i}" for i in range(R)),
                                          collective=CollectiveConfig("RingAnalytic", path),
-                                         gradient_markers=("grad_conv_*",), hardware="synth-hw", sync=sync)
+                                         gradient_markers=("grad_conv_*",), hardware="synth-hw", sync=sync,
+                                         # the planted profiles hold no PSAggregate records
+                                         overrides={"aggregate_*": 2.0} if sync == "parameter_server" else {})
                     out.append((cfg, gi))
     return out
 
@@ -119,6 +127,13 @@ def test_paths_merge_unless_roles_differ(grouped):
     s_nv = _structure(graphs[3], configs[classes[g3["NVLink"]][0]], db)
     s_pc = _structure(graphs[3], configs[classes[g3["PCIeSwitch"]][0]], db)
     assert s_nv[5] == s_pc[5] - 1
+    # g4's link is the NVLink PS up-link of gpu0: PS NVLink is split off at R = 2 and 3 alike
+    for R in (2, 3):
+        g4 = {p: cls(4, R, "parameter_server", p) for p in PATHS}
+        assert g4["PCIeSwitch"] == g4["RDMA"] != g4["NVLink"] != g4["QPI"]
+        assert len({cls(4, R, "allreduce", p) for p in PATHS}) == 1
+        # g5's link is the PS device: every path expands alike (the device keeps its name)
+        assert cls(5, R, "parameter_server", "PCIeSwitch") == cls(5, R, "parameter_server", "NVLink")
 
 
 def test_per_candidate_objects_group_by_value():
