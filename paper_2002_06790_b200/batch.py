@@ -14,6 +14,7 @@ process) and reduces one 16-byte winner record per GPU (NCCL all-gather / P2P).
 
 from __future__ import annotations
 
+import itertools
 import operator
 import os
 import threading
@@ -44,8 +45,30 @@ def class_key(cfg) -> tuple:
     return ("dp", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers))
 
 
-_R, _DMAP = operator.attrgetter("replicas"), operator.attrgetter("device_map")
-_MARKERS, _PATH = operator.attrgetter("gradient_markers"), operator.attrgetter("collective.path")
+
+# class fields: (attribute, by value, default when absent -- the reference's own StrategyConfig
+# has no PS extension fields; None: required)
+_FIELDS = (("replicas", False, None), ("device_map", True, None), ("gradient_markers", True, None),
+           ("collective.path", False, None), ("sync", False, "allreduce"), ("ps_device", False, "ps0"))
+
+
+_COLLECTIVE = operator.attrgetter("collective")
+# the fast path's fields (the whole collective: comparing one object is cheaper than a dotted get)
+_CLASS_FIELDS = operator.attrgetter("replicas", "device_map", "gradient_markers", "collective", "sync", "ps_device")
+
+
+def _column(configs, name, default) -> list:
+    try:
+        return list(map(operator.attrgetter(name), configs))
+    except AttributeError:
+        if default is None:
+            raise
+        return [getattr(c, name, default) for c in configs]
+
+
+def _all_same(col) -> bool:
+    """Every entry is the first one (identity; a C-level pass)."""
+    return all(map(operator.is_, col, itertools.repeat(col[0]))) if col else True
 
 
 def _value_codes(objs, key) -> list:
@@ -70,19 +93,28 @@ def group_classes(graphs, configs, graph_of, db=None) -> list:
     # every class-key lookup below
     canon: dict = {}
     skeys = {gi: canon.setdefault(structure_key(graphs[gi]), len(canon)) for gi in dict.fromkeys(graph_of)}
-    try:
-        sync = list(map(operator.attrgetter("sync"), configs))
-        psd = list(map(operator.attrgetter("ps_device"), configs))
-    except AttributeError:  # e.g. the reference's own StrategyConfig (no PS extension fields)
-        sync = [getattr(c, "sync", "allreduce") for c in configs]
-        psd = [getattr(c, "ps_device", None) for c in configs]
-    # field values (tuples of strings hash cheaply; sweeps often build per-candidate objects,
-    # so object identities would make every config its own combination)
-    cols = [list(map(_R, configs)), _value_codes(map(_DMAP, configs), tuple),
-            _value_codes(map(_MARKERS, configs), tuple), list(map(_PATH, configs)), sync, psd, list(graph_of)]
-    cols = [c for c in cols if len(dict.fromkeys(c)) > 1]  # fields shared by every config drop out
+    if not configs:
+        return []
+    # field columns; a column whose objects are all one object (the common case: sweeps share
+    # them) drops out after one identity pass, without hashing any value
+    cols = []
+    try:  # one pass when every class field is shared (equal tuples compare by identity first)
+        t0 = _CLASS_FIELDS(configs[0])
+        uniform = all(map(operator.eq, map(_CLASS_FIELDS, configs), itertools.repeat(t0)))
+    except AttributeError:
+        uniform = False
+    for name, by_value, default in () if uniform else _FIELDS:
+        col = _column(configs, name, default)
+        if _all_same(col):
+            continue
+        if by_value:  # tuples by value (sweeps often build per-candidate objects), coded per object
+            col = _value_codes(col, tuple)
+        if len(dict.fromkeys(col)) > 1:
+            cols.append(col)
+    if not _all_same(graph_of) and len(dict.fromkeys(graph_of)) > 1:
+        cols.append(list(graph_of))
     if not cols:
-        return [list(range(len(configs)))] if configs else []
+        return [list(range(len(configs)))]
     raw = list(zip(*cols))
     # first config of each distinct field combination (reversed: the smallest index is written last)
     first = dict(zip(reversed(raw), range(len(raw) - 1, -1, -1)))
@@ -139,7 +171,8 @@ class TopologyClass:
         self.ids = self.lg.ids
         self.configs = list(configs)
         variant_rows, strat_gv = None, None
-        multi = graphs is not None and len(set(graph_of)) > 1
+        one_graph = graphs is None or _all_same(graph_of) or len(dict.fromkeys(graph_of)) == 1
+        multi = not one_graph
         self._db = db
         self._path_objects = {}  # path -> (graph objects, device names) of the other paths in the class
         if multi or kind != "plain":
@@ -149,17 +182,24 @@ class TopologyClass:
 
             if graphs is None:
                 graphs, graph_of = [g], [0] * len(configs)
-            if kind == "ps":  # the PS links' attributes depend on the path: a variant per (graph, path)
+            if one_graph and (kind != "ps" or _all_same(list(map(_COLLECTIVE, configs)))):
+                vkeys = None  # one variant (the common case): no per-candidate keys
+            elif kind == "ps":  # the PS links' attributes depend on the path: a variant per (graph, path)
                 paths = [c.collective.path for c in configs]
                 vkeys = list(zip(graph_of, paths))
             else:
                 vkeys = list(graph_of)
-            gv_of = {vk: k for k, vk in enumerate(dict.fromkeys(vkeys))}
-            first_i = dict(zip(reversed(vkeys), range(len(vkeys) - 1, -1, -1)))  # first config of each key
-            first_cfg = {vk: configs[i] for vk, i in first_i.items()}
+            if vkeys is None:
+                vk0 = (graph_of[0], cfg0.collective.path) if kind == "ps" else graph_of[0]
+                gv_of, first_cfg = {vk0: 0}, {vk0: cfg0}
+                strat_gv = np.zeros(len(configs), np.int32)
+            else:
+                gv_of = {vk: k for k, vk in enumerate(dict.fromkeys(vkeys))}
+                first_i = dict(zip(reversed(vkeys), range(len(vkeys) - 1, -1, -1)))  # first config of each key
+                first_cfg = {vk: configs[i] for vk, i in first_i.items()}
+                strat_gv = np.fromiter(map(gv_of.__getitem__, vkeys), np.int32, len(vkeys))
             variant_rows = variant_arrays_many(kind, self.ids, [graphs[vk[0] if kind == "ps" else vk] for vk in gv_of],
                                                structure, cfg0, db, cfgs=[first_cfg[vk] for vk in gv_of])
-            strat_gv = np.fromiter(map(gv_of.__getitem__, vkeys), np.int32, len(vkeys))
         self.lp = LoweredProfiles(g if self.plan is not None else self.graph, self.ids, db, self.configs,
                                   ctx.device, None, strat_gv, fit_cache=fit_cache, variant_arrays=variant_rows,
                                   op_kind=self.plan.op_kind() if self.plan is not None else None)
@@ -698,9 +738,11 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
     built = []
     fits: dict = {}  # fitted models shared by the classes of this sweep (costmodel.py:313-316 fits per call)
     for idx in groups:
+        whole = len(idx) == S  # one class (idx == range(S)): no per-candidate gathers
         try:
-            built.append((idx, TopologyClass(graphs[graph_of[idx[0]]], db, [configs[i] for i in idx], ctx.device,
-                                             fused=fused, graphs=graphs, graph_of=[graph_of[i] for i in idx],
+            built.append((idx, TopologyClass(graphs[graph_of[idx[0]]], db, configs if whole else [configs[i] for i in idx],
+                                             ctx.device, fused=fused, graphs=graphs,
+                                             graph_of=graph_of if whole else [graph_of[i] for i in idx],
                                              fit_cache=fits)))
         except NativeError:
             raise
@@ -726,10 +768,16 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
             if tc.fallback_if_needed(o):
                 tc.critical_path_only(o)
     for pos, ((idx, tc), o) in enumerate(zip(built, outs)):
-        t_idx = torch.as_tensor(idx, dtype=torch.int64, device=dev)
-        makespan.index_copy_(0, t_idx, o["makespan"])
-        if "cp_len" in o:
-            cp_len.index_copy_(0, t_idx, o["cp_len"])
+        lo = idx[0]
+        if idx[-1] - lo + 1 == len(idx):  # a contiguous run of candidates (indices ascend in a class)
+            makespan[lo:lo + len(idx)].copy_(o["makespan"])
+            if "cp_len" in o:
+                cp_len[lo:lo + len(idx)].copy_(o["cp_len"])
+        else:
+            t_idx = torch.as_tensor(idx, dtype=torch.int64, device=dev)
+            makespan.index_copy_(0, t_idx, o["makespan"])
+            if "cp_len" in o:
+                cp_len.index_copy_(0, t_idx, o["cp_len"])
         bad = o["bad"].cpu().numpy()
         placed = o["n_placed"].cpu().numpy()
         rows = np.nonzero((bad > 0) | (placed != tc.lg.n))[0]
@@ -740,7 +788,7 @@ def sweep_local(graphs, db, configs, graph_of, device: int | None = None, keep_s
             for k in ("start", "finish", "sched"):
                 o.pop(k, None)
         result.classes.append((tc, idx, o))
-        ia = np.asarray(idx, np.int64)
+        ia = slice(lo, lo + len(idx)) if idx[-1] - lo + 1 == len(idx) else np.asarray(idx, np.int64)
         where_cls[ia] = pos
         where_row[ia] = np.arange(len(idx), dtype=np.int32)
     failure = min(failures, key=lambda f: f[0]) if failures else None

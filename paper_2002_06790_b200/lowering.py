@@ -18,6 +18,7 @@ Runs once per graph / topology class; everything per-strategy runs on the GPU.
 
 from __future__ import annotations
 
+import itertools
 import math
 import operator
 import threading
@@ -519,9 +520,12 @@ class LoweredProfiles:
             self.hw_ids[h] = len(self.hw_ids)
         self.strat_hw = np.fromiter(map(self.hw_ids.__getitem__, hws), np.int32, n)
         self.strat_gap = np.fromiter(map(float, map(_GAP, configs)), np.float64, n)
-        # collective algorithm and path by value (sweeps often build a config object per candidate)
-        algos = list(map(_ALGO, configs))
-        paths = list(map(_PATH, configs))
+        # collective algorithm and path by value (sweeps often build a config object per candidate);
+        # one identity pass when every candidate shares one collective object
+        colls = list(map(_COLLECTIVE, configs))
+        shared = bool(colls) and all(map(operator.is_, colls, itertools.repeat(colls[0])))
+        algos, paths = ([colls[0].algo], [colls[0].path]) if shared else \
+            (list(map(_ALGO, configs)), list(map(_PATH, configs)))
         algo_code = {}
         for al in dict.fromkeys(algos):
             if al not in (ALGO_MEASURED, ALGO_RING):
@@ -529,8 +533,12 @@ class LoweredProfiles:
             algo_code[al] = 0 if al == ALGO_MEASURED else 1
         for pth in dict.fromkeys(paths):
             self.path_ids[pth] = len(self.path_ids)
-        self.strat_algo = np.fromiter(map(algo_code.__getitem__, algos), np.uint8, n)
-        self.strat_path = np.fromiter(map(self.path_ids.__getitem__, paths), np.int32, n)
+        if shared:
+            self.strat_algo = np.full(n, algo_code[algos[0]], np.uint8)
+            self.strat_path = np.full(n, self.path_ids[paths[0]], np.int32)
+        else:
+            self.strat_algo = np.fromiter(map(algo_code.__getitem__, algos), np.uint8, n)
+            self.strat_path = np.fromiter(map(self.path_ids.__getitem__, paths), np.int32, n)
         self.strat_ov = np.full(n, -1, np.int32)
         ovs = list(map(_OVERRIDES, configs))
         for i in np.flatnonzero(np.fromiter(map(bool, ovs), bool, n)).tolist():
