@@ -342,6 +342,86 @@ def fit_linear(records) -> LinearCostModel:
                            FitStats(r2, max_rel, n))
 
 
+def fit_linear_many(record_lists, uniform: bool = False) -> list:
+    """``fit_linear`` of many record lists: element i is ``fit_linear(record_lists[i])`` or the
+    FitError it raises, bit for bit.  Lists of one (records, features) shape share the stacked
+    numpy calls that have a per-matrix loop inside (matrix_rank's SVD, the residual sums along
+    the last axis: the same LAPACK call and the same pairwise summation per row); the least
+    squares and the prediction stay one call per list, on the same C-contiguous design.  Lists
+    that would raise, warn (a zero duration divides by zero) or need the collinearity
+    diagnosis run through fit_linear itself.  ``uniform``: every list is known to share one op
+    type, hardware tag and feature-name tuple (fit_for_grid's groups).  tests/test_fits.py pins
+    the equality."""
+    out: list = [None] * len(record_lists)
+    shapes: dict = {}
+    for i, recs in enumerate(record_lists):
+        if recs:
+            sig0 = recs[0].signature
+            names = tuple(n for n, _ in sig0.arg_features)
+            if len(recs) >= len(names) + 1 and (uniform or all(
+                    r.signature.op_type == sig0.op_type and r.signature.hardware == sig0.hardware
+                    and tuple(n for n, _ in r.signature.arg_features) == names for r in recs)):
+                shapes.setdefault((len(recs), len(names)), []).append(i)
+                continue
+        out[i] = _fit_or_error(recs)
+    for (n, k), items in shapes.items():
+        x = np.array([[[v for _, v in r.signature.arg_features] for r in record_lists[i]] for i in items],
+                     dtype=float).reshape(len(items), n, k)
+        y = np.array([[r.mean_duration_us for r in record_lists[i]] for i in items], dtype=float)
+        design = np.concatenate([x, np.ones((len(items), n, 1))], axis=2)
+        rank = np.linalg.matrix_rank(design)
+        fine = (rank == k + 1) & np.all(y != 0.0, axis=1) & np.all(np.isfinite(y), axis=1)
+        ok = np.flatnonzero(fine)
+        for j in np.flatnonzero(~fine).tolist():
+            out[items[j]] = _fit_or_error(record_lists[items[j]])
+        if not len(ok):
+            continue
+        d, yy = design[ok], y[ok]
+        coef = _lstsq_stacked(d, yy)
+        pred = np.empty_like(yy)
+        for t in range(len(ok)):
+            pred[t] = d[t] @ coef[t]
+        ss_res = np.sum((yy - pred) ** 2, axis=-1)
+        ss_tot = np.sum((yy - np.mean(yy, axis=-1, keepdims=True)) ** 2, axis=-1)
+        max_rel = np.max(np.abs(pred - yy) / np.abs(yy), axis=-1)
+        for t, j in enumerate(ok.tolist()):
+            recs = record_lists[items[j]]
+            sig0 = recs[0].signature
+            res, tot = float(ss_res[t]), float(ss_tot[t])
+            if tot == 0.0:
+                r2 = 1.0 if res < 1e-18 else 0.0
+            else:
+                r2 = min(1.0, max(0.0, 1.0 - res / tot))
+            out[items[j]] = LinearCostModel(sig0.op_type, sig0.hardware, tuple(nm for nm, _ in sig0.arg_features),
+                                            tuple(float(c) for c in coef[t, :k]), float(coef[t, k]),
+                                            FitStats(r2, float(max_rel[t]), n))
+    return out
+
+
+def _lstsq_stacked(d, y):
+    """``np.linalg.lstsq(d[t], y[t], rcond=None)[0]`` for every t: one call of the gufunc that
+    lstsq wraps (numpy/linalg/_linalg.py: dgelsd per matrix, on the same copies), with lstsq's
+    rcond and error state; one lstsq call per matrix where that gufunc is not available."""
+    m, n = d.shape[-2:]
+    gufunc = getattr(getattr(np.linalg, "_umath_linalg", None), "lstsq", None)
+    if gufunc is None:
+        return np.stack([np.linalg.lstsq(d[t], y[t], rcond=None)[0] for t in range(len(d))])
+    with np.errstate(call=_lstsq_error, invalid="call", over="ignore", divide="ignore", under="ignore"):
+        x = gufunc(d, y[..., None], np.finfo(np.float64).eps * max(n, m), signature="ddd->ddid")[0]
+    return x[..., 0]
+
+
+def _lstsq_error(err, flag):
+    raise np.linalg.LinAlgError("SVD did not converge in Linear Least Squares")
+
+
+def _fit_or_error(recs):
+    try:
+        return fit_linear(recs)
+    except FitError as e:
+        return e
+
+
 def _collinear(x, names):
     kept = np.ones((x.shape[0], 1))
     bad = []
@@ -373,6 +453,33 @@ def fit_for_grid(db, op_type: str, hardware: str):
         warnings.warn(f"linear model for {op_type}/{hardware} has r_squared={model.fit_stats.r_squared:.4f}; "
                       "estimates may be unreliable", FitQualityWarning, stacklevel=3)
     return model
+
+
+def fit_for_grid_many(db, pairs) -> dict:
+    """``fit_for_grid`` of every (op type, hardware) pair, the fits batched (fit_linear_many);
+    warnings in the order of ``pairs``."""
+    chosen = {}
+    for op_type, hardware in pairs:
+        grid_map = db.op_records.get((op_type, hardware), {})
+        if not grid_map:
+            continue
+        groups = {}
+        for key in sorted(grid_map):  # grid keys are the records' feature tuples
+            groups.setdefault(tuple(map(_FIRST, key)), []).append(grid_map[key])
+        best = max(len(r) for r in groups.values())
+        chosen[(op_type, hardware)] = groups[min(k for k in groups if len(groups[k]) == best)]
+    fits = dict(zip(chosen, fit_linear_many(list(chosen.values()), uniform=True)))
+    out = {}
+    for pair in pairs:
+        m = fits.get(pair)
+        if m is None or isinstance(m, FitError):
+            out[pair] = None
+            continue
+        if m.fit_stats.r_squared < R_SQUARED_WARN:
+            warnings.warn(f"linear model for {pair[0]}/{pair[1]} has r_squared={m.fit_stats.r_squared:.4f}; "
+                          "estimates may be unreliable", FitQualityWarning, stacklevel=3)
+        out[pair] = m
+    return out
 
 
 def match_pattern(pattern: str, nid: str) -> bool:
@@ -491,6 +598,7 @@ def base_arrays(g):
     return arr, index
 
 
+_FIRST = operator.itemgetter(0)
 _HARDWARE, _GAP = operator.attrgetter("hardware"), operator.attrgetter("op_gap_us")
 _COLLECTIVE, _OVERRIDES = operator.attrgetter("collective"), operator.attrgetter("overrides")
 _ALGO, _PATH = operator.attrgetter("collective.algo"), operator.attrgetter("collective.path")
@@ -648,23 +756,18 @@ class LoweredProfiles:
             name_pool = {FEATURES.name_list[k] for k in np.unique(g_names).tolist()}
         else:
             name_pool = {nm for feats in sig_ids for nm, _ in feats}
-        fitted = []
+        fitted, wanted = [], []
         for hw, h in self.hw_ids.items():
             need = self._ops_needing_models(h, op, sig, exact_keys, ids, ov_sets)
-            for opname, o in op_ids.items():
-                if o not in need or not db.op_records.get((opname, hw)):
-                    continue
-                if fit_cache is not None and (opname, hw) in fit_cache:  # one fit per (op, hw) per sweep
-                    m = fit_cache[(opname, hw)]
-                else:
-                    m = fit_for_grid(db, opname, hw)
-                    if fit_cache is not None:
-                        fit_cache[(opname, hw)] = m
-                self.models[(opname, hw)] = m
-                if m is None:
-                    continue
+            wanted += [(opname, hw, (h << 21) | o) for opname, o in op_ids.items()
+                       if o in need and db.op_records.get((opname, hw))]
+        fit_cache = {} if fit_cache is None else fit_cache  # one fit per (op, hw) per sweep
+        fit_cache.update(fit_for_grid_many(db, [(op_, hw) for op_, hw, _ in wanted if (op_, hw) not in fit_cache]))
+        for opname, hw, key in wanted:
+            m = self.models[(opname, hw)] = fit_cache[(opname, hw)]
+            if m is not None:
                 name_pool.update(m.feature_names)
-                fitted.append(((h << 21) | o, m))
+                fitted.append((key, m))
         names_sorted = sorted(name_pool)
         name_id = {nm: i for i, nm in enumerate(names_sorted)}
         fitted.sort(key=lambda kv: kv[0])
