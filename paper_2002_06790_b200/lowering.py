@@ -630,10 +630,9 @@ class LoweredProfiles:
         self.strat_gap = np.fromiter(map(float, map(_GAP, configs)), np.float64, n)
         # collective algorithm and path by value (sweeps often build a config object per candidate);
         # one identity pass when every candidate shares one collective object
-        colls = list(map(_COLLECTIVE, configs))
-        shared = bool(colls) and all(map(operator.is_, colls, itertools.repeat(colls[0])))
-        algos, paths = ([colls[0].algo], [colls[0].path]) if shared else \
-            (list(map(_ALGO, configs)), list(map(_PATH, configs)))
+        c0 = configs[0].collective if n else None
+        shared = n > 0 and all(map(operator.is_, map(_COLLECTIVE, configs), itertools.repeat(c0)))
+        algos, paths = ([c0.algo], [c0.path]) if shared else (list(map(_ALGO, configs)), list(map(_PATH, configs)))
         algo_code = {}
         for al in dict.fromkeys(algos):
             if al not in (ALGO_MEASURED, ALGO_RING):
@@ -649,7 +648,7 @@ class LoweredProfiles:
             self.strat_path = np.fromiter(map(self.path_ids.__getitem__, paths), np.int32, n)
         self.strat_ov = np.full(n, -1, np.int32)
         ovs = list(map(_OVERRIDES, configs))
-        for i in np.flatnonzero(np.fromiter(map(bool, ovs), bool, n)).tolist():
+        for i in itertools.compress(range(n), ovs):  # candidates with overrides
             ov_key = tuple(ovs[i].items())
             if ov_key not in ov_key_to_id:
                 ov_key_to_id[ov_key] = len(ov_sets)
