@@ -49,7 +49,7 @@ from .batch import SweepResult, TopologyClass, gather_best, sweep, sweep_variant
 from .sharded import sweep_sharded  # noqa: F401
 from .estimate import estimate_all, estimate_batch  # noqa: F401
 from .expansion import expand_class, expand_data_parallel  # noqa: F401
-from .lowering import fit_for_grid, fit_linear, node_features  # noqa: F401
+from .lowering import fit_for_grid, fit_for_grid_many, fit_linear, fit_linear_many, node_features  # noqa: F401
 from .document import DocumentGraph, load_graph  # noqa: F401
 from .ps import expand_parameter_server  # noqa: F401
 from .reporting import SummaryReport, render_summary_text, summarize, to_trace, trace_intervals  # noqa: F401
