@@ -1,0 +1,143 @@
+"""GPU: differential fuzz of the class-sharing sweep against the drop-in path.
+
+Random training graphs with extra transfers and collectives on devices whose names collide
+with what expansions add (fabric, PS links, PS device, worker names); random candidates
+mixing plain / allreduce / parameter-server strategies, 1-4 replicas, device maps with
+duplicates and colliding names, three collective paths (one without link rows), both
+algorithms, per-candidate gaps and override patterns that hit added nodes.  Every candidate
+that the drop-in path (its own expansion -> estimate_all -> simulate -> critical_path)
+evaluates must get the same schedule, makespan and critical path from one batched
+sweep_variants call over all of them; every candidate the drop-in path rejects must make a
+sweep of it raise the same exception."""
+
+from __future__ import annotations
+
+import dataclasses
+import warnings
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PATHS = ("PCIeSwitch", "NVLink", "QPI")
+
+
+def _graph(rng, layers, batch):
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.model import (COLLECTIVE, DEVICE_COLLECTIVE, DEVICE_LINK, TRANSFER, DeviceSpec,
+                                             OpNode)
+
+    g = W.layered_cnn(layers, batch)
+    g = dataclasses.replace(g, nodes=dict(g.nodes), devices=dict(g.devices))
+    ids = list(g.nodes)
+    pool = ["link0", "collective:NVLink:gpu0+gpu1", "link:NVLink:gpu0->ps0", "link:PCIeSwitch:ps0->gpu1", "ps0",
+            "collective:PCIeSwitch:gpu0+gpu1+gpu2"]
+    for t in range(int(rng.integers(0, 4))):
+        dev = pool[int(rng.integers(0, len(pool)))]
+        if dev not in g.devices:
+            g.devices[dev] = DeviceSpec(dev, DEVICE_LINK, "", float(rng.choice([800.0, 1200.0])), 1.0)
+        if g.devices[dev].kind != DEVICE_LINK:
+            continue
+        src = ids[int(rng.integers(0, len(ids) - 1))]
+        g.nodes[f"xfer_{t}"] = OpNode(f"xfer_{t}", "Copy", dev, kind=TRANSFER, inputs=((src, 0),),
+                                      attrs={"src_device": "gpu0", "dst_device": "host0",
+                                             "bytes": int(rng.integers(1, 1 << 20))})
+    if rng.uniform() < 0.5:
+        dev = "fabric0"
+        g.devices[dev] = DeviceSpec(dev, DEVICE_COLLECTIVE, "", 1.0, 0.0)
+        src = ids[int(rng.integers(0, len(ids) - 1))]
+        g.nodes["coll_x"] = OpNode("coll_x", "AllReduce", dev, kind=COLLECTIVE, inputs=((src, 0),),
+                                   attrs={"group": ["gpu0", "gpu1"], "bytes": 4096})
+    return g
+
+
+def _configs(rng, n):
+    """Candidates drawn around a few class bases (replicas, device map, markers, sync, PS
+    device), so classes hold many candidates that differ in path, algorithm, gap, overrides."""
+    from paper_2002_06790_b200.model import CollectiveConfig, StrategyConfig
+
+    names = ["gpu0", "gpu1", "gpu2", "gpu3", "link0", "ps0"]
+    bases = []
+    for _ in range(5):
+        R = int(rng.integers(1, 5))
+        dmap = tuple(names[int(k)] for k in rng.integers(0, 4 if rng.uniform() < 0.8 else 6, R))
+        bases.append(dict(replicas=R, device_map=() if rng.uniform() < 0.15 else dmap,
+                          gradient_markers=(str(rng.choice(["grad_conv_*", "grad_conv_01", "nomatch*"])),),
+                          sync="parameter_server" if rng.uniform() < 0.4 else "allreduce",
+                          ps_device=str(rng.choice(["ps0", "ps0", "ps0", "gpu1", "link0"]))))
+    out = []
+    for _ in range(n):
+        base = bases[int(rng.integers(0, len(bases)))]
+        ov = {}
+        if rng.uniform() < 0.4:
+            ov[str(rng.choice(["conv_0*", "relu_01", "aggregate_*", "push_grad_conv_00@r0", "allreduce_*",
+                               "pull_*", "nomatch"]))] = float(rng.choice([0.0, 1.5, 4.0]))
+        if base["sync"] == "parameter_server" and "aggregate_*" not in ov:
+            ov["aggregate_*"] = 2.0  # the planted profiles hold no PSAggregate records
+        out.append(StrategyConfig(
+            collective=CollectiveConfig(str(rng.choice(["RingAnalytic", "MeasuredThroughput"])),
+                                        PATHS[int(rng.integers(0, 3))]),
+            hardware="synth-hw", op_gap_us=float(rng.choice([0.0, 0.25, 1.0])), overrides=ov, **base))
+    return out
+
+
+def _drop_in(g, cfg, db):
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200.batch import class_key
+    from paper_2002_06790_b200.ps import expand_parameter_server
+
+    key = class_key(cfg)
+    if key == ("plain",):
+        gx = g
+    elif key[0] == "ps":
+        gx = expand_parameter_server(g, cfg, db, cfg.ps_device).graph
+    else:
+        gx = fw.expand_data_parallel(g, cfg).graph
+    table = fw.estimate_all(gx, db, cfg)
+    s = fw.simulate(gx, table)
+    cp = fw.critical_path(gx, {e.node_id: e.finish_us - e.start_us for e in s.entries})[0]
+    return s, cp
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_class_sharing_matches_drop_in(seed):
+    import paper_2002_06790_b200 as fw
+    from paper_2002_06790_b200 import workloads as W
+
+    rng = np.random.default_rng(1000 + seed)
+    db = W.planted_profiles(W.CNN_LAWS, links=W.SYNTH_LINKS + W.SYNTH_FABRIC_LINKS)
+    graphs = [_graph(rng, int(rng.integers(2, 5)), int(rng.choice([16, 32]))) for _ in range(3)]
+    graphs.append(dataclasses.replace(graphs[0], nodes=dict(graphs[0].nodes)))  # a same-structure variant
+    configs = _configs(rng, 64)
+    graph_of = [int(rng.choice([0, 0, 1, 2, 3])) for _ in configs]
+    ok, failing = [], []
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for cfg, gi in zip(configs, graph_of):
+            try:
+                ok.append((cfg, gi) + _drop_in(graphs[gi], cfg, db))
+            except fw.DfsimError as e:
+                failing.append((cfg, gi, e))
+            except ValueError as e:
+                failing.append((cfg, gi, e))
+    assert len(ok) >= 8, len(ok)
+    for cfg, gi, e in failing:
+        with warnings.catch_warnings(), pytest.raises(type(e)) as got:
+            warnings.simplefilter("ignore")
+            fw.sweep_variants(graphs, db, [cfg], [gi])
+        assert str(got.value) == str(e), (cfg, gi)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = fw.sweep_variants(graphs, db, [c for c, *_ in ok], [gi for _, gi, *_ in ok], keep_schedules=True)
+    for i, (cfg, gi, want, cp) in enumerate(ok):
+        with warnings.catch_warnings():  # schedules build their node objects on first use
+            warnings.simplefilter("ignore")
+            got = res.schedule(i)
+        assert [(e.node_id, e.device, e.start_us, e.finish_us, e.source) for e in got.entries] == \
+               [(e.node_id, e.device, e.start_us, e.finish_us, e.source) for e in want.entries], (seed, i, cfg)
+        assert got.per_device_busy_us == want.per_device_busy_us, (seed, i)
+        assert res.makespan[i] == want.makespan_us and res.cp_len[i] == cp, (seed, i, cfg)
+    best = min(range(len(ok)), key=lambda i: (ok[i][2].makespan_us, i))
+    assert res.best_index == best
+    print(f"seed {seed}: {len(ok)} evaluated, {len(failing)} rejected, {len(res.classes)} classes")
