@@ -82,18 +82,23 @@ def _configs(rng, n):
     return out
 
 
-def _drop_in(g, cfg, db):
+def _expanded(g, cfg, db):
     import paper_2002_06790_b200 as fw
     from paper_2002_06790_b200.batch import class_key
     from paper_2002_06790_b200.ps import expand_parameter_server
 
     key = class_key(cfg)
     if key == ("plain",):
-        gx = g
-    elif key[0] == "ps":
-        gx = expand_parameter_server(g, cfg, db, cfg.ps_device).graph
-    else:
-        gx = fw.expand_data_parallel(g, cfg).graph
+        return g
+    if key[0] == "ps":
+        return expand_parameter_server(g, cfg, db, cfg.ps_device).graph
+    return fw.expand_data_parallel(g, cfg).graph
+
+
+def _drop_in(g, cfg, db):
+    import paper_2002_06790_b200 as fw
+
+    gx = _expanded(g, cfg, db)
     table = fw.estimate_all(gx, db, cfg)
     s = fw.simulate(gx, table)
     cp = fw.critical_path(gx, {e.node_id: e.finish_us - e.start_us for e in s.entries})[0]
@@ -140,4 +145,13 @@ def test_class_sharing_matches_drop_in(seed):
         assert res.makespan[i] == want.makespan_us and res.cp_len[i] == cp, (seed, i, cfg)
     best = min(range(len(ok)), key=lambda i: (ok[i][2].makespan_us, i))
     assert res.best_index == best
+    # reports of a few candidates from the schedules still in HBM, and the unfused path
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for i in range(0, len(ok), 7):
+            cfg, gi, want, _ = ok[i]
+            gx = _expanded(graphs[gi], cfg, db)
+            assert res.summary(i) == fw.summarize(want, gx), (seed, i)
+        plain = fw.sweep_variants(graphs, db, [c for c, *_ in ok], [gi for _, gi, *_ in ok], fused=False)
+    assert plain.makespan.tolist() == res.makespan.tolist() and plain.cp_len.tolist() == res.cp_len.tolist()
     print(f"seed {seed}: {len(ok)} evaluated, {len(failing)} rejected, {len(res.classes)} classes")
