@@ -45,7 +45,6 @@ def class_key(cfg) -> tuple:
     return ("dp", cfg.replicas, tuple(cfg.device_map), tuple(cfg.gradient_markers))
 
 
-
 # class fields: (attribute, by value, default when absent -- the reference's own StrategyConfig
 # has no PS extension fields; None: required)
 _FIELDS = (("replicas", False, None), ("device_map", True, None), ("gradient_markers", True, None),
