@@ -152,3 +152,31 @@ def test_per_candidate_objects_group_by_value():
     classes = group_classes([g], cfgs, [0] * len(cfgs), db)
     assert [list(c) for c in classes] == [list(range(50)), list(range(50, 57))]
     assert np.all([c.device_map == ("gpu1", "gpu0") for c in cfgs[50:]])
+
+
+def test_configs_without_ps_fields():
+    """The reference's own StrategyConfig has no ``sync`` / ``ps_device`` (PS is an extension):
+    such configs group as allreduce / plain, on the column path."""
+    from paper_2002_06790_b200 import workloads as W
+    from paper_2002_06790_b200.batch import group_classes
+    from paper_2002_06790_b200.model import CollectiveConfig
+
+    @dataclasses.dataclass(frozen=True)
+    class RefConfig:  # the reference's strategy.py:31-58 fields only
+        replicas: int = 1
+        device_map: tuple = ()
+        collective: CollectiveConfig = CollectiveConfig()
+        gradient_markers: tuple = ()
+        hardware: str = "synth-hw"
+        op_gap_us: float = 0.0
+        overrides: dict = dataclasses.field(default_factory=dict)
+
+    db = W.planted_profiles(W.CNN_LAWS)
+    g = W.layered_cnn(3)
+    dp = dict(replicas=2, device_map=("gpu0", "gpu1"), gradient_markers=("grad_conv_*",))
+    cfgs = [RefConfig(**dp, collective=CollectiveConfig("RingAnalytic", p)) for p in ("PCIeSwitch", "NVLink")]
+    cfgs += [RefConfig(), RefConfig(op_gap_us=1.0), RefConfig(**dp)]
+    classes = group_classes([g], cfgs, [0] * len(cfgs), db)
+    assert [list(c) for c in classes] == [[0, 1, 4], [2, 3]]
+    same = [RefConfig(**dp, op_gap_us=0.1 * k) for k in range(5)]
+    assert [list(c) for c in group_classes([g], same, [0] * 5, db)] == [list(range(5))]
