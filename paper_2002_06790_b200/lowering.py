@@ -404,11 +404,14 @@ def _lstsq_stacked(d, y):
     rcond and error state; one lstsq call per matrix where that gufunc is not available."""
     m, n = d.shape[-2:]
     gufunc = getattr(getattr(np.linalg, "_umath_linalg", None), "lstsq", None)
-    if gufunc is None:
-        return np.stack([np.linalg.lstsq(d[t], y[t], rcond=None)[0] for t in range(len(d))])
-    with np.errstate(call=_lstsq_error, invalid="call", over="ignore", divide="ignore", under="ignore"):
-        x = gufunc(d, y[..., None], np.finfo(np.float64).eps * max(n, m), signature="ddd->ddid")[0]
-    return x[..., 0]
+    if gufunc is not None:
+        try:
+            with np.errstate(call=_lstsq_error, invalid="call", over="ignore", divide="ignore", under="ignore"):
+                x = gufunc(d, y[..., None], np.finfo(np.float64).eps * max(n, m), signature="ddd->ddid")[0]
+            return x[..., 0]
+        except TypeError:  # a numpy whose private gufunc has another signature
+            pass
+    return np.stack([np.linalg.lstsq(d[t], y[t], rcond=None)[0] for t in range(len(d))])
 
 
 def _lstsq_error(err, flag):

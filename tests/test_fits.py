@@ -126,3 +126,19 @@ def test_random_grids(seed):
         many = fit_linear_many(lists)
         for recs, m in zip(lists, many):
             assert _same(m, _per_list(recs)), recs[:2]
+
+
+def test_without_the_stacked_gufunc(monkeypatch):
+    """The per-matrix lstsq fallback (a numpy without the private gufunc) gives the same fits."""
+    import paper_2002_06790_b200.lowering as L
+
+    class NoGufunc:
+        pass
+
+    lists = _random_lists(7)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        want = [_per_list(r) for r in lists]
+        monkeypatch.setattr(L.np.linalg, "_umath_linalg", NoGufunc(), raising=False)
+        got = L.fit_linear_many(lists)
+    assert all(_same(a, b) for a, b in zip(got, want))
