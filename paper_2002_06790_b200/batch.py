@@ -100,7 +100,7 @@ def group_classes(graphs, configs, graph_of, db=None) -> list:
     try:  # one pass when every class field is shared (equal tuples compare by identity first)
         t0 = _CLASS_FIELDS(configs[0])
         uniform = all(map(operator.eq, map(_CLASS_FIELDS, configs), itertools.repeat(t0)))
-    except AttributeError:
+    except (AttributeError, TypeError, ValueError):  # missing PS fields; array-valued fields
         uniform = False
     for name, by_value, default in () if uniform else _FIELDS:
         col = _column(configs, name, default)
