@@ -158,10 +158,11 @@ def test_class_sharing_matches_drop_in(seed):
     assert plain.makespan.tolist() == res.makespan.tolist() and plain.cp_len.tolist() == res.cp_len.tolist()
     import torch
 
-    if torch.cuda.device_count() >= 2:  # the same candidates split over two GPUs of this process
+    if torch.cuda.device_count() >= 2:  # the same candidates split over every GPU of this process
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
-            sh = fw.sweep_sharded(graphs, db, [c for c, *_ in ok], [gi for _, gi, *_ in ok], devices=[0, 1])
+            sh = fw.sweep_sharded(graphs, db, [c for c, *_ in ok], [gi for _, gi, *_ in ok],
+                                  devices=list(range(torch.cuda.device_count())))
         assert sh.makespan.tolist() == res.makespan.tolist() and sh.cp_len.tolist() == res.cp_len.tolist()
         assert (sh.best_index, sh.best_makespan) == (res.best_index, res.best_makespan)
     print(f"seed {seed}: {len(ok)} evaluated, {len(failing)} rejected, {len(res.classes)} classes")
